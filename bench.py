@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Reshard benchmark: PTC state transformation on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+A step is one apply_plan of the workload's reconfiguration over state already resident
+in HBM (synthetic random-init payload of the named model shapes).  `value` is the reshard
+time in ms (max over ranks, CUDA events on the launch stream); `e2e` is the same metric
+through the C-ABI with host buffers (H2D of the source arena from pinned memory, the
+reshard kernel, D2H of the destination arena).  Inputs (>= 18 GB) exceed the 126 MB L2, so
+no flush is needed between steps.  N>1 runs under torchrun, one process per GPU: logical
+device d lives on GPU d % N, destination arenas are exchanged through CUDA IPC and
+cross-GPU fragments are pushed over NVLink by the source GPU's kernel.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reshard time (ms) + effective GB/s vs HBM/NVLink roofline for TP/PP/DP A->B"
+
+# name: (catalog args (h, L, S, V, kind), from (T, P, D, devices), to (T, P, D, devices), failed)
+WORKLOADS = {
+    # BASELINE configs[1]: GPT-3 1.3B bf16+fp32 Adam scale-out (TP2,PP1,DP1)->(TP2,PP1,DP2), 2->4
+    "gpt3-1.3b-dp-scaleout": ((2048, 24, 2048, 50304, 1), (2, 1, 1, [0, 1]), (2, 1, 2, [0, 1, 2, 3]), []),
+    # configs[0]: GPT-2 small fp32+Adam (TP2,PP1,DP1)->(TP1,PP2,DP1), 2 ranks
+    "gpt2-small-tp2-to-pp2": ((768, 12, 1024, 50304, 0), (2, 1, 1, [0, 1]), (1, 2, 1, [0, 1]), []),
+    # configs[2]: GPT-3 6.7B (TP4,PP2,DP1)->(TP2,PP2,DP2), 8 GPUs (needs >= 2 GPUs of HBM)
+    "gpt3-6.7b-tp4pp2-to-tp2pp2dp2": ((4096, 32, 2048, 50304, 1), (4, 2, 1, list(range(8))),
+                                       (2, 2, 2, list(range(8))), []),
+    # configs[3]: GPT-3 6.7B failure recovery (TP2,PP2,DP2)->(TP2,PP2,DP1), failed {1,3,4,6}
+    "gpt3-6.7b-recovery": ((4096, 32, 2048, 50304, 1), (2, 2, 2, list(range(8))), (2, 2, 1, [0, 2, 5, 7]),
+                           [1, 3, 4, 6]),
+}
+DEFAULT_WORKLOAD = "gpt3-1.3b-dp-scaleout"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x1: "gpu_idle",
+    }
+
+    def __init__(self, cuda_index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        self.period = period_s
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[cuda_index]) if vis else cuda_index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def ncu_traffic(workload: str):
+    """dram read+write bytes per copy_tiles launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_copy_tiles.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(workload)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def build_plan(rs, name, n_gpus):
+    (h, L, S, V, kind), (T1, P1, D1, devs1), (T2, P2, D2, devs2), failed = WORKLOADS[name]
+    cat = rs.Catalog.gpt(h, L, S, V, kind)
+    a = cat.build_strategy([(0, d) for d in devs1], T1, P1, D1)
+    b = cat.build_strategy([(0, d) for d in devs2], T2, P2, D2)
+    plan = rs.recover(a, [(0, d) for d in failed], b) if failed else rs.generate_plan(a, b)
+    src_gpu = [d % n_gpus for d in devs1]
+    dst_gpu = [d % n_gpus for d in devs2]
+    return cat, a, b, plan, src_gpu, dst_gpu
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_reference_leg(name: str, sample_frac: float, steps: int, warmup: int):
+    """The reference's CPU path on this host: SPEC-restated planner/executor over the
+    reference's own compiled slice()/merge() (oracle/_ref/libptc_ref.so), one thread per
+    destination device, on a bounded sample of the catalog.  Falls back to the
+    restated oracle (kind "port") when the reference build is absent."""
+    from oracle.oracle import Oracle, lib_path
+
+    ref = os.path.exists(lib_path(True))
+    o = Oracle(reference=ref)
+    (h, L, S, V, kind), (T1, P1, D1, devs1), (T2, P2, D2, devs2), failed = WORKLOADS[name]
+    cat = o.catalog_gpt(h, L, S, V, kind)
+    a = cat.build_strategy([(0, d) for d in devs1], T1, P1, D1)
+    b = cat.build_strategy([(0, d) for d in devs2], T2, P2, D2)
+    plan = a.plan(b, failed=[(0, d) for d in failed])
+    st = plan.stats()
+    n_t = len(cat)
+    t1 = max(1, int(round(n_t * sample_frac)))
+    src = a.fill(0, t1)
+    threads = min(len(devs2), os.cpu_count() or 1)
+    times, sample_bytes = [], 0
+    for i in range(warmup + steps):
+        out, rep = plan.apply(src, n_threads=threads, t0=0, t1=t1)
+        del out
+        if i >= warmup:
+            times.append(rep["seconds"])
+            sample_bytes = rep["moved"] + rep["local"]
+    full_bytes = st["moved_bytes"] + st["relayout_bytes"]
+    scale = full_bytes / max(sample_bytes, 1)
+    ms = [t * 1e3 * scale for t in times]
+    return {
+        "value": statistics.mean(ms), "ms_samples": ms, "unit": "ms", "cores": threads,
+        "kind": "reference" if ref else "port",
+        "sample": (f"tensors [0,{t1}) of {n_t} ({sample_bytes / 1e9:.2f} of {full_bytes / 1e9:.2f} GB moved), "
+                   f"time scaled by bytes; {threads} threads (one per destination device, SPEC.md:504); "
+                   f"host nproc={os.cpu_count()}"),
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    leg = cpu_reference_leg(args.workload, args.sample_frac, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(leg["value"], 3), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(leg["value"], 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (splitmix64 payload of the model shapes)",
+        "config": {"workload": args.workload, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(leg["value"], 3), "unit": "ms", "cores": leg["cores"], "kind": leg["kind"],
+                         "sample": leg["sample"]},
+        "e2e": {"value": round(leg["value"], 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import paper_2312_05181_b200 as rs
+
+    rank, world, local = dist_env()
+    N = args.gpus
+    if world > 1 and world != N:
+        raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}")
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cat, a, b, plan, src_gpu, dst_gpu = build_plan(rs, args.workload, N)
+    ctx = rs.Context(N, [rank], [local])
+    ex = rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10)
+    s_bytes, d_bytes = ex.arena_bytes(rank)
+    src_ptr, dst_ptr = ctx.malloc(rank, max(s_bytes, 256)), ctx.malloc(rank, max(d_bytes, 256))
+    ex.bind(rank, src_ptr, dst_ptr)
+    opened = []
+    if dist is not None:
+        # destination arenas of every GPU, mapped into this process (CUDA IPC over NVLink)
+        mine = ctx.ipc_handle(rank, dst_ptr) if d_bytes else None
+        handles = [None] * world
+        dist.all_gather_object(handles, mine)
+        for g in range(world):
+            if g != rank and handles[g] is not None:
+                p = ctx.ipc_open(rank, handles[g])
+                opened.append(p)
+                ex.bind(g, 0, p)
+    ex.prepare()
+    ex.fill_sources()
+    stats = plan.stats()
+    tiles, copy_bytes = ex.tiles(rank)
+
+    def barrier():
+        ctx.sync(rank)
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        ex.apply()
+    barrier()
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step_ms.append(ex.apply()[0]["ms"])
+        barrier()
+        wall = time.perf_counter() - t0
+    total_ms = sum(step_ms)
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    bad = ex.verify()
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([bad], device=f"cuda:{local}", dtype=torch.int64)
+        dist.all_reduce(t)
+        bad = int(t.item())
+
+    # e2e through the C-ABI with host buffers (single-GPU world)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        try:
+            hs, hd = rs.host_alloc(s_bytes), rs.host_alloc(max(d_bytes, 1))
+            ctx.dtoh(0, hs, src_ptr, s_bytes)
+            for _ in range(1):
+                ex.run_host(0, hs, hd)
+            e2e_ms = [ex.run_host(0, hs, hd)["ms"] for _ in range(args.e2e_steps)]
+            bad_e2e = ex.verify()
+            rs.host_free(hs)
+            rs.host_free(hd)
+            e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms", "h2d_bytes_per_step": s_bytes,
+                   "d2h_bytes_per_step": d_bytes, "steps": args.e2e_steps, "mismatched_bytes": bad_e2e}
+        except Exception as exc:  # e.g. not enough pinned host memory
+            e2e = {"value": None, "unit": "ms", "h2d_bytes_per_step": s_bytes, "d2h_bytes_per_step": d_bytes,
+                   "error": str(exc)[:200]}
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peaks()
+    # roofline of the dominant (only) kernel: HBM read + write of every copied byte
+    alg_bytes = 2 * copy_bytes
+    achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
+    traffic = ncu_traffic(args.workload)
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": N, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 payload of the model shapes)",
+        "config": {"workload": args.workload, "parallelism": f"{N} GPU" + ("s" if N > 1 else "") +
+                   (" (1-GPU emulation of all logical devices)" if N == 1 else ", logical device d on GPU d%N"),
+                   "l2": "inputs larger than L2 (no flush)", "tile_kib": args.tile_kib},
+        "effective_gbs": round((stats["moved_bytes"] + stats["relayout_bytes"]) / (ms * 1e-3) / 1e9, 1),
+        "moved_bytes": stats["moved_bytes"], "relayout_bytes": stats["relayout_bytes"],
+        "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "copy_tiles_kernel", "algorithmic_bytes_per_launch": alg_bytes},
+        "e2e": e2e, "gpu_launches": args.steps * (1 if tiles else 0),
+        "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "wall_s": round(wall, 4),
+        "ms_min": round(min(step_ms), 4), "tiles": tiles,
+    }
+    if N == 1 and not args.no_cpu_baseline:
+        try:
+            leg = cpu_reference_leg(args.workload, args.sample_frac, 1, 0)
+            line["cpu_baseline"] = {"value": round(leg["value"], 3), "unit": "ms", "cores": leg["cores"],
+                                    "kind": leg["kind"], "sample": leg["sample"]}
+        except Exception as exc:
+            line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+    print(json.dumps(line), flush=True)
+    for p in opened:
+        pass
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--tile-kib", type=int, default=256)
+    ap.add_argument("--sample-frac", type=float, default=0.125)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+/* reshard_b200.h — C ABI of the B200-native PTC reshard path (drop-in boundary).
+ *
+ * The reference (arxiv 2312.05181 "Tenplex"; /root/reference) is a C++20 library,
+ * namespace `reshard`, with no FFI of its own.  These entry points are the flat C binding a
+ * maintainer would put in front of it (ctypes / cgo / JNI), one per reference operation:
+ *
+ *   rs_slice                 reshard::slice             proj/include/reshard/tensor/tensor.hpp:42
+ *                                                        proj/src/tensor/tensor.cpp:61-78
+ *   rs_merge                 reshard::merge             tensor.hpp:47, tensor.cpp:80-114
+ *   rs_range_parse/_format   Range::parse / to_string   range.hpp:59-60, range.cpp:92-144
+ *   rs_grid_cells            SplitGrid::cells           split_grid.hpp:37, split_grid.cpp:62-86
+ *   rs_grid_refine           grid_refine                split_grid.hpp:55, split_grid.cpp:119-130
+ *   rs_even_split            SplitGrid::even_split      split_grid.hpp:23, split_grid.cpp:9-18
+ *   rs_errc_name             errc_name                  proj/include/reshard/error.hpp:50, error.cpp:5-41
+ *   rs_fnv1a64               fnv1a64                    proj/include/reshard/util/hash.hpp:42
+ *   rs_build_strategy        build_strategy
+ *   rs_hosted_subtensors     hosted_subtensors
+ *   rs_validate              validate
+ *   rs_generate_plan         generate_plan              SPEC.md:224-234 (Alg. 1)
+ *   rs_recover               recover
+ *   rs_plan_cost / _text     plan_cost / serialization
+ *   rs_executor_*            apply_plan (distributed)
+ *
+ * Conventions.  Every int-returning call returns 0 on success, else 1 + errc where errc is
+ * the reference's `enum class Errc` value (error.hpp:8-48, numbering unchanged) or one of
+ * the codes appended after ScriptError (RS_ERRC_CUDA ...).  rs_last_error() returns the
+ * thread's last message, formatted "<ErrcName>: <detail>" like reshard::Error::what()
+ * (error.hpp:55-56).  No C++ exception crosses this boundary.  Device pointers are plain
+ * CUDA device addresses; the caller owns all payload buffers, handles own descriptors,
+ * streams and events.  There is no CPU fallback: without a GPU the device calls fail with
+ * RS_ERRC_DEVICE_UNAVAILABLE.
+ */
+#ifndef RESHARD_B200_H
+#define RESHARD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_MAX_RANK 8
+
+/* error codes (errc values; the call's return is 1 + errc) */
+#define RS_ERRC_CHECKPOINT_REQUIRED 28
+#define RS_ERRC_SCRIPT_ERROR 31
+#define RS_ERRC_CUDA 32
+#define RS_ERRC_DEVICE_UNAVAILABLE 33
+#define RS_ERRC_INVALID_ARGUMENT 34
+
+/* dtype codes: reference Dtype (dtype.hpp:12-17) plus BF16 (2-byte opaque payload) */
+enum rs_dtype { RS_F32 = 0, RS_F16 = 1, RS_I64 = 2, RS_U8 = 3, RS_BF16 = 4 };
+
+/* state kinds of the GPT catalog preset */
+enum rs_state_kind { RS_FP32_ADAM = 0, RS_MIXED_ADAM = 1, RS_FP32_PARAM = 2 };
+
+/* layer tags of catalog entries that are not in a transformer layer */
+#define RS_LAYER_PRE (-1)
+#define RS_LAYER_POST (-2)
+
+typedef struct rs_range {
+  int32_t rank;
+  uint64_t lo[RS_MAX_RANK];
+  uint64_t hi[RS_MAX_RANK];
+} rs_range;
+
+typedef struct rs_tensor {  /* a dense row-major tensor in device memory */
+  int32_t dtype;
+  int32_t rank;
+  uint64_t shape[RS_MAX_RANK];
+  const void* data;
+} rs_tensor;
+
+typedef struct rs_device {
+  uint32_t worker;
+  uint32_t local;
+} rs_device;
+
+typedef struct rs_plan_stats {
+  uint64_t n_split, n_move, n_merge;
+  uint64_t moved_bytes;    /* sum of Move bytes */
+  uint64_t relayout_bytes; /* resident fragments copied into a re-shaped cell */
+  uint64_t kept_bytes;     /* resident cells reused in place */
+  uint64_t dst_bytes;      /* all destination cells */
+} rs_plan_stats;
+
+typedef struct rs_timing {
+  float ms;                /* CUDA-event time of the copy kernel on its launch stream */
+  uint64_t tiles;
+  uint64_t bytes;          /* algorithmic bytes copied by this GPU */
+  uint64_t launches;       /* kernels launched in the timed region */
+} rs_timing;
+
+typedef struct rs_cell_binding {
+  int32_t gpu;             /* world GPU index */
+  int32_t arena;           /* 0: src arena, 1: dst arena */
+  uint64_t offset;
+  uint64_t bytes;
+} rs_cell_binding;
+
+typedef struct rs_context rs_context;
+typedef struct rs_catalog rs_catalog;
+typedef struct rs_ptc rs_ptc;
+typedef struct rs_plan rs_plan;
+typedef struct rs_executor rs_executor;
+
+/* ---- errors / hashing ---------------------------------------------------------------- */
+const char* rs_last_error(void);
+const char* rs_errc_name(int errc);
+int rs_errc_count(void);
+uint64_t rs_fnv1a64(const void* data, uint64_t n);
+uint64_t rs_payload_seed(const char* path);
+const char* rs_build_info(void);
+
+/* ---- box algebra (host) ----------------------------------------------------------------- */
+int rs_range_parse(const char* text, rs_range* out);
+int rs_range_format(const rs_range* r, char* buf, uint64_t cap);
+/* grid: npts[d] points for dim d, concatenated in pts */
+int rs_grid_cells(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts, int cap,
+                  rs_range* cells, int* n_cells);
+int rs_grid_refine(int rank_a, const int32_t* npts_a, const uint64_t* pts_a, int rank_b, const int32_t* npts_b,
+                   const uint64_t* pts_b, int32_t* npts_out, uint64_t* pts_out);
+int rs_even_split(int rank, const uint64_t* shape, int dim, uint64_t ways, int32_t* npts_out, uint64_t* pts_out);
+
+/* ---- device runtime -------------------------------------------------------------------- */
+int rs_device_count(int* n);
+/* A context drives `n_local` GPUs of a world of `world` GPUs: world_ids[i] runs on CUDA
+ * device cuda_devices[i].  Single process: world = n_local, world_ids = 0..n-1. */
+int rs_init(int world, int n_local, const int32_t* world_ids, const int32_t* cuda_devices, rs_context** out);
+void rs_destroy(rs_context* ctx);
+int rs_malloc(rs_context* ctx, int gpu, uint64_t bytes, void** out);
+int rs_free(rs_context* ctx, int gpu, void* ptr);
+int rs_host_alloc(uint64_t bytes, void** out); /* pinned host memory */
+int rs_host_free(void* ptr);
+int rs_memcpy_htod(rs_context* ctx, int gpu, void* dst, const void* src, uint64_t n);
+int rs_memcpy_dtoh(rs_context* ctx, int gpu, void* dst, const void* src, uint64_t n);
+int rs_memset(rs_context* ctx, int gpu, void* dst, int value, uint64_t n);
+int rs_sync(rs_context* ctx, int gpu);
+/* CUDA IPC for one-process-per-GPU worlds: 64-byte opaque handles */
+int rs_ipc_get_handle(rs_context* ctx, int gpu, void* ptr, void* handle64);
+int rs_ipc_open_handle(rs_context* ctx, int gpu, const void* handle64, void** out);
+int rs_ipc_close_handle(rs_context* ctx, int gpu, void* ptr);
+
+/* ---- tensor core on device (reference slice / merge semantics and error precedence) --- */
+int rs_slice(rs_context* ctx, int gpu, const rs_tensor* t, const rs_range* r, void* out);
+int rs_merge(rs_context* ctx, int gpu, int n_parts, const rs_range* ranges, const rs_tensor* parts, int rank,
+             const uint64_t* target_shape, void* out);
+
+/* ---- collection description ------------------------------------------------------------- */
+int rs_catalog_create(rs_catalog** out);
+int rs_catalog_gpt(uint64_t hidden, uint64_t layers, uint64_t seq, uint64_t vocab, int state_kind, rs_catalog** out);
+int rs_catalog_add(rs_catalog* c, const char* path, int dtype, int rank, const uint64_t* shape, int tp_dim, int layer);
+int rs_catalog_size(const rs_catalog* c);
+int rs_catalog_get(const rs_catalog* c, int i, char* path, int cap, int32_t* dtype, int32_t* rank, uint64_t* shape,
+                   int32_t* tp_dim, int32_t* layer);
+uint64_t rs_catalog_bytes(const rs_catalog* c);
+void rs_catalog_destroy(rs_catalog* c);
+
+int rs_build_strategy(const rs_catalog* c, int n_devices, const rs_device* devices, int tp, int pp, int dp,
+                      rs_ptc** out);
+void rs_ptc_destroy(rs_ptc* p);
+/* test hooks mirroring the SPEC validate() examples */
+int rs_ptc_set_alpha(rs_ptc* p, int partition, int n, const rs_device* devices);
+int rs_ptc_set_sigma(rs_ptc* p, int tensor, int rank, const int32_t* npts, const uint64_t* pts);
+int rs_validate(const rs_ptc* p, char* buf, uint64_t cap, int* n_violations);
+int rs_hosted_subtensors(const rs_ptc* p, rs_device dev, int cap, int32_t* tensor, rs_range* cells, int* n);
+int rs_ptc_devices(const rs_ptc* p, int cap, rs_device* out, int* n);
+/* sigma cell `cell` of tensor `tensor` (lexicographic cell order, split_grid.cpp:62-86) */
+int rs_ptc_cell(const rs_ptc* p, int tensor, int cell, rs_range* out);
+int rs_ptc_cell_count(const rs_ptc* p, int tensor, int* n);
+
+/* ---- planner ---------------------------------------------------------------------------- */
+int rs_generate_plan(const rs_ptc* from, const rs_ptc* to, rs_plan** out);
+int rs_recover(const rs_ptc* from, int n_failed, const rs_device* failed, const rs_ptc* to, rs_plan** out);
+void rs_plan_destroy(rs_plan* p);
+int rs_plan_get_stats(const rs_plan* p, rs_plan_stats* out);
+int rs_plan_cost(const rs_plan* p, int cap, rs_device* devices, uint64_t* ingress, uint64_t* egress, int* n);
+/* returns the bytes needed including NUL; writes at most cap bytes */
+int64_t rs_plan_text(const rs_plan* p, char* buf, int64_t cap);
+int rs_choose_source(int n, const rs_device* candidates, const uint64_t* egress, rs_device dst, rs_device* out);
+
+/* ---- executor (apply_plan data plane) --------------------------------------------------- */
+/* src_gpu[i]: world GPU of from-device i; dst_gpu[j]: world GPU of to-device j */
+int rs_executor_create(rs_context* ctx, const rs_plan* plan, const int32_t* src_gpu, const int32_t* dst_gpu,
+                       uint64_t tile_bytes, rs_executor** out);
+void rs_executor_destroy(rs_executor* e);
+int rs_executor_arena_bytes(const rs_executor* e, int gpu, uint64_t* src_bytes, uint64_t* dst_bytes);
+int rs_executor_bind(rs_executor* e, int gpu, void* src_arena, void* dst_arena);
+int rs_executor_prepare(rs_executor* e);
+int rs_executor_run(rs_executor* e);                     /* async launch on every local GPU */
+int rs_executor_wait(rs_executor* e, int cap, rs_timing* out, int* n); /* per local GPU */
+/* end to end on host buffers (single-GPU world): H2D src arena, copy kernel, D2H dst arena,
+ * all on the GPU's stream and bracketed by CUDA events; arenas must be bound */
+int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src_arena, void* host_dst_arena, rs_timing* out);
+int rs_executor_fill_sources(rs_executor* e);
+int rs_executor_verify(rs_executor* e, uint64_t* mismatched_bytes);
+/* bindings: src cells in (from-device, tensor, cell) order; dst cells in plan order */
+int rs_executor_src_cells(const rs_executor* e, int cap, rs_cell_binding* out, int* n);
+int rs_executor_dst_cells(const rs_executor* e, int cap, rs_cell_binding* out, int32_t* dst_device, int32_t* tensor,
+                          int32_t* cell, int* n);
+int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RESHARD_B200_H */

@@ -794,16 +794,30 @@ static std::vector<uint8_t> gen_box(const Entry& e, const Box& b) {
 
 static bool in_range(size_t t, size_t t0, size_t t1) { return t >= t0 && t < t1; }
 
+// One thread per device (input generation is not timed).
 static State fill_state(const Ptc& p, size_t t0, size_t t1) {
   State s;
-  for (auto& d : p.devices) {
-    auto& st = s.store[d];
-    for (auto [t, i] : hosted(p, d)) {
-      if (!in_range(t, t0, t1)) continue;
-      const Entry& e = p.cat.e[t];
-      st[CellKey{t, p.cells[t][i]}] = std::make_shared<const core::Tensor>(core::make(e.dtype, extents_of(p.cells[t][i]), gen_box(e, p.cells[t][i])));
-    }
-  }
+  for (auto& d : p.devices) s.store[d];
+  std::vector<std::thread> th;
+  std::vector<Fault> errs(p.devices.size(), Fault{-1, ""});
+  for (size_t k = 0; k < p.devices.size(); ++k)
+    th.emplace_back([&, k] {
+      try {
+        const Dev& d = p.devices[k];
+        auto& st = s.store.at(d);
+        for (auto [t, i] : hosted(p, d)) {
+          if (!in_range(t, t0, t1)) continue;
+          const Entry& e = p.cat.e[t];
+          st[CellKey{t, p.cells[t][i]}] =
+              std::make_shared<const core::Tensor>(core::make(e.dtype, extents_of(p.cells[t][i]), gen_box(e, p.cells[t][i])));
+        }
+      } catch (const Fault& f) {
+        errs[k] = f;
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& f : errs)
+    if (f.code >= 0) throw f;
   return s;
 }
 

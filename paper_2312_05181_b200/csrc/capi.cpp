@@ -1,0 +1,511 @@
+// extern "C" boundary (include/reshard_b200.h).  Every entry point catches reshard::Error
+// and maps it to 1 + Errc; no exception crosses the boundary.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/reshard_b200.h"
+#include "reshard/executor.hpp"
+
+using namespace reshard;
+
+struct rs_context {
+  std::unique_ptr<Context> ctx;
+};
+struct rs_catalog {
+  Catalog c;
+};
+struct rs_ptc {
+  std::shared_ptr<const PTC> p;
+};
+struct rs_plan {
+  std::shared_ptr<const ReconfigPlan> p;
+};
+struct rs_executor {
+  std::unique_ptr<Executor> e;
+};
+
+namespace {
+
+thread_local std::string g_last;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_last = e.what();
+    return 1 + static_cast<int>(e.code());
+  } catch (const std::bad_alloc&) {
+    g_last = "InvalidArgument: host allocation failed";
+    return 1 + static_cast<int>(Errc::InvalidArgument);
+  } catch (const std::exception& e) {
+    g_last = std::string("InvalidArgument: ") + e.what();
+    return 1 + static_cast<int>(Errc::InvalidArgument);
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) raise(Errc::InvalidArgument, std::string("null ") + what);
+}
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Range to_range(const rs_range& r) {
+  if (r.rank < 0 || r.rank > RS_MAX_RANK) raise(Errc::RankMismatch, "rank out of [0, 8]");
+  std::vector<Interval> v;
+  for (int i = 0; i < r.rank; ++i) v.push_back({r.lo[i], r.hi[i]});
+  return Range(v);
+}
+rs_range from_range(const Range& r) {
+  rs_range o{};
+  o.rank = r.rank();
+  for (int i = 0; i < r.rank(); ++i) o.lo[i] = r.dim(i).lo, o.hi[i] = r.dim(i).hi;
+  return o;
+}
+Shape to_shape(int rank, const uint64_t* s) {
+  if (rank < 0 || rank > RS_MAX_RANK) raise(Errc::RankMismatch, "rank out of [0, 8]");
+  if (rank) need(s, "shape");
+  return Shape(s, s + rank);
+}
+SplitGrid to_grid(int rank, const int32_t* npts, const uint64_t* pts) {
+  if (rank < 0 || rank > RS_MAX_RANK) raise(Errc::RankMismatch, "rank out of [0, 8]");
+  std::vector<std::vector<uint64_t>> g(static_cast<size_t>(rank));
+  size_t k = 0;
+  for (int d = 0; d < rank; ++d)
+    for (int i = 0; i < npts[d]; ++i) g[size_t(d)].push_back(pts[k++]);
+  return SplitGrid(std::move(g));
+}
+void from_grid(const SplitGrid& g, int32_t* npts, uint64_t* pts) {
+  size_t k = 0;
+  for (size_t d = 0; d < g.rank(); ++d) {
+    npts[d] = int32_t(g.points()[d].size());
+    for (auto p : g.points()[d]) pts[k++] = p;
+  }
+}
+DeviceId to_dev(const rs_device& d) { return DeviceId{d.worker, d.local}; }
+DeviceTensorView to_view(const rs_tensor& t) {
+  return DeviceTensorView{dtype_from_code(t.dtype), to_shape(t.rank, t.shape), t.data};
+}
+Context& ctx_of(rs_context* c) {
+  need(c, "context");
+  return *c->ctx;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rs_last_error(void) { return g_last.c_str(); }
+const char* rs_errc_name(int c) { return errc_name(static_cast<Errc>(c)); }
+int rs_errc_count(void) { return kErrcCount; }
+uint64_t rs_fnv1a64(const void* data, uint64_t n) { return fnv1a64(data, n); }
+uint64_t rs_payload_seed(const char* path) { return payload_seed(path ? path : ""); }
+const char* rs_build_info(void) {
+  return "reshard_b200 sm_100a (K1/K2 tile copy, K6 fill, K7 verify); CUDA " RESHARD_CUDA_VERSION;
+}
+
+// ---- box algebra ------------------------------------------------------------------------
+int rs_range_parse(const char* text, rs_range* out) {
+  return guard([&] {
+    need(text, "text"), need(out, "out");
+    *out = from_range(Range::parse(text));
+  });
+}
+int rs_range_format(const rs_range* r, char* buf, uint64_t cap) {
+  return guard([&] {
+    need(r, "range"), need(buf, "buf");
+    std::string s = to_range(*r).to_string();
+    if (s.size() + 1 > cap) raise(Errc::InvalidArgument, "buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+int rs_grid_cells(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts, int cap, rs_range* cells,
+                  int* n) {
+  return guard([&] {
+    auto v = to_grid(rank, npts, pts).cells(to_shape(rank, shape));
+    *n = int(v.size());
+    for (int i = 0; i < int(v.size()) && i < cap; ++i) cells[i] = from_range(v[size_t(i)]);
+  });
+}
+int rs_grid_refine(int ra, const int32_t* na, const uint64_t* pa, int rb, const int32_t* nb, const uint64_t* pb,
+                   int32_t* nout, uint64_t* pout) {
+  return guard([&] { from_grid(grid_refine(to_grid(ra, na, pa), to_grid(rb, nb, pb)), nout, pout); });
+}
+int rs_even_split(int rank, const uint64_t* shape, int dim, uint64_t ways, int32_t* nout, uint64_t* pout) {
+  return guard([&] {
+    if (dim < 0) raise(Errc::RankMismatch, "negative split dim");
+    from_grid(SplitGrid::even_split(to_shape(rank, shape), size_t(dim), ways), nout, pout);
+  });
+}
+
+// ---- device runtime ------------------------------------------------------------------------
+int rs_device_count(int* n) {
+  return guard([&] {
+    need(n, "n");
+    *n = 0;
+    if (cudaGetDeviceCount(n) != cudaSuccess) {
+      cudaGetLastError();
+      *n = 0;
+    }
+  });
+}
+int rs_init(int world, int n_local, const int32_t* world_ids, const int32_t* cuda_devices, rs_context** out) {
+  return guard([&] {
+    need(out, "out");
+    if (n_local > 0) need(world_ids, "world_ids"), need(cuda_devices, "cuda_devices");
+    auto c = std::make_unique<rs_context>();
+    c->ctx = std::make_unique<Context>(world, std::vector<int>(world_ids, world_ids + n_local),
+                                       std::vector<int>(cuda_devices, cuda_devices + n_local));
+    *out = c.release();
+  });
+}
+void rs_destroy(rs_context* c) { delete c; }
+
+int rs_malloc(rs_context* c, int gpu, uint64_t bytes, void** out) {
+  return guard([&] {
+    need(out, "out");
+    cuda_ok(cudaSetDevice(ctx_of(c).cuda_device(gpu)), "cudaSetDevice");
+    cuda_ok(cudaMalloc(out, bytes ? bytes : 256), "cudaMalloc");
+  });
+}
+int rs_free(rs_context* c, int gpu, void* p) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx_of(c).cuda_device(gpu)), "cudaSetDevice");
+    cuda_ok(cudaFree(p), "cudaFree");
+  });
+}
+int rs_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] { cuda_ok(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable), "cudaHostAlloc"); });
+}
+int rs_host_free(void* p) {
+  return guard([&] { cuda_ok(cudaFreeHost(p), "cudaFreeHost"); });
+}
+static int copy_impl(rs_context* c, int gpu, void* dst, const void* src, uint64_t n, cudaMemcpyKind kind) {
+  return guard([&] {
+    Context& x = ctx_of(c);
+    cuda_ok(cudaSetDevice(x.cuda_device(gpu)), "cudaSetDevice");
+    auto s = static_cast<cudaStream_t>(x.stream(gpu));
+    cuda_ok(cudaMemcpyAsync(dst, src, n, kind, s), "cudaMemcpyAsync");
+    cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+int rs_memcpy_htod(rs_context* c, int gpu, void* dst, const void* src, uint64_t n) {
+  return copy_impl(c, gpu, dst, src, n, cudaMemcpyHostToDevice);
+}
+int rs_memcpy_dtoh(rs_context* c, int gpu, void* dst, const void* src, uint64_t n) {
+  return copy_impl(c, gpu, dst, src, n, cudaMemcpyDeviceToHost);
+}
+int rs_memset(rs_context* c, int gpu, void* dst, int value, uint64_t n) {
+  return guard([&] {
+    Context& x = ctx_of(c);
+    cuda_ok(cudaSetDevice(x.cuda_device(gpu)), "cudaSetDevice");
+    auto s = static_cast<cudaStream_t>(x.stream(gpu));
+    cuda_ok(cudaMemsetAsync(dst, value, n, s), "cudaMemsetAsync");
+    cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+int rs_sync(rs_context* c, int gpu) {
+  return guard([&] {
+    Context& x = ctx_of(c);
+    cuda_ok(cudaSetDevice(x.cuda_device(gpu)), "cudaSetDevice");
+    cuda_ok(cudaStreamSynchronize(static_cast<cudaStream_t>(x.stream(gpu))), "cudaStreamSynchronize");
+  });
+}
+int rs_ipc_get_handle(rs_context* c, int gpu, void* ptr, void* h64) {
+  return guard([&] {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    cuda_ok(cudaSetDevice(ctx_of(c).cuda_device(gpu)), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    cuda_ok(cudaIpcGetMemHandle(&h, ptr), "cudaIpcGetMemHandle");
+    std::memcpy(h64, &h, 64);
+  });
+}
+int rs_ipc_open_handle(rs_context* c, int gpu, const void* h64, void** out) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx_of(c).cuda_device(gpu)), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, h64, 64);
+    cuda_ok(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+int rs_ipc_close_handle(rs_context* c, int gpu, void* ptr) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx_of(c).cuda_device(gpu)), "cudaSetDevice");
+    cuda_ok(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+  });
+}
+
+// ---- tensor core on device ----------------------------------------------------------------
+int rs_slice(rs_context* c, int gpu, const rs_tensor* t, const rs_range* r, void* out) {
+  return guard([&] {
+    need(t, "tensor"), need(r, "range");
+    device_slice(ctx_of(c), gpu, to_view(*t), to_range(*r), out);
+  });
+}
+int rs_merge(rs_context* c, int gpu, int n, const rs_range* ranges, const rs_tensor* parts, int rank,
+             const uint64_t* target, void* out) {
+  return guard([&] {
+    std::vector<std::pair<Range, DeviceTensorView>> v;
+    for (int i = 0; i < n; ++i) v.emplace_back(to_range(ranges[i]), to_view(parts[i]));
+    device_merge(ctx_of(c), gpu, v, to_shape(rank, target), out);
+  });
+}
+
+// ---- collection description ----------------------------------------------------------------
+int rs_catalog_create(rs_catalog** out) {
+  return guard([&] { *out = new rs_catalog(); });
+}
+int rs_catalog_gpt(uint64_t h, uint64_t L, uint64_t S, uint64_t V, int kind, rs_catalog** out) {
+  return guard([&] {
+    if (kind < 0 || kind > 2) raise(Errc::MalformedConfig, "unknown state kind");
+    if (h == 0 || S == 0 || V == 0) raise(Errc::InvalidTensor, "zero model dimension");
+    *out = new rs_catalog{Catalog::gpt(h, L, S, V, static_cast<StateKind>(kind))};
+  });
+}
+int rs_catalog_add(rs_catalog* c, const char* path, int dtype, int rank, const uint64_t* shape, int tp_dim, int layer) {
+  return guard([&] {
+    need(c, "catalog"), need(path, "path");
+    if (!*path) raise(Errc::MalformedConfig, "empty tensor path");
+    c->c.add(TensorSpec{path, dtype_from_code(dtype), to_shape(rank, shape), tp_dim, layer});
+  });
+}
+int rs_catalog_size(const rs_catalog* c) { return c ? int(c->c.tensors.size()) : 0; }
+int rs_catalog_get(const rs_catalog* c, int i, char* path, int cap, int32_t* dtype, int32_t* rank, uint64_t* shape,
+                   int32_t* tp_dim, int32_t* layer) {
+  return guard([&] {
+    need(c, "catalog");
+    if (i < 0 || size_t(i) >= c->c.tensors.size()) raise(Errc::IndexOutOfRange, "catalog index");
+    const TensorSpec& t = c->c.tensors[size_t(i)];
+    if (path && cap > 0) std::snprintf(path, size_t(cap), "%s", t.path.c_str());
+    *dtype = int32_t(t.dtype), *rank = int32_t(t.shape.size()), *tp_dim = t.tp_dim, *layer = t.layer;
+    for (size_t d = 0; d < t.shape.size(); ++d) shape[d] = t.shape[d];
+  });
+}
+uint64_t rs_catalog_bytes(const rs_catalog* c) { return c ? c->c.total_bytes() : 0; }
+void rs_catalog_destroy(rs_catalog* c) { delete c; }
+
+int rs_build_strategy(const rs_catalog* c, int n, const rs_device* devs, int tp, int pp, int dp, rs_ptc** out) {
+  return guard([&] {
+    need(c, "catalog"), need(out, "out");
+    std::vector<DeviceId> d;
+    for (int i = 0; i < n; ++i) d.push_back(to_dev(devs[i]));
+    *out = new rs_ptc{std::make_shared<const PTC>(build_strategy(c->c, d, JobConfig{tp, pp, dp}))};
+  });
+}
+void rs_ptc_destroy(rs_ptc* p) { delete p; }
+int rs_ptc_set_alpha(rs_ptc* p, int part, int n, const rs_device* devs) {
+  return guard([&] {
+    need(p, "ptc");
+    auto q = std::make_shared<PTC>(*p->p);
+    if (part < 0 || size_t(part) >= q->alpha.size()) raise(Errc::IndexOutOfRange, "partition");
+    q->alpha[size_t(part)].clear();
+    for (int i = 0; i < n; ++i) {
+      int o = q->ordinal(to_dev(devs[i]));
+      q->alpha[size_t(part)].push_back(o < 0 ? uint32_t(q->devices.size() + size_t(i)) : uint32_t(o));
+    }
+    p->p = q;
+  });
+}
+int rs_ptc_set_sigma(rs_ptc* p, int t, int rank, const int32_t* npts, const uint64_t* pts) {
+  return guard([&] {
+    need(p, "ptc");
+    auto q = std::make_shared<PTC>(*p->p);
+    if (t < 0 || size_t(t) >= q->sigma.size()) raise(Errc::IndexOutOfRange, "tensor");
+    q->sigma[size_t(t)] = to_grid(rank, npts, pts);
+    p->p = q;
+  });
+}
+int rs_validate(const rs_ptc* p, char* buf, uint64_t cap, int* n) {
+  return guard([&] {
+    need(p, "ptc");
+    auto v = validate(*p->p);
+    std::string s;
+    for (auto& x : v) s += x + "\n";
+    if (buf && cap) std::snprintf(buf, size_t(cap), "%s", s.c_str());
+    *n = int(v.size());
+  });
+}
+int rs_hosted_subtensors(const rs_ptc* p, rs_device dev, int cap, int32_t* tensor, rs_range* cells, int* n) {
+  return guard([&] {
+    need(p, "ptc");
+    auto h = hosted_subtensors(*p->p, to_dev(dev));
+    *n = int(h.size());
+    for (int i = 0; i < int(h.size()) && i < cap; ++i) {
+      tensor[i] = int32_t(h[size_t(i)].first);
+      cells[i] = from_range(p->p->cells[h[size_t(i)].first][h[size_t(i)].second]);
+    }
+  });
+}
+int rs_ptc_devices(const rs_ptc* p, int cap, rs_device* out, int* n) {
+  return guard([&] {
+    need(p, "ptc");
+    *n = int(p->p->devices.size());
+    for (int i = 0; i < *n && i < cap; ++i) out[i] = rs_device{p->p->devices[size_t(i)].worker, p->p->devices[size_t(i)].local};
+  });
+}
+
+int rs_ptc_cell(const rs_ptc* p, int t, int c, rs_range* out) {
+  return guard([&] {
+    need(p, "ptc"), need(out, "out");
+    const auto& cells = p->p->cells;
+    if (t < 0 || size_t(t) >= cells.size() || c < 0 || size_t(c) >= cells[size_t(t)].size())
+      raise(Errc::IndexOutOfRange, "tensor/cell index");
+    *out = from_range(cells[size_t(t)][size_t(c)]);
+  });
+}
+int rs_ptc_cell_count(const rs_ptc* p, int t, int* n) {
+  return guard([&] {
+    need(p, "ptc"), need(n, "out");
+    if (t < 0 || size_t(t) >= p->p->cells.size()) raise(Errc::IndexOutOfRange, "tensor index");
+    *n = int(p->p->cells[size_t(t)].size());
+  });
+}
+
+// ---- planner ------------------------------------------------------------------------------
+int rs_generate_plan(const rs_ptc* a, const rs_ptc* b, rs_plan** out) {
+  return guard([&] {
+    need(a, "from"), need(b, "to"), need(out, "out");
+    *out = new rs_plan{generate_plan(a->p, b->p)};
+  });
+}
+int rs_recover(const rs_ptc* a, int nf, const rs_device* failed, const rs_ptc* b, rs_plan** out) {
+  return guard([&] {
+    need(a, "from"), need(b, "to"), need(out, "out");
+    std::vector<DeviceId> f;
+    for (int i = 0; i < nf; ++i) f.push_back(to_dev(failed[i]));
+    *out = new rs_plan{recover(a->p, f, b->p)};
+  });
+}
+void rs_plan_destroy(rs_plan* p) { delete p; }
+int rs_plan_get_stats(const rs_plan* p, rs_plan_stats* out) {
+  return guard([&] {
+    need(p, "plan"), need(out, "out");
+    PlanStats s = plan_stats(*p->p);
+    *out = rs_plan_stats{s.n_split, s.n_move, s.n_merge, s.moved_bytes, s.relayout_bytes, s.kept_bytes, s.dst_bytes};
+  });
+}
+int rs_plan_cost(const rs_plan* p, int cap, rs_device* devs, uint64_t* in, uint64_t* eg, int* n) {
+  return guard([&] {
+    need(p, "plan");
+    PlanCost c = plan_cost(*p->p);
+    *n = int(c.devices.size());
+    for (int i = 0; i < *n && i < cap; ++i)
+      devs[i] = rs_device{c.devices[size_t(i)].worker, c.devices[size_t(i)].local}, in[i] = c.ingress[size_t(i)],
+      eg[i] = c.egress[size_t(i)];
+  });
+}
+int64_t rs_plan_text(const rs_plan* p, char* buf, int64_t cap) {
+  if (!p) return -1;
+  std::string s = plan_text(*p->p);
+  if (buf && cap > 0) std::snprintf(buf, size_t(cap), "%s", s.c_str());
+  return int64_t(s.size()) + 1;
+}
+int rs_choose_source(int n, const rs_device* cand, const uint64_t* egress, rs_device dst, rs_device* out) {
+  return guard([&] {
+    std::vector<DeviceId> c;
+    std::map<DeviceId, uint64_t> eg;
+    for (int i = 0; i < n; ++i) c.push_back(to_dev(cand[i])), eg[to_dev(cand[i])] = egress ? egress[i] : 0;
+    DeviceId d = choose_source(c, to_dev(dst), eg);
+    *out = rs_device{d.worker, d.local};
+  });
+}
+
+// ---- executor ---------------------------------------------------------------------------------
+int rs_executor_create(rs_context* c, const rs_plan* p, const int32_t* src_gpu, const int32_t* dst_gpu,
+                       uint64_t tile_bytes, rs_executor** out) {
+  return guard([&] {
+    need(p, "plan"), need(out, "out");
+    std::vector<int> s(src_gpu, src_gpu + p->p->from->devices.size());
+    std::vector<int> d(dst_gpu, dst_gpu + p->p->to->devices.size());
+    *out = new rs_executor{std::make_unique<Executor>(ctx_of(c), p->p, s, d, tile_bytes ? tile_bytes : (256u << 10))};
+  });
+}
+void rs_executor_destroy(rs_executor* e) { delete e; }
+int rs_executor_arena_bytes(const rs_executor* e, int gpu, uint64_t* s, uint64_t* d) {
+  return guard([&] {
+    need(e, "executor");
+    *s = e->e->src_arena_bytes(gpu), *d = e->e->dst_arena_bytes(gpu);
+  });
+}
+int rs_executor_bind(rs_executor* e, int gpu, void* s, void* d) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->bind(gpu, s, d);
+  });
+}
+int rs_executor_prepare(rs_executor* e) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->prepare();
+  });
+}
+int rs_executor_run(rs_executor* e) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->run();
+  });
+}
+int rs_executor_wait(rs_executor* e, int cap, rs_timing* out, int* n) {
+  return guard([&] {
+    need(e, "executor");
+    auto t = e->e->wait();
+    *n = int(t.size());
+    for (int i = 0; i < *n && i < cap; ++i)
+      out[i] = rs_timing{t[size_t(i)].ms, t[size_t(i)].tiles, t[size_t(i)].bytes, t[size_t(i)].launches};
+  });
+}
+int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src, void* host_dst, rs_timing* out) {
+  return guard([&] {
+    need(e, "executor"), need(out, "out");
+    Timing t = e->e->run_host(gpu, host_src, host_dst);
+    *out = rs_timing{t.ms, t.tiles, t.bytes, t.launches};
+  });
+}
+int rs_executor_fill_sources(rs_executor* e) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->fill_sources();
+  });
+}
+int rs_executor_verify(rs_executor* e, uint64_t* bad) {
+  return guard([&] {
+    need(e, "executor"), need(bad, "out");
+    *bad = e->e->verify_destinations();
+  });
+}
+int rs_executor_src_cells(const rs_executor* e, int cap, rs_cell_binding* out, int* n) {
+  return guard([&] {
+    need(e, "executor");
+    const auto& v = e->e->src_bindings();
+    *n = int(v.size());
+    for (int i = 0; i < *n && i < cap; ++i) out[i] = rs_cell_binding{v[size_t(i)].gpu, v[size_t(i)].arena, v[size_t(i)].offset, v[size_t(i)].bytes};
+  });
+}
+int rs_executor_dst_cells(const rs_executor* e, int cap, rs_cell_binding* out, int32_t* dev, int32_t* tensor, int32_t* cell,
+                          int* n) {
+  return guard([&] {
+    need(e, "executor");
+    const auto& v = e->e->dst_bindings();
+    const auto& dc = e->e->plan().dst_cells;
+    *n = int(v.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+      out[i] = rs_cell_binding{v[size_t(i)].gpu, v[size_t(i)].arena, v[size_t(i)].offset, v[size_t(i)].bytes};
+      if (dev) dev[i] = int32_t(dc[size_t(i)].dst_device);
+      if (tensor) tensor[i] = int32_t(dc[size_t(i)].tensor);
+      if (cell) cell[i] = int32_t(dc[size_t(i)].cell);
+    }
+  });
+}
+int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes) {
+  return guard([&] {
+    need(e, "executor");
+    *tiles = e->e->tiles_for(gpu), *bytes = e->e->copy_bytes_for(gpu);
+  });
+}
+
+}  // extern "C"

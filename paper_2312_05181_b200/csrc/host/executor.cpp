@@ -1,0 +1,445 @@
+// Executor: lowers a ReconfigPlan to copy tiles and runs them (see reshard/executor.hpp).
+#include "reshard/executor.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+
+#include "cuda/kernels.hpp"
+
+namespace reshard {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr uint64_t kCellAlign = 256;
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Emit the copy of box `ext` from (src cell shape ss, origin sl) to (dst cell shape ds,
+// origin dl), collapsing dimensions that are full on both sides into one contiguous run
+// and cutting the rest into tiles of about `tile` bytes.
+template <class Emit>
+void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& dl, const Shape& ds, uint64_t w,
+               uint64_t tile, Emit&& emit) {
+  const int r = int(ext.size());
+  std::vector<uint64_t> sst(size_t(r), w), dst(size_t(r), w);
+  for (int d = r - 1; d > 0; --d) sst[size_t(d - 1)] = sst[size_t(d)] * ss[size_t(d)], dst[size_t(d - 1)] = dst[size_t(d)] * ds[size_t(d)];
+  uint64_t soff = 0, doff = 0;
+  for (int d = 0; d < r; ++d) soff += sl[size_t(d)] * sst[size_t(d)], doff += dl[size_t(d)] * dst[size_t(d)];
+  if (r == 0) {
+    emit(soff, doff, 0, 0, 1, w);
+    return;
+  }
+  // innermost run: dims k..r-1, where every dim > k is full on both sides
+  int k = r - 1;
+  uint64_t run = ext[size_t(k)] * w;
+  while (k > 0 && ext[size_t(k)] == ss[size_t(k)] && ext[size_t(k)] == ds[size_t(k)]) {
+    --k;
+    run *= ext[size_t(k)];
+  }
+  // rows = dim k-1 (if any); dims 0..k-2 enumerated here
+  const uint64_t rows = k > 0 ? ext[size_t(k - 1)] : 1;
+  const uint64_t sp = k > 0 ? sst[size_t(k - 1)] : run, dp = k > 0 ? dst[size_t(k - 1)] : run;
+  const int outer = std::max(k - 1, 0);
+  std::vector<uint64_t> idx(size_t(outer), 0);
+  for (;;) {
+    uint64_t so = soff, dof = doff;
+    for (int d = 0; d < outer; ++d) so += idx[size_t(d)] * sst[size_t(d)], dof += idx[size_t(d)] * dst[size_t(d)];
+    if (run >= tile) {
+      for (uint64_t row = 0; row < rows; ++row)
+        for (uint64_t c = 0; c < run; c += tile) emit(so + row * sp + c, dof + row * dp + c, 0, 0, 1, std::min(tile, run - c));
+    } else {
+      const uint64_t per = std::max<uint64_t>(1, tile / run);
+      for (uint64_t row = 0; row < rows; row += per)
+        emit(so + row * sp, dof + row * dp, sp, dp, std::min(per, rows - row), run);
+    }
+    int d = outer - 1;
+    for (; d >= 0; --d) {
+      if (++idx[size_t(d)] < ext[size_t(d)]) break;
+      idx[size_t(d)] = 0;
+    }
+    if (d < 0) return;
+  }
+}
+
+int copy_grid(int sms, uint64_t tiles) { return int(std::min<uint64_t>(tiles, uint64_t(sms) * 4)); }
+constexpr int kCopyBlock = 512;
+
+}  // namespace
+
+// ---- Context ---------------------------------------------------------------------------
+Context::Context(int world, std::vector<int> world_ids, std::vector<int> cuda_devices)
+    : world_(world), world_ids_(std::move(world_ids)), cuda_devs_(std::move(cuda_devices)) {
+  if (world_ids_.size() != cuda_devs_.size()) raise(Errc::InvalidArgument, "world ids / cuda devices length");
+  if (world_ < 1) raise(Errc::InvalidArgument, "world must have at least one GPU");
+  // A context with no local GPU is a planning-only view of the world: layouts and tiles can
+  // be computed (and compared across ranks) but nothing runs.
+  int n = 0;
+  if (!cuda_devs_.empty() && (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)) {
+    cudaGetLastError();
+    raise(Errc::DeviceUnavailable, "no CUDA device visible");
+  }
+  for (size_t i = 0; i < cuda_devs_.size(); ++i) {
+    if (cuda_devs_[i] < 0 || cuda_devs_[i] >= n) raise(Errc::DeviceUnavailable, "cuda device " + std::to_string(cuda_devs_[i]));
+    if (world_ids_[i] < 0 || world_ids_[i] >= world_) raise(Errc::InvalidArgument, "world id out of range");
+    DeviceGuard g(cuda_devs_[i]);
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    streams_.push_back(s);
+    int sm = 0;
+    ck(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, cuda_devs_[i]), "sm count");
+    sms_.push_back(sm);
+    // direct peer access between the local GPUs (single-process multi-GPU runs)
+    for (size_t j = 0; j < cuda_devs_.size(); ++j) {
+      if (j == i) continue;
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, cuda_devs_[i], cuda_devs_[j]);
+      if (ok) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(cuda_devs_[j], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else ck(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  }
+}
+Context::~Context() {
+  for (size_t i = 0; i < streams_.size(); ++i) {
+    cudaSetDevice(cuda_devs_[i]);
+    cudaStreamDestroy(static_cast<cudaStream_t>(streams_[i]));
+  }
+}
+int Context::local_of(int w) const {
+  auto it = std::find(world_ids_.begin(), world_ids_.end(), w);
+  return it == world_ids_.end() ? -1 : int(it - world_ids_.begin());
+}
+int Context::cuda_device(int w) const {
+  int l = local_of(w);
+  if (l < 0) raise(Errc::DeviceUnavailable, "world GPU " + std::to_string(w) + " is not driven by this process");
+  return cuda_devs_[size_t(l)];
+}
+void* Context::stream(int w) const {
+  int l = local_of(w);
+  if (l < 0) raise(Errc::DeviceUnavailable, "world GPU " + std::to_string(w) + " is not local");
+  return streams_[size_t(l)];
+}
+int Context::sm_count(int w) const {
+  int l = local_of(w);
+  return l < 0 ? 148 : sms_[size_t(l)];
+}
+
+// ---- Executor --------------------------------------------------------------------------
+struct Executor::Local {
+  int world = -1, dev = -1;
+  CopyTile* d_tiles = nullptr;
+  uint64_t n_tiles = 0, bytes = 0;
+  cudaEvent_t start = nullptr, stop = nullptr;
+  unsigned long long* d_count = nullptr;
+  ~Local() {
+    if (dev < 0) return;
+    cudaSetDevice(dev);
+    if (d_tiles) cudaFree(d_tiles);
+    if (d_count) cudaFree(d_count);
+    if (start) cudaEventDestroy(start);
+    if (stop) cudaEventDestroy(stop);
+  }
+};
+
+Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu,
+                   std::vector<int> dst_gpu, uint64_t tile_bytes)
+    : ctx_(ctx), plan_(std::move(plan)), src_gpu_(std::move(src_gpu)), dst_gpu_(std::move(dst_gpu)),
+      tile_bytes_(std::max<uint64_t>(4096, tile_bytes / 16 * 16)) {
+  const PTC& a = *plan_->from;
+  const PTC& b = *plan_->to;
+  const int G = ctx_.world();
+  if (src_gpu_.size() != a.devices.size() || dst_gpu_.size() != b.devices.size())
+    raise(Errc::InvalidArgument, "device -> GPU maps must cover both layouts");
+  for (int g : src_gpu_)
+    if (g < 0 || g >= G) raise(Errc::InvalidArgument, "src GPU out of range");
+  for (int g : dst_gpu_)
+    if (g < 0 || g >= G) raise(Errc::InvalidArgument, "dst GPU out of range");
+  src_size_.assign(size_t(G), 0);
+  dst_size_.assign(size_t(G), 0);
+  src_base_.assign(size_t(G), nullptr);
+  dst_base_.assign(size_t(G), nullptr);
+
+  // src arena layout
+  std::vector<std::unordered_map<uint64_t, size_t>> src_lookup(a.devices.size());
+  for (uint32_t i = 0; i < a.devices.size(); ++i)
+    for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
+      const int g = src_gpu_[i];
+      CellBinding bnd{g, 0, src_size_[size_t(g)], a.cells[t][c].elements() * dtype_width(a.catalog.tensors[t].dtype)};
+      src_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
+      src_lookup[i][(uint64_t(t) << 32) | c] = src_bind_.size();
+      src_bind_.push_back(bnd);
+    }
+  // dst arena layout (kept cells alias their src cell when the logical device stays on its GPU)
+  for (const PlanDstCell& dc : plan_->dst_cells) {
+    const int g = dst_gpu_[dc.dst_device];
+    const uint64_t bytes = b.cells[dc.tensor][dc.cell].elements() * dtype_width(b.catalog.tensors[dc.tensor].dtype);
+    if (dc.kept) {
+      const PlanFragment& f = plan_->fragments[dc.first];
+      const CellBinding& sb = src_bind_[src_lookup[f.src_device].at((uint64_t(dc.tensor) << 32) | f.src_cell)];
+      if (sb.gpu == g) {
+        dst_bind_.push_back(sb);
+        continue;
+      }
+    }
+    CellBinding bnd{g, 1, dst_size_[size_t(g)], bytes};
+    dst_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
+    dst_bind_.push_back(bnd);
+  }
+  // fragments -> logical tiles, grouped by the executing (source) GPU
+  logical_.assign(size_t(G), {});
+  for (size_t j = 0; j < plan_->dst_cells.size(); ++j) {
+    const PlanDstCell& dc = plan_->dst_cells[j];
+    const CellBinding& db = dst_bind_[j];
+    if (db.arena == 0) continue;  // kept in place
+    const Range& dbox = b.cells[dc.tensor][dc.cell];
+    const uint64_t w = dtype_width(b.catalog.tensors[dc.tensor].dtype);
+    for (uint32_t k = dc.first; k < dc.first + dc.count; ++k) {
+      const PlanFragment& f = plan_->fragments[k];
+      const CellBinding& sb = src_bind_[src_lookup[f.src_device].at((uint64_t(dc.tensor) << 32) | f.src_cell)];
+      const Range& sbox = a.cells[dc.tensor][f.src_cell];
+      const Range rs = f.box.rebase_into(sbox), rd = f.box.rebase_into(dbox);
+      Shape sl, dl;
+      for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo), dl.push_back(rd.dim(d).lo);
+      auto& out = logical_[size_t(sb.gpu)];
+      lower_box(f.box.extents(), sl, sbox.extents(), dl, dbox.extents(), w, tile_bytes_,
+                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+                  out.push_back(Logical{sb.gpu, db.gpu, sb.offset + so, db.offset + dof, sp, dp, uint32_t(rows),
+                                        uint32_t(run)});
+                });
+    }
+  }
+  for (int w : ctx_.local_world_ids()) {
+    auto l = std::make_unique<Local>();
+    l->world = w;
+    l->dev = ctx_.cuda_device(w);
+    DeviceGuard g(l->dev);
+    ck(cudaEventCreate(&l->start), "cudaEventCreate");
+    ck(cudaEventCreate(&l->stop), "cudaEventCreate");
+    ck(cudaMalloc(&l->d_count, sizeof(unsigned long long)), "cudaMalloc");
+    local_.push_back(std::move(l));
+  }
+}
+
+Executor::~Executor() = default;
+
+void Executor::bind(int gpu, void* src, void* dst) {
+  if (gpu < 0 || gpu >= ctx_.world()) raise(Errc::InvalidArgument, "bind: GPU out of range");
+  // null is allowed for an arena this process never touches (e.g. a peer's src arena)
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % kCellAlign)
+    raise(Errc::InvalidArgument, "bind: arenas must be 256-byte aligned");
+  src_base_[size_t(gpu)] = src;
+  dst_base_[size_t(gpu)] = dst;
+}
+
+void Executor::prepare() {
+  for (auto& l : local_) {
+    const auto& lt = logical_[size_t(l->world)];
+    std::vector<CopyTile> tiles;
+    tiles.reserve(lt.size());
+    uint64_t bytes = 0;
+    for (const Logical& x : lt) {
+      char* s = static_cast<char*>(src_base_[size_t(x.src_gpu)]);
+      char* d = static_cast<char*>(dst_base_[size_t(x.dst_gpu)]);
+      if (!s || !d) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(!s ? x.src_gpu : x.dst_gpu) + " not bound");
+      tiles.push_back(CopyTile{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), uint64_t(reinterpret_cast<uintptr_t>(d + x.dst_off)),
+                               x.src_pitch, x.dst_pitch, x.rows, x.row_bytes});
+      bytes += uint64_t(x.rows) * x.row_bytes;
+    }
+    DeviceGuard g(l->dev);
+    if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
+    if (!tiles.empty()) {
+      ck(cudaMalloc(&l->d_tiles, tiles.size() * sizeof(CopyTile)), "cudaMalloc tiles");
+      ck(cudaMemcpy(l->d_tiles, tiles.data(), tiles.size() * sizeof(CopyTile), cudaMemcpyHostToDevice), "upload tiles");
+    }
+    l->n_tiles = tiles.size();
+    l->bytes = bytes;
+  }
+}
+
+void Executor::run() {
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    auto s = static_cast<cudaStream_t>(ctx_.stream(l->world));
+    ck(cudaEventRecord(l->start, s), "cudaEventRecord");
+    cuda::launch_copy_tiles(l->d_tiles, l->n_tiles, copy_grid(ctx_.sm_count(l->world), l->n_tiles), kCopyBlock, s);
+    ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
+  }
+}
+
+std::vector<Timing> Executor::wait() {
+  std::vector<Timing> out;
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
+    Timing t;
+    ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
+    t.tiles = l->n_tiles;
+    t.bytes = l->bytes;
+    t.launches = l->n_tiles ? 1 : 0;
+    out.push_back(t);
+  }
+  return out;
+}
+
+Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
+  Local* l = nullptr;
+  for (auto& x : local_)
+    if (x->world == gpu) l = x.get();
+  if (!l) raise(Errc::DeviceUnavailable, "run_host: GPU " + std::to_string(gpu) + " is not local");
+  if (ctx_.world() != 1) raise(Errc::InvalidArgument, "run_host: single-GPU worlds only");
+  DeviceGuard g(l->dev);
+  auto s = static_cast<cudaStream_t>(ctx_.stream(gpu));
+  ck(cudaEventRecord(l->start, s), "cudaEventRecord");
+  ck(cudaMemcpyAsync(src_base_[size_t(gpu)], host_src, src_size_[size_t(gpu)], cudaMemcpyHostToDevice, s), "h2d src arena");
+  cuda::launch_copy_tiles(l->d_tiles, l->n_tiles, copy_grid(ctx_.sm_count(gpu), l->n_tiles), kCopyBlock, s);
+  ck(cudaMemcpyAsync(host_dst, dst_base_[size_t(gpu)], dst_size_[size_t(gpu)], cudaMemcpyDeviceToHost, s), "d2h dst arena");
+  ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
+  ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
+  Timing t;
+  ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
+  t.tiles = l->n_tiles, t.bytes = l->bytes, t.launches = l->n_tiles ? 1 : 0;
+  return t;
+}
+
+uint64_t Executor::tiles_for(int gpu) const { return logical_[size_t(gpu)].size(); }
+uint64_t Executor::copy_bytes_for(int gpu) const {
+  uint64_t n = 0;
+  for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes;
+  return n;
+}
+
+void Executor::fill_sources() {
+  const PTC& a = *plan_->from;
+  size_t k = 0;
+  for (uint32_t i = 0; i < a.devices.size(); ++i)
+    for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
+      const CellBinding& b = src_bind_[k++];
+      if (ctx_.local_of(b.gpu) < 0) continue;
+      const TensorSpec& e = a.catalog.tensors[t];
+      DeviceGuard g(ctx_.cuda_device(b.gpu));
+      cuda::launch_fill(static_cast<char*>(src_base_[size_t(b.gpu)]) + b.offset, payload_seed(e.path),
+                        cuda::make_geom(e.shape, dtype_width(e.dtype), a.cells[t][c]), ctx_.stream(b.gpu));
+    }
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(ctx_.stream(l->world))), "fill sync");
+  }
+}
+
+uint64_t Executor::verify_destinations() {
+  const PTC& b = *plan_->to;
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    ck(cudaMemsetAsync(l->d_count, 0, sizeof(unsigned long long), static_cast<cudaStream_t>(ctx_.stream(l->world))), "memset");
+  }
+  for (size_t j = 0; j < plan_->dst_cells.size(); ++j) {
+    const CellBinding& bd = dst_bind_[j];
+    int li = ctx_.local_of(bd.gpu);
+    if (li < 0) continue;
+    const PlanDstCell& dc = plan_->dst_cells[j];
+    const TensorSpec& e = b.catalog.tensors[dc.tensor];
+    const char* base = static_cast<const char*>(bd.arena == 0 ? src_base_[size_t(bd.gpu)] : dst_base_[size_t(bd.gpu)]);
+    DeviceGuard g(ctx_.cuda_device(bd.gpu));
+    Local* l = nullptr;
+    for (auto& x : local_)
+      if (x->world == bd.gpu) l = x.get();
+    cuda::launch_verify(base + bd.offset, payload_seed(e.path), cuda::make_geom(e.shape, dtype_width(e.dtype), b.cells[dc.tensor][dc.cell]),
+                        l->d_count, ctx_.stream(bd.gpu));
+  }
+  uint64_t bad = 0;
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    unsigned long long h = 0;
+    ck(cudaMemcpyAsync(&h, l->d_count, sizeof(h), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(ctx_.stream(l->world))), "count d2h");
+    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(ctx_.stream(l->world))), "verify sync");
+    bad += h;
+  }
+  return bad;
+}
+
+// ---- device slice / merge ----------------------------------------------------------------
+namespace {
+void run_tiles_once(Context& ctx, int gpu, const std::vector<CopyTile>& tiles) {
+  if (tiles.empty()) return;
+  DeviceGuard g(ctx.cuda_device(gpu));
+  auto s = static_cast<cudaStream_t>(ctx.stream(gpu));
+  CopyTile* d = nullptr;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&d), tiles.size() * sizeof(CopyTile), s), "cudaMallocAsync");
+  ck(cudaMemcpyAsync(d, tiles.data(), tiles.size() * sizeof(CopyTile), cudaMemcpyHostToDevice, s), "tiles h2d");
+  cuda::launch_copy_tiles(d, tiles.size(), copy_grid(ctx.sm_count(gpu), tiles.size()), kCopyBlock, s);
+  ck(cudaFreeAsync(d, s), "cudaFreeAsync");
+  ck(cudaStreamSynchronize(s), "slice/merge sync");
+}
+void append_box(std::vector<CopyTile>& tiles, const char* src, char* dst, const Shape& ext, const Shape& sl, const Shape& ss,
+                const Shape& dl, const Shape& ds, uint64_t w) {
+  lower_box(ext, sl, ss, dl, ds, w, 256 << 10, [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+    tiles.push_back(CopyTile{uint64_t(reinterpret_cast<uintptr_t>(src + so)), uint64_t(reinterpret_cast<uintptr_t>(dst + dof)), sp, dp,
+                             uint32_t(rows), uint32_t(run)});
+  });
+}
+}  // namespace
+
+void device_slice(Context& ctx, int gpu, const DeviceTensorView& t, const Range& r, void* out) {
+  for (auto e : t.shape)
+    if (e == 0) raise(Errc::InvalidTensor, "zero extent");
+  const uint64_t w = dtype_width(t.dtype);
+  r.check_against(t.shape);
+  Shape lo;
+  for (int d = 0; d < r.rank(); ++d) lo.push_back(r.dim(d).lo);
+  std::vector<CopyTile> tiles;
+  append_box(tiles, static_cast<const char*>(t.data), static_cast<char*>(out), r.extents(), lo, t.shape,
+             Shape(lo.size(), 0), r.extents(), w);
+  run_tiles_once(ctx, gpu, tiles);
+}
+
+void device_merge(Context& ctx, int gpu, const std::vector<std::pair<Range, DeviceTensorView>>& parts, const Shape& target,
+                  void* out) {
+  // validation order of the reference merge (tensor.cpp:81-98)
+  if (parts.empty()) raise(Errc::TilingGap, "no parts");
+  const Dtype dt = parts.front().second.dtype;
+  uint64_t covered = 0;
+  for (const auto& [r, p] : parts) {
+    r.check_against(target);
+    if (p.dtype != dt) raise(Errc::DtypeMismatch, "parts disagree on dtype");
+    if (p.shape != r.extents()) raise(Errc::ShapeMismatch, "part shape does not match its range " + r.to_string());
+    covered += r.elements();
+  }
+  for (size_t i = 0; i < parts.size(); ++i)
+    for (size_t j = i + 1; j < parts.size(); ++j)
+      if (parts[i].first.overlaps(parts[j].first))
+        raise(Errc::TilingOverlap, parts[i].first.to_string() + " overlaps " + parts[j].first.to_string());
+  if (covered != shape_elements(target))
+    raise(Errc::TilingGap, "parts cover " + std::to_string(covered) + " of " + std::to_string(shape_elements(target)) + " elements");
+  for (auto e : target)
+    if (e == 0) raise(Errc::InvalidTensor, "zero extent");
+  const uint64_t w = dtype_width(dt);
+  std::vector<CopyTile> tiles;
+  for (const auto& [r, p] : parts) {
+    Shape lo;
+    for (int d = 0; d < r.rank(); ++d) lo.push_back(r.dim(d).lo);
+    append_box(tiles, static_cast<const char*>(p.data), static_cast<char*>(out), r.extents(), Shape(lo.size(), 0), r.extents(),
+               lo, target, w);
+  }
+  run_tiles_once(ctx, gpu, tiles);
+}
+
+}  // namespace reshard

@@ -1,0 +1,133 @@
+// reshard/executor.hpp — the B200 State Transformer: executes a ReconfigPlan as device copy
+// tiles.  Replaces the SPEC executor's apply_plan, whose data
+// plane is the reference's slice()/merge() row walker (proj/src/tensor/tensor.cpp:35-114).
+//
+// Layout in HBM: every GPU of the world owns two arenas.
+//   src arena: the cells of `from` hosted by the logical devices mapped to the GPU, in
+//              (device, tensor, cell) order, each 256-byte aligned;
+//   dst arena: the cells of `to` that are NOT kept (a kept cell is a resident cell whose
+//              range does not change; it stays where it is in the src arena).
+// Every refined fragment becomes one strided 2-D copy (rows x row_bytes, two pitches)
+// from its source cell into its final offset of the destination cell, i.e. split, move
+// and merge are fused into a single write; no staging, no merge pass.  Copies are split
+// into ~256 KiB tiles and executed by one persistent kernel per source GPU (push: a
+// cross-GPU tile stores straight into the peer's dst arena over NVLink).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "reshard/planner.hpp"
+
+namespace reshard {
+
+// Must match the device struct in cuda/kernels.cuh.
+struct CopyTile {
+  uint64_t src, dst;              // absolute device addresses (dst may be a peer mapping)
+  uint64_t src_pitch, dst_pitch;  // bytes between consecutive rows
+  uint32_t rows, row_bytes;
+};
+static_assert(sizeof(CopyTile) == 40, "CopyTile layout");
+
+struct CellBinding {
+  int32_t gpu = -1;    // world GPU index
+  int32_t arena = 0;   // 0: src arena, 1: dst arena
+  uint64_t offset = 0; // byte offset inside the arena
+  uint64_t bytes = 0;
+};
+
+struct Timing {
+  float ms = 0;        // device time of the copy kernel(s), CUDA events on the launch stream
+  uint64_t tiles = 0;
+  uint64_t bytes = 0;  // algorithmic bytes copied (each counted once)
+  uint64_t launches = 0;
+};
+
+// The GPUs this process drives.  World GPU w is local iff local_of(w) >= 0.
+class Context {
+ public:
+  Context(int world_gpus, std::vector<int> world_ids, std::vector<int> cuda_devices);
+  ~Context();
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  int world() const { return world_; }
+  int local_of(int world_gpu) const;
+  int cuda_device(int world_gpu) const;       // DeviceUnavailable when not local
+  void* stream(int world_gpu) const;          // cudaStream_t
+  const std::vector<int>& local_world_ids() const { return world_ids_; }
+  int sm_count(int world_gpu) const;
+
+ private:
+  int world_;
+  std::vector<int> world_ids_, cuda_devs_;
+  std::vector<void*> streams_;
+  std::vector<int> sms_;
+};
+
+class Executor {
+ public:
+  // src_gpu[i]: world GPU of from->devices[i]; dst_gpu[j]: world GPU of to->devices[j].
+  Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu, std::vector<int> dst_gpu,
+           uint64_t tile_bytes = 256 << 10);
+  ~Executor();
+
+  uint64_t src_arena_bytes(int gpu) const { return src_size_[size_t(gpu)]; }
+  uint64_t dst_arena_bytes(int gpu) const { return dst_size_[size_t(gpu)]; }
+  // Arena base addresses as seen by THIS process (own GPUs: local pointers; peers: P2P/IPC
+  // mappings).  Every GPU that a local tile reads from or writes to must be bound.
+  void bind(int gpu, void* src_base, void* dst_base);
+  void prepare();  // lower fragments to tiles for the local GPUs and upload them
+
+  void run();                       // launch on every local GPU (async)
+  std::vector<Timing> wait();       // per local GPU, after completion
+  // End-to-end on host buffers (single-GPU world): H2D of the whole src arena from
+  // `host_src`, the copy kernel, D2H of the whole dst arena into `host_dst`; CUDA events
+  // bracket all three.  Pinned host memory gives full PCIe bandwidth.
+  Timing run_host(int gpu, const void* host_src, void* host_dst);
+
+  // Synthetic payload (K6) into the src cells of local GPUs; K7 verification of every
+  // destination cell on local GPUs (kept cells included).  Returns mismatching bytes.
+  void fill_sources();
+  uint64_t verify_destinations();
+
+  const std::vector<CellBinding>& src_bindings() const { return src_bind_; }  // per (from dev, t, cell) in order
+  const std::vector<CellBinding>& dst_bindings() const { return dst_bind_; }  // per plan->dst_cells entry
+  const ReconfigPlan& plan() const { return *plan_; }
+  uint64_t tiles_for(int gpu) const;
+  uint64_t copy_bytes_for(int gpu) const;
+
+ private:
+  struct Logical {  // a tile before arena bases are known
+    int32_t src_gpu, dst_gpu;
+    uint64_t src_off, dst_off, src_pitch, dst_pitch;
+    uint32_t rows, row_bytes;
+  };
+  void lower();
+
+  Context& ctx_;
+  std::shared_ptr<const ReconfigPlan> plan_;
+  std::vector<int> src_gpu_, dst_gpu_;
+  uint64_t tile_bytes_;
+  std::vector<uint64_t> src_size_, dst_size_;
+  std::vector<CellBinding> src_bind_, dst_bind_;
+  std::vector<std::vector<size_t>> src_index_;  // [from dev][(t, cell) hosted order] -> src_bind_ index
+  std::vector<std::vector<Logical>> logical_;   // per executing (source) world GPU
+  std::vector<void*> src_base_, dst_base_;
+  struct Local;
+  std::vector<std::unique_ptr<Local>> local_;   // per local GPU: device tiles, events
+};
+
+// Device-side slice / merge on one GPU (reference slice tensor.cpp:61-78, merge :80-114):
+// same validation and error precedence, bytes moved by the tile kernel.
+struct DeviceTensorView {
+  Dtype dtype;
+  Shape shape;
+  const void* data;
+};
+void device_slice(Context& ctx, int gpu, const DeviceTensorView& t, const Range& r, void* out);
+void device_merge(Context& ctx, int gpu, const std::vector<std::pair<Range, DeviceTensorView>>& parts,
+                  const Shape& target, void* out);
+
+}  // namespace reshard

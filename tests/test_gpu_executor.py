@@ -1,0 +1,218 @@
+"""GPU parity of the apply_plan data plane: every destination cell produced by the sm_100a
+tile kernel, read back through the C-ABI, must equal the oracle's apply_plan result
+(bytes moved by the reference's slice/merge, tensor.cpp:61-114) byte for byte."""
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DEV = lambda n, w=0: [(w, i) for i in range(n)]  # noqa: E731
+
+
+def _run(rs, ctx, plan, n_src, n_dst, tile=256 << 10):
+    ex = rs.Executor(ctx, plan, [0] * n_src, [0] * n_dst, tile)
+    ex.allocate_local()
+    ex.prepare()
+    ex.fill_sources()
+    t = ex.apply()
+    return ex, t
+
+
+def _compare_with_oracle(rs, ctx, ex, b_ptc, ostate, devs):
+    n = 0
+    for dev, t, c, bnd in ex.dst_cells():
+        got = np.zeros(bnd.nbytes, np.uint8)
+        ctx.dtoh(0, got.ctypes.data, ex.cell_ptr(bnd), bnd.nbytes)
+        want = ostate.cell(devs[dev], t, b_ptc.cell(t, c))
+        assert np.array_equal(got, want), f"tensor {t} cell {c} on device {devs[dev]}"
+        n += 1
+    return n
+
+
+def _pair(rs, orc, entries, a_cfg, b_cfg, failed=()):
+    cat = rs.Catalog.from_entries(entries)
+    ocat = orc.catalog(entries)
+    (T1, P1, D1, d1), (T2, P2, D2, d2) = a_cfg, b_cfg
+    a, b = cat.build_strategy(d1, T1, P1, D1), cat.build_strategy(d2, T2, P2, D2)
+    oa, ob = ocat.build_strategy(d1, T1, P1, D1), ocat.build_strategy(d2, T2, P2, D2)
+    plan = rs.recover(a, failed, b) if failed else rs.generate_plan(a, b)
+    oplan = oa.plan(ob, failed=list(failed))
+    assert plan.text() == oplan.text()
+    return a, b, plan, oa, ob, oplan
+
+
+def test_fig6_end_to_end(rs, orc, ctx):
+    entries = [("t1", 0, (6,), 0, 0), ("t2", 0, (6,), 0, 1)]
+    a, b, plan, oa, ob, oplan = _pair(rs, orc, entries, (2, 1, 1, DEV(2)), (3, 2, 1, DEV(6)))
+    ex, _ = _run(rs, ctx, plan, 2, 6)
+    ost, _ = oplan.apply(oa.fill(), n_threads=6)
+    assert _compare_with_oracle(rs, ctx, ex, b, ost, DEV(6)) == 6
+    assert ex.verify() == 0
+
+
+def _random_entries(rng, n_t):
+    ent = []
+    for i in range(n_t):
+        rank = rng.choice([1, 2, 2, 3])
+        shape = tuple(rng.choice([2, 4, 6, 8, 12, 24]) for _ in range(rank))
+        dtype = rng.choice([0, 1, 2, 3])
+        tp = rng.choice([-1] + list(range(rank)))
+        ent.append((f"t{i}", dtype, shape, tp, i))
+    return ent
+
+
+def _configs(n_dev_max=8):
+    out = []
+    for T in (1, 2, 3, 4):
+        for P in (1, 2, 3):
+            for D in (1, 2, 4):
+                if T * P * D <= n_dev_max:
+                    out.append((T, P, D))
+    return out
+
+
+def test_random_transitions_bytes_exact(rs, orc, ctx):
+    """SPEC acceptance #1 on the GPU: random DP/TP/PP transitions, bit-identical."""
+    rng = random.Random(1234)
+    cfgs = _configs()
+    done = 0
+    while done < 60:
+        n_t = rng.randint(1, 6)
+        ents = _random_entries(rng, n_t)
+        (T1, P1, D1), (T2, P2, D2) = rng.choice(cfgs), rng.choice(cfgs)
+        if P1 > n_t or P2 > n_t:
+            continue
+        # TP must divide every sliced extent
+        ok = all(tp < 0 or (shape[tp] % T1 == 0 and shape[tp] % T2 == 0) for _, _, shape, tp, _ in ents)
+        if not ok:
+            continue
+        n1, n2 = T1 * P1 * D1, T2 * P2 * D2
+        base = rng.choice([0, 0, n1])  # sometimes fresh destination devices
+        d1, d2 = DEV(n1), [(0, base + i) for i in range(n2)]
+        a, b, plan, oa, ob, oplan = _pair(rs, orc, ents, (T1, P1, D1, d1), (T2, P2, D2, d2))
+        tile = rng.choice([4096, 65536, 256 << 10])
+        ex, _ = _run(rs, ctx, plan, n1, n2, tile)
+        ost, _ = oplan.apply(oa.fill(), n_threads=4)
+        _compare_with_oracle(rs, ctx, ex, b, ost, d2)
+        assert ex.verify() == 0
+        done += 1
+
+
+def test_gpt2_small_config1_bytes_exact(rs, orc, ctx):
+    """BASELINE configs[0]: GPT-2 small fp32+Adam (TP2,PP1,DP1)->(TP1,PP2,DP1), every
+    destination byte compared with the oracle running the reference's slice/merge."""
+    cat = rs.Catalog.gpt(768, 12, 1024, 50304, rs.FP32_ADAM)
+    a, b = cat.build_strategy(DEV(2), 2, 1, 1), cat.build_strategy(DEV(2), 1, 2, 1)
+    plan = rs.generate_plan(a, b)
+    ex, t = _run(rs, ctx, plan, 2, 2)
+    from oracle.oracle import Oracle, lib_path
+    import os
+
+    o = Oracle(reference=os.path.exists(lib_path(True)))
+    ocat = o.catalog_gpt(768, 12, 1024, 50304, 0)
+    oa, ob = ocat.build_strategy(DEV(2), 2, 1, 1), ocat.build_strategy(DEV(2), 1, 2, 1)
+    oplan = oa.plan(ob)
+    assert oplan.text() == plan.text()
+    ost, rep = oplan.apply(oa.fill(), n_threads=2)
+    n = _compare_with_oracle(rs, ctx, ex, b, ost, DEV(2))
+    assert n == 444
+    assert ex.verify() == 0
+    assert t[0]["bytes"] == rep["moved"] + rep["local"]
+
+
+def test_recovery_plan_on_gpu(rs, orc, ctx):
+    """configs[3] structure at toy size: (2,2,2) -> (2,2,1) on survivors, failed {1,3,4,6}."""
+    h, L, S, V = 64, 4, 16, 128
+    cat = rs.Catalog.gpt(h, L, S, V, rs.MIXED_ADAM)
+    a = cat.build_strategy(DEV(8), 2, 2, 2)
+    surv = [(0, 0), (0, 2), (0, 5), (0, 7)]
+    b = cat.build_strategy(surv, 2, 2, 1)
+    plan = rs.recover(a, [(0, 1), (0, 3), (0, 4), (0, 6)], b)
+    st = plan.stats()
+    assert st["n_split"] == 0 and st["n_merge"] == 0 and st["relayout_bytes"] == 0
+    assert st["moved_bytes"] * 2 == st["dst_bytes"]
+    ex, _ = _run(rs, ctx, plan, 8, 4)
+    assert ex.verify() == 0
+
+
+def test_gpt3_1p3b_config2_full_size(rs, ctx):
+    """BASELINE configs[1] at full size (36.97 GB of destination state on one GPU):
+    size-independent property check — every destination byte equals the regenerated
+    base-tensor payload (K7), which the oracle pins at small sizes."""
+    cat = rs.Catalog.gpt(2048, 24, 2048, 50304, rs.MIXED_ADAM)
+    a, b = cat.build_strategy(DEV(2), 2, 1, 1), cat.build_strategy(DEV(4), 2, 1, 2)
+    plan = rs.generate_plan(a, b)
+    st = plan.stats()
+    assert st["n_move"] == 2336 and st["moved_bytes"] == 18484379648
+    ex, t = _run(rs, ctx, plan, 2, 4)
+    assert t[0]["bytes"] == st["moved_bytes"]
+    assert ex.verify() == 0
+
+
+def test_device_slice_merge_vs_reference(rs, orc, ctx):
+    """rs_slice / rs_merge (device) vs the oracle slice/merge on random boxes."""
+    rng = random.Random(7)
+    for _ in range(200):
+        rank = rng.randint(1, 4)
+        shape = tuple(rng.randint(1, 9) for _ in range(rank))
+        dtype = rng.choice([0, 1, 2, 3])
+        w = {0: 4, 1: 2, 2: 8, 3: 1}[dtype]
+        n = int(np.prod(shape)) * w
+        host = np.frombuffer(rng.randbytes(n), np.uint8).copy()
+        box = []
+        for e in shape:
+            lo = rng.randint(0, e - 1)
+            box.append((lo, rng.randint(lo + 1, e)))
+        want = orc.slice(dtype, shape, host, box)
+        src = ctx.malloc(0, n)
+        out = ctx.malloc(0, max(want.size, 1))
+        ctx.htod(0, src, host.ctypes.data, n)
+        rs.slice(ctx, 0, rs.DeviceTensor(dtype, shape, src), box, out)
+        got = np.zeros(want.size, np.uint8)
+        ctx.dtoh(0, got.ctypes.data, out, want.size)
+        assert np.array_equal(got, want)
+        # merge the grid cells of a random grid back
+        pts = []
+        for e in shape:
+            k = rng.randint(0, min(2, e - 1))
+            pts.append(sorted(rng.sample(range(1, e), k)) if k else [])
+        cells = orc.grid_cells(shape, pts)
+        parts, ptrs = [], []
+        for c in cells:
+            data = orc.slice(dtype, shape, host, c)
+            p = ctx.malloc(0, data.size)
+            ctx.htod(0, p, data.ctypes.data, data.size)
+            ptrs.append(p)
+            parts.append((c, rs.DeviceTensor(dtype, tuple(z - a for a, z in c), p)))
+        mo = ctx.malloc(0, n)
+        rs.merge(ctx, 0, parts, shape, mo)
+        got = np.zeros(n, np.uint8)
+        ctx.dtoh(0, got.ctypes.data, mo, n)
+        assert np.array_equal(got, host)
+        for p in ptrs + [src, out, mo]:
+            ctx.free(0, p)
+
+
+def test_device_merge_error_precedence(rs, ctx):
+    """Error order of reference merge (tensor.cpp:84-98): per part check_against ->
+    DtypeMismatch -> ShapeMismatch, then TilingOverlap, then TilingGap."""
+    buf = ctx.malloc(0, 1024)
+    T = lambda dt, sh: rs.DeviceTensor(dt, sh, buf)  # noqa: E731
+
+    def err(parts, target):
+        with pytest.raises(rs.ReshardError) as e:
+            rs.merge(ctx, 0, parts, target, buf)
+        return e.value.name
+
+    assert err([], (6,)) == "TilingGap"
+    assert err([([(0, 7)], T(0, (7,)))], (6,)) == "RangeOutOfBounds"
+    assert err([([(0, 3), (0, 1)], T(0, (3, 1)))], (6,)) == "RankMismatch"
+    assert err([([(0, 3)], T(0, (3,))), ([(3, 6)], T(1, (3,)))], (6,)) == "DtypeMismatch"
+    assert err([([(0, 3)], T(0, (2,)))], (6,)) == "ShapeMismatch"
+    assert err([([(0, 4)], T(0, (4,))), ([(3, 6)], T(0, (3,)))], (6,)) == "TilingOverlap"
+    assert err([([(0, 3)], T(0, (3,)))], (6,)) == "TilingGap"
+    # a later part's range error wins over an earlier part's dtype? no: checks are per part in order
+    assert err([([(0, 3)], T(0, (3,))), ([(3, 6)], T(1, (2,))), ([(0, 9)], T(0, (9,)))], (6,)) == "DtypeMismatch"
+    ctx.free(0, buf)
