@@ -36,6 +36,7 @@
 #include "reshard/error.hpp"
 #include "reshard/tensor/split_grid.hpp"
 #include "reshard/tensor/tensor.hpp"
+#include "reshard/util/hash.hpp"
 #endif
 
 namespace orc {
@@ -397,7 +398,7 @@ static std::vector<std::string> bracket_items(const std::string& t) {
   return items;
 }
 // spec=true: RangeSpec::parse (":" leaves a dim unconstrained, reported as lo=hi=UINT64_MAX)
-static Box parse_box(const std::string& t, bool spec) {
+[[maybe_unused]] static Box parse_box(const std::string& t, bool spec) {
   Box b;
   for (auto& item : bracket_items(t)) {
     if (spec && item == ":") {
@@ -1079,7 +1080,22 @@ int orc_even_split(int rank, const uint64_t* shape, int dim, uint64_t ways, int*
 // spec=1 parses a RangeSpec; unconstrained dims come back as lo=hi=UINT64_MAX
 int orc_range_parse(const char* text, int spec, int* rank, uint64_t* lo, uint64_t* hi) {
   return guard([&] {
+#ifdef ORACLE_REFERENCE_CORE
+    // the reference's own Range::parse / RangeSpec::parse (range.cpp:135-193)
+    Box b = core::guarded([&] {
+      Box r;
+      if (spec) {
+        const reshard::RangeSpec rs = reshard::RangeSpec::parse(text);
+        for (auto& d : rs.dims())
+          r.push_back(d ? Iv{d->lo, d->hi} : Iv{UINT64_MAX, UINT64_MAX});
+      } else {
+        r = core::from_ref(reshard::Range::parse(text));
+      }
+      return r;
+    });
+#else
     Box b = parse_box(text, spec != 0);
+#endif
     if (b.size() > kMaxRank) fail(MalformedFrame, "rank too large");
     *rank = int(b.size());
     for (size_t i = 0; i < b.size(); ++i) lo[i] = b[i].lo, hi[i] = b[i].hi;
@@ -1087,6 +1103,18 @@ int orc_range_parse(const char* text, int spec, int* rank, uint64_t* lo, uint64_
 }
 
 // ---- hash / rng ------------------------------------------------------------------------
+#ifdef ORACLE_REFERENCE_CORE
+// the reference's header-only hash.hpp
+uint64_t orc_fnv1a64(const uint8_t* p, uint64_t n) { return reshard::fnv1a64(std::span<const uint8_t>(p, n)); }
+uint64_t orc_splitmix64_next(uint64_t* state) { return reshard::splitmix64_next(*state); }
+uint64_t orc_next_below(uint64_t* state, uint64_t n) {
+  // SplitMix64 keeps its state private; replay from the seed through the public API
+  reshard::SplitMix64 r(*state);
+  uint64_t v = r.next_below(n);
+  if (n != 0) reshard::splitmix64_next(*state);
+  return v;
+}
+#else
 uint64_t orc_fnv1a64(const uint8_t* p, uint64_t n) { return fnv1a(p, n); }
 uint64_t orc_splitmix64_next(uint64_t* state) { return mix64(*state += kGolden); }
 uint64_t orc_next_below(uint64_t* state, uint64_t n) {
@@ -1095,6 +1123,7 @@ uint64_t orc_next_below(uint64_t* state, uint64_t n) {
   *state = r.s;
   return v;
 }
+#endif
 void orc_stream_bytes(uint64_t seed, uint64_t off, uint64_t n, uint8_t* out) { stream_bytes(seed, off, n, out); }
 uint64_t orc_path_seed(const char* path) { return path_seed(path); }
 
