@@ -200,6 +200,38 @@ int rs_executor_dst_cells(const rs_executor* e, int cap, rs_cell_binding* out, i
                           int32_t* cell, int* n);
 int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes);
 
+/* ---- dataset index repartitioning ------------------------------------- */
+/* shuffle_epoch: Fisher-Yates (i = N-1 .. 1, j = next_below(i+1)), splitmix64 seeded seed^epoch */
+int rs_shuffle_epoch(uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm_host);
+int rs_repartition_count(uint64_t n, uint64_t global_batch, uint64_t at_step, uint64_t new_dp, uint64_t rank,
+                         uint64_t* count);
+int rs_repartition_position(uint64_t n, uint64_t global_batch, uint64_t at_step, uint64_t new_dp, uint64_t rank,
+                            uint64_t k, uint64_t* pos);
+/* locate_sample on host arrays: out = {file, offset, length, locator class} */
+int rs_locate_sample(uint64_t n, uint64_t global_batch, uint64_t at_step, uint64_t new_dp, uint64_t rank,
+                     uint64_t k, const uint64_t* perm, const uint64_t* samples, const uint8_t* file_class,
+                     uint64_t* out4);
+
+typedef struct rs_dataset_index {  /* device pointers */
+  const uint64_t* perm;          /* N: epoch permutation */
+  const uint64_t* samples;       /* N x {file, offset, length} */
+  const uint8_t* file_class;     /* per file: 0 local, 1 peer, 2 remote for the calling rank */
+  uint64_t n;
+} rs_dataset_index;
+
+typedef struct rs_partition_out {  /* device pointers, capacity = the rank's count */
+  uint64_t* pos;                 /* global positions */
+  uint64_t* ent;                 /* 3 x u64 per sample */
+  uint64_t* boff;                /* exclusive prefix sum of lengths */
+  uint32_t* queue[3];            /* sample indices k per locator class, increasing */
+  uint64_t* qcount;              /* 3 counts, written by the kernel */
+} rs_partition_out;
+
+int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
+/* K5: gather + scan + compaction for one rank in one kernel launch (timed with events) */
+int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,
+                   uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
+
 #ifdef __cplusplus
 }
 #endif

@@ -511,3 +511,96 @@ def apply_plan(ctx: Context, plan: Plan, src_gpu=None, dst_gpu=None) -> Executor
     ex.fill_sources()
     ex.apply()
     return ex
+
+
+# ---- dataset index repartitioning -------------------------------------------
+def shuffle_epoch(n: int, seed: int, epoch: int):
+    import numpy as np
+
+    perm = np.empty(max(n, 1), np.uint64)
+    _chk(lib.rs_shuffle_epoch(n, seed, epoch, perm.ctypes.data))
+    return perm[:n]
+
+
+def repartition_count(n, global_batch, at_step, new_dp, rank) -> int:
+    c = C.c_uint64()
+    _chk(lib.rs_repartition_count(n, global_batch, at_step, new_dp, rank, C.byref(c)))
+    return c.value
+
+
+def repartition_position(n, global_batch, at_step, new_dp, rank, k) -> int:
+    c = C.c_uint64()
+    _chk(lib.rs_repartition_position(n, global_batch, at_step, new_dp, rank, k, C.byref(c)))
+    return c.value
+
+
+def locate_sample(n, global_batch, at_step, new_dp, rank, k, perm, samples, file_class):
+    """(file, offset, length, locator class) of the rank's k-th remaining sample (host arrays)."""
+    import numpy as np
+
+    out = (C.c_uint64 * 4)()
+    perm = np.ascontiguousarray(perm, np.uint64)
+    samples = np.ascontiguousarray(samples, np.uint64)
+    file_class = np.ascontiguousarray(file_class, np.uint8)
+    _chk(lib.rs_locate_sample(n, global_batch, at_step, new_dp, rank, k, perm.ctypes.data, samples.ctypes.data,
+                              file_class.ctypes.data, out))
+    return tuple(int(x) for x in out)
+
+
+class Partition:
+    """Device buffers of one rank's repartition output (K5)."""
+
+    def __init__(self, ctx: Context, gpu: int, count: int):
+        self.ctx, self.gpu, self.count = ctx, gpu, count
+        n = max(count, 1)
+        self.pos = ctx.malloc(gpu, 8 * n)
+        self.ent = ctx.malloc(gpu, 24 * n)
+        self.boff = ctx.malloc(gpu, 8 * n)
+        self.queue = [ctx.malloc(gpu, 4 * n) for _ in range(3)]
+        self.qcount = ctx.malloc(gpu, 24)
+        sb = C.c_uint64()
+        _chk(lib.rs_repartition_scratch_bytes(count, C.byref(sb)))
+        self.scratch = ctx.malloc(gpu, max(sb.value, 256))
+
+    def c(self):
+        o = _capi.rs_partition_out()
+        o.pos, o.ent, o.boff, o.qcount = self.pos, self.ent, self.boff, self.qcount
+        for i in range(3):
+            o.queue[i] = self.queue[i]
+        return o
+
+    def free(self):
+        for p in [self.pos, self.ent, self.boff, self.qcount, self.scratch, *self.queue]:
+            self.ctx.free(self.gpu, p)
+
+    def fetch(self) -> dict:
+        import numpy as np
+
+        n = self.count
+        out = {}
+        for name, ptr, dt, width in [("pos", self.pos, np.uint64, 1), ("ent", self.ent, np.uint64, 3),
+                                     ("boff", self.boff, np.uint64, 1)]:
+            a = np.empty(max(n * width, 1), dt)
+            self.ctx.dtoh(self.gpu, a.ctypes.data, ptr, n * width * 8)
+            out[name] = a[: n * width].reshape(n, width) if width > 1 else a[:n]
+        qc = np.empty(3, np.uint64)
+        self.ctx.dtoh(self.gpu, qc.ctypes.data, self.qcount, 24)
+        out["qcount"] = [int(x) for x in qc]
+        qs = []
+        for c in range(3):
+            q = np.empty(max(int(qc[c]), 1), np.uint32)
+            if qc[c]:
+                self.ctx.dtoh(self.gpu, q.ctypes.data, self.queue[c], int(qc[c]) * 4)
+            qs.append(q[: int(qc[c])])
+        out["qidx"] = np.concatenate(qs) if n else np.empty(0, np.uint32)
+        return out
+
+
+def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_ptr: int, n: int, global_batch: int,
+                at_step: int, new_dp: int, rank: int, part: "Partition") -> dict:
+    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, class_ptr, n)
+    t = _capi.rs_timing()
+    out = part.c()
+    _chk(lib.rs_repartition(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, C.byref(out),
+                            part.scratch, C.byref(t)))
+    return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches)

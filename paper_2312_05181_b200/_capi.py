@@ -119,7 +119,23 @@ SIGNATURES = {
     "rs_executor_dst_cells": (C.c_int, [P, C.c_int, C.POINTER(rs_cell_binding), I32P, I32P, I32P,
                                         C.POINTER(C.c_int)]),
     "rs_executor_tiles": (C.c_int, [P, C.c_int, U64P, U64P]),
+    "rs_shuffle_epoch": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, P]),
+    "rs_repartition_count": (C.c_int, [C.c_uint64] * 5 + [U64P]),
+    "rs_repartition_position": (C.c_int, [C.c_uint64] * 6 + [U64P]),
+    "rs_locate_sample": (C.c_int, [C.c_uint64] * 6 + [P, P, P, U64P]),
+    "rs_repartition_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
+    "rs_repartition": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
+                                 P, C.POINTER(rs_timing)]),
 }
+
+
+class rs_dataset_index(C.Structure):
+    _fields_ = [("perm", C.c_void_p), ("samples", C.c_void_p), ("file_class", C.c_void_p), ("n", C.c_uint64)]
+
+
+class rs_partition_out(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("ent", C.c_void_p), ("boff", C.c_void_p), ("queue", C.c_void_p * 3),
+                ("qcount", C.c_void_p)]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:

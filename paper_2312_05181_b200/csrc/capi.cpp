@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/reshard_b200.h"
+#include "reshard/dataset.hpp"
 #include "reshard/executor.hpp"
 
 using namespace reshard;
@@ -505,6 +506,52 @@ int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* 
   return guard([&] {
     need(e, "executor");
     *tiles = e->e->tiles_for(gpu), *bytes = e->e->copy_bytes_for(gpu);
+  });
+}
+
+// ---- dataset ---------------------------------------------------------------------------------
+int rs_shuffle_epoch(uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm) {
+  return guard([&] {
+    if (n) need(perm, "perm");
+    shuffle_epoch(n, seed, epoch, perm);
+  });
+}
+int rs_repartition_count(uint64_t n, uint64_t B, uint64_t at_step, uint64_t dp, uint64_t rank, uint64_t* count) {
+  return guard([&] {
+    need(count, "count");
+    *count = repartition_count(n, B, at_step, dp, rank);
+  });
+}
+int rs_repartition_position(uint64_t n, uint64_t B, uint64_t at_step, uint64_t dp, uint64_t rank, uint64_t k,
+                            uint64_t* pos) {
+  return guard([&] {
+    need(pos, "pos");
+    *pos = repartition_position(n, B, at_step, dp, rank, k);
+  });
+}
+int rs_locate_sample(uint64_t n, uint64_t B, uint64_t at_step, uint64_t dp, uint64_t rank, uint64_t k, const uint64_t* perm,
+                     const uint64_t* samples, const uint8_t* file_class, uint64_t* out4) {
+  return guard([&] {
+    need(perm, "perm"), need(samples, "samples"), need(file_class, "file_class"), need(out4, "out");
+    const uint64_t pos = repartition_position(n, B, at_step, dp, rank, k);
+    const uint64_t* e = samples + 3 * perm[pos];
+    out4[0] = e[0], out4[1] = e[1], out4[2] = e[2], out4[3] = file_class[e[0]];
+  });
+}
+int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes) {
+  return guard([&] {
+    need(bytes, "bytes");
+    *bytes = repartition_scratch_bytes(count);
+  });
+}
+int rs_repartition(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t B, uint64_t at_step, uint64_t dp,
+                   uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing) {
+  return guard([&] {
+    need(idx, "index"), need(out, "out"), need(scratch, "scratch");
+    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n};
+    PartitionOut o{out->pos, out->ent, out->boff, {out->queue[0], out->queue[1], out->queue[2]}, out->qcount};
+    Timing t = repartition_device(ctx_of(c), gpu, v, B, at_step, dp, rank, o, scratch);
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches};
   });
 }
 

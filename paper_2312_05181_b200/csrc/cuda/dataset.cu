@@ -1,0 +1,214 @@
+// K5 dataset_repartition (sm_100a): for one new DP rank, in ONE pass over its remaining
+// samples —
+//   pos[k]  = closed-form global position,
+//   ent[k]  = samples[perm[pos[k]]]                (24-byte gather through the permutation),
+//   boff[k] = exclusive prefix sum of lengths       (the sample's offset in the read buffer),
+//   queue[class] += k                               (stable compaction by locator class,
+//                                                    local > peer > remote).
+// The scan is a single-pass decoupled look-back: each CTA takes the next tile from an
+// atomic counter (so it only ever waits on tiles already owned by running CTAs), scans its
+// 2048 items with warp shuffles, publishes its aggregate, looks back over predecessors'
+// aggregates / inclusive prefixes, and publishes its inclusive prefix.
+// Replaces the CPU loops of oracle.cpp orc_dataset_gather (SPEC restatement).
+#include <cuda/atomic>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "reshard/dataset.hpp"
+
+namespace reshard {
+
+namespace {
+
+constexpr int kThreads = 256, kItems = 8, kTile = kThreads * kItems, kWarps = kThreads / 32;
+
+struct Agg {
+  unsigned long long len, c0, c1, c2;
+};
+__device__ __forceinline__ Agg operator+(const Agg& a, const Agg& b) { return {a.len + b.len, a.c0 + b.c0, a.c1 + b.c1, a.c2 + b.c2}; }
+
+struct Params {
+  const unsigned long long* perm;
+  const unsigned long long* samples;
+  const unsigned char* file_class;
+  unsigned long long n, B, at_step, b, rank, count, in_full, full;
+};
+struct Outs {
+  unsigned long long *pos, *ent, *boff;
+  unsigned *q0, *q1, *q2;
+  unsigned long long* qcount;
+};
+struct Scratch {
+  unsigned* counter;
+  unsigned* flags;  // 0 empty, 1 aggregate, 2 inclusive prefix
+  Agg* agg;
+  Agg* inc;
+  unsigned ntiles;
+};
+
+__device__ __forceinline__ Agg shfl_up(const Agg& v, int d) {
+  return {__shfl_up_sync(0xffffffffu, v.len, d), __shfl_up_sync(0xffffffffu, v.c0, d),
+          __shfl_up_sync(0xffffffffu, v.c1, d), __shfl_up_sync(0xffffffffu, v.c2, d)};
+}
+__device__ __forceinline__ Agg ldcg(const Agg* p) {
+  return {__ldcg(&p->len), __ldcg(&p->c0), __ldcg(&p->c1), __ldcg(&p->c2)};
+}
+__device__ __forceinline__ void stcg(Agg* p, const Agg& v) {
+  __stcg(&p->len, v.len), __stcg(&p->c0, v.c0), __stcg(&p->c1, v.c1), __stcg(&p->c2, v.c2);
+}
+
+__global__ void __launch_bounds__(kThreads) repartition_kernel(Params p, Outs o, Scratch s) {
+  __shared__ unsigned tile_sh;
+  __shared__ Agg warp_tot[kWarps];
+  __shared__ Agg tile_prefix;
+  if (threadIdx.x == 0) tile_sh = atomicAdd(s.counter, 1u);
+  __syncthreads();
+  const unsigned tile = tile_sh;
+  const unsigned long long k0 = (unsigned long long)tile * kTile + (unsigned long long)threadIdx.x * kItems;
+
+  // position of k0, then advanced incrementally
+  unsigned long long batch = 0, r = 0;
+  if (k0 < p.in_full) batch = p.at_step + k0 / p.b, r = k0 % p.b;
+  unsigned long long len[kItems];
+  unsigned char cls[kItems];
+  Agg mine{0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long k = k0 + j;
+    len[j] = 0, cls[j] = 3;
+    if (k >= p.count) continue;
+    unsigned long long pos;
+    if (k < p.in_full) {
+      pos = batch * p.B + p.rank * p.b + r;
+      if (++r == p.b) r = 0, ++batch;
+    } else {
+      pos = p.full * p.B + p.rank * p.b + (k - p.in_full);
+    }
+    const unsigned long long idx = __ldg(p.perm + pos);
+    const unsigned long long* e = p.samples + 3 * idx;
+    const unsigned long long f = __ldg(e), off = __ldg(e + 1), L = __ldg(e + 2);
+    o.pos[k] = pos;
+    o.ent[3 * k] = f, o.ent[3 * k + 1] = off, o.ent[3 * k + 2] = L;
+    const unsigned char c = __ldg(p.file_class + f);
+    len[j] = L, cls[j] = c;
+    mine.len += L;
+    mine.c0 += c == 0, mine.c1 += c == 1, mine.c2 += c == 2;
+  }
+  // block exclusive scan of the per-thread aggregates
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Agg inc = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Agg up = shfl_up(inc, d);
+    if (lane >= d) inc = inc + up;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  Agg warp_base{0, 0, 0, 0}, total{0, 0, 0, 0};
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) warp_base = warp_base + warp_tot[w];
+    total = total + warp_tot[w];
+  }
+  const Agg excl_in_tile = warp_base + (Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2});
+
+  // decoupled look-back (thread 0)
+  if (threadIdx.x == 0) {
+    Agg prefix{0, 0, 0, 0};
+    if (tile == 0) {
+      stcg(&s.inc[0], total);
+      __threadfence();
+      cuda::atomic_ref<unsigned, cuda::thread_scope_device>(s.flags[0]).store(2u, cuda::memory_order_release);
+    } else {
+      stcg(&s.agg[tile], total);
+      __threadfence();
+      cuda::atomic_ref<unsigned, cuda::thread_scope_device>(s.flags[tile]).store(1u, cuda::memory_order_release);
+      for (long long j = (long long)tile - 1; j >= 0; --j) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> fl(s.flags[j]);
+        unsigned f;
+        while ((f = fl.load(cuda::memory_order_acquire)) == 0u) {
+        }
+        if (f == 2u) {
+          prefix = prefix + ldcg(&s.inc[j]);
+          break;
+        }
+        prefix = prefix + ldcg(&s.agg[j]);
+      }
+      stcg(&s.inc[tile], prefix + total);
+      __threadfence();
+      cuda::atomic_ref<unsigned, cuda::thread_scope_device>(s.flags[tile]).store(2u, cuda::memory_order_release);
+    }
+    tile_prefix = prefix;
+    if (tile == s.ntiles - 1) {
+      const Agg all = prefix + total;
+      o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
+    }
+  }
+  __syncthreads();
+  Agg run = tile_prefix + excl_in_tile;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long k = k0 + j;
+    if (k >= p.count) break;
+    o.boff[k] = run.len;
+    run.len += len[j];
+    if (cls[j] == 0) o.q0[run.c0++] = unsigned(k);
+    else if (cls[j] == 1) o.q1[run.c1++] = unsigned(k);
+    else o.q2[run.c2++] = unsigned(k);
+  }
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace
+
+uint64_t repartition_scratch_bytes(uint64_t count) {
+  const uint64_t tiles = (count + kTile - 1) / kTile;
+  return 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg));
+}
+
+Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
+                          uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch) {
+  const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
+  if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
+  const uint64_t tiles = (count + kTile - 1) / kTile;
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  char* sc = static_cast<char*>(scratch);
+  Scratch s{reinterpret_cast<unsigned*>(sc), reinterpret_cast<unsigned*>(sc + 256),
+            reinterpret_cast<Agg*>(sc + 256 + align256(tiles * 4)),
+            reinterpret_cast<Agg*>(sc + 256 + align256(tiles * 4) + align256(tiles * sizeof(Agg))), unsigned(tiles)};
+  const uint64_t b = B / new_dp, full = idx.n / B;
+  using ull = unsigned long long;
+  Params p{reinterpret_cast<const ull*>(idx.perm), reinterpret_cast<const ull*>(idx.samples), idx.file_class, idx.n, B,
+           at_step, b, rank, count, full > at_step ? (full - at_step) * b : 0, full};
+  Outs o{reinterpret_cast<ull*>(out.pos), reinterpret_cast<ull*>(out.ent), reinterpret_cast<ull*>(out.boff),
+         out.queue[0], out.queue[1], out.queue[2], reinterpret_cast<ull*>(out.qcount)};
+  ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
+  ck(cudaEventRecord(e0, st), "event");
+  if (tiles) {
+    repartition_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
+    ck(cudaGetLastError(), "repartition launch");
+  } else {
+    ck(cudaMemsetAsync(out.qcount, 0, 3 * sizeof(uint64_t), st), "qcount");
+  }
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  Timing t;
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t.tiles = tiles;
+  t.bytes = count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
+  t.launches = tiles ? 1 : 0;
+  return t;
+}
+
+}  // namespace reshard

@@ -1,0 +1,51 @@
+// reshard/dataset.hpp — dataset index repartitioning (SPEC tensor-store module,
+// SPEC.md:336-362, 378-383): epoch shuffle, per-rank positions after a DP change, and the
+// sample location lookup, with the per-rank gather/scan/compaction done on the GPU (K5).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "reshard/executor.hpp"
+
+namespace reshard {
+
+// shuffle_epoch: Fisher-Yates, i from N-1 down to 1, j =
+// next_below(i+1) of splitmix64 seeded (seed XOR epoch).  Host, O(N) sequential.
+void shuffle_epoch(uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm);
+
+// repartition: batches i >= at_step; new rank d owns positions
+// [i*B + d*B/D', i*B + (d+1)*B/D') of batch i, clipped at N for a trailing partial batch.
+// Errors: InvalidJobConfig (B or D' zero), IndivisibleBatch, StepBeyondEpoch.
+void repartition_check(uint64_t n, uint64_t B, uint64_t at_step, uint64_t new_dp);
+uint64_t repartition_count(uint64_t n, uint64_t B, uint64_t at_step, uint64_t new_dp, uint64_t rank);
+uint64_t repartition_position(uint64_t n, uint64_t B, uint64_t at_step, uint64_t new_dp, uint64_t rank, uint64_t k);
+
+// Device-resident dataset index.  samples: N x {file, offset, length} (u64 each);
+// file_class: the calling rank's locator class per file, 0 local / 1 peer / 2 remote
+// (priority order of SPEC.md:357).
+struct DatasetIndexView {
+  const uint64_t* perm;
+  const uint64_t* samples;
+  const uint8_t* file_class;
+  uint64_t n;
+};
+// Outputs of one rank (device).  For the rank's k-th remaining sample: pos[k],
+// ent[3k..3k+2] = samples[perm[pos[k]]], boff[k] = exclusive prefix sum of lengths (the
+// sample's offset in the rank's read buffer); queue[c] lists the k with locator class c in
+// increasing k, qcount[c] their number (written by the kernel).
+struct PartitionOut {
+  uint64_t* pos;
+  uint64_t* ent;
+  uint64_t* boff;
+  uint32_t* queue[3];
+  uint64_t* qcount;
+};
+
+uint64_t repartition_scratch_bytes(uint64_t count);
+// K5: one launch for one rank.  `scratch` (repartition_scratch_bytes) must be device
+// memory; it is cleared on the stream before the launch.
+Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
+                          uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch);
+
+}  // namespace reshard
