@@ -41,6 +41,112 @@ WORKLOADS = {
                            [1, 3, 4, 6]),
 }
 DEFAULT_WORKLOAD = "gpt3-1.3b-dp-scaleout"
+# configs[4]: dataset index repartition of a 100M-sample corpus under DP 2 -> 4 -> 8
+DATASET = {"dataset-100m-dp2to4to8": dict(n=100_000_000, B=1280, seed=0x5EED, epoch=0, files=1000,
+                                          per_file=100_000, sample_bytes=8206, events=[(25_000, 4), (50_000, 8)])}
+DATASET_BYTES_PER_SAMPLE = 8 + 24 + 8 + 24 + 8 + 4  # read perm+entry, write pos+entry+boff+queue index
+
+
+def dataset_inputs(spec):
+    import numpy as np
+
+    n = spec["n"]
+    k = np.arange(n, dtype=np.uint64)
+    samples = np.empty((n, 3), np.uint64)
+    samples[:, 0] = k // np.uint64(spec["per_file"])
+    samples[:, 1] = (k % np.uint64(spec["per_file"])) * np.uint64(spec["sample_bytes"])
+    samples[:, 2] = spec["sample_bytes"]
+    return samples
+
+
+def dataset_classes(files, dp, d):
+    """Locator class of every file for rank d: round-robin holders, one in dp+1 remote-only."""
+    import numpy as np
+
+    m = np.arange(files) % (dp + 1)
+    return np.where(m == d, 0, np.where(m == dp, 2, 1)).astype(np.uint8)
+
+
+def run_dataset(args, rs):
+    import numpy as np
+
+    rank, world, local = dist_env()
+    spec = DATASET[args.workload]
+    n = spec["n"]
+    perm = rs.shuffle_epoch(n, spec["seed"], spec["epoch"])  # host, once per epoch (off the clock)
+    samples = dataset_inputs(spec)
+    ctx = rs.Context(world, [rank], [local])
+    d_perm, d_samp = ctx.malloc(rank, 8 * n), ctx.malloc(rank, 24 * n)
+    ctx.htod(rank, d_perm, perm.ctypes.data, 8 * n)
+    ctx.htod(rank, d_samp, samples.ctypes.data, 24 * n)
+    jobs = []  # (at_step, dp, d, class ptr, partition)
+    for at, dp in spec["events"]:
+        for d in range(dp):
+            if d % world != rank:
+                continue
+            fc = dataset_classes(spec["files"], dp, d)
+            p_fc = ctx.malloc(rank, spec["files"])
+            ctx.htod(rank, p_fc, fc.ctypes.data, spec["files"])
+            jobs.append((at, dp, d, p_fc, rs.Partition(ctx, rank, rs.repartition_count(n, spec["B"], at, dp, d))))
+
+    def step():
+        ms, samples_done, launches = 0.0, 0, 0
+        for at, dp, d, p_fc, part in jobs:
+            t = rs.repartition(ctx, rank, d_perm, d_samp, p_fc, n, spec["B"], at, dp, d, part)
+            ms += t["ms"]
+            samples_done += part.count
+            launches += t["launches"]
+        return ms, samples_done, launches
+
+    for _ in range(args.warmup):
+        step()
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            ms, done, launches = step()
+            step_ms.append(ms)
+    # parity spot check of the last step against the host restatement of one rank
+    at, dp, d, _, part = jobs[-1]
+    got = part.fetch()
+    pos_ok = all(int(got["pos"][k]) == rs.repartition_position(n, spec["B"], at, dp, d, k)
+                 for k in range(0, part.count, max(1, part.count // 1000)))
+    ent_ok = bool(np.array_equal(got["ent"][:: max(1, part.count // 1000)],
+                                 samples[perm[got["pos"][:: max(1, part.count // 1000)]]]))
+    if rank != 0:
+        return
+    ms = statistics.mean(step_ms)
+    peak, peak_kind = measured_peaks()
+    alg = done * DATASET_BYTES_PER_SAMPLE
+    achieved = alg / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (100M-sample index, 1000 files)",
+        "config": {"workload": args.workload, "events": spec["events"], "B": spec["B"], "n": n,
+                   "l2": "inputs larger than L2 (no flush)"},
+        "samples_per_step": done, "gsamples_per_s": round(done / (ms * 1e-3) / 1e9, 3),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "repartition_kernel", "algorithmic_bytes_per_launch": alg // max(launches, 1)},
+        "gpu_launches": launches * args.steps, "clocks": clocks.summary(), "spot_check": {"pos": pos_ok, "ent": ent_ok},
+        "e2e": None,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        from oracle.oracle import Oracle
+
+        o = Oracle()
+        threads = os.cpu_count() or 1
+        secs = 0.0
+        for at, dp in spec["events"]:
+            for d in range(dp):
+                r = o.dataset_gather(n, spec["B"], at, dp, d, perm, samples, dataset_classes(spec["files"], dp, d),
+                                     n_threads=threads)
+                secs += r["seconds"]
+                del r
+        line["cpu_baseline"] = {"value": round(secs * 1e3, 3), "unit": "ms", "cores": threads, "kind": "port",
+                                "sample": "full workload (all ranks of both DP events), restated gather with "
+                                          f"{threads} threads"}
+    print(json.dumps(line), flush=True)
 
 
 def dist_env():
@@ -180,7 +286,26 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    leg = cpu_reference_leg(args.workload, args.sample_frac, args.steps, args.warmup)
+    if args.workload in DATASET:
+        import paper_2312_05181_b200 as rs
+        from oracle.oracle import Oracle
+
+        spec = DATASET[args.workload]
+        perm = rs.shuffle_epoch(spec["n"], spec["seed"], spec["epoch"])
+        samples = dataset_inputs(spec)
+        o, threads, ms = Oracle(), os.cpu_count() or 1, []
+        for i in range(args.warmup + args.steps):
+            secs = 0.0
+            for at, dp in spec["events"]:
+                for d in range(dp):
+                    secs += o.dataset_gather(spec["n"], spec["B"], at, dp, d, perm, samples,
+                                             dataset_classes(spec["files"], dp, d), n_threads=threads)["seconds"]
+            if i >= args.warmup:
+                ms.append(secs * 1e3)
+        leg = {"value": statistics.mean(ms), "cores": threads, "kind": "port",
+               "sample": f"full workload, restated gather (oracle.cpp orc_dataset_gather), {threads} threads"}
+    else:
+        leg = cpu_reference_leg(args.workload, args.sample_frac, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(leg["value"], 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(leg["value"], 3),
@@ -202,6 +327,8 @@ def run_ours(args):
     N = args.gpus
     if world > 1 and world != N:
         raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}")
+    if args.workload in DATASET:
+        return run_dataset(args, rs)
     dist = None
     if world > 1:
         import torch
@@ -322,7 +449,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS) + sorted(DATASET))
     ap.add_argument("--tile-kib", type=int, default=256)
     ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--e2e-steps", type=int, default=3)

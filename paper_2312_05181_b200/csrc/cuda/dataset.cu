@@ -119,15 +119,15 @@ __global__ void __launch_bounds__(kThreads) repartition_kernel(Params p, Outs o,
     if (tile == 0) {
       stcg(&s.inc[0], total);
       __threadfence();
-      cuda::atomic_ref<unsigned, cuda::thread_scope_device>(s.flags[0]).store(2u, cuda::memory_order_release);
+      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[0]).store(2u, ::cuda::memory_order_release);
     } else {
       stcg(&s.agg[tile], total);
       __threadfence();
-      cuda::atomic_ref<unsigned, cuda::thread_scope_device>(s.flags[tile]).store(1u, cuda::memory_order_release);
+      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(1u, ::cuda::memory_order_release);
       for (long long j = (long long)tile - 1; j >= 0; --j) {
-        cuda::atomic_ref<unsigned, cuda::thread_scope_device> fl(s.flags[j]);
+        ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device> fl(s.flags[j]);
         unsigned f;
-        while ((f = fl.load(cuda::memory_order_acquire)) == 0u) {
+        while ((f = fl.load(::cuda::memory_order_acquire)) == 0u) {
         }
         if (f == 2u) {
           prefix = prefix + ldcg(&s.inc[j]);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads) repartition_kernel(Params p, Outs o,
       }
       stcg(&s.inc[tile], prefix + total);
       __threadfence();
-      cuda::atomic_ref<unsigned, cuda::thread_scope_device>(s.flags[tile]).store(2u, cuda::memory_order_release);
+      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(2u, ::cuda::memory_order_release);
     }
     tile_prefix = prefix;
     if (tile == s.ntiles - 1) {

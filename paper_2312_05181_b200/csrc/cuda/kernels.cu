@@ -12,6 +12,7 @@
 //  K7 verify_cell    — regenerates K6's bytes and counts mismatches (off the clock).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -52,47 +53,152 @@ __device__ __forceinline__ void st_na<uint4>(uint4* p, const uint4& v) {
 }
 
 // Copy one tile with vectors of type V.  Thread i of the CTA handles vectors i, i+B, ...
-// of the flattened rows x (row_bytes/W) index space; (row, col) advance incrementally, so
-// there is no per-vector division.  U vectors are loaded before any is stored.
+// of the flattened rows x (row_bytes/W) index space.  Byte offsets inside the tile are
+// 32-bit (the host keeps (rows-1)*pitch + row_bytes < 2^31) and advance incrementally:
+// +step per B vectors, +wrap when the column wraps into the next row, so there is no
+// per-vector division or 64-bit multiply.  U vectors are loaded before any is stored.
 template <typename V, int U>
 __device__ __forceinline__ void copy_tile(const DevTile& t) {
   constexpr unsigned W = sizeof(V);
   const unsigned vpr = t.row_bytes / W;
-  const unsigned long long n = (unsigned long long)t.rows * vpr;
+  const unsigned n = t.rows * vpr;
   const unsigned B = blockDim.x;
   const unsigned drow = B / vpr, dcol = B % vpr;
-  unsigned row = threadIdx.x / vpr, col = threadIdx.x % vpr;
-  const char* __restrict__ s = reinterpret_cast<const char*>(t.src);
-  char* __restrict__ d = reinterpret_cast<char*>(t.dst);
-  for (unsigned long long i = threadIdx.x; i < n; i += (unsigned long long)U * B) {
+  const unsigned sp = unsigned(t.src_pitch), dp = unsigned(t.dst_pitch);
+  const unsigned s_step = drow * sp + dcol * W, s_wrap = sp - vpr * W;
+  const unsigned d_step = drow * dp + dcol * W, d_wrap = dp - vpr * W;
+  unsigned col = threadIdx.x % vpr;
+  unsigned so = (threadIdx.x / vpr) * sp + col * W, doff = (threadIdx.x / vpr) * dp + col * W;
+  const char* s = reinterpret_cast<const char*>(t.src);
+  char* d = reinterpret_cast<char*>(t.dst);
+  for (unsigned i = threadIdx.x; i < n; i += U * B) {
     V v[U];
-    unsigned rr[U], cc[U];
+    const unsigned col0 = col;  // the store pass replays the column walk from here
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      rr[u] = row, cc[u] = col;
-      if (i + (unsigned long long)u * B < n)
-        v[u] = ld_nc(reinterpret_cast<const V*>(s + (unsigned long long)row * t.src_pitch + (unsigned long long)col * W));
-      col += dcol, row += drow;
-      if (col >= vpr) col -= vpr, ++row;
+      if (i + u * B < n) v[u] = ld_nc(reinterpret_cast<const V*>(s + so));
+      col += dcol, so += s_step;
+      if (col >= vpr) col -= vpr, so += s_wrap;
     }
+    unsigned c = col0;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i + (unsigned long long)u * B < n)
-        st_na(reinterpret_cast<V*>(d + (unsigned long long)rr[u] * t.dst_pitch + (unsigned long long)cc[u] * W), v[u]);
+    for (int u = 0; u < U; ++u) {
+      if (i + u * B < n) st_na(reinterpret_cast<V*>(d + doff), v[u]);
+      c += dcol, doff += d_step;
+      if (c >= vpr) c -= vpr, doff += d_wrap;
+    }
   }
 }
 
-__global__ void __launch_bounds__(512) copy_tiles_kernel(const DevTile* __restrict__ tiles, unsigned long long n) {
+// K1 fast path: every tile 16-byte aligned (the host routes the others to copy_any_kernel).
+// Only the uint4 path is instantiated, so register use stays low enough for MINB CTAs/SM.
+template <int U, int MINB>
+__global__ void __launch_bounds__(512, MINB) copy_v16_kernel(const DevTile* __restrict__ tiles, unsigned long long n) {
+  for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
+    const DevTile t = tiles[k];
+    copy_tile<uint4, U>(t);
+  }
+}
+
+// K1 general path: widest common alignment per tile.
+__global__ void __launch_bounds__(256) copy_any_kernel(const DevTile* __restrict__ tiles, unsigned long long n) {
   for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
     const DevTile t = tiles[k];
     if (t.rows == 0 || t.row_bytes == 0) continue;
     const unsigned long long a = t.src | t.dst | t.row_bytes | (t.rows > 1 ? (t.src_pitch | t.dst_pitch) : 0ull);
     if ((a & 15) == 0) copy_tile<uint4, 4>(t);
-    else if ((a & 7) == 0) copy_tile<uint2, 8>(t);
-    else if ((a & 3) == 0) copy_tile<unsigned, 8>(t);
-    else if ((a & 1) == 0) copy_tile<unsigned short, 8>(t);
-    else copy_tile<unsigned char, 8>(t);
+    else if ((a & 7) == 0) copy_tile<uint2, 4>(t);
+    else if ((a & 3) == 0) copy_tile<unsigned, 4>(t);
+    else if ((a & 1) == 0) copy_tile<unsigned short, 4>(t);
+    else copy_tile<unsigned char, 4>(t);
   }
+}
+
+// ---- K3: TMA bulk-copy pipeline ------------------------------------------------------------
+// One elected thread per CTA streams its tiles through a ring of shared-memory stages:
+//   cp.async.bulk (global -> smem, completion on a per-stage mbarrier)   one op per row
+//   cp.async.bulk (smem -> global, bulk_group)                           one op per row
+// Loads run `stages-2` chunks ahead of stores; a stage is refilled only once the bulk store
+// that read it has finished reading (cp.async.bulk.wait_group.read).  Tiles are sized by
+// the host to fit one stage and are 16-byte aligned (bulk-copy requirement).  SM threads
+// do no data movement at all: the TMA engine moves every byte (SASS: UBLKCP).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst_smem, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, unsigned src_smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+constexpr int kBulkMaxStages = 16;
+
+__global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevTile* __restrict__ tiles, unsigned long long n,
+                                                          int stages, unsigned stage_bytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  // my tiles: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const unsigned long long first = blockIdx.x, step = gridDim.x;
+  const unsigned long long mine = first < n ? (n - first + step - 1) / step : 0;
+  const int ahead = stages > 2 ? stages - 2 : 1;
+  auto issue_load = [&](unsigned long long i) {
+    const DevTile t = tiles[first + i * step];
+    const int s = int(i % stages);
+    const unsigned bar = smem_u32(&bars[s]);
+    const unsigned base = smem_u32(smem + size_t(s) * stage_bytes);
+    mbar_expect_tx(bar, t.rows * t.row_bytes);
+    for (unsigned r = 0; r < t.rows; ++r)
+      bulk_g2s(base + r * t.row_bytes, reinterpret_cast<const char*>(t.src) + r * t.src_pitch, t.row_bytes, bar);
+  };
+  for (unsigned long long i = 0; i < mine && i < (unsigned long long)ahead; ++i) issue_load(i);
+  for (unsigned long long i = 0; i < mine; ++i) {
+    const unsigned long long j = i + ahead;
+    if (j < mine) {
+      // stage of chunk j was last read by the store of chunk j - stages (<= i - 2): allow
+      // the most recent store group (chunk i - 1) to still be reading.
+      bulk_wait_read<1>();
+      issue_load(j);
+    }
+    const DevTile t = tiles[first + i * step];
+    const int s = int(i % stages);
+    mbar_wait(smem_u32(&bars[s]), unsigned((i / stages) & 1));
+    const unsigned base = smem_u32(smem + size_t(s) * stage_bytes);
+    for (unsigned r = 0; r < t.rows; ++r)
+      bulk_s2g(reinterpret_cast<char*>(t.dst) + r * t.dst_pitch, base + r * t.row_bytes, t.row_bytes);
+    bulk_commit();
+  }
+  bulk_wait_all();
 }
 
 // ---- synthetic payload ------------------------------------------------------------------
@@ -140,9 +246,15 @@ __device__ __forceinline__ int nonzero_bytes(unsigned long long x) {
   return 8 - __popcll(t);
 }
 
+// One launch for a whole batch of cells: blockIdx.y (+ y_base) picks the cell, blockIdx.x
+// strides over its 16-byte chunks.
 template <bool kVerify>
-__global__ void __launch_bounds__(256) payload_kernel(unsigned char* data, unsigned long long seed, CellGeom g,
+__global__ void __launch_bounds__(256) payload_kernel(const PayloadTask* __restrict__ tasks, unsigned y_base,
                                                       unsigned long long* count) {
+  const PayloadTask& task = tasks[y_base + blockIdx.y];
+  unsigned char* data = static_cast<unsigned char*>(task.data);
+  const unsigned long long seed = task.seed;
+  const CellGeom& g = task.g;
   unsigned long long bad = 0;
   const unsigned long long chunks = (g.bytes + 15) / 16;
   const bool aligned = (reinterpret_cast<unsigned long long>(data) & 15) == 0;
@@ -178,33 +290,44 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-int payload_grid(const CellGeom& g) {
-  unsigned long long chunks = (g.bytes + 15) / 16;
-  unsigned long long blocks = (chunks + 255) / 256;
-  return int(blocks < 148 * 16 ? (blocks ? blocks : 1) : 148 * 16);
-}
-
 }  // namespace
 
-void launch_copy_tiles(const CopyTile* d_tiles, uint64_t n_tiles, int grid, int block, void* stream) {
+void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
+                 void* stream) {
   if (n_tiles == 0) return;
-  copy_tiles_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevTile*>(d_tiles),
-                                                                             n_tiles);
-  check(cudaGetLastError(), "copy_tiles launch");
+  auto s = static_cast<cudaStream_t>(stream);
+  auto tiles = reinterpret_cast<const DevTile*>(d_tiles);
+  auto grid = [&](int per_sm) { return int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(per_sm))); };
+  if (!aligned16) {
+    copy_any_kernel<<<grid(8), 256, 0, s>>>(tiles, n_tiles);
+  } else if (cfg.kernel == CopyKernel::Bulk) {
+    if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
+    const size_t smem = size_t(cfg.stages) * cfg.stage_bytes;
+    check(cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+          "bulk smem attribute");
+    copy_bulk_kernel<<<grid(cfg.ctas_per_sm), 32, smem, s>>>(tiles, n_tiles, cfg.stages, cfg.stage_bytes);
+  } else if (cfg.kernel == CopyKernel::Ldg8) {
+    copy_v16_kernel<8, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
+  } else if (cfg.ctas_per_sm >= 3) {
+    copy_v16_kernel<4, 3><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
+  } else {
+    copy_v16_kernel<4, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
+  }
+  check(cudaGetLastError(), "copy launch");
 }
 
-void launch_fill(void* dst, uint64_t seed, const CellGeom& g, void* stream) {
-  if (g.bytes == 0) return;
-  payload_kernel<false><<<payload_grid(g), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<unsigned char*>(dst), seed, g, nullptr);
-  check(cudaGetLastError(), "fill launch");
-}
-
-void launch_verify(const void* data, uint64_t seed, const CellGeom& g, unsigned long long* d_count, void* stream) {
-  if (g.bytes == 0) return;
-  payload_kernel<true><<<payload_grid(g), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<unsigned char*>(const_cast<void*>(data)), seed, g, d_count);
-  check(cudaGetLastError(), "verify launch");
+void launch_payload(const PayloadTask* d_tasks, uint64_t n_tasks, uint64_t max_bytes, bool verify,
+                    unsigned long long* d_count, void* stream) {
+  if (n_tasks == 0) return;
+  const unsigned long long chunks = (max_bytes + 15) / 16;
+  const unsigned gx = unsigned(std::max<unsigned long long>(1, std::min<unsigned long long>((chunks + 255) / 256, 512)));
+  auto s = static_cast<cudaStream_t>(stream);
+  for (uint64_t y = 0; y < n_tasks; y += 65535) {
+    dim3 grid(gx, unsigned(std::min<uint64_t>(65535, n_tasks - y)));
+    if (verify) payload_kernel<true><<<grid, 256, 0, s>>>(d_tasks, unsigned(y), d_count);
+    else payload_kernel<false><<<grid, 256, 0, s>>>(d_tasks, unsigned(y), nullptr);
+    check(cudaGetLastError(), "payload launch");
+  }
 }
 
 CellGeom make_geom(const Shape& base, size_t width, const Range& cell) {

@@ -18,12 +18,19 @@ struct CellGeom {
   uint32_t rank, width;
 };
 
-// K1/K2: persistent tile copy.  `grid` CTAs of `block` threads walk the tile list.
-void launch_copy_tiles(const CopyTile* d_tiles, uint64_t n_tiles, int grid, int block, void* stream);
-// K6: write the splitmix64 payload of `g` at dst.
-void launch_fill(void* dst, uint64_t seed, const CellGeom& g, void* stream);
-// K7: count bytes of `data` that differ from the payload of `g` into *d_count (atomic add).
-void launch_verify(const void* data, uint64_t seed, const CellGeom& g, unsigned long long* d_count, void* stream);
+// K1/K2 (LDG/STG, 16-byte vectors) or K3 (TMA bulk pipeline): persistent tile copy over a
+// tile list.  aligned16: every tile is 16-byte aligned (else the generic-width kernel runs).
+void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
+                 void* stream);
+// K6 / K7 over a batch of cells (device array of tasks): write the splitmix64 payload, or
+// count the bytes that differ from it into *d_count (atomic add).  One launch per 65535 cells.
+struct PayloadTask {
+  void* data;
+  uint64_t seed;
+  CellGeom g;
+};
+void launch_payload(const PayloadTask* d_tasks, uint64_t n_tasks, uint64_t max_bytes, bool verify,
+                    unsigned long long* d_count, void* stream);
 
 // Fill a CellGeom from a base shape and a cell box.
 CellGeom make_geom(const Shape& base, size_t width, const Range& cell);

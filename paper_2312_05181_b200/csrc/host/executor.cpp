@@ -65,7 +65,9 @@ void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& 
       for (uint64_t row = 0; row < rows; ++row)
         for (uint64_t c = 0; c < run; c += tile) emit(so + row * sp + c, dof + row * dp + c, 0, 0, 1, std::min(tile, run - c));
     } else {
-      const uint64_t per = std::max<uint64_t>(1, tile / run);
+      // rows per tile: ~tile bytes, and in-tile byte offsets must fit 31 bits (kernel math)
+      const uint64_t span = std::max<uint64_t>(std::max(sp, dp), 1);
+      const uint64_t per = std::max<uint64_t>(1, std::min<uint64_t>(tile / run, ((1ull << 31) - run) / span + 1));
       for (uint64_t row = 0; row < rows; row += per)
         emit(so + row * sp, dof + row * dp, sp, dp, std::min(per, rows - row), run);
     }
@@ -78,10 +80,31 @@ void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& 
   }
 }
 
-int copy_grid(int sms, uint64_t tiles) { return int(std::min<uint64_t>(tiles, uint64_t(sms) * 4)); }
-constexpr int kCopyBlock = 512;
+bool aligned16(const CopyTile& t) {
+  return ((t.src | t.dst | t.row_bytes | (t.rows > 1 ? (t.src_pitch | t.dst_pitch) : 0)) & 15) == 0;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
 
 }  // namespace
+
+CopyConfig CopyConfig::from_env() {
+  CopyConfig c;
+  if (const char* k = std::getenv("RESHARD_COPY_KERNEL")) {
+    std::string s(k);
+    if (s == "ldg") c.kernel = CopyKernel::Ldg;
+    else if (s == "ldg8") c.kernel = CopyKernel::Ldg8;
+    else if (s == "bulk") c.kernel = CopyKernel::Bulk;
+    else if (!s.empty()) raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8 or bulk");
+  }
+  c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", c.kernel == CopyKernel::Bulk ? 1 : c.ctas_per_sm));
+  c.stages = env_int("RESHARD_BULK_STAGES", c.stages);
+  c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
+  return c;
+}
 
 // ---- Context ---------------------------------------------------------------------------
 Context::Context(int world, std::vector<int> world_ids, std::vector<int> cuda_devices)
@@ -146,10 +169,11 @@ int Context::sm_count(int w) const {
 // ---- Executor --------------------------------------------------------------------------
 struct Executor::Local {
   int world = -1, dev = -1;
-  CopyTile* d_tiles = nullptr;
-  uint64_t n_tiles = 0, bytes = 0;
+  CopyTile* d_tiles = nullptr;  // [aligned tiles | misaligned tiles]
+  uint64_t n_aligned = 0, n_misc = 0, bytes = 0;
   cudaEvent_t start = nullptr, stop = nullptr;
   unsigned long long* d_count = nullptr;
+  uint64_t launches() const { return (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
   ~Local() {
     if (dev < 0) return;
     cudaSetDevice(dev);
@@ -160,10 +184,18 @@ struct Executor::Local {
   }
 };
 
+void Executor::launch_local(Local& l, void* stream) {
+  const int sms = ctx_.sm_count(l.world);
+  cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, stream);
+  cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, stream);
+}
+
 Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu,
-                   std::vector<int> dst_gpu, uint64_t tile_bytes)
-    : ctx_(ctx), plan_(std::move(plan)), src_gpu_(std::move(src_gpu)), dst_gpu_(std::move(dst_gpu)),
-      tile_bytes_(std::max<uint64_t>(4096, tile_bytes / 16 * 16)) {
+                   std::vector<int> dst_gpu, uint64_t tile_bytes, CopyConfig cfg)
+    : ctx_(ctx), plan_(std::move(plan)), src_gpu_(std::move(src_gpu)), dst_gpu_(std::move(dst_gpu)), cfg_(cfg),
+      tile_bytes_(std::max<uint64_t>(4096, std::min<uint64_t>(tile_bytes, cfg.kernel == CopyKernel::Bulk ? cfg.stage_bytes
+                                                                                                        : UINT64_MAX) /
+                                               16 * 16)) {
   const PTC& a = *plan_->from;
   const PTC& b = *plan_->to;
   const int G = ctx_.world();
@@ -253,24 +285,29 @@ void Executor::bind(int gpu, void* src, void* dst) {
 void Executor::prepare() {
   for (auto& l : local_) {
     const auto& lt = logical_[size_t(l->world)];
-    std::vector<CopyTile> tiles;
-    tiles.reserve(lt.size());
+    std::vector<CopyTile> aligned, misc;
+    aligned.reserve(lt.size());
     uint64_t bytes = 0;
     for (const Logical& x : lt) {
       char* s = static_cast<char*>(src_base_[size_t(x.src_gpu)]);
       char* d = static_cast<char*>(dst_base_[size_t(x.dst_gpu)]);
       if (!s || !d) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(!s ? x.src_gpu : x.dst_gpu) + " not bound");
-      tiles.push_back(CopyTile{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), uint64_t(reinterpret_cast<uintptr_t>(d + x.dst_off)),
-                               x.src_pitch, x.dst_pitch, x.rows, x.row_bytes});
+      CopyTile t{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), uint64_t(reinterpret_cast<uintptr_t>(d + x.dst_off)),
+                 x.src_pitch, x.dst_pitch, x.rows, x.row_bytes};
+      (aligned16(t) ? aligned : misc).push_back(t);
       bytes += uint64_t(x.rows) * x.row_bytes;
     }
     DeviceGuard g(l->dev);
     if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
-    if (!tiles.empty()) {
-      ck(cudaMalloc(&l->d_tiles, tiles.size() * sizeof(CopyTile)), "cudaMalloc tiles");
-      ck(cudaMemcpy(l->d_tiles, tiles.data(), tiles.size() * sizeof(CopyTile), cudaMemcpyHostToDevice), "upload tiles");
+    const size_t n = aligned.size() + misc.size();
+    if (n) {
+      ck(cudaMalloc(&l->d_tiles, n * sizeof(CopyTile)), "cudaMalloc tiles");
+      ck(cudaMemcpy(l->d_tiles, aligned.data(), aligned.size() * sizeof(CopyTile), cudaMemcpyHostToDevice), "upload tiles");
+      ck(cudaMemcpy(l->d_tiles + aligned.size(), misc.data(), misc.size() * sizeof(CopyTile), cudaMemcpyHostToDevice),
+         "upload tiles");
     }
-    l->n_tiles = tiles.size();
+    l->n_aligned = aligned.size();
+    l->n_misc = misc.size();
     l->bytes = bytes;
   }
 }
@@ -280,7 +317,7 @@ void Executor::run() {
     DeviceGuard g(l->dev);
     auto s = static_cast<cudaStream_t>(ctx_.stream(l->world));
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
-    cuda::launch_copy_tiles(l->d_tiles, l->n_tiles, copy_grid(ctx_.sm_count(l->world), l->n_tiles), kCopyBlock, s);
+    launch_local(*l, s);
     ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
   }
 }
@@ -292,9 +329,9 @@ std::vector<Timing> Executor::wait() {
     ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
     Timing t;
     ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
-    t.tiles = l->n_tiles;
+    t.tiles = l->n_aligned + l->n_misc;
     t.bytes = l->bytes;
-    t.launches = l->n_tiles ? 1 : 0;
+    t.launches = l->launches();
     out.push_back(t);
   }
   return out;
@@ -310,13 +347,13 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   auto s = static_cast<cudaStream_t>(ctx_.stream(gpu));
   ck(cudaEventRecord(l->start, s), "cudaEventRecord");
   ck(cudaMemcpyAsync(src_base_[size_t(gpu)], host_src, src_size_[size_t(gpu)], cudaMemcpyHostToDevice, s), "h2d src arena");
-  cuda::launch_copy_tiles(l->d_tiles, l->n_tiles, copy_grid(ctx_.sm_count(gpu), l->n_tiles), kCopyBlock, s);
+  launch_local(*l, s);
   ck(cudaMemcpyAsync(host_dst, dst_base_[size_t(gpu)], dst_size_[size_t(gpu)], cudaMemcpyDeviceToHost, s), "d2h dst arena");
   ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
   ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
   Timing t;
   ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
-  t.tiles = l->n_tiles, t.bytes = l->bytes, t.launches = l->n_tiles ? 1 : 0;
+  t.tiles = l->n_aligned + l->n_misc, t.bytes = l->bytes, t.launches = l->launches();
   return t;
 }
 
@@ -327,53 +364,62 @@ uint64_t Executor::copy_bytes_for(int gpu) const {
   return n;
 }
 
+// Upload a batch of payload tasks per local GPU and run K6 (fill) or K7 (verify) in one
+// launch each; returns the mismatch count (verify).
+uint64_t Executor::payload_pass(const std::vector<std::vector<cuda::PayloadTask>>& per_local, bool verify) {
+  uint64_t bad = 0;
+  for (size_t li = 0; li < local_.size(); ++li) {
+    Local& l = *local_[li];
+    const auto& tasks = per_local[li];
+    DeviceGuard g(l.dev);
+    auto s = static_cast<cudaStream_t>(ctx_.stream(l.world));
+    if (tasks.empty()) continue;
+    uint64_t max_bytes = 0;
+    for (auto& t : tasks) max_bytes = std::max(max_bytes, t.g.bytes);
+    cuda::PayloadTask* d = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&d), tasks.size() * sizeof(cuda::PayloadTask), s), "cudaMallocAsync");
+    ck(cudaMemcpyAsync(d, tasks.data(), tasks.size() * sizeof(cuda::PayloadTask), cudaMemcpyHostToDevice, s), "tasks h2d");
+    if (verify) ck(cudaMemsetAsync(l.d_count, 0, sizeof(unsigned long long), s), "memset");
+    cuda::launch_payload(d, tasks.size(), max_bytes, verify, l.d_count, s);
+    ck(cudaFreeAsync(d, s), "cudaFreeAsync");
+    unsigned long long h = 0;
+    if (verify) ck(cudaMemcpyAsync(&h, l.d_count, sizeof(h), cudaMemcpyDeviceToHost, s), "count d2h");
+    ck(cudaStreamSynchronize(s), "payload sync");
+    bad += h;
+  }
+  return bad;
+}
+
 void Executor::fill_sources() {
   const PTC& a = *plan_->from;
+  std::vector<std::vector<cuda::PayloadTask>> per(local_.size());
   size_t k = 0;
   for (uint32_t i = 0; i < a.devices.size(); ++i)
     for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
       const CellBinding& b = src_bind_[k++];
-      if (ctx_.local_of(b.gpu) < 0) continue;
+      const int li = ctx_.local_of(b.gpu);
+      if (li < 0) continue;
       const TensorSpec& e = a.catalog.tensors[t];
-      DeviceGuard g(ctx_.cuda_device(b.gpu));
-      cuda::launch_fill(static_cast<char*>(src_base_[size_t(b.gpu)]) + b.offset, payload_seed(e.path),
-                        cuda::make_geom(e.shape, dtype_width(e.dtype), a.cells[t][c]), ctx_.stream(b.gpu));
+      per[size_t(li)].push_back({static_cast<char*>(src_base_[size_t(b.gpu)]) + b.offset, payload_seed(e.path),
+                                 cuda::make_geom(e.shape, dtype_width(e.dtype), a.cells[t][c])});
     }
-  for (auto& l : local_) {
-    DeviceGuard g(l->dev);
-    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(ctx_.stream(l->world))), "fill sync");
-  }
+  payload_pass(per, false);
 }
 
 uint64_t Executor::verify_destinations() {
   const PTC& b = *plan_->to;
-  for (auto& l : local_) {
-    DeviceGuard g(l->dev);
-    ck(cudaMemsetAsync(l->d_count, 0, sizeof(unsigned long long), static_cast<cudaStream_t>(ctx_.stream(l->world))), "memset");
-  }
+  std::vector<std::vector<cuda::PayloadTask>> per(local_.size());
   for (size_t j = 0; j < plan_->dst_cells.size(); ++j) {
     const CellBinding& bd = dst_bind_[j];
-    int li = ctx_.local_of(bd.gpu);
+    const int li = ctx_.local_of(bd.gpu);
     if (li < 0) continue;
     const PlanDstCell& dc = plan_->dst_cells[j];
     const TensorSpec& e = b.catalog.tensors[dc.tensor];
-    const char* base = static_cast<const char*>(bd.arena == 0 ? src_base_[size_t(bd.gpu)] : dst_base_[size_t(bd.gpu)]);
-    DeviceGuard g(ctx_.cuda_device(bd.gpu));
-    Local* l = nullptr;
-    for (auto& x : local_)
-      if (x->world == bd.gpu) l = x.get();
-    cuda::launch_verify(base + bd.offset, payload_seed(e.path), cuda::make_geom(e.shape, dtype_width(e.dtype), b.cells[dc.tensor][dc.cell]),
-                        l->d_count, ctx_.stream(bd.gpu));
+    char* base = static_cast<char*>(bd.arena == 0 ? src_base_[size_t(bd.gpu)] : dst_base_[size_t(bd.gpu)]);
+    per[size_t(li)].push_back({base + bd.offset, payload_seed(e.path),
+                               cuda::make_geom(e.shape, dtype_width(e.dtype), b.cells[dc.tensor][dc.cell])});
   }
-  uint64_t bad = 0;
-  for (auto& l : local_) {
-    DeviceGuard g(l->dev);
-    unsigned long long h = 0;
-    ck(cudaMemcpyAsync(&h, l->d_count, sizeof(h), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(ctx_.stream(l->world))), "count d2h");
-    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(ctx_.stream(l->world))), "verify sync");
-    bad += h;
-  }
-  return bad;
+  return payload_pass(per, true);
 }
 
 // ---- device slice / merge ----------------------------------------------------------------
@@ -385,7 +431,7 @@ void run_tiles_once(Context& ctx, int gpu, const std::vector<CopyTile>& tiles) {
   CopyTile* d = nullptr;
   ck(cudaMallocAsync(reinterpret_cast<void**>(&d), tiles.size() * sizeof(CopyTile), s), "cudaMallocAsync");
   ck(cudaMemcpyAsync(d, tiles.data(), tiles.size() * sizeof(CopyTile), cudaMemcpyHostToDevice, s), "tiles h2d");
-  cuda::launch_copy_tiles(d, tiles.size(), copy_grid(ctx.sm_count(gpu), tiles.size()), kCopyBlock, s);
+  cuda::launch_copy(d, tiles.size(), CopyConfig{}, ctx.sm_count(gpu), false, s);
   ck(cudaFreeAsync(d, s), "cudaFreeAsync");
   ck(cudaStreamSynchronize(s), "slice/merge sync");
 }

@@ -22,6 +22,10 @@
 
 namespace reshard {
 
+namespace cuda {
+struct PayloadTask;
+}
+
 // Must match the device struct in cuda/kernels.cuh.
 struct CopyTile {
   uint64_t src, dst;              // absolute device addresses (dst may be a peer mapping)
@@ -29,6 +33,18 @@ struct CopyTile {
   uint32_t rows, row_bytes;
 };
 static_assert(sizeof(CopyTile) == 40, "CopyTile layout");
+
+// Which copy kernel moves the 16-byte-aligned tiles (misaligned ones always take the
+// generic-width LDG/STG kernel).  Defaults can be overridden by RESHARD_COPY_KERNEL
+// (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
+enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2 };
+struct CopyConfig {
+  CopyKernel kernel = CopyKernel::Ldg;
+  int ctas_per_sm = 2;
+  int stages = 6;               // bulk: shared-memory ring depth
+  unsigned stage_bytes = 32768; // bulk: bytes per stage (tiles are cut to fit one stage)
+  static CopyConfig from_env();
+};
 
 struct CellBinding {
   int32_t gpu = -1;    // world GPU index
@@ -70,7 +86,8 @@ class Executor {
  public:
   // src_gpu[i]: world GPU of from->devices[i]; dst_gpu[j]: world GPU of to->devices[j].
   Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu, std::vector<int> dst_gpu,
-           uint64_t tile_bytes = 256 << 10);
+           uint64_t tile_bytes = 256 << 10, CopyConfig cfg = CopyConfig::from_env());
+  const CopyConfig& copy_config() const { return cfg_; }
   ~Executor();
 
   uint64_t src_arena_bytes(int gpu) const { return src_size_[size_t(gpu)]; }
@@ -104,18 +121,20 @@ class Executor {
     uint64_t src_off, dst_off, src_pitch, dst_pitch;
     uint32_t rows, row_bytes;
   };
-  void lower();
+  struct Local;
+  void launch_local(Local& l, void* stream);
+  uint64_t payload_pass(const std::vector<std::vector<cuda::PayloadTask>>& per_local, bool verify);
 
   Context& ctx_;
   std::shared_ptr<const ReconfigPlan> plan_;
   std::vector<int> src_gpu_, dst_gpu_;
+  CopyConfig cfg_;
   uint64_t tile_bytes_;
   std::vector<uint64_t> src_size_, dst_size_;
   std::vector<CellBinding> src_bind_, dst_bind_;
   std::vector<std::vector<size_t>> src_index_;  // [from dev][(t, cell) hosted order] -> src_bind_ index
   std::vector<std::vector<Logical>> logical_;   // per executing (source) world GPU
   std::vector<void*> src_base_, dst_base_;
-  struct Local;
   std::vector<std::unique_ptr<Local>> local_;   // per local GPU: device tiles, events
 };
 

@@ -1,0 +1,133 @@
+"""Dataset index repartitioning: host functions vs the oracle (CPU), the
+SPEC examples and acceptance #8, and the K5 GPU kernel vs the oracle's gather (gpu)."""
+import random
+
+import numpy as np
+import pytest
+
+
+def corpus(n, n_files, rng, varlen=True):
+    per = (n + n_files - 1) // n_files
+    k = np.arange(n, dtype=np.uint64)
+    files = k // np.uint64(per)
+    lens = (np.array([rng.randint(1, 9000) for _ in range(n)], np.uint64) if varlen
+            else np.full(n, 8206, np.uint64))
+    offs = np.zeros(n, np.uint64)
+    for f in range(n_files):
+        sel = files == f
+        offs[sel] = np.concatenate([[0], np.cumsum(lens[sel])[:-1]]).astype(np.uint64) if sel.any() else offs[sel]
+    return np.stack([files, offs, lens], axis=1).copy()
+
+
+def classes(n_files, dp, d):
+    f = np.arange(n_files)
+    m = f % (dp + 1)
+    return np.where(m == d, 0, np.where(m == dp, 2, 1)).astype(np.uint8)
+
+
+def test_shuffle_matches_oracle(rs, orc):
+    for n, seed, ep in [(1, 0, 0), (8, 7, 1), (1000, 0x5EED, 0), (54321, 3, 9)]:
+        p = rs.shuffle_epoch(n, seed, ep)
+        assert np.array_equal(p, orc.shuffle_epoch(n, seed, ep))
+        assert np.array_equal(np.sort(p), np.arange(n, dtype=np.uint64))
+    assert not np.array_equal(rs.shuffle_epoch(64, 1, 0), rs.shuffle_epoch(64, 1, 1))
+    assert rs.shuffle_epoch(1, 5, 5).tolist() == [0]
+
+
+def test_repartition_examples_and_errors(rs, orc):
+    # N=16, B=4, at_step=2, dp 2->4: batch 2 gives ranks {8},{9},{10},{11}
+    assert [rs.repartition_position(16, 4, 2, 4, d, 0) for d in range(4)] == [8, 9, 10, 11]
+    assert [rs.repartition_count(16, 4, 2, 4, d) for d in range(4)] == [2, 2, 2, 2]
+    assert rs.repartition_count(16, 4, 0, 1, 0) == 16
+    assert [rs.repartition_count(16, 4, 4, 2, d) for d in range(2)] == [0, 0]
+    for args in [(17, 4, 1, 2), (103, 8, 3, 4), (5, 4, 0, 2), (10, 4, 2, 4)]:
+        n, B, at, dp = args
+        for d in range(dp):
+            c = rs.repartition_count(n, B, at, dp, d)
+            assert [rs.repartition_position(n, B, at, dp, d, k) for k in range(c)] == \
+                list(orc.repartition_positions(n, B, at, dp, d))
+
+    def err(fn):
+        with pytest.raises(rs.ReshardError) as e:
+            fn()
+        return e.value.name
+
+    assert err(lambda: rs.repartition_count(16, 6, 0, 4, 0)) == "IndivisibleBatch"
+    assert err(lambda: rs.repartition_count(16, 4, 5, 2, 0)) == "StepBeyondEpoch"
+    assert err(lambda: rs.repartition_count(16, 4, 0, 2, 2)) == "IndexOutOfRange"
+    assert err(lambda: rs.repartition_position(16, 4, 2, 4, 0, 2)) == "IndexOutOfRange"
+
+
+def test_locate_sample_priority(rs, orc):
+    rng = random.Random(1)
+    n, nf = 500, 7
+    samples = corpus(n, nf, rng)
+    perm = rs.shuffle_epoch(n, 9, 0)
+    for dp in (1, 2, 4):
+        for d in range(dp):
+            fc = classes(nf, dp, d)
+            for k in range(0, rs.repartition_count(n, 20, 3, dp, d), 7):
+                got = rs.locate_sample(n, 20, 3, dp, d, k, perm, samples, fc)
+                assert got == orc.locate_sample(n, 20, 3, dp, d, k, perm, samples, fc)
+                assert got[3] == fc[got[0]]
+
+
+def test_acceptance8_exactly_once_under_dp_changes(rs):
+    """SPEC acceptance #8: N <= 10,000, B <= 64, dp changed mid-epoch at 3 random steps:
+    the concatenated global read order equals the permutation, each position once."""
+    rng = random.Random(8)
+    for trial in range(20):
+        B = rng.choice([8, 16, 32, 64])
+        n = rng.randint(B, 10_000)
+        perm = rs.shuffle_epoch(n, 1234 + trial, trial)
+        batches = (n + B - 1) // B
+        steps = sorted(rng.sample(range(1, batches), min(3, batches - 1)))
+        dps = [d for d in (1, 2, 4, 8) if B % d == 0]
+        dp = rng.choice(dps)
+        order = []
+        edges = [0] + steps + [batches]
+        for seg in range(len(edges) - 1):
+            at, end = edges[seg], edges[seg + 1]
+            parts = [[rs.repartition_position(n, B, at, dp, d, k) for k in range(rs.repartition_count(n, B, at, dp, d))]
+                     for d in range(dp)]
+            b = B // dp
+            # replay global order: batch by batch, rank slices in rank order
+            ptr = [0] * dp
+            for i in range(at, end):
+                for d in range(dp):
+                    take = [p for p in parts[d][ptr[d]:ptr[d] + b] if p < (i + 1) * B]
+                    ptr[d] += len(take)
+                    order += [int(perm[p]) for p in take]
+            dp = rng.choice(dps)  # B constant, b recomputed
+        assert order == [int(x) for x in perm]
+
+
+@pytest.mark.gpu
+def test_k5_kernel_matches_oracle(rs, orc, ctx):
+    rng = random.Random(42)
+    for n, nf, B, at, dp in [(50_000, 13, 64, 100, 4), (12_345, 5, 40, 7, 8), (4096, 3, 16, 256, 2),
+                             (4096, 3, 16, 0, 1), (300_017, 29, 128, 500, 4)]:
+        samples = corpus(n, nf, rng)
+        perm = rs.shuffle_epoch(n, n, 1)
+        d_perm, d_samp = ctx.malloc(0, 8 * n), ctx.malloc(0, 24 * n)
+        ctx.htod(0, d_perm, perm.ctypes.data, 8 * n)
+        ctx.htod(0, d_samp, samples.ctypes.data, 24 * n)
+        for d in range(dp):
+            fc = classes(nf, dp, d)
+            d_fc = ctx.malloc(0, nf)
+            ctx.htod(0, d_fc, fc.ctypes.data, nf)
+            cnt = rs.repartition_count(n, B, at, dp, d)
+            part = rs.Partition(ctx, 0, cnt)
+            t = rs.repartition(ctx, 0, d_perm, d_samp, d_fc, n, B, at, dp, d, part)
+            got = part.fetch()
+            want = orc.dataset_gather(n, B, at, dp, d, perm, samples, fc, n_threads=3)
+            assert np.array_equal(got["pos"], want["pos"])
+            assert np.array_equal(got["ent"], want["ent"])
+            assert np.array_equal(got["boff"], want["boff"])
+            assert got["qcount"] == want["qcount"]
+            assert np.array_equal(got["qidx"], want["qidx"])
+            assert t["launches"] == (1 if cnt else 0)
+            part.free()
+            ctx.free(0, d_fc)
+        ctx.free(0, d_perm)
+        ctx.free(0, d_samp)
