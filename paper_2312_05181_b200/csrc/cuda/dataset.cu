@@ -73,27 +73,38 @@ __global__ void __launch_bounds__(kThreads) repartition_kernel(Params p, Outs o,
   unsigned long long len[kItems];
   unsigned char cls[kItems];
   Agg mine{0, 0, 0, 0};
+  // Three dependent gathers per sample (perm -> entry -> file class).  Issue each level for
+  // all kItems samples before consuming any, so kItems independent random loads are in
+  // flight per thread at every level (memory-level parallelism, not latency chains).
+  unsigned long long pos[kItems], idx[kItems], f[kItems], off[kItems];
+  const unsigned nv = p.count > k0 ? unsigned(min(p.count - k0, (unsigned long long)kItems)) : 0u;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const unsigned long long k = k0 + j;
-    len[j] = 0, cls[j] = 3;
-    if (k >= p.count) continue;
-    unsigned long long pos;
     if (k < p.in_full) {
-      pos = batch * p.B + p.rank * p.b + r;
+      pos[j] = batch * p.B + p.rank * p.b + r;
       if (++r == p.b) r = 0, ++batch;
     } else {
-      pos = p.full * p.B + p.rank * p.b + (k - p.in_full);
+      pos[j] = p.full * p.B + p.rank * p.b + (k - p.in_full);
     }
-    const unsigned long long idx = __ldg(p.perm + pos);
-    const unsigned long long* e = p.samples + 3 * idx;
-    const unsigned long long f = __ldg(e), off = __ldg(e + 1), L = __ldg(e + 2);
-    o.pos[k] = pos;
-    o.ent[3 * k] = f, o.ent[3 * k + 1] = off, o.ent[3 * k + 2] = L;
-    const unsigned char c = __ldg(p.file_class + f);
-    len[j] = L, cls[j] = c;
-    mine.len += L;
-    mine.c0 += c == 0, mine.c1 += c == 1, mine.c2 += c == 2;
+    idx[j] = j < nv ? __ldg(p.perm + pos[j]) : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long* e = p.samples + 3 * idx[j];
+    if (j < nv) f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
+    else f[j] = 0, off[j] = 0, len[j] = 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    cls[j] = j < nv ? __ldg(p.file_class + f[j]) : (unsigned char)3;
+    if (j < nv) {
+      const unsigned long long k = k0 + j;
+      o.pos[k] = pos[j];
+      o.ent[3 * k] = f[j], o.ent[3 * k + 1] = off[j], o.ent[3 * k + 2] = len[j];
+      mine.len += len[j];
+      mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
+    }
   }
   // block exclusive scan of the per-thread aggregates
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

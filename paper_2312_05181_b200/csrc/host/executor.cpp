@@ -19,6 +19,7 @@ void ck(cudaError_t e, const char* what) {
 
 constexpr uint64_t kCellAlign = 256;
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+constexpr uint64_t kHostChunks = 32;  // pipeline depth of the host-buffer path
 
 struct DeviceGuard {
   int prev = -1;
@@ -100,7 +101,7 @@ CopyConfig CopyConfig::from_env() {
     else if (s == "bulk") c.kernel = CopyKernel::Bulk;
     else if (!s.empty()) raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8 or bulk");
   }
-  c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", c.kernel == CopyKernel::Bulk ? 1 : c.ctas_per_sm));
+  c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", c.kernel == CopyKernel::Bulk ? 1 : 3));
   c.stages = env_int("RESHARD_BULK_STAGES", c.stages);
   c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
   return c;
@@ -167,12 +168,21 @@ int Context::sm_count(int w) const {
 }
 
 // ---- Executor --------------------------------------------------------------------------
+// A slice of the (destination-ordered) aligned tile list for the pipelined host path: it
+// reads src arena bytes below src_end and writes the dst arena byte range [dst_lo, dst_hi).
+struct HostChunk {
+  uint64_t t0, t1, src_end, dst_lo, dst_hi;
+};
+
 struct Executor::Local {
   int world = -1, dev = -1;
-  CopyTile* d_tiles = nullptr;  // [aligned tiles | misaligned tiles]
+  CopyTile* d_tiles = nullptr;  // [aligned tiles, sorted by dst | misaligned tiles]
   uint64_t n_aligned = 0, n_misc = 0, bytes = 0;
   cudaEvent_t start = nullptr, stop = nullptr;
   unsigned long long* d_count = nullptr;
+  std::vector<HostChunk> chunks;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev;
   uint64_t launches() const { return (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
   ~Local() {
     if (dev < 0) return;
@@ -181,6 +191,9 @@ struct Executor::Local {
     if (d_count) cudaFree(d_count);
     if (start) cudaEventDestroy(start);
     if (stop) cudaEventDestroy(stop);
+    for (auto e : ev) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
   }
 };
 
@@ -297,6 +310,31 @@ void Executor::prepare() {
       (aligned16(t) ? aligned : misc).push_back(t);
       bytes += uint64_t(x.rows) * x.row_bytes;
     }
+    // destination order: sequential writes, and contiguous dst ranges per chunk for the
+    // pipelined host path
+    std::sort(aligned.begin(), aligned.end(), [](const CopyTile& p, const CopyTile& q) { return p.dst < q.dst; });
+    l->chunks.clear();
+    if (ctx_.world() == 1 && !aligned.empty()) {
+      const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
+      const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
+      const uint64_t target = std::max<uint64_t>(bytes / kHostChunks, 1);
+      HostChunk c{0, 0, 0, aligned[0].dst - db, 0};
+      uint64_t acc = 0;
+      for (size_t i = 0; i < aligned.size(); ++i) {
+        const CopyTile& t = aligned[i];
+        const uint64_t span_s = (t.rows ? (t.rows - 1) * t.src_pitch : 0) + t.row_bytes;
+        const uint64_t span_d = (t.rows ? (t.rows - 1) * t.dst_pitch : 0) + t.row_bytes;
+        c.src_end = std::max(c.src_end, t.src - sb + span_s);
+        c.dst_hi = std::max(c.dst_hi, t.dst - db + span_d);
+        acc += uint64_t(t.rows) * t.row_bytes;
+        if (acc >= target || i + 1 == aligned.size()) {
+          c.t1 = i + 1;
+          l->chunks.push_back(c);
+          if (i + 1 < aligned.size()) c = HostChunk{i + 1, 0, 0, aligned[i + 1].dst - db, 0};
+          acc = 0;
+        }
+      }
+    }
     DeviceGuard g(l->dev);
     if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
     const size_t n = aligned.size() + misc.size();
@@ -345,15 +383,68 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   if (ctx_.world() != 1) raise(Errc::InvalidArgument, "run_host: single-GPU worlds only");
   DeviceGuard g(l->dev);
   auto s = static_cast<cudaStream_t>(ctx_.stream(gpu));
-  ck(cudaEventRecord(l->start, s), "cudaEventRecord");
-  ck(cudaMemcpyAsync(src_base_[size_t(gpu)], host_src, src_size_[size_t(gpu)], cudaMemcpyHostToDevice, s), "h2d src arena");
-  launch_local(*l, s);
-  ck(cudaMemcpyAsync(host_dst, dst_base_[size_t(gpu)], dst_size_[size_t(gpu)], cudaMemcpyDeviceToHost, s), "d2h dst arena");
+  char* dsrc = static_cast<char*>(src_base_[size_t(gpu)]);
+  char* ddst = static_cast<char*>(dst_base_[size_t(gpu)]);
+  const char* hsrc = static_cast<const char*>(host_src);
+  char* hdst = static_cast<char*>(host_dst);
+  const uint64_t ssize = src_size_[size_t(gpu)], dsize = dst_size_[size_t(gpu)];
+  Timing t;
+  t.tiles = l->n_aligned + l->n_misc, t.bytes = l->bytes;
+  if (l->n_misc || l->chunks.empty()) {  // sequential: H2D, kernels, D2H
+    ck(cudaEventRecord(l->start, s), "cudaEventRecord");
+    ck(cudaMemcpyAsync(dsrc, hsrc, ssize, cudaMemcpyHostToDevice, s), "h2d src arena");
+    launch_local(*l, s);
+    ck(cudaMemcpyAsync(hdst, ddst, dsize, cudaMemcpyDeviceToHost, s), "d2h dst arena");
+    t.launches = l->launches();
+  } else {
+    // Pipelined over destination-ordered chunks: H2D of src pieces (copy engine 1), the
+    // chunk's kernel once the src bytes it reads have landed, D2H of the dst bytes no later
+    // chunk can touch (copy engine 2).  Both PCIe directions stream concurrently.
+    const size_t K = l->chunks.size();
+    if (!l->s_h2d) {
+      ck(cudaStreamCreateWithFlags(&l->s_h2d, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&l->s_d2h, cudaStreamNonBlocking), "stream");
+    }
+    while (l->ev.size() < 2 * K + 1) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      l->ev.push_back(e);
+    }
+    cudaEvent_t* eh = l->ev.data();
+    cudaEvent_t* ec = l->ev.data() + K;
+    cudaEvent_t done = l->ev[2 * K];
+    ck(cudaEventRecord(l->start, s), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(l->s_h2d, l->start, 0), "wait");
+    ck(cudaStreamWaitEvent(l->s_d2h, l->start, 0), "wait");
+    uint64_t up = 0, down = 0;
+    for (size_t k = 0; k < K; ++k) {
+      const uint64_t want = std::max(up, l->chunks[k].src_end);
+      if (want > up) ck(cudaMemcpyAsync(dsrc + up, hsrc + up, want - up, cudaMemcpyHostToDevice, l->s_h2d), "h2d piece");
+      up = want;
+      ck(cudaEventRecord(eh[k], l->s_h2d), "event");
+    }
+    if (up < ssize) ck(cudaMemcpyAsync(dsrc + up, hsrc + up, ssize - up, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
+    const int sms = ctx_.sm_count(gpu);
+    for (size_t k = 0; k < K; ++k) {
+      ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");
+      cuda::launch_copy(l->d_tiles + l->chunks[k].t0, l->chunks[k].t1 - l->chunks[k].t0, cfg_, sms, true, s);
+      ck(cudaEventRecord(ec[k], s), "event");
+    }
+    for (size_t k = 0; k < K; ++k) {
+      const uint64_t safe = k + 1 < K ? l->chunks[k + 1].dst_lo : dsize;
+      ck(cudaStreamWaitEvent(l->s_d2h, ec[k], 0), "wait");
+      if (safe > down) ck(cudaMemcpyAsync(hdst + down, ddst + down, safe - down, cudaMemcpyDeviceToHost, l->s_d2h), "d2h piece");
+      down = std::max(down, safe);
+    }
+    ck(cudaEventRecord(done, l->s_d2h), "event");
+    ck(cudaStreamWaitEvent(s, done, 0), "wait");
+    ck(cudaEventRecord(done, l->s_h2d), "event");  // the H2D tail must land too
+    ck(cudaStreamWaitEvent(s, done, 0), "wait");
+    t.launches = K;
+  }
   ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
   ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
-  Timing t;
   ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
-  t.tiles = l->n_aligned + l->n_misc, t.bytes = l->bytes, t.launches = l->launches();
   return t;
 }
 

@@ -37,12 +37,14 @@ static_assert(sizeof(CopyTile) == 40, "CopyTile layout");
 // Which copy kernel moves the 16-byte-aligned tiles (misaligned ones always take the
 // generic-width LDG/STG kernel).  Defaults can be overridden by RESHARD_COPY_KERNEL
 // (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
+// Defaults from the round-1 B200 sweep (profiles/r02_sweep.json): TMA bulk, 1 CTA/SM,
+// 8 stages x 24 KiB reached 6.59 TB/s on GPT-3 1.3B vs 6.17 TB/s for LDG/STG at 3 CTAs/SM.
 enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2 };
 struct CopyConfig {
-  CopyKernel kernel = CopyKernel::Ldg;
-  int ctas_per_sm = 2;
-  int stages = 6;               // bulk: shared-memory ring depth
-  unsigned stage_bytes = 32768; // bulk: bytes per stage (tiles are cut to fit one stage)
+  CopyKernel kernel = CopyKernel::Bulk;
+  int ctas_per_sm = 1;
+  int stages = 8;               // bulk: shared-memory ring depth
+  unsigned stage_bytes = 24576; // bulk: bytes per stage (tiles are cut to fit one stage)
   static CopyConfig from_env();
 };
 

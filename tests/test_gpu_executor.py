@@ -1,6 +1,7 @@
 """GPU parity of the apply_plan data plane: every destination cell produced by the sm_100a
 tile kernel, read back through the C-ABI, must equal the oracle's apply_plan result
 (bytes moved by the reference's slice/merge, tensor.cpp:61-114) byte for byte."""
+import ctypes
 import random
 
 import numpy as np
@@ -216,3 +217,28 @@ def test_device_merge_error_precedence(rs, ctx):
     # a later part's range error wins over an earlier part's dtype? no: checks are per part in order
     assert err([([(0, 3)], T(0, (3,))), ([(3, 6)], T(1, (2,))), ([(0, 9)], T(0, (9,)))], (6,)) == "DtypeMismatch"
     ctx.free(0, buf)
+
+
+def test_run_host_pipelined_matches_device_result(rs, ctx):
+    """e2e path (host buffers, pipelined H2D / kernels / D2H): the host copy of the dst arena
+    equals the device arena and every destination cell verifies."""
+    cat = rs.Catalog.gpt(256, 6, 64, 1024, rs.MIXED_ADAM)
+    for (a_cfg, b_cfg) in [((2, 1, 1, 2), (2, 1, 2, 4)), ((2, 1, 1, 2), (1, 2, 1, 2)), ((4, 2, 1, 8), (2, 2, 2, 8))]:
+        a = cat.build_strategy(DEV(a_cfg[3]), *a_cfg[:3])
+        b = cat.build_strategy(DEV(b_cfg[3]), *b_cfg[:3])
+        plan = rs.generate_plan(a, b)
+        ex, _ = _run(rs, ctx, plan, a_cfg[3], b_cfg[3], 64 << 10)
+        s_bytes, d_bytes = ex.arena_bytes(0)
+        hs, hd = rs.host_alloc(s_bytes), rs.host_alloc(max(d_bytes, 1))
+        src_ptr, dst_ptr = ex.arenas[0]
+        ctx.dtoh(0, hs, src_ptr, s_bytes)
+        ctx.memset(0, dst_ptr, 0, d_bytes)
+        t = ex.run_host(0, hs, hd)
+        assert t["launches"] >= 1
+        assert ex.verify() == 0
+        dev = np.zeros(d_bytes, np.uint8)
+        ctx.dtoh(0, dev.ctypes.data, dst_ptr, d_bytes)
+        host = np.ctypeslib.as_array((ctypes.c_uint8 * d_bytes).from_address(hd))
+        assert np.array_equal(dev, host)
+        rs.host_free(hs)
+        rs.host_free(hd)
