@@ -73,12 +73,19 @@ def run_dataset(args, rs):
     rank, world, local = dist_env()
     spec = DATASET[args.workload]
     n = spec["n"]
-    perm = rs.shuffle_epoch(n, spec["seed"], spec["epoch"])  # host, once per epoch (off the clock)
+    t_host = time.perf_counter()
+    perm = rs.shuffle_epoch(n, spec["seed"], spec["epoch"])  # host reference of the epoch order
+    host_shuffle_ms = (time.perf_counter() - t_host) * 1e3
     samples = dataset_inputs(spec)
     ctx = rs.Context(world, [rank], [local])
     d_perm, d_samp = ctx.malloc(rank, 8 * n), ctx.malloc(rank, 24 * n)
-    ctx.htod(rank, d_perm, perm.ctypes.data, 8 * n)
     ctx.htod(rank, d_samp, samples.ctypes.data, 24 * n)
+    # K8: the epoch permutation on the GPU (bit-identical to the host shuffle, checked here)
+    shuf = [rs.shuffle_epoch_device(ctx, rank, n, spec["seed"], spec["epoch"], d_perm) for _ in range(2)][-1]
+    dev_perm = np.empty(n, np.uint64)
+    ctx.dtoh(rank, dev_perm.ctypes.data, d_perm, 8 * n)
+    shuffle_identical = bool(np.array_equal(dev_perm, perm))
+    del dev_perm
     jobs = []  # (at_step, dp, d, class ptr, partition)
     for at, dp in spec["events"]:
         for d in range(dp):
@@ -130,6 +137,9 @@ def run_dataset(args, rs):
                      "kernel": "repartition_kernel", "algorithmic_bytes_per_launch": alg // max(launches, 1)},
         "gpu_launches": launches * args.steps, "clocks": clocks.summary(), "spot_check": {"pos": pos_ok, "ent": ent_ok},
         "e2e": None,
+        "shuffle_epoch_gpu": {"ms": round(shuf["ms"], 3), "rounds": shuf["rounds"], "launches": shuf["launches"],
+                              "bit_identical_to_host": shuffle_identical,
+                              "host_shuffle_ms_1thread": round(host_shuffle_ms, 1)},
     }
     if not args.no_cpu_baseline and world == 1:
         from oracle.oracle import Oracle
@@ -220,13 +230,18 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic(workload: str):
-    """dram read+write bytes per copy_tiles launch from the committed ncu --set full capture."""
+def copy_kernel_name() -> str:
+    k = os.environ.get("RESHARD_COPY_KERNEL", "bulk") or "bulk"
+    return {"bulk": "copy_bulk_kernel", "ldg": "copy_v16_kernel", "ldg8": "copy_v16_kernel"}.get(k, k)
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_copy_tiles.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(workload)
+        e = d.get(workload, {}).get(kernel)
         return None if e is None else float(e["dram_bytes_per_launch"])
     except Exception:
         return None
@@ -413,7 +428,8 @@ def run_ours(args):
     # roofline of the dominant (only) kernel: HBM read + write of every copied byte
     alg_bytes = 2 * copy_bytes
     achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
-    traffic = ncu_traffic(args.workload)
+    kname = copy_kernel_name()
+    traffic = ncu_traffic(args.workload, kname)
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
@@ -426,7 +442,7 @@ def run_ours(args):
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "copy_tiles_kernel", "algorithmic_bytes_per_launch": alg_bytes},
+                     "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": e2e, "gpu_launches": args.steps * (1 if tiles else 0),
         "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "wall_s": round(wall, 4),
         "ms_min": round(min(step_ms), 4), "tiles": tiles,

@@ -227,6 +227,12 @@ typedef struct rs_partition_out {  /* device pointers, capacity = the rank's cou
   uint64_t* qcount;              /* 3 counts, written by the kernel */
 } rs_partition_out;
 
+/* K8: shuffle_epoch on the GPU, bit-identical to rs_shuffle_epoch (deterministic
+ * reservations); perm_dev: n x u64 device buffer; scratch: rs_shuffle_scratch_bytes(n) */
+int rs_shuffle_scratch_bytes(uint64_t n, uint64_t* bytes);
+int rs_shuffle_epoch_device(rs_context* ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm_dev,
+                            void* scratch, rs_timing* timing);
+
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
 /* K5: gather + scan + compaction for one rank in one kernel launch (timed with events) */
 int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,

@@ -604,3 +604,17 @@ def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_p
     _chk(lib.rs_repartition(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, C.byref(out),
                             part.scratch, C.byref(t)))
     return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches)
+
+
+def shuffle_epoch_device(ctx: Context, gpu: int, n: int, seed: int, epoch: int, perm_ptr: int) -> dict:
+    """K8: the shuffle_epoch permutation computed on the GPU into perm_ptr (n x u64),
+    bit-identical to the host shuffle.  Returns the timing (tiles = rounds)."""
+    sb = C.c_uint64()
+    _chk(lib.rs_shuffle_scratch_bytes(n, C.byref(sb)))
+    scratch = ctx.malloc(gpu, max(sb.value, 256))
+    try:
+        t = _capi.rs_timing()
+        _chk(lib.rs_shuffle_epoch_device(ctx.h, gpu, n, seed, epoch, perm_ptr, scratch, C.byref(t)))
+    finally:
+        ctx.free(gpu, scratch)
+    return dict(ms=t.ms, rounds=t.tiles, bytes=t.bytes, launches=t.launches)

@@ -124,6 +124,9 @@ SIGNATURES = {
     "rs_repartition_position": (C.c_int, [C.c_uint64] * 6 + [U64P]),
     "rs_locate_sample": (C.c_int, [C.c_uint64] * 6 + [P, P, P, U64P]),
     "rs_repartition_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
+    "rs_shuffle_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
+    "rs_shuffle_epoch_device": (C.c_int, [P, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, P, P,
+                                          C.POINTER(rs_timing)]),
     "rs_repartition": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
                                  P, C.POINTER(rs_timing)]),
 }

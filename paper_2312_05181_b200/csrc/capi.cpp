@@ -538,6 +538,20 @@ int rs_locate_sample(uint64_t n, uint64_t B, uint64_t at_step, uint64_t dp, uint
     out4[0] = e[0], out4[1] = e[1], out4[2] = e[2], out4[3] = file_class[e[0]];
   });
 }
+int rs_shuffle_scratch_bytes(uint64_t n, uint64_t* bytes) {
+  return guard([&] {
+    need(bytes, "bytes");
+    *bytes = shuffle_scratch_bytes(n);
+  });
+}
+int rs_shuffle_epoch_device(rs_context* c, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm,
+                            void* scratch, rs_timing* timing) {
+  return guard([&] {
+    need(perm, "perm"), need(scratch, "scratch");
+    Timing t = shuffle_epoch_device(ctx_of(c), gpu, n, seed, epoch, perm, scratch);
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches};
+  });
+}
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes) {
   return guard([&] {
     need(bytes, "bytes");

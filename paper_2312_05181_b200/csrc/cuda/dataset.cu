@@ -175,7 +175,127 @@ void ck(cudaError_t e, const char* what) {
 }
 uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 
+// ---- K8: bit-exact parallel Fisher-Yates (deterministic reservations) -----------------------
+// The sequential shuffle (host shuffle_epoch) performs swap(A[i], A[H[i]]) for i = N-1 .. 1
+// with H[i] = splitmix64 draw (N-1-i) mod (i+1).  The draws are counter-based, so every
+// H[i] is computed up front.  Iteration i may run once no earlier (higher-index) pending
+// iteration touches location i or H[i]: each round, every pending iteration reserves both
+// its locations with atomicMax of (round << 32 | i); an iteration holding both
+// reservations swaps, the others carry over to the next round.  The result is identical
+// to the sequential loop (Shun et al., SODA'15, "deterministic reservations"); rounds are
+// O(log N) (about 70 for N = 10^8).
+__device__ __forceinline__ unsigned long long mix64d(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void shuffle_init_kernel(unsigned long long* perm, unsigned long long* resv, unsigned long long* list,
+                                    unsigned long long n, unsigned long long s0) {
+  for (unsigned long long x = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; x < n;
+       x += (unsigned long long)gridDim.x * blockDim.x) {
+    perm[x] = x;
+    resv[x] = 0;
+    if (x >= 1) {
+      const unsigned long long draw = mix64d(s0 + (n - x) * 0x9e3779b97f4a7c15ull);  // draw number n-1-x
+      list[x - 1] = (x << 32) | (draw % (x + 1));
+    }
+  }
+}
+
+__global__ void shuffle_reserve_kernel(const unsigned long long* __restrict__ list, const unsigned* __restrict__ count,
+                                       unsigned long long* resv, unsigned long long round) {
+  const unsigned n = *count;
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const unsigned long long e = list[k], i = e >> 32, h = e & 0xffffffffull;
+    const unsigned long long key = (round << 32) | i;
+    atomicMax(resv + i, key);
+    if (h != i) atomicMax(resv + h, key);
+  }
+}
+
+__global__ void shuffle_commit_kernel(const unsigned long long* __restrict__ list, const unsigned* __restrict__ count,
+                                      const unsigned long long* __restrict__ resv, unsigned long long* perm,
+                                      unsigned long long* next, unsigned* next_count, unsigned long long round) {
+  const unsigned n = *count;
+  const unsigned lane = threadIdx.x & 31;
+  // grid-stride with whole-warp trip counts so the ballot below is warp-uniform
+  for (unsigned base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < n; base += gridDim.x * blockDim.x) {
+    const unsigned k = base + lane;
+    bool pending = false;
+    unsigned long long e = 0;
+    if (k < n) {
+      e = list[k];
+      const unsigned long long i = e >> 32, h = e & 0xffffffffull, key = (round << 32) | i;
+      if (__ldcg(resv + i) == key && __ldcg(resv + h) == key) {
+        if (h != i) {
+          const unsigned long long a = perm[i];
+          perm[i] = perm[h];
+          perm[h] = a;
+        }
+      } else {
+        pending = true;
+      }
+    }
+    // warp-aggregated append of the iterations that wait for the next round (any order)
+    const unsigned mask = __ballot_sync(0xffffffffu, pending);
+    unsigned slot = 0;
+    if (lane == 0 && mask) slot = atomicAdd(next_count, unsigned(__popc(mask)));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (pending) next[slot + __popc(mask & ((1u << lane) - 1u))] = e;
+  }
+}
+
 }  // namespace
+
+uint64_t shuffle_scratch_bytes(uint64_t n) { return 256 + 3 * align256(n * 8); }
+
+Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm, void* scratch) {
+  if (n >= (1ull << 32)) raise(Errc::InvalidArgument, "GPU shuffle supports N < 2^32");
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  char* sc = static_cast<char*>(scratch);
+  auto* counts = reinterpret_cast<unsigned*>(sc);  // [2] list sizes (ping-pong)
+  auto* resv = reinterpret_cast<unsigned long long*>(sc + 256);
+  unsigned long long* lists[2] = {reinterpret_cast<unsigned long long*>(sc + 256 + align256(n * 8)),
+                                  reinterpret_cast<unsigned long long*>(sc + 256 + 2 * align256(n * 8))};
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventRecord(e0, st), "event");
+  Timing t;
+  unsigned* pinned = nullptr;
+  ck(cudaMallocHost(&pinned, sizeof(unsigned)), "pinned");
+  const unsigned init = n ? unsigned(n - 1) : 0u;
+  ck(cudaMemcpyAsync(counts, &init, sizeof(unsigned), cudaMemcpyHostToDevice, st), "count");
+  const int grid_full = 148 * 8;
+  shuffle_init_kernel<<<grid_full, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(perm), resv, lists[0], n,
+                                                 seed ^ epoch);
+  ck(cudaGetLastError(), "shuffle init");
+  t.launches = 1;
+  unsigned pending = init;
+  for (unsigned long long round = 1, cur = 0; pending > 0; ++round, cur ^= 1) {
+    const int grid = int(std::min<unsigned long long>(grid_full, (pending + 255) / 256));
+    ck(cudaMemsetAsync(counts + (cur ^ 1), 0, sizeof(unsigned), st), "reset count");
+    shuffle_reserve_kernel<<<grid, 256, 0, st>>>(lists[cur], counts + cur, resv, round);
+    shuffle_commit_kernel<<<grid, 256, 0, st>>>(lists[cur], counts + cur, resv, reinterpret_cast<unsigned long long*>(perm),
+                                                lists[cur ^ 1], counts + (cur ^ 1), round);
+    ck(cudaGetLastError(), "shuffle round");
+    t.launches += 2;
+    ck(cudaMemcpyAsync(pinned, counts + (cur ^ 1), sizeof(unsigned), cudaMemcpyDeviceToHost, st), "count d2h");
+    ck(cudaStreamSynchronize(st), "shuffle sync");
+    pending = *pinned;
+    t.tiles = round;  // rounds
+  }
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeHost(pinned);
+  t.bytes = n * 8;
+  return t;
+}
 
 uint64_t repartition_scratch_bytes(uint64_t count) {
   const uint64_t tiles = (count + kTile - 1) / kTile;

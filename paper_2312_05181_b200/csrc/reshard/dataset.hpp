@@ -42,6 +42,13 @@ struct PartitionOut {
   uint64_t* qcount;
 };
 
+// K8: the same permutation as shuffle_epoch, computed on the GPU (bit-identical; parallel
+// Fisher-Yates by deterministic reservations).  perm: device, n entries; scratch:
+// shuffle_scratch_bytes(n) of device memory.  Timing.tiles = rounds.
+uint64_t shuffle_scratch_bytes(uint64_t n);
+Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm,
+                            void* scratch);
+
 uint64_t repartition_scratch_bytes(uint64_t count);
 // K5: one launch for one rank.  `scratch` (repartition_scratch_bytes) must be device
 // memory; it is cleared on the stream before the launch.

@@ -131,3 +131,15 @@ def test_k5_kernel_matches_oracle(rs, orc, ctx):
             ctx.free(0, d_fc)
         ctx.free(0, d_perm)
         ctx.free(0, d_samp)
+
+
+@pytest.mark.gpu
+def test_k8_gpu_shuffle_bit_identical(rs, ctx):
+    for n, seed, ep in [(1, 3, 0), (2, 3, 1), (1000, 0x5EED, 0), (123_457, 9, 4), (3_000_000, 0x5EED, 2)]:
+        p = ctx.malloc(0, 8 * n)
+        t = rs.shuffle_epoch_device(ctx, 0, n, seed, ep, p)
+        got = np.empty(n, np.uint64)
+        ctx.dtoh(0, got.ctypes.data, p, 8 * n)
+        assert np.array_equal(got, rs.shuffle_epoch(n, seed, ep)), n
+        assert n < 3 or t["rounds"] >= 1
+        ctx.free(0, p)
