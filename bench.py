@@ -41,6 +41,8 @@ WORKLOADS = {
                            [1, 3, 4, 6]),
 }
 DEFAULT_WORKLOAD = "gpt3-1.3b-dp-scaleout"
+# (workload, n_gpus) -> waves needed to fit 180 GB per GPU
+WAVES = {("gpt3-6.7b-tp4pp2-to-tp2pp2dp2", 1): 3, ("gpt3-6.7b-recovery", 1): 2}
 # configs[4]: dataset index repartition of a 100M-sample corpus under DP 2 -> 4 -> 8
 DATASET = {"dataset-100m-dp2to4to8": dict(n=100_000_000, B=1280, seed=0x5EED, epoch=0, files=1000,
                                           per_file=100_000, sample_bytes=8206, events=[(25_000, 4), (50_000, 8)])}
@@ -353,10 +355,25 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cat, a, b, plan, src_gpu, dst_gpu = build_plan(rs, args.workload, N)
     ctx = rs.Context(N, [rank], [local])
-    ex = rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10)
-    s_bytes, d_bytes = ex.arena_bytes(rank)
+    # waves: catalog windows of ~equal bytes executed one after another over reused arenas
+    # (a plan larger than the world's HBM, e.g. GPT-3 6.7B on one GPU)
+    waves = max(1, args.waves if args.waves else WAVES.get((args.workload, N), 1))
+    ent = cat.entries()
+    per_t = [rs.WIDTH[e[1]] * int(__import__("math").prod(e[2])) for e in ent]
+    total_b, bounds, acc = sum(per_t), [0], 0
+    for t, nb in enumerate(per_t):
+        acc += nb
+        if len(bounds) < waves and acc >= total_b * len(bounds) / waves:
+            bounds.append(t + 1)
+    bounds.append(len(ent))
+    windows = [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
+    exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10, window=w if len(windows) > 1 else None)
+           for w in windows]
+    s_bytes = max(e.arena_bytes(rank)[0] for e in exs)
+    d_bytes = max(e.arena_bytes(rank)[1] for e in exs)
     src_ptr, dst_ptr = ctx.malloc(rank, max(s_bytes, 256)), ctx.malloc(rank, max(d_bytes, 256))
-    ex.bind(rank, src_ptr, dst_ptr)
+    for ex in exs:
+        ex.bind(rank, src_ptr, dst_ptr)
     opened = []
     if dist is not None:
         # destination arenas of every GPU, mapped into this process (CUDA IPC over NVLink)
@@ -367,25 +384,42 @@ def run_ours(args):
             if g != rank and handles[g] is not None:
                 p = ctx.ipc_open(rank, handles[g])
                 opened.append(p)
-                ex.bind(g, 0, p)
-    ex.prepare()
-    ex.fill_sources()
+                for ex in exs:
+                    ex.bind(g, 0, p)
+    for ex in exs:
+        ex.prepare()
+    if len(exs) == 1:
+        exs[0].fill_sources()
     stats = plan.stats()
-    tiles, copy_bytes = ex.tiles(rank)
+    tiles = sum(ex.tiles(rank)[0] for ex in exs)
+    copy_bytes = sum(ex.tiles(rank)[1] for ex in exs)
 
     def barrier():
         ctx.sync(rank)
         if dist is not None:
             dist.barrier()
 
+    def step(verify=False):
+        ms, bad, launches = 0.0, 0, 0
+        for ex in exs:
+            if len(exs) > 1:
+                ex.fill_sources()  # the window's sources (off the clock: events bracket the kernel only)
+            t = ex.apply()[0]
+            ms, launches = ms + t["ms"], launches + t["launches"]
+            if verify and len(exs) > 1:
+                bad += ex.verify()
+        return ms, bad, launches
+
     for _ in range(args.warmup):
-        ex.apply()
+        step()
     barrier()
-    step_ms = []
+    step_ms, launches_total = [], 0
     with ClockSampler(local) as clocks:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            step_ms.append(ex.apply()[0]["ms"])
+        for i in range(args.steps):
+            ms_i, bad_w, l_i = step(verify=(i == args.steps - 1))
+            step_ms.append(ms_i)
+            launches_total += l_i
         barrier()
         wall = time.perf_counter() - t0
     total_ms = sum(step_ms)
@@ -396,7 +430,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
-    bad = ex.verify()
+    bad = exs[0].verify() if len(exs) == 1 else bad_w
+    ex = exs[0]
     if dist is not None:
         import torch
 
@@ -406,7 +441,9 @@ def run_ours(args):
 
     # e2e through the C-ABI with host buffers (single-GPU world)
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if len(exs) > 1:
+        e2e = {"value": None, "unit": "ms", "note": "waves: host-buffer path not run (state exceeds one GPU)"}
+    elif world == 1 and not args.no_e2e:
         try:
             hs, hd = rs.host_alloc(s_bytes), rs.host_alloc(max(d_bytes, 1))
             ctx.dtoh(0, hs, src_ptr, s_bytes)
@@ -443,7 +480,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes},
-        "e2e": e2e, "gpu_launches": args.steps * (1 if tiles else 0),
+        "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs),
         "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "wall_s": round(wall, 4),
         "ms_min": round(min(step_ms), 4), "tiles": tiles,
     }
@@ -467,6 +504,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS) + sorted(DATASET))
     ap.add_argument("--tile-kib", type=int, default=256)
+    ap.add_argument("--waves", type=int, default=0, help="catalog windows run one after another (0: automatic)")
     ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

@@ -183,6 +183,10 @@ int rs_choose_source(int n, const rs_device* candidates, const uint64_t* egress,
 /* src_gpu[i]: world GPU of from-device i; dst_gpu[j]: world GPU of to-device j */
 int rs_executor_create(rs_context* ctx, const rs_plan* plan, const int32_t* src_gpu, const int32_t* dst_gpu,
                        uint64_t tile_bytes, rs_executor** out);
+/* same, restricted to catalog tensors [t_begin, t_end): plans larger than the world's HBM
+ * run as several windows (waves) over reused arenas */
+int rs_executor_create_window(rs_context* ctx, const rs_plan* plan, const int32_t* src_gpu, const int32_t* dst_gpu,
+                              uint64_t tile_bytes, uint32_t t_begin, uint32_t t_end, rs_executor** out);
 void rs_executor_destroy(rs_executor* e);
 int rs_executor_arena_bytes(const rs_executor* e, int gpu, uint64_t* src_bytes, uint64_t* dst_bytes);
 int rs_executor_bind(rs_executor* e, int gpu, void* src_arena, void* dst_arena);

@@ -408,9 +408,13 @@ class Executor:
     """apply_plan data plane: arenas per GPU, one tile-copy kernel per source GPU."""
 
     def __init__(self, ctx: Context, plan: Plan, src_gpu: Sequence[int], dst_gpu: Sequence[int],
-                 tile_bytes: int = 256 << 10):
+                 tile_bytes: int = 256 << 10, window: tuple[int, int] | None = None):
         h = C.c_void_p()
-        _chk(lib.rs_executor_create(ctx.h, plan.h, _i32(src_gpu), _i32(dst_gpu), tile_bytes, C.byref(h)))
+        if window is None:
+            _chk(lib.rs_executor_create(ctx.h, plan.h, _i32(src_gpu), _i32(dst_gpu), tile_bytes, C.byref(h)))
+        else:
+            _chk(lib.rs_executor_create_window(ctx.h, plan.h, _i32(src_gpu), _i32(dst_gpu), tile_bytes,
+                                               int(window[0]), int(window[1]), C.byref(h)))
         self.h, self.ctx, self.plan = h.value, ctx, plan
         self.arenas: dict[int, tuple[int, int]] = {}
         self._owned: list[tuple[int, int]] = []

@@ -204,11 +204,13 @@ void Executor::launch_local(Local& l, void* stream) {
 }
 
 Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu,
-                   std::vector<int> dst_gpu, uint64_t tile_bytes, CopyConfig cfg)
+                   std::vector<int> dst_gpu, uint64_t tile_bytes, CopyConfig cfg, uint32_t t_begin, uint32_t t_end)
     : ctx_(ctx), plan_(std::move(plan)), src_gpu_(std::move(src_gpu)), dst_gpu_(std::move(dst_gpu)), cfg_(cfg),
       tile_bytes_(std::max<uint64_t>(4096, std::min<uint64_t>(tile_bytes, cfg.kernel == CopyKernel::Bulk ? cfg.stage_bytes
                                                                                                         : UINT64_MAX) /
-                                               16 * 16)) {
+                                               16 * 16)),
+      t_begin_(t_begin), t_end_(t_end) {
+  auto in = [&](uint32_t t) { return t >= t_begin_ && t < t_end_; };
   const PTC& a = *plan_->from;
   const PTC& b = *plan_->to;
   const int G = ctx_.world();
@@ -227,6 +229,11 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
   std::vector<std::unordered_map<uint64_t, size_t>> src_lookup(a.devices.size());
   for (uint32_t i = 0; i < a.devices.size(); ++i)
     for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
+      if (!in(t)) {  // outside this executor's tensor window: no storage, no work
+        src_lookup[i][(uint64_t(t) << 32) | c] = src_bind_.size();
+        src_bind_.push_back(CellBinding{-1, 0, 0, 0});
+        continue;
+      }
       const int g = src_gpu_[i];
       CellBinding bnd{g, 0, src_size_[size_t(g)], a.cells[t][c].elements() * dtype_width(a.catalog.tensors[t].dtype)};
       src_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
@@ -235,6 +242,10 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     }
   // dst arena layout (kept cells alias their src cell when the logical device stays on its GPU)
   for (const PlanDstCell& dc : plan_->dst_cells) {
+    if (!in(dc.tensor)) {
+      dst_bind_.push_back(CellBinding{-1, 1, 0, 0});
+      continue;
+    }
     const int g = dst_gpu_[dc.dst_device];
     const uint64_t bytes = b.cells[dc.tensor][dc.cell].elements() * dtype_width(b.catalog.tensors[dc.tensor].dtype);
     if (dc.kept) {
@@ -254,7 +265,7 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
   for (size_t j = 0; j < plan_->dst_cells.size(); ++j) {
     const PlanDstCell& dc = plan_->dst_cells[j];
     const CellBinding& db = dst_bind_[j];
-    if (db.arena == 0) continue;  // kept in place
+    if (db.arena == 0 || db.gpu < 0) continue;  // kept in place / outside the tensor window
     const Range& dbox = b.cells[dc.tensor][dc.cell];
     const uint64_t w = dtype_width(b.catalog.tensors[dc.tensor].dtype);
     for (uint32_t k = dc.first; k < dc.first + dc.count; ++k) {

@@ -87,8 +87,11 @@ class Context {
 class Executor {
  public:
   // src_gpu[i]: world GPU of from->devices[i]; dst_gpu[j]: world GPU of to->devices[j].
+  // [t_begin, t_end): only the tensors of this catalog window get storage and work — a plan
+  // too large for the world's HBM is executed as several windows (waves) over the same arenas.
   Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu, std::vector<int> dst_gpu,
-           uint64_t tile_bytes = 256 << 10, CopyConfig cfg = CopyConfig::from_env());
+           uint64_t tile_bytes = 256 << 10, CopyConfig cfg = CopyConfig::from_env(), uint32_t t_begin = 0,
+           uint32_t t_end = UINT32_MAX);
   const CopyConfig& copy_config() const { return cfg_; }
   ~Executor();
 
@@ -132,6 +135,7 @@ class Executor {
   std::vector<int> src_gpu_, dst_gpu_;
   CopyConfig cfg_;
   uint64_t tile_bytes_;
+  uint32_t t_begin_, t_end_;
   std::vector<uint64_t> src_size_, dst_size_;
   std::vector<CellBinding> src_bind_, dst_bind_;
   std::vector<std::vector<size_t>> src_index_;  // [from dev][(t, cell) hosted order] -> src_bind_ index
