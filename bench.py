@@ -161,10 +161,15 @@ def run_dataset(args, rs):
     print(json.dumps(line), flush=True)
 
 
+DIST_BACKEND = os.environ.get("RESHARD_DIST_BACKEND", "nccl")
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if os.environ.get("RESHARD_SAME_GPU"):  # every rank on cuda:0 (IPC correctness on one GPU)
+        local = 0
     return rank, world, local
 
 
@@ -351,8 +356,11 @@ def run_ours(args):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # gloo plumbing: lets several ranks share one GPU (multi-process correctness runs)
+            dist.init_process_group("gloo")
     cat, a, b, plan, src_gpu, dst_gpu = build_plan(rs, args.workload, N)
     ctx = rs.Context(N, [rank], [local])
     # waves: catalog windows of ~equal bytes executed one after another over reused arenas
@@ -426,7 +434,7 @@ def run_ours(args):
     if dist is not None:
         import torch
 
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        t = torch.tensor([total_ms], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
@@ -435,7 +443,7 @@ def run_ours(args):
     if dist is not None:
         import torch
 
-        t = torch.tensor([bad], device=f"cuda:{local}", dtype=torch.int64)
+        t = torch.tensor([bad], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu", dtype=torch.int64)
         dist.all_reduce(t)
         bad = int(t.item())
 

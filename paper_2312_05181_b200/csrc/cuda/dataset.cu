@@ -58,7 +58,7 @@ __device__ __forceinline__ void stcg(Agg* p, const Agg& v) {
   __stcg(&p->len, v.len), __stcg(&p->c0, v.c0), __stcg(&p->c1, v.c1), __stcg(&p->c2, v.c2);
 }
 
-__global__ void __launch_bounds__(kThreads) repartition_kernel(Params p, Outs o, Scratch s) {
+__global__ void __launch_bounds__(kThreads, 3) repartition_kernel(Params p, Outs o, Scratch s) {
   __shared__ unsigned tile_sh;
   __shared__ Agg warp_tot[kWarps];
   __shared__ Agg tile_prefix;
@@ -124,36 +124,57 @@ __global__ void __launch_bounds__(kThreads) repartition_kernel(Params p, Outs o,
   }
   const Agg excl_in_tile = warp_base + (Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2});
 
-  // decoupled look-back (thread 0)
-  if (threadIdx.x == 0) {
+  // decoupled look-back, warp-parallel (warp 0): lane l inspects predecessor tile-1-l-32*w;
+  // the window stops at the nearest predecessor that already published an inclusive prefix.
+  if (warp == 0) {
     Agg prefix{0, 0, 0, 0};
     if (tile == 0) {
-      stcg(&s.inc[0], total);
-      __threadfence();
-      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[0]).store(2u, ::cuda::memory_order_release);
-    } else {
-      stcg(&s.agg[tile], total);
-      __threadfence();
-      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(1u, ::cuda::memory_order_release);
-      for (long long j = (long long)tile - 1; j >= 0; --j) {
-        ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device> fl(s.flags[j]);
-        unsigned f;
-        while ((f = fl.load(::cuda::memory_order_acquire)) == 0u) {
-        }
-        if (f == 2u) {
-          prefix = prefix + ldcg(&s.inc[j]);
-          break;
-        }
-        prefix = prefix + ldcg(&s.agg[j]);
+      if (lane == 0) {
+        stcg(&s.inc[0], total);
+        __threadfence();
+        ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[0]).store(2u, ::cuda::memory_order_release);
       }
-      stcg(&s.inc[tile], prefix + total);
-      __threadfence();
-      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(2u, ::cuda::memory_order_release);
+    } else {
+      if (lane == 0) {
+        stcg(&s.agg[tile], total);
+        __threadfence();
+        ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(1u, ::cuda::memory_order_release);
+      }
+      for (long long base = (long long)tile - 1;; base -= 32) {
+        const long long j = base - lane;
+        unsigned f = 2u;  // before tile 0: an inclusive prefix of zero
+        Agg v{0, 0, 0, 0};
+        if (j >= 0) {
+          ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device> fl(s.flags[j]);
+          while ((f = fl.load(::cuda::memory_order_acquire)) == 0u) {
+          }
+          v = f == 2u ? ldcg(&s.inc[j]) : ldcg(&s.agg[j]);
+        }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, f == 2u);
+        const int stop = inc_mask ? __ffs(inc_mask) - 1 : 31;  // nearest inclusive predecessor
+        if (lane > stop) v = Agg{0, 0, 0, 0};
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+          v.len += __shfl_xor_sync(0xffffffffu, v.len, d);
+          v.c0 += __shfl_xor_sync(0xffffffffu, v.c0, d);
+          v.c1 += __shfl_xor_sync(0xffffffffu, v.c1, d);
+          v.c2 += __shfl_xor_sync(0xffffffffu, v.c2, d);
+        }
+        prefix = prefix + v;
+        if (inc_mask) break;
+      }
+      if (lane == 0) {
+        stcg(&s.inc[tile], prefix + total);
+        __threadfence();
+        ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(2u, ::cuda::memory_order_release);
+      }
     }
-    tile_prefix = prefix;
-    if (tile == s.ntiles - 1) {
-      const Agg all = prefix + total;
-      o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
+    if (lane == 0) {
+      tile_prefix = prefix;
+      if (tile == s.ntiles - 1) {
+        const Agg all = prefix + total;
+        o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
+      }
     }
   }
   __syncthreads();

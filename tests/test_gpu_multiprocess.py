@@ -1,0 +1,34 @@
+"""The one-process-per-GPU path end to end on the single available GPU: two torchrun ranks
+share cuda:0, exchange CUDA-IPC handles of their destination arenas, and push their
+fragments into each other's arenas (K1/K2/K3 kernels writing through IPC mappings).
+Correctness only (both ranks compete for one GPU): every destination byte must verify."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("kernel", ["bulk", "ldg"])
+def test_two_ranks_one_gpu_ipc_push(kernel):
+    env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1", RESHARD_COPY_KERNEL=kernel)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--workload", "gpt2-small-tp2-to-pp2", "--no-e2e", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["verify_mismatched_bytes"] == 0
