@@ -400,7 +400,8 @@ def run_ours(args):
         exs[0].fill_sources()
     stats = plan.stats()
     tiles = sum(ex.tiles(rank)[0] for ex in exs)
-    copy_bytes = sum(ex.tiles(rank)[1] for ex in exs)
+    copy_bytes = sum(ex.tiles(rank)[1] for ex in exs)  # bytes written
+    read_bytes = sum(ex.read_bytes(rank) for ex in exs)  # bytes read (fan-out tiles read once)
 
     def barrier():
         ctx.sync(rank)
@@ -471,7 +472,7 @@ def run_ours(args):
         return
     peak, peak_kind = measured_peaks()
     # roofline of the dominant (only) kernel: HBM read + write of every copied byte
-    alg_bytes = 2 * copy_bytes
+    alg_bytes = read_bytes + copy_bytes
     achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
     kname = copy_kernel_name()
     traffic = ncu_traffic(args.workload, kname)

@@ -87,8 +87,9 @@ typedef struct rs_plan_stats {
 typedef struct rs_timing {
   float ms;                /* CUDA-event time of the copy kernel on its launch stream */
   uint64_t tiles;
-  uint64_t bytes;          /* algorithmic bytes copied by this GPU */
+  uint64_t bytes;          /* algorithmic bytes written by this GPU */
   uint64_t launches;       /* kernels launched in the timed region */
+  uint64_t read_bytes;     /* algorithmic bytes read (fan-out tiles read their source once) */
 } rs_timing;
 
 typedef struct rs_cell_binding {
@@ -203,6 +204,7 @@ int rs_executor_src_cells(const rs_executor* e, int cap, rs_cell_binding* out, i
 int rs_executor_dst_cells(const rs_executor* e, int cap, rs_cell_binding* out, int32_t* dst_device, int32_t* tensor,
                           int32_t* cell, int* n);
 int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes);
+int rs_executor_read_bytes(const rs_executor* e, int gpu, uint64_t* bytes);
 
 /* ---- dataset index repartitioning ------------------------------------- */
 /* shuffle_epoch: Fisher-Yates (i = N-1 .. 1, j = next_below(i+1)), splitmix64 seeded seed^epoch */

@@ -458,7 +458,8 @@ class Executor:
         t = (_capi.rs_timing * cap)()
         n = C.c_int()
         _chk(lib.rs_executor_wait(self.h, cap, t, C.byref(n)))
-        return [dict(ms=t[i].ms, tiles=t[i].tiles, bytes=t[i].bytes, launches=t[i].launches) for i in range(n.value)]
+        return [dict(ms=t[i].ms, tiles=t[i].tiles, bytes=t[i].bytes, launches=t[i].launches, read_bytes=t[i].read_bytes)
+                for i in range(n.value)]
 
     def apply(self) -> list[dict]:
         self.run()
@@ -467,7 +468,7 @@ class Executor:
     def run_host(self, gpu: int, host_src: int, host_dst: int) -> dict:
         t = _capi.rs_timing()
         _chk(lib.rs_executor_run_host(self.h, gpu, host_src, host_dst, C.byref(t)))
-        return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches)
+        return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, read_bytes=t.read_bytes)
 
     def fill_sources(self) -> None:
         _chk(lib.rs_executor_fill_sources(self.h))
@@ -494,6 +495,11 @@ class Executor:
         _chk(lib.rs_executor_dst_cells(self.h, n.value, arr, dv, tt, cc, C.byref(n)))
         return [(dv[i], tt[i], cc[i], Binding(arr[i].gpu, arr[i].arena, arr[i].offset, arr[i].bytes))
                 for i in range(n.value)]
+
+    def read_bytes(self, gpu: int) -> int:
+        b = C.c_uint64()
+        _chk(lib.rs_executor_read_bytes(self.h, gpu, C.byref(b)))
+        return b.value
 
     def tiles(self, gpu: int) -> tuple[int, int]:
         t, b = C.c_uint64(), C.c_uint64()

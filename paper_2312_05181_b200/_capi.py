@@ -42,7 +42,8 @@ class rs_plan_stats(C.Structure):
 
 
 class rs_timing(C.Structure):
-    _fields_ = [("ms", C.c_float), ("tiles", C.c_uint64), ("bytes", C.c_uint64), ("launches", C.c_uint64)]
+    _fields_ = [("ms", C.c_float), ("tiles", C.c_uint64), ("bytes", C.c_uint64), ("launches", C.c_uint64),
+                ("read_bytes", C.c_uint64)]
 
 
 class rs_cell_binding(C.Structure):
@@ -120,6 +121,7 @@ SIGNATURES = {
     "rs_executor_dst_cells": (C.c_int, [P, C.c_int, C.POINTER(rs_cell_binding), I32P, I32P, I32P,
                                         C.POINTER(C.c_int)]),
     "rs_executor_tiles": (C.c_int, [P, C.c_int, U64P, U64P]),
+    "rs_executor_read_bytes": (C.c_int, [P, C.c_int, U64P]),
     "rs_shuffle_epoch": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, P]),
     "rs_repartition_count": (C.c_int, [C.c_uint64] * 5 + [U64P]),
     "rs_repartition_position": (C.c_int, [C.c_uint64] * 6 + [U64P]),

@@ -160,7 +160,19 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 
 constexpr int kBulkMaxStages = 16;
 
-__global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevTile* __restrict__ tiles, unsigned long long n,
+// FanTile: one source box read ONCE into shared memory and stored to up to kMaxFan
+// destinations (DP replicas of the same fragment: the same source bytes feed several new
+// cells, e.g. GPT-3 6.7B (4,2,1)->(2,2,2) where every TP4 fragment goes to both dp
+// replicas).  Saves one HBM read per extra replica (and one NVLink read when remote).
+struct DevFanTile {
+  unsigned long long src, src_pitch;
+  unsigned rows, row_bytes, n_dst, pad;
+  unsigned long long dst[kMaxFan];
+  unsigned long long dst_pitch[kMaxFan];
+};
+static_assert(sizeof(DevFanTile) == sizeof(FanTile), "fan tile layout");
+
+__global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevFanTile* __restrict__ tiles, unsigned long long n,
                                                           int stages, unsigned stage_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
@@ -173,13 +185,15 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevTile* __restr
   const unsigned long long mine = first < n ? (n - first + step - 1) / step : 0;
   const int ahead = stages > 2 ? stages - 2 : 1;
   auto issue_load = [&](unsigned long long i) {
-    const DevTile t = tiles[first + i * step];
+    const DevFanTile& t = tiles[first + i * step];
+    const unsigned rows = t.rows, rb = t.row_bytes;
+    const char* src = reinterpret_cast<const char*>(t.src);
+    const unsigned long long sp = t.src_pitch;
     const int s = int(i % stages);
     const unsigned bar = smem_u32(&bars[s]);
     const unsigned base = smem_u32(smem + size_t(s) * stage_bytes);
-    mbar_expect_tx(bar, t.rows * t.row_bytes);
-    for (unsigned r = 0; r < t.rows; ++r)
-      bulk_g2s(base + r * t.row_bytes, reinterpret_cast<const char*>(t.src) + r * t.src_pitch, t.row_bytes, bar);
+    mbar_expect_tx(bar, rows * rb);
+    for (unsigned r = 0; r < rows; ++r) bulk_g2s(base + r * rb, src + r * sp, rb, bar);
   };
   for (unsigned long long i = 0; i < mine && i < (unsigned long long)ahead; ++i) issue_load(i);
   for (unsigned long long i = 0; i < mine; ++i) {
@@ -190,12 +204,16 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevTile* __restr
       bulk_wait_read<1>();
       issue_load(j);
     }
-    const DevTile t = tiles[first + i * step];
+    const DevFanTile& t = tiles[first + i * step];
+    const unsigned rows = t.rows, rb = t.row_bytes, nd = t.n_dst;
     const int s = int(i % stages);
     mbar_wait(smem_u32(&bars[s]), unsigned((i / stages) & 1));
     const unsigned base = smem_u32(smem + size_t(s) * stage_bytes);
-    for (unsigned r = 0; r < t.rows; ++r)
-      bulk_s2g(reinterpret_cast<char*>(t.dst) + r * t.dst_pitch, base + r * t.row_bytes, t.row_bytes);
+    for (unsigned d = 0; d < nd; ++d) {
+      char* dst = reinterpret_cast<char*>(t.dst[d]);
+      const unsigned long long dp = t.dst_pitch[d];
+      for (unsigned r = 0; r < rows; ++r) bulk_s2g(dst + r * dp, base + r * rb, rb);
+    }
     bulk_commit();
   }
   bulk_wait_all();
@@ -300,12 +318,6 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
   auto grid = [&](int per_sm) { return int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(per_sm))); };
   if (!aligned16) {
     copy_any_kernel<<<grid(8), 256, 0, s>>>(tiles, n_tiles);
-  } else if (cfg.kernel == CopyKernel::Bulk) {
-    if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
-    const size_t smem = size_t(cfg.stages) * cfg.stage_bytes;
-    check(cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-          "bulk smem attribute");
-    copy_bulk_kernel<<<grid(cfg.ctas_per_sm), 32, smem, s>>>(tiles, n_tiles, cfg.stages, cfg.stage_bytes);
   } else if (cfg.kernel == CopyKernel::Ldg8) {
     copy_v16_kernel<8, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
   } else if (cfg.ctas_per_sm >= 3) {
@@ -314,6 +326,18 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
     copy_v16_kernel<4, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
   }
   check(cudaGetLastError(), "copy launch");
+}
+
+void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
+  if (n_tiles == 0) return;
+  if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
+  const size_t smem = size_t(cfg.stages) * cfg.stage_bytes;
+  check(cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+        "bulk smem attribute");
+  const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(cfg.ctas_per_sm)));
+  copy_bulk_kernel<<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTile*>(d_tiles),
+                                                                         n_tiles, cfg.stages, cfg.stage_bytes);
+  check(cudaGetLastError(), "bulk copy launch");
 }
 
 void launch_payload(const PayloadTask* d_tasks, uint64_t n_tasks, uint64_t max_bytes, bool verify,

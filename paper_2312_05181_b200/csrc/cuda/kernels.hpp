@@ -22,6 +22,8 @@ struct CellGeom {
 // tile list.  aligned16: every tile is 16-byte aligned (else the generic-width kernel runs).
 void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
                  void* stream);
+// K3 with fan-out: every tile 16-byte aligned and <= cfg.stage_bytes.
+void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);
 // K6 / K7 over a batch of cells (device array of tasks): write the splitmix64 payload, or
 // count the bytes that differ from it into *d_count (atomic add).  One launch per 65535 cells.
 struct PayloadTask {

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <unordered_map>
 
 #include "cuda/kernels.hpp"
@@ -168,25 +169,27 @@ int Context::sm_count(int w) const {
 }
 
 // ---- Executor --------------------------------------------------------------------------
-// A slice of the (destination-ordered) aligned tile list for the pipelined host path: it
-// reads src arena bytes below src_end and writes the dst arena byte range [dst_lo, dst_hi).
+// A slice of the destination-ordered tile list for the pipelined host path: it reads src
+// arena bytes below src_end and writes nothing below dst_min.
 struct HostChunk {
-  uint64_t t0, t1, src_end, dst_lo, dst_hi;
+  uint64_t t0, t1, src_end, dst_min;
 };
 
 struct Executor::Local {
   int world = -1, dev = -1;
-  CopyTile* d_tiles = nullptr;  // [aligned tiles, sorted by dst | misaligned tiles]
-  uint64_t n_aligned = 0, n_misc = 0, bytes = 0;
+  FanTile* d_fan = nullptr;     // bulk kernel tiles (sorted by first destination)
+  CopyTile* d_tiles = nullptr;  // [LDG aligned tiles, sorted by dst | misaligned tiles]
+  uint64_t n_fan = 0, n_aligned = 0, n_misc = 0, bytes = 0, read_bytes = 0;
   cudaEvent_t start = nullptr, stop = nullptr;
   unsigned long long* d_count = nullptr;
   std::vector<HostChunk> chunks;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev;
-  uint64_t launches() const { return (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
+  uint64_t launches() const { return (n_fan ? 1 : 0) + (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
   ~Local() {
     if (dev < 0) return;
     cudaSetDevice(dev);
+    if (d_fan) cudaFree(d_fan);
     if (d_tiles) cudaFree(d_tiles);
     if (d_count) cudaFree(d_count);
     if (start) cudaEventDestroy(start);
@@ -199,6 +202,7 @@ struct Executor::Local {
 
 void Executor::launch_local(Local& l, void* stream) {
   const int sms = ctx_.sm_count(l.world);
+  cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, stream);
   cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, stream);
   cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, stream);
 }
@@ -260,28 +264,88 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     dst_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
     dst_bind_.push_back(bnd);
   }
-  // fragments -> logical tiles, grouped by the executing (source) GPU
-  logical_.assign(size_t(G), {});
+  // fragments -> logical tiles, grouped by the executing (source) GPU.  Fragments that read
+  // the same source box for several destination cells (DP replicas) are grouped; with the
+  // bulk kernel their tiles are fused into fan-out tiles (source read once).
+  const char* fan_env = std::getenv("RESHARD_FANOUT");
+  const bool fan = cfg_.kernel == CopyKernel::Bulk && !(fan_env && std::string(fan_env) == "0");
+  struct Member {
+    int32_t dst_gpu;
+    uint64_t dst_base;
+    Shape dl, dshape;
+  };
+  struct Group {
+    size_t src_bind;
+    uint32_t tensor, src_cell;
+    Range box;
+    std::vector<Member> members;
+  };
+  std::vector<Group> groups;
+  std::map<std::pair<size_t, Range>, size_t> group_of;
   for (size_t j = 0; j < plan_->dst_cells.size(); ++j) {
     const PlanDstCell& dc = plan_->dst_cells[j];
     const CellBinding& db = dst_bind_[j];
     if (db.arena == 0 || db.gpu < 0) continue;  // kept in place / outside the tensor window
     const Range& dbox = b.cells[dc.tensor][dc.cell];
-    const uint64_t w = dtype_width(b.catalog.tensors[dc.tensor].dtype);
     for (uint32_t k = dc.first; k < dc.first + dc.count; ++k) {
       const PlanFragment& f = plan_->fragments[k];
-      const CellBinding& sb = src_bind_[src_lookup[f.src_device].at((uint64_t(dc.tensor) << 32) | f.src_cell)];
-      const Range& sbox = a.cells[dc.tensor][f.src_cell];
-      const Range rs = f.box.rebase_into(sbox), rd = f.box.rebase_into(dbox);
-      Shape sl, dl;
-      for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo), dl.push_back(rd.dim(d).lo);
-      auto& out = logical_[size_t(sb.gpu)];
-      lower_box(f.box.extents(), sl, sbox.extents(), dl, dbox.extents(), w, tile_bytes_,
+      const size_t si = src_lookup[f.src_device].at((uint64_t(dc.tensor) << 32) | f.src_cell);
+      const Range rd = f.box.rebase_into(dbox);
+      Shape dl;
+      for (int d = 0; d < rd.rank(); ++d) dl.push_back(rd.dim(d).lo);
+      auto key = std::make_pair(si, f.box);
+      auto it = group_of.find(key);
+      if (it == group_of.end() || !fan) {
+        group_of[key] = groups.size();
+        groups.push_back(Group{si, dc.tensor, f.src_cell, f.box, {}});
+        it = group_of.find(key);
+      }
+      groups[fan ? it->second : groups.size() - 1].members.push_back(Member{db.gpu, db.offset, dl, dbox.extents()});
+    }
+  }
+  logical_.assign(size_t(G), {});
+  for (const Group& grp : groups) {
+    const CellBinding& sb = src_bind_[grp.src_bind];
+    const Range& sbox = a.cells[grp.tensor][grp.src_cell];
+    const Range rs = grp.box.rebase_into(sbox);
+    Shape sl;
+    for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo);
+    const uint64_t w = dtype_width(a.catalog.tensors[grp.tensor].dtype);
+    std::vector<std::vector<Logical>> per(grp.members.size());
+    for (size_t m = 0; m < grp.members.size(); ++m) {
+      const Member& mem = grp.members[m];
+      lower_box(grp.box.extents(), sl, sbox.extents(), mem.dl, mem.dshape, w, tile_bytes_,
                 [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                  out.push_back(Logical{sb.gpu, db.gpu, sb.offset + so, db.offset + dof, sp, dp, uint32_t(rows),
-                                        uint32_t(run)});
+                  Logical x{};
+                  x.src_gpu = sb.gpu, x.n_dst = 1, x.src_off = sb.offset + so, x.src_pitch = sp;
+                  x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
+                  x.dst_gpu[0] = mem.dst_gpu, x.dst_off[0] = mem.dst_base + dof, x.dst_pitch[0] = dp;
+                  per[m].push_back(x);
                 });
     }
+    auto& out = logical_[size_t(sb.gpu)];
+    bool same = per.size() > 1;
+    for (size_t m = 1; same && m < per.size(); ++m) {
+      same = per[m].size() == per[0].size();
+      for (size_t t = 0; same && t < per[0].size(); ++t)
+        same = per[m][t].src_off == per[0][t].src_off && per[m][t].rows == per[0][t].rows &&
+               per[m][t].row_bytes == per[0][t].row_bytes && (per[0][t].rows == 1 || per[m][t].src_pitch == per[0][t].src_pitch);
+    }
+    if (!same) {
+      for (auto& v : per) out.insert(out.end(), v.begin(), v.end());
+      continue;
+    }
+    for (size_t m0 = 0; m0 < per.size(); m0 += kMaxFan)
+      for (size_t t = 0; t < per[0].size(); ++t) {
+        Logical x = per[m0][t];
+        x.n_dst = 0;
+        for (size_t m = m0; m < per.size() && m < m0 + kMaxFan; ++m, ++x.n_dst) {
+          x.dst_gpu[x.n_dst] = per[m][t].dst_gpu[0];
+          x.dst_off[x.n_dst] = per[m][t].dst_off[0];
+          x.dst_pitch[x.n_dst] = per[m][t].dst_pitch[0];
+        }
+        out.push_back(x);
+      }
   }
   for (int w : ctx_.local_world_ids()) {
     auto l = std::make_unique<Local>();
@@ -307,47 +371,71 @@ void Executor::bind(int gpu, void* src, void* dst) {
 }
 
 void Executor::prepare() {
+  const bool bulk = cfg_.kernel == CopyKernel::Bulk;
   for (auto& l : local_) {
     const auto& lt = logical_[size_t(l->world)];
+    std::vector<FanTile> fans;
     std::vector<CopyTile> aligned, misc;
-    aligned.reserve(lt.size());
-    uint64_t bytes = 0;
+    uint64_t bytes = 0, read_bytes = 0;
     for (const Logical& x : lt) {
       char* s = static_cast<char*>(src_base_[size_t(x.src_gpu)]);
-      char* d = static_cast<char*>(dst_base_[size_t(x.dst_gpu)]);
-      if (!s || !d) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(!s ? x.src_gpu : x.dst_gpu) + " not bound");
-      CopyTile t{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), uint64_t(reinterpret_cast<uintptr_t>(d + x.dst_off)),
-                 x.src_pitch, x.dst_pitch, x.rows, x.row_bytes};
-      (aligned16(t) ? aligned : misc).push_back(t);
-      bytes += uint64_t(x.rows) * x.row_bytes;
+      if (!s) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.src_gpu) + " not bound");
+      FanTile f{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), x.src_pitch, x.rows, x.row_bytes, x.n_dst, 0, {}, {}};
+      uint64_t bits = f.src | f.row_bytes | (x.rows > 1 ? x.src_pitch : 0);
+      for (uint32_t d = 0; d < x.n_dst; ++d) {
+        char* dp = static_cast<char*>(dst_base_[size_t(x.dst_gpu[d])]);
+        if (!dp) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.dst_gpu[d]) + " not bound");
+        f.dst[d] = uint64_t(reinterpret_cast<uintptr_t>(dp + x.dst_off[d]));
+        f.dst_pitch[d] = x.dst_pitch[d];
+        bits |= f.dst[d] | (x.rows > 1 ? x.dst_pitch[d] : 0);
+      }
+      const uint64_t tb = uint64_t(x.rows) * x.row_bytes;
+      bytes += tb * x.n_dst;
+      if (bulk && (bits & 15) == 0 && tb <= cfg_.stage_bytes) {
+        fans.push_back(f);
+        read_bytes += tb;
+        continue;
+      }
+      for (uint32_t d = 0; d < x.n_dst; ++d) {
+        CopyTile t{f.src, f.dst[d], x.src_pitch, f.dst_pitch[d], x.rows, x.row_bytes};
+        (aligned16(t) ? aligned : misc).push_back(t);
+        read_bytes += tb;
+      }
     }
-    // destination order: sequential writes, and contiguous dst ranges per chunk for the
-    // pipelined host path
+    // destination order: sequential writes, and monotone destinations per host chunk
+    std::sort(fans.begin(), fans.end(), [](const FanTile& p, const FanTile& q) { return p.dst[0] < q.dst[0]; });
     std::sort(aligned.begin(), aligned.end(), [](const CopyTile& p, const CopyTile& q) { return p.dst < q.dst; });
     l->chunks.clear();
-    if (ctx_.world() == 1 && !aligned.empty()) {
+    const bool one_list = misc.empty() && (fans.empty() != aligned.empty());
+    if (ctx_.world() == 1 && one_list) {
       const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
       const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
       const uint64_t target = std::max<uint64_t>(bytes / kHostChunks, 1);
-      HostChunk c{0, 0, 0, aligned[0].dst - db, 0};
+      const size_t n = fans.empty() ? aligned.size() : fans.size();
+      HostChunk c{0, 0, 0, UINT64_MAX};
       uint64_t acc = 0;
-      for (size_t i = 0; i < aligned.size(); ++i) {
-        const CopyTile& t = aligned[i];
-        const uint64_t span_s = (t.rows ? (t.rows - 1) * t.src_pitch : 0) + t.row_bytes;
-        const uint64_t span_d = (t.rows ? (t.rows - 1) * t.dst_pitch : 0) + t.row_bytes;
-        c.src_end = std::max(c.src_end, t.src - sb + span_s);
-        c.dst_hi = std::max(c.dst_hi, t.dst - db + span_d);
-        acc += uint64_t(t.rows) * t.row_bytes;
-        if (acc >= target || i + 1 == aligned.size()) {
+      for (size_t i = 0; i < n; ++i) {
+        FanTile f = fans.empty() ? FanTile{aligned[i].src, aligned[i].src_pitch, aligned[i].rows, aligned[i].row_bytes, 1, 0,
+                                           {aligned[i].dst}, {aligned[i].dst_pitch}}
+                                 : fans[i];
+        c.src_end = std::max(c.src_end, f.src - sb + (f.rows ? (f.rows - 1) * f.src_pitch : 0) + f.row_bytes);
+        for (uint32_t d = 0; d < f.n_dst; ++d) c.dst_min = std::min(c.dst_min, f.dst[d] - db);
+        acc += uint64_t(f.rows) * f.row_bytes * f.n_dst;
+        if (acc >= target || i + 1 == n) {
           c.t1 = i + 1;
           l->chunks.push_back(c);
-          if (i + 1 < aligned.size()) c = HostChunk{i + 1, 0, 0, aligned[i + 1].dst - db, 0};
+          c = HostChunk{i + 1, 0, 0, UINT64_MAX};
           acc = 0;
         }
       }
     }
     DeviceGuard g(l->dev);
+    if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
     if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
+    if (!fans.empty()) {
+      ck(cudaMalloc(&l->d_fan, fans.size() * sizeof(FanTile)), "cudaMalloc tiles");
+      ck(cudaMemcpy(l->d_fan, fans.data(), fans.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
+    }
     const size_t n = aligned.size() + misc.size();
     if (n) {
       ck(cudaMalloc(&l->d_tiles, n * sizeof(CopyTile)), "cudaMalloc tiles");
@@ -355,9 +443,11 @@ void Executor::prepare() {
       ck(cudaMemcpy(l->d_tiles + aligned.size(), misc.data(), misc.size() * sizeof(CopyTile), cudaMemcpyHostToDevice),
          "upload tiles");
     }
+    l->n_fan = fans.size();
     l->n_aligned = aligned.size();
     l->n_misc = misc.size();
     l->bytes = bytes;
+    l->read_bytes = read_bytes;
   }
 }
 
@@ -378,8 +468,9 @@ std::vector<Timing> Executor::wait() {
     ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
     Timing t;
     ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
-    t.tiles = l->n_aligned + l->n_misc;
+    t.tiles = l->n_fan + l->n_aligned + l->n_misc;
     t.bytes = l->bytes;
+    t.read_bytes = l->read_bytes;
     t.launches = l->launches();
     out.push_back(t);
   }
@@ -400,8 +491,8 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   char* hdst = static_cast<char*>(host_dst);
   const uint64_t ssize = src_size_[size_t(gpu)], dsize = dst_size_[size_t(gpu)];
   Timing t;
-  t.tiles = l->n_aligned + l->n_misc, t.bytes = l->bytes;
-  if (l->n_misc || l->chunks.empty()) {  // sequential: H2D, kernels, D2H
+  t.tiles = l->n_fan + l->n_aligned + l->n_misc, t.bytes = l->bytes, t.read_bytes = l->read_bytes;
+  if (l->chunks.empty()) {  // sequential: H2D, kernels, D2H
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     ck(cudaMemcpyAsync(dsrc, hsrc, ssize, cudaMemcpyHostToDevice, s), "h2d src arena");
     launch_local(*l, s);
@@ -409,8 +500,8 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     t.launches = l->launches();
   } else {
     // Pipelined over destination-ordered chunks: H2D of src pieces (copy engine 1), the
-    // chunk's kernel once the src bytes it reads have landed, D2H of the dst bytes no later
-    // chunk can touch (copy engine 2).  Both PCIe directions stream concurrently.
+    // chunk's kernel once the src bytes it reads have landed, D2H of the dst bytes that no
+    // later chunk writes (below the minimum destination of all later chunks; copy engine 2).
     const size_t K = l->chunks.size();
     if (!l->s_h2d) {
       ck(cudaStreamCreateWithFlags(&l->s_h2d, cudaStreamNonBlocking), "stream");
@@ -424,6 +515,12 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     cudaEvent_t* eh = l->ev.data();
     cudaEvent_t* ec = l->ev.data() + K;
     cudaEvent_t done = l->ev[2 * K];
+    std::vector<uint64_t> safe(K);
+    uint64_t m = dsize;
+    for (size_t k = K; k-- > 0;) {
+      safe[k] = m;
+      m = std::min(m, l->chunks[k].dst_min);
+    }
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     ck(cudaStreamWaitEvent(l->s_h2d, l->start, 0), "wait");
     ck(cudaStreamWaitEvent(l->s_d2h, l->start, 0), "wait");
@@ -438,14 +535,15 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     const int sms = ctx_.sm_count(gpu);
     for (size_t k = 0; k < K; ++k) {
       ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");
-      cuda::launch_copy(l->d_tiles + l->chunks[k].t0, l->chunks[k].t1 - l->chunks[k].t0, cfg_, sms, true, s);
+      const uint64_t n = l->chunks[k].t1 - l->chunks[k].t0;
+      if (l->n_fan) cuda::launch_bulk(l->d_fan + l->chunks[k].t0, n, cfg_, sms, s);
+      else cuda::launch_copy(l->d_tiles + l->chunks[k].t0, n, cfg_, sms, true, s);
       ck(cudaEventRecord(ec[k], s), "event");
     }
     for (size_t k = 0; k < K; ++k) {
-      const uint64_t safe = k + 1 < K ? l->chunks[k + 1].dst_lo : dsize;
       ck(cudaStreamWaitEvent(l->s_d2h, ec[k], 0), "wait");
-      if (safe > down) ck(cudaMemcpyAsync(hdst + down, ddst + down, safe - down, cudaMemcpyDeviceToHost, l->s_d2h), "d2h piece");
-      down = std::max(down, safe);
+      if (safe[k] > down) ck(cudaMemcpyAsync(hdst + down, ddst + down, safe[k] - down, cudaMemcpyDeviceToHost, l->s_d2h), "d2h piece");
+      down = std::max(down, safe[k]);
     }
     ck(cudaEventRecord(done, l->s_d2h), "event");
     ck(cudaStreamWaitEvent(s, done, 0), "wait");
@@ -462,7 +560,13 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
 uint64_t Executor::tiles_for(int gpu) const { return logical_[size_t(gpu)].size(); }
 uint64_t Executor::copy_bytes_for(int gpu) const {
   uint64_t n = 0;
-  for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes;
+  for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes * x.n_dst;
+  return n;
+}
+uint64_t Executor::read_bytes_for(int gpu) const {
+  uint64_t n = 0;
+  const bool bulk = cfg_.kernel == CopyKernel::Bulk;
+  for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes * (bulk ? 1 : x.n_dst);
   return n;
 }
 

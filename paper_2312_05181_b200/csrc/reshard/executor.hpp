@@ -34,6 +34,17 @@ struct CopyTile {
 };
 static_assert(sizeof(CopyTile) == 40, "CopyTile layout");
 
+// Bulk (TMA) kernel tile: one source box, up to kMaxFan destinations with the same row
+// structure (DP replicas of one fragment are read once, stored n_dst times).
+constexpr int kMaxFan = 4;
+struct FanTile {
+  uint64_t src, src_pitch;
+  uint32_t rows, row_bytes, n_dst, pad;
+  uint64_t dst[kMaxFan];
+  uint64_t dst_pitch[kMaxFan];
+};
+static_assert(sizeof(FanTile) == 96, "FanTile layout");
+
 // Which copy kernel moves the 16-byte-aligned tiles (misaligned ones always take the
 // generic-width LDG/STG kernel).  Defaults can be overridden by RESHARD_COPY_KERNEL
 // (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
@@ -58,8 +69,9 @@ struct CellBinding {
 struct Timing {
   float ms = 0;        // device time of the copy kernel(s), CUDA events on the launch stream
   uint64_t tiles = 0;
-  uint64_t bytes = 0;  // algorithmic bytes copied (each counted once)
+  uint64_t bytes = 0;       // algorithmic bytes written (each destination byte once)
   uint64_t launches = 0;
+  uint64_t read_bytes = 0;  // algorithmic bytes read (a fan-out tile reads its source once)
 };
 
 // The GPUs this process drives.  World GPU w is local iff local_of(w) >= 0.
@@ -118,13 +130,17 @@ class Executor {
   const std::vector<CellBinding>& dst_bindings() const { return dst_bind_; }  // per plan->dst_cells entry
   const ReconfigPlan& plan() const { return *plan_; }
   uint64_t tiles_for(int gpu) const;
-  uint64_t copy_bytes_for(int gpu) const;
+  uint64_t copy_bytes_for(int gpu) const;  // bytes written by the tiles GPU `gpu` executes
+  uint64_t read_bytes_for(int gpu) const;  // bytes they read (fan-out reads once)
 
  private:
-  struct Logical {  // a tile before arena bases are known
-    int32_t src_gpu, dst_gpu;
-    uint64_t src_off, dst_off, src_pitch, dst_pitch;
+  struct Logical {  // a tile before arena bases are known; n_dst > 1: fan-out (DP replicas)
+    int32_t src_gpu;
+    uint32_t n_dst;
+    uint64_t src_off, src_pitch;
     uint32_t rows, row_bytes;
+    int32_t dst_gpu[kMaxFan];
+    uint64_t dst_off[kMaxFan], dst_pitch[kMaxFan];
   };
   struct Local;
   void launch_local(Local& l, void* stream);
