@@ -13,6 +13,7 @@
 #include <cuda/atomic>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "reshard/dataset.hpp"
@@ -196,6 +197,28 @@ void ck(cudaError_t e, const char* what) {
 }
 uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 
+// The dataset kernels are random 8- and 24-byte gathers: with the default L2 fetch
+// granularity every miss pulls a full 128-byte line from HBM (measured 154 DRAM bytes per
+// 24-byte entry, profiles/r03_repartition_ncu.json).  Lower the granularity for the
+// duration of the launch (RESHARD_L2_FETCH bytes, default 32), restore it afterwards.
+struct L2FetchScope {
+  size_t old = 0;
+  bool set = false;
+  L2FetchScope() {
+    const char* v = std::getenv("RESHARD_L2_FETCH");
+    const size_t want = v && *v ? size_t(std::atoi(v)) : 32;
+    if (want == 0 || cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    set = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, want) == cudaSuccess;
+    if (!set) cudaGetLastError();
+  }
+  ~L2FetchScope() {
+    if (set) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, old);
+  }
+};
+
 // ---- K8: bit-exact parallel Fisher-Yates (deterministic reservations) -----------------------
 // The sequential shuffle (host shuffle_epoch) performs swap(A[i], A[H[i]]) for i = N-1 .. 1
 // with H[i] = splitmix64 draw (N-1-i) mod (i+1).  The draws are counter-based, so every
@@ -274,6 +297,7 @@ uint64_t shuffle_scratch_bytes(uint64_t n) { return 256 + 3 * align256(n * 8); }
 Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm, void* scratch) {
   if (n >= (1ull << 32)) raise(Errc::InvalidArgument, "GPU shuffle supports N < 2^32");
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
   char* sc = static_cast<char*>(scratch);
   auto* counts = reinterpret_cast<unsigned*>(sc);  // [2] list sizes (ping-pong)
@@ -329,6 +353,7 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
   const uint64_t tiles = (count + kTile - 1) / kTile;
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
   cudaEvent_t e0, e1;
   ck(cudaEventCreate(&e0), "event");

@@ -54,8 +54,8 @@ enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2 };
 struct CopyConfig {
   CopyKernel kernel = CopyKernel::Bulk;
   int ctas_per_sm = 1;
-  int stages = 8;               // bulk: shared-memory ring depth
-  unsigned stage_bytes = 24576; // bulk: bytes per stage (tiles are cut to fit one stage)
+  int stages = 7;               // bulk: shared-memory ring depth
+  unsigned stage_bytes = 29696; // bulk: bytes per stage (tiles are cut to fit one stage); r04 sweep
   static CopyConfig from_env();
 };
 
