@@ -176,6 +176,9 @@ int rs_recover(const rs_ptc* from, int n_failed, const rs_device* failed, const 
 void rs_plan_destroy(rs_plan* p);
 int rs_plan_get_stats(const rs_plan* p, rs_plan_stats* out);
 int rs_plan_cost(const rs_plan* p, int cap, rs_device* devices, uint64_t* ingress, uint64_t* egress, int* n);
+/* central-mode attribution: every Move routed through `central` */
+int rs_plan_cost_central(const rs_plan* p, rs_device central, int cap, rs_device* devices, uint64_t* ingress,
+                         uint64_t* egress, int* n);
 /* returns the bytes needed including NUL; writes at most cap bytes */
 int64_t rs_plan_text(const rs_plan* p, char* buf, int64_t cap);
 int rs_choose_source(int n, const rs_device* candidates, const uint64_t* egress, rs_device dst, rs_device* out);
@@ -205,6 +208,16 @@ int rs_executor_dst_cells(const rs_executor* e, int cap, rs_cell_binding* out, i
                           int32_t* cell, int* n);
 int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes);
 int rs_executor_read_bytes(const rs_executor* e, int gpu, uint64_t* bytes);
+
+/* ---- PTX1 container and checkpoints (ptx_io.hpp:10-20) ------------ */
+int rs_ptx_encoded_size(int dtype, int rank, const uint64_t* shape, uint64_t* bytes);
+int rs_ptx_encode_header(int dtype, int rank, const uint64_t* shape, uint8_t* out, uint64_t cap, uint64_t* written);
+/* validates a whole PTX1 buffer (header + payload) */
+int rs_ptx_decode_header(const uint8_t* bytes, uint64_t n, int32_t* dtype, int32_t* rank, uint64_t* shape,
+                         uint64_t* header_bytes);
+/* side 0: the plan's source layout (src arena); side 1: its destination layout */
+int rs_checkpoint_save(rs_executor* e, int side, const char* dir, uint64_t* files, uint64_t* bytes, double* seconds);
+int rs_checkpoint_load(rs_executor* e, const char* dir, uint64_t* files, uint64_t* bytes, double* seconds);
 
 /* ---- dataset index repartitioning ------------------------------------- */
 /* shuffle_epoch: Fisher-Yates (i = N-1 .. 1, j = next_below(i+1)), splitmix64 seeded seed^epoch */

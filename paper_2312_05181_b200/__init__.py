@@ -365,6 +365,14 @@ class Plan:
         _chk(lib.rs_plan_cost(self.h, cap, devs, ing, eg, C.byref(n)))
         return {(int(devs[i].worker), int(devs[i].local)): (int(ing[i]), int(eg[i])) for i in range(n.value)}
 
+    def cost_central(self, central) -> dict:
+        cap = 4096
+        devs = (rs_device * cap)()
+        ing, eg = (C.c_uint64 * cap)(), (C.c_uint64 * cap)()
+        n = C.c_int()
+        _chk(lib.rs_plan_cost_central(self.h, rs_device(*central), cap, devs, ing, eg, C.byref(n)))
+        return {(int(devs[i].worker), int(devs[i].local)): (int(ing[i]), int(eg[i])) for i in range(n.value)}
+
     def text(self) -> str:
         n = lib.rs_plan_text(self.h, None, 0)
         buf = C.create_string_buffer(int(n))

@@ -105,6 +105,7 @@ SIGNATURES = {
     "rs_plan_get_stats": (C.c_int, [P, C.POINTER(rs_plan_stats)]),
     "rs_plan_cost": (C.c_int, [P, C.c_int, C.POINTER(rs_device), U64P, U64P, C.POINTER(C.c_int)]),
     "rs_plan_text": (C.c_int64, [P, C.c_char_p, C.c_int64]),
+    "rs_plan_cost_central": (C.c_int, [P, rs_device, C.c_int, C.POINTER(rs_device), U64P, U64P, C.POINTER(C.c_int)]),
     "rs_choose_source": (C.c_int, [C.c_int, C.POINTER(rs_device), U64P, rs_device, C.POINTER(rs_device)]),
     "rs_executor_create": (C.c_int, [P, P, I32P, I32P, C.c_uint64, C.POINTER(P)]),
     "rs_executor_create_window": (C.c_int, [P, P, I32P, I32P, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(P)]),
@@ -122,6 +123,11 @@ SIGNATURES = {
                                         C.POINTER(C.c_int)]),
     "rs_executor_tiles": (C.c_int, [P, C.c_int, U64P, U64P]),
     "rs_executor_read_bytes": (C.c_int, [P, C.c_int, U64P]),
+    "rs_ptx_encoded_size": (C.c_int, [C.c_int, C.c_int, U64P, U64P]),
+    "rs_ptx_encode_header": (C.c_int, [C.c_int, C.c_int, U64P, P, C.c_uint64, U64P]),
+    "rs_ptx_decode_header": (C.c_int, [P, C.c_uint64, I32P, I32P, U64P, U64P]),
+    "rs_checkpoint_save": (C.c_int, [P, C.c_int, C.c_char_p, U64P, U64P, C.POINTER(C.c_double)]),
+    "rs_checkpoint_load": (C.c_int, [P, C.c_char_p, U64P, U64P, C.POINTER(C.c_double)]),
     "rs_shuffle_epoch": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, P]),
     "rs_repartition_count": (C.c_int, [C.c_uint64] * 5 + [U64P]),
     "rs_repartition_position": (C.c_int, [C.c_uint64] * 6 + [U64P]),

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/reshard_b200.h"
+#include "reshard/checkpoint.hpp"
 #include "reshard/dataset.hpp"
 #include "reshard/executor.hpp"
 
@@ -400,6 +401,17 @@ int rs_plan_cost(const rs_plan* p, int cap, rs_device* devs, uint64_t* in, uint6
       eg[i] = c.egress[size_t(i)];
   });
 }
+int rs_plan_cost_central(const rs_plan* p, rs_device central, int cap, rs_device* devs, uint64_t* in, uint64_t* eg,
+                         int* n) {
+  return guard([&] {
+    need(p, "plan");
+    PlanCost c = plan_cost_central(*p->p, to_dev(central));
+    *n = int(c.devices.size());
+    for (int i = 0; i < *n && i < cap; ++i)
+      devs[i] = rs_device{c.devices[size_t(i)].worker, c.devices[size_t(i)].local}, in[i] = c.ingress[size_t(i)],
+      eg[i] = c.egress[size_t(i)];
+  });
+}
 int64_t rs_plan_text(const rs_plan* p, char* buf, int64_t cap) {
   if (!p) return -1;
   std::string s = plan_text(*p->p);
@@ -522,6 +534,51 @@ int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* 
   return guard([&] {
     need(e, "executor");
     *tiles = e->e->tiles_for(gpu), *bytes = e->e->copy_bytes_for(gpu);
+  });
+}
+
+// ---- PTX1 / checkpoint -----------------------------------------------------------------------
+int rs_ptx_encoded_size(int dtype, int rank, const uint64_t* shape, uint64_t* bytes) {
+  return guard([&] {
+    need(bytes, "bytes");
+    *bytes = ptx_encoded_size(dtype_from_code(dtype), to_shape(rank, shape));
+  });
+}
+int rs_ptx_encode_header(int dtype, int rank, const uint64_t* shape, uint8_t* out, uint64_t cap, uint64_t* written) {
+  return guard([&] {
+    need(out, "out"), need(written, "written");
+    auto h = ptx_encode_header(dtype_from_code(dtype), to_shape(rank, shape));
+    if (h.size() > cap) raise(Errc::InvalidArgument, "buffer too small");
+    std::memcpy(out, h.data(), h.size());
+    *written = h.size();
+  });
+}
+int rs_ptx_decode_header(const uint8_t* bytes, uint64_t n, int32_t* dtype, int32_t* rank, uint64_t* shape,
+                         uint64_t* header_bytes) {
+  return guard([&] {
+    need(bytes, "bytes");
+    PtxHeader h = ptx_decode_header(bytes, n);
+    if (h.shape.size() > RS_MAX_RANK) raise(Errc::InvalidTensor, "rank above 8");
+    *dtype = int32_t(h.dtype), *rank = int32_t(h.shape.size()), *header_bytes = h.header_bytes;
+    for (size_t d = 0; d < h.shape.size(); ++d) shape[d] = h.shape[d];
+  });
+}
+int rs_checkpoint_save(rs_executor* e, int side, const char* dir, uint64_t* files, uint64_t* bytes, double* seconds) {
+  return guard([&] {
+    need(e, "executor"), need(dir, "dir");
+    IoStats s = checkpoint_save(*e->e, side, dir);
+    if (files) *files = s.files;
+    if (bytes) *bytes = s.bytes;
+    if (seconds) *seconds = s.seconds;
+  });
+}
+int rs_checkpoint_load(rs_executor* e, const char* dir, uint64_t* files, uint64_t* bytes, double* seconds) {
+  return guard([&] {
+    need(e, "executor"), need(dir, "dir");
+    IoStats s = checkpoint_load(*e->e, dir);
+    if (files) *files = s.files;
+    if (bytes) *bytes = s.bytes;
+    if (seconds) *seconds = s.seconds;
   });
 }
 

@@ -1,0 +1,231 @@
+// PTX1 codec and per-device checkpoints of executor cells (see reshard/checkpoint.hpp).
+// Device <-> file traffic is staged through two pinned buffers so the D2H (H2D) of one
+// chunk overlaps the write (read) of the previous one.
+#include "reshard/checkpoint.hpp"
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <set>
+
+namespace reshard {
+
+namespace fs = std::filesystem;
+
+namespace {
+
+constexpr uint8_t kMagic[4] = {0x50, 0x54, 0x58, 0x31};  // "PTX1"
+constexpr size_t kChunk = 64ull << 20;
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+uint8_t wire_code(Dtype d) { return d == Dtype::BF16 ? uint8_t(Dtype::F16) : uint8_t(d); }
+
+struct File {
+  std::FILE* f = nullptr;
+  File(const fs::path& p, const char* mode) : f(std::fopen(p.c_str(), mode)) {
+    if (!f) raise(Errc::IoError, "cannot open " + p.string());
+  }
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+// Two pinned staging buffers and a stream on the current device.
+struct Staging {
+  void* buf[2] = {nullptr, nullptr};
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  Staging() {
+    ck(cudaHostAlloc(&buf[0], kChunk, cudaHostAllocDefault), "pinned staging");
+    ck(cudaHostAlloc(&buf[1], kChunk, cudaHostAllocDefault), "pinned staging");
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming), "event");
+  }
+  ~Staging() {
+    cudaStreamSynchronize(s);
+    for (int i = 0; i < 2; ++i) cudaFreeHost(buf[i]), cudaEventDestroy(ev[i]);
+    cudaStreamDestroy(s);
+  }
+};
+
+void write_cell(Staging& st, const fs::path& p, Dtype dt, const Shape& shape, const char* dev, uint64_t bytes) {
+  fs::create_directories(p.parent_path());
+  File f(p, "wb");
+  auto hdr = ptx_encode_header(dt, shape);
+  if (std::fwrite(hdr.data(), 1, hdr.size(), f.f) != hdr.size()) raise(Errc::IoError, "write " + p.string());
+  const uint64_t n = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](uint64_t i) {
+    const uint64_t off = i * kChunk, len = std::min<uint64_t>(kChunk, bytes - off);
+    ck(cudaMemcpyAsync(st.buf[i & 1], dev + off, len, cudaMemcpyDeviceToHost, st.s), "d2h");
+    ck(cudaEventRecord(st.ev[i & 1], st.s), "event");
+  };
+  if (n) issue(0);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (i + 1 < n) issue(i + 1);  // next chunk's D2H overlaps this chunk's write
+    ck(cudaEventSynchronize(st.ev[i & 1]), "sync");
+    const uint64_t len = std::min<uint64_t>(kChunk, bytes - i * kChunk);
+    if (std::fwrite(st.buf[i & 1], 1, len, f.f) != len) raise(Errc::IoError, "write " + p.string());
+  }
+}
+
+void read_cell(Staging& st, const fs::path& p, Dtype dt, const Shape& shape, char* dev, uint64_t bytes) {
+  std::error_code ec;
+  const auto fsize = fs::file_size(p, ec);
+  if (ec) raise(Errc::LayoutMismatch, "missing checkpoint file " + p.string());
+  File f(p, "rb");
+  std::vector<uint8_t> head(std::min<uintmax_t>(fsize, ptx_header_size(kMaxRank)));
+  if (std::fread(head.data(), 1, head.size(), f.f) != head.size()) raise(Errc::IoError, "read " + p.string());
+  // validate the header against the file size without reading the payload twice
+  if (head.size() < 6 || std::memcmp(head.data(), kMagic, 4) != 0) raise(Errc::InvalidTensor, "bad PTX1 magic in " + p.string());
+  const size_t hb = ptx_header_size(head[5]);
+  if (head.size() < hb) raise(Errc::InvalidTensor, "truncated PTX1 header in " + p.string());
+  head.resize(hb);
+  // same checks as ptx_decode_header, with the payload size taken from the file size
+  const PtxHeader h = [&] {
+    Shape s(head[5]);
+    for (size_t d = 0; d < s.size(); ++d) std::memcpy(&s[d], head.data() + 6 + 8 * d, 8);
+    if (head[4] > 3) raise(Errc::InvalidTensor, "unknown dtype code in " + p.string());
+    for (auto e : s)
+      if (e == 0) raise(Errc::InvalidTensor, "zero extent in " + p.string());
+    PtxHeader r{static_cast<Dtype>(head[4]), s, hb, shape_elements(s) * dtype_width(static_cast<Dtype>(head[4]))};
+    if (hb + r.payload_bytes != fsize) raise(Errc::InvalidTensor, "payload size mismatch in " + p.string());
+    return r;
+  }();
+  if (h.shape != shape || dtype_width(h.dtype) != dtype_width(dt))
+    raise(Errc::LayoutMismatch, p.string() + " does not hold this layout's cell");
+  if (std::fseek(f.f, long(hb), SEEK_SET) != 0) raise(Errc::IoError, "seek " + p.string());
+  const uint64_t n = (bytes + kChunk - 1) / kChunk;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t off = i * kChunk, len = std::min<uint64_t>(kChunk, bytes - off);
+    if (i >= 2) ck(cudaEventSynchronize(st.ev[i & 1]), "sync");  // buffer free again
+    if (std::fread(st.buf[i & 1], 1, len, f.f) != len) raise(Errc::IoError, "read " + p.string());
+    ck(cudaMemcpyAsync(dev + off, st.buf[i & 1], len, cudaMemcpyHostToDevice, st.s), "h2d");
+    ck(cudaEventRecord(st.ev[i & 1], st.s), "event");
+  }
+  ck(cudaStreamSynchronize(st.s), "sync");
+}
+
+}  // namespace
+
+size_t ptx_header_size(size_t rank) { return 4 + 1 + 1 + 8 * rank; }
+size_t ptx_encoded_size(Dtype d, const Shape& s) { return ptx_header_size(s.size()) + shape_elements(s) * dtype_width(d); }
+
+std::vector<uint8_t> ptx_encode_header(Dtype d, const Shape& s) {
+  if (s.size() > 255) raise(Errc::InvalidTensor, "rank above 255");
+  std::vector<uint8_t> h(ptx_header_size(s.size()));
+  std::memcpy(h.data(), kMagic, 4);
+  h[4] = wire_code(d);
+  h[5] = uint8_t(s.size());
+  for (size_t i = 0; i < s.size(); ++i)
+    for (int b = 0; b < 8; ++b) h[6 + 8 * i + size_t(b)] = uint8_t(s[i] >> (8 * b));  // little-endian
+  return h;
+}
+
+PtxHeader ptx_decode_header(const uint8_t* p, size_t n) {
+  if (n < 6 || std::memcmp(p, kMagic, 4) != 0) raise(Errc::InvalidTensor, "bad PTX1 magic");
+  if (p[4] > 3) raise(Errc::InvalidTensor, "unknown dtype code " + std::to_string(p[4]));
+  const size_t rank = p[5], hb = ptx_header_size(rank);
+  if (n < hb) raise(Errc::InvalidTensor, "truncated PTX1 header");
+  Shape s(rank);
+  for (size_t i = 0; i < rank; ++i) {
+    uint64_t v = 0;
+    for (int b = 7; b >= 0; --b) v = (v << 8) | p[6 + 8 * i + size_t(b)];
+    if (v == 0) raise(Errc::InvalidTensor, "zero extent");
+    s[i] = v;
+  }
+  const Dtype d = static_cast<Dtype>(p[4]);
+  const uint64_t payload = shape_elements(s) * dtype_width(d);
+  if (n - hb != payload)
+    raise(Errc::InvalidTensor, "payload " + std::to_string(n - hb) + " bytes, expected " + std::to_string(payload));
+  return PtxHeader{d, s, hb, payload};
+}
+
+IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const ReconfigPlan& plan = ex.plan();
+  Context& ctx = ex.context();
+  IoStats io;
+  std::unique_ptr<Staging> st;
+  int cur_gpu = -1;
+  auto stage_for = [&](int gpu) -> Staging& {
+    if (gpu != cur_gpu) {
+      st.reset();
+      ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+      st = std::make_unique<Staging>();
+      cur_gpu = gpu;
+    }
+    return *st;
+  };
+  auto save = [&](const PTC& ptc, uint32_t dev, uint32_t t, uint32_t c, const CellBinding& b) {
+    if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) return;
+    const TensorSpec& e = ptc.catalog.tensors[t];
+    const fs::path p = fs::path(dir) / std::to_string(dev) / (e.path + ".ptx");
+    const char* base = static_cast<const char*>(ex.arena_base(b.gpu, b.arena));
+    if (!base) raise(Errc::InvalidArgument, "checkpoint_save: arena not bound");
+    write_cell(stage_for(b.gpu), p, e.dtype, ptc.cells[t][c].extents(), base + b.offset, b.bytes);
+    io.files += 1, io.bytes += b.bytes;
+  };
+  if (side == 0) {
+    const PTC& a = *plan.from;
+    size_t k = 0;
+    for (uint32_t i = 0; i < a.devices.size(); ++i)
+      for (auto [t, c] : hosted_subtensors(a, a.devices[i])) save(a, i, t, c, ex.src_bindings()[k++]);
+  } else {
+    const PTC& b = *plan.to;
+    for (size_t j = 0; j < plan.dst_cells.size(); ++j) {
+      const PlanDstCell& dc = plan.dst_cells[j];
+      save(b, dc.dst_device, dc.tensor, dc.cell, ex.dst_bindings()[j]);
+    }
+  }
+  io.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return io;
+}
+
+IoStats checkpoint_load(Executor& ex, const std::string& dir) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const PTC& a = *ex.plan().from;
+  Context& ctx = ex.context();
+  // the directory must hold exactly this layout's ranks
+  std::set<std::string> ranks;
+  std::error_code ec;
+  for (auto& entry : fs::directory_iterator(dir, ec))
+    if (entry.is_directory()) ranks.insert(entry.path().filename().string());
+  if (ec) raise(Errc::IoError, "cannot list " + dir);
+  std::set<std::string> want;
+  for (size_t i = 0; i < a.devices.size(); ++i) want.insert(std::to_string(i));
+  if (ranks != want)
+    raise(Errc::LayoutMismatch, "checkpoint has " + std::to_string(ranks.size()) + " ranks, layout has " +
+                                    std::to_string(want.size()));
+  IoStats io;
+  std::unique_ptr<Staging> st;
+  int cur_gpu = -1;
+  size_t k = 0;
+  for (uint32_t i = 0; i < a.devices.size(); ++i)
+    for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
+      const CellBinding& b = ex.src_bindings()[k++];
+      if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) continue;
+      if (b.gpu != cur_gpu) {
+        st.reset();
+        ck(cudaSetDevice(ctx.cuda_device(b.gpu)), "cudaSetDevice");
+        st = std::make_unique<Staging>();
+        cur_gpu = b.gpu;
+      }
+      char* base = static_cast<char*>(ex.arena_base(b.gpu, 0));
+      if (!base) raise(Errc::InvalidArgument, "checkpoint_load: arena not bound");
+      const TensorSpec& e = a.catalog.tensors[t];
+      read_cell(*st, fs::path(dir) / std::to_string(i) / (e.path + ".ptx"), e.dtype, a.cells[t][c].extents(),
+                base + b.offset, b.bytes);
+      io.files += 1, io.bytes += b.bytes;
+    }
+  io.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return io;
+}
+
+}  // namespace reshard

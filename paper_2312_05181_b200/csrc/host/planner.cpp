@@ -188,6 +188,29 @@ PlanCost plan_cost(const ReconfigPlan& p) {
   return c;
 }
 
+PlanCost plan_cost_central(const ReconfigPlan& p, const DeviceId& central) {
+  PlanCost c = plan_cost(p);  // device set (sorted union)
+  if (!std::binary_search(c.devices.begin(), c.devices.end(), central)) {
+    c.devices.insert(std::lower_bound(c.devices.begin(), c.devices.end(), central), central);
+  }
+  c.ingress.assign(c.devices.size(), 0);
+  c.egress.assign(c.devices.size(), 0);
+  c.total = 0;
+  auto at = [&](const DeviceId& d) { return size_t(std::lower_bound(c.devices.begin(), c.devices.end(), d) - c.devices.begin()); };
+  auto leg = [&](const DeviceId& from, const DeviceId& to, uint64_t b) {
+    if (from == to) return;
+    c.egress[at(from)] += b;
+    c.ingress[at(to)] += b;
+    c.total += b;
+  };
+  for (size_t i = p.split_end; i < p.move_end; ++i) {
+    const PlanOp& op = p.ops[i];
+    leg(op.dev, central, op.bytes);
+    leg(central, op.dst, op.bytes);
+  }
+  return c;
+}
+
 PlanStats plan_stats(const ReconfigPlan& p) {
   PlanStats s;
   s.n_split = p.n_split(), s.n_move = p.n_move(), s.n_merge = p.n_merge();

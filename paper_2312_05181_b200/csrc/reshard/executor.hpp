@@ -126,6 +126,8 @@ class Executor {
   void fill_sources();
   uint64_t verify_destinations();
 
+  void* arena_base(int gpu, int arena) const { return arena == 0 ? src_base_[size_t(gpu)] : dst_base_[size_t(gpu)]; }
+  Context& context() const { return ctx_; }
   const std::vector<CellBinding>& src_bindings() const { return src_bind_; }  // per (from dev, t, cell) in order
   const std::vector<CellBinding>& dst_bindings() const { return dst_bind_; }  // per plan->dst_cells entry
   const ReconfigPlan& plan() const { return *plan_; }

@@ -80,6 +80,11 @@ struct PlanCost {
   uint64_t total = 0;
 };
 PlanCost plan_cost(const ReconfigPlan& plan);
+// Traffic attribution of apply_plan's central mode (the paper's baseline,
+// PAPER.md:523-527): every moved fragment is fetched by `central` and re-uploaded from it,
+// so it is charged src -> central and central -> dst (legs that start and end on `central`
+// cost nothing).  Same final state as the distributed mode.
+PlanCost plan_cost_central(const ReconfigPlan& plan, const DeviceId& central);
 PlanStats plan_stats(const ReconfigPlan& plan);
 std::string plan_text(const ReconfigPlan& plan);
 
