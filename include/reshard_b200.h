@@ -170,6 +170,12 @@ int rs_ptc_devices(const rs_ptc* p, int cap, rs_device* out, int* n);
 int rs_ptc_cell(const rs_ptc* p, int tensor, int cell, rs_range* out);
 int rs_ptc_cell_count(const rs_ptc* p, int tensor, int* n);
 
+/* parallelization-configuration JSON: list by rank of model trees
+ * whose leaves are {base, shape, range|null, dtype}.  devices may be NULL: rank r -> (0, r). */
+int rs_parse_parallel_config(const char* json, int n_devices, const rs_device* devices, rs_ptc** out);
+/* returns the bytes needed including NUL; writes at most cap bytes */
+int64_t rs_serialize_parallel_config(const rs_ptc* p, char* buf, int64_t cap);
+
 /* ---- planner ---------------------------------------------------------------------------- */
 int rs_generate_plan(const rs_ptc* from, const rs_ptc* to, rs_plan** out);
 int rs_recover(const rs_ptc* from, int n_failed, const rs_device* failed, const rs_ptc* to, rs_plan** out);

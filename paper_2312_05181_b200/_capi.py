@@ -99,6 +99,8 @@ SIGNATURES = {
     "rs_ptc_devices": (C.c_int, [P, C.c_int, C.POINTER(rs_device), C.POINTER(C.c_int)]),
     "rs_ptc_cell": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(rs_range)]),
     "rs_ptc_cell_count": (C.c_int, [P, C.c_int, C.POINTER(C.c_int)]),
+    "rs_parse_parallel_config": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(rs_device), C.POINTER(P)]),
+    "rs_serialize_parallel_config": (C.c_int64, [P, C.c_char_p, C.c_int64]),
     "rs_generate_plan": (C.c_int, [P, P, C.POINTER(P)]),
     "rs_recover": (C.c_int, [P, C.c_int, C.POINTER(rs_device), P, C.POINTER(P)]),
     "rs_plan_destroy": (None, [P]),

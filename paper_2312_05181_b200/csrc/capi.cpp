@@ -8,6 +8,7 @@
 
 #include "../../include/reshard_b200.h"
 #include "reshard/checkpoint.hpp"
+#include "reshard/config.hpp"
 #include "reshard/dataset.hpp"
 #include "reshard/executor.hpp"
 
@@ -400,6 +401,26 @@ int rs_plan_cost(const rs_plan* p, int cap, rs_device* devs, uint64_t* in, uint6
       devs[i] = rs_device{c.devices[size_t(i)].worker, c.devices[size_t(i)].local}, in[i] = c.ingress[size_t(i)],
       eg[i] = c.egress[size_t(i)];
   });
+}
+int rs_parse_parallel_config(const char* json, int n, const rs_device* devs, rs_ptc** out) {
+  return guard([&] {
+    need(json, "json"), need(out, "out");
+    std::vector<DeviceId> d;
+    if (devs)
+      for (int i = 0; i < n; ++i) d.push_back(to_dev(devs[i]));
+    *out = new rs_ptc{std::make_shared<const PTC>(parse_parallel_config(json, d))};
+  });
+}
+int64_t rs_serialize_parallel_config(const rs_ptc* p, char* buf, int64_t cap) {
+  if (!p) return -1;
+  try {
+    std::string s = serialize_parallel_config(*p->p);
+    if (buf && cap > 0) std::snprintf(buf, size_t(cap), "%s", s.c_str());
+    return int64_t(s.size()) + 1;
+  } catch (const Error& e) {
+    g_last = e.what();
+    return -1;
+  }
 }
 int rs_plan_cost_central(const rs_plan* p, rs_device central, int cap, rs_device* devs, uint64_t* in, uint64_t* eg,
                          int* n) {

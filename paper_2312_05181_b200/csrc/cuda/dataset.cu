@@ -206,7 +206,7 @@ struct L2FetchScope {
   bool set = false;
   L2FetchScope() {
     const char* v = std::getenv("RESHARD_L2_FETCH");
-    const size_t want = v && *v ? size_t(std::atoi(v)) : 32;
+    const size_t want = v && *v ? size_t(std::atoi(v)) : 0;  // r05: 32/64/128 made no difference; off by default
     if (want == 0 || cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity) != cudaSuccess) {
       cudaGetLastError();
       return;

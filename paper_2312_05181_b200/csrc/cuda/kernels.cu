@@ -172,28 +172,60 @@ struct DevFanTile {
 };
 static_assert(sizeof(DevFanTile) == sizeof(FanTile), "fan tile layout");
 
+// Descriptors are themselves streamed by the TMA engine: each CTA owns a contiguous run of
+// tiles and pulls them 32 at a time (3 KiB bulk copies) into a 2-slot shared-memory ring,
+// so the issuing thread never waits on a global load of a descriptor (profiles/r05: 65% of
+// stall samples were descriptor loads when each tile was read from global on demand).
+constexpr int kDescBatch = 32;
+constexpr size_t kDescRingBytes = 2 * kDescBatch * sizeof(DevFanTile);
+
 __global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevFanTile* __restrict__ tiles, unsigned long long n,
                                                           int stages, unsigned stage_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
+  __shared__ __align__(8) unsigned long long dbars[2];
   if (threadIdx.x != 0) return;
+  DevFanTile* desc = reinterpret_cast<DevFanTile*>(smem + size_t(stages) * stage_bytes);
   for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
+  mbar_init(smem_u32(&dbars[0]), 1);
+  mbar_init(smem_u32(&dbars[1]), 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
-  // my tiles: blockIdx.x, blockIdx.x + gridDim.x, ...
-  const unsigned long long first = blockIdx.x, step = gridDim.x;
-  const unsigned long long mine = first < n ? (n - first + step - 1) / step : 0;
+  // my tiles: a contiguous, balanced run [t0, t0 + mine)
+  const unsigned long long t0 = n * blockIdx.x / gridDim.x, mine = n * (blockIdx.x + 1) / gridDim.x - t0;
+  const unsigned long long batches = (mine + kDescBatch - 1) / kDescBatch;
+  auto fetch_batch = [&](unsigned long long b) {
+    const unsigned cnt = unsigned(min((unsigned long long)kDescBatch, mine - b * kDescBatch));
+    const unsigned bar = smem_u32(&dbars[b & 1]);
+    mbar_expect_tx(bar, cnt * unsigned(sizeof(DevFanTile)));
+    bulk_g2s(smem_u32(desc + (b & 1) * kDescBatch), tiles + t0 + b * kDescBatch, cnt * unsigned(sizeof(DevFanTile)), bar);
+  };
+  if (batches > 0) fetch_batch(0);
+  if (batches > 1) fetch_batch(1);
+  unsigned long long waited = ~0ull;  // last descriptor batch known to have landed
+  auto D = [&](unsigned long long i) -> const DevFanTile& {
+    const unsigned long long b = i / kDescBatch;
+    if (waited == ~0ull || b > waited) {
+      mbar_wait(smem_u32(&dbars[b & 1]), unsigned((b >> 1) & 1));
+      waited = b;
+    }
+    return desc[(b & 1) * kDescBatch + (i % kDescBatch)];
+  };
+
   const int ahead = stages > 2 ? stages - 2 : 1;
+  int s_load = 0;                // stage of the next load
+  int s_store = 0;               // stage of the next store
+  unsigned phase = 0;            // parity of the store side's next wait
   auto issue_load = [&](unsigned long long i) {
-    const DevFanTile& t = tiles[first + i * step];
+    const DevFanTile& t = D(i);
     const unsigned rows = t.rows, rb = t.row_bytes;
     const char* src = reinterpret_cast<const char*>(t.src);
     const unsigned long long sp = t.src_pitch;
-    const int s = int(i % stages);
-    const unsigned bar = smem_u32(&bars[s]);
-    const unsigned base = smem_u32(smem + size_t(s) * stage_bytes);
+    const unsigned bar = smem_u32(&bars[s_load]);
+    const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
     mbar_expect_tx(bar, rows * rb);
     for (unsigned r = 0; r < rows; ++r) bulk_g2s(base + r * rb, src + r * sp, rb, bar);
+    if (++s_load == stages) s_load = 0;
   };
   for (unsigned long long i = 0; i < mine && i < (unsigned long long)ahead; ++i) issue_load(i);
   for (unsigned long long i = 0; i < mine; ++i) {
@@ -204,17 +236,23 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevFanTile* __re
       bulk_wait_read<1>();
       issue_load(j);
     }
-    const DevFanTile& t = tiles[first + i * step];
+    const DevFanTile& t = D(i);
     const unsigned rows = t.rows, rb = t.row_bytes, nd = t.n_dst;
-    const int s = int(i % stages);
-    mbar_wait(smem_u32(&bars[s]), unsigned((i / stages) & 1));
-    const unsigned base = smem_u32(smem + size_t(s) * stage_bytes);
+    mbar_wait(smem_u32(&bars[s_store]), phase);
+    const unsigned base = smem_u32(smem + size_t(s_store) * stage_bytes);
     for (unsigned d = 0; d < nd; ++d) {
       char* dst = reinterpret_cast<char*>(t.dst[d]);
       const unsigned long long dp = t.dst_pitch[d];
       for (unsigned r = 0; r < rows; ++r) bulk_s2g(dst + r * dp, base + r * rb, rb);
     }
     bulk_commit();
+    if (++s_store == stages) s_store = 0, phase ^= 1u;
+    // last chunk of a descriptor batch: its slot is free (all loads up to i + ahead and all
+    // stores up to i are issued); refill it with the batch after next
+    if (i % kDescBatch == kDescBatch - 1 && i / kDescBatch + 2 < batches) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fetch_batch(i / kDescBatch + 2);
+    }
   }
   bulk_wait_all();
 }
@@ -331,7 +369,8 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
   if (n_tiles == 0) return;
   if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
-  const size_t smem = size_t(cfg.stages) * cfg.stage_bytes;
+  const size_t smem = size_t(cfg.stages) * cfg.stage_bytes + kDescRingBytes;
+  if (smem > 227 * 1024) raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
   check(cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
         "bulk smem attribute");
   const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(cfg.ctas_per_sm)));
