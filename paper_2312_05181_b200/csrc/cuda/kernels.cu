@@ -191,8 +191,12 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevFanTile* __re
   mbar_init(smem_u32(&dbars[1]), 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
-  // my tiles: a contiguous, balanced run [t0, t0 + mine)
-  const unsigned long long t0 = n * blockIdx.x / gridDim.x, mine = n * (blockIdx.x + 1) / gridDim.x - t0;
+  // my tiles: a contiguous run [t0, t0 + mine); CTAs below n % grid take one extra.  The
+  // host stores CTA c's run as the original tiles c, c + grid, c + 2 grid, ... (see
+  // interleave_for_grid), so descriptors are contiguous per CTA while the CTAs still sweep
+  // memory together as one window (r06: a plain blocked split lost 10% of bandwidth).
+  const unsigned long long q = n / gridDim.x, rem = n % gridDim.x, c = blockIdx.x;
+  const unsigned long long t0 = c * q + (c < rem ? c : rem), mine = q + (c < rem ? 1 : 0);
   const unsigned long long batches = (mine + kDescBatch - 1) / kDescBatch;
   auto fetch_batch = [&](unsigned long long b) {
     const unsigned cnt = unsigned(min((unsigned long long)kDescBatch, mine - b * kDescBatch));
@@ -373,7 +377,7 @@ void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg
   if (smem > 227 * 1024) raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
   check(cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
         "bulk smem attribute");
-  const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(cfg.ctas_per_sm)));
+  const int grid = bulk_grid(n_tiles, sms, cfg);
   copy_bulk_kernel<<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTile*>(d_tiles),
                                                                          n_tiles, cfg.stages, cfg.stage_bytes);
   check(cudaGetLastError(), "bulk copy launch");

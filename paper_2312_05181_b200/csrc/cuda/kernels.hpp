@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "reshard/executor.hpp"
 
@@ -22,8 +23,23 @@ struct CellGeom {
 // tile list.  aligned16: every tile is 16-byte aligned (else the generic-width kernel runs).
 void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
                  void* stream);
-// K3 with fan-out: every tile 16-byte aligned and <= cfg.stage_bytes.
+// K3 with fan-out: every tile 16-byte aligned and <= cfg.stage_bytes.  The array must be in
+// interleave_for_grid order for bulk_grid(n_tiles, sms, cfg) CTAs.
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);
+inline int bulk_grid(uint64_t n_tiles, int sms, const CopyConfig& cfg) {
+  const uint64_t g = uint64_t(sms) * uint64_t(cfg.ctas_per_sm > 0 ? cfg.ctas_per_sm : 1);
+  return int(n_tiles < g ? n_tiles : g);
+}
+// Reorder tiles so that CTA c of a `grid`-CTA launch finds original tiles c, c+grid, ... as
+// one contiguous run (the bulk kernel fetches its descriptors in contiguous batches).
+template <class T>
+std::vector<T> interleave_for_grid(const T* tiles, size_t n, size_t grid) {
+  std::vector<T> out;
+  out.reserve(n);
+  for (size_t c = 0; c < grid; ++c)
+    for (size_t i = c; i < n; i += grid) out.push_back(tiles[i]);
+  return out;
+}
 // K6 / K7 over a batch of cells (device array of tasks): write the splitmix64 payload, or
 // count the bytes that differ from it into *d_count (atomic add).  One launch per 65535 cells.
 struct PayloadTask {

@@ -177,7 +177,8 @@ struct HostChunk {
 
 struct Executor::Local {
   int world = -1, dev = -1;
-  FanTile* d_fan = nullptr;     // bulk kernel tiles (sorted by first destination)
+  FanTile* d_fan = nullptr;     // bulk kernel tiles (sorted by first destination, interleaved for the grid)
+  FanTile* d_fan_chunks = nullptr;  // the same tiles, interleaved per host chunk (pipelined host path)
   CopyTile* d_tiles = nullptr;  // [LDG aligned tiles, sorted by dst | misaligned tiles]
   uint64_t n_fan = 0, n_aligned = 0, n_misc = 0, bytes = 0, read_bytes = 0;
   cudaEvent_t start = nullptr, stop = nullptr;
@@ -190,6 +191,7 @@ struct Executor::Local {
     if (dev < 0) return;
     cudaSetDevice(dev);
     if (d_fan) cudaFree(d_fan);
+    if (d_fan_chunks) cudaFree(d_fan_chunks);
     if (d_tiles) cudaFree(d_tiles);
     if (d_count) cudaFree(d_count);
     if (start) cudaEventDestroy(start);
@@ -372,6 +374,8 @@ void Executor::bind(int gpu, void* src, void* dst) {
 
 void Executor::prepare() {
   const bool bulk = cfg_.kernel == CopyKernel::Bulk;
+  const char* bp = std::getenv("RESHARD_BULK_PEER");
+  const bool bulk_peer = bp && std::string(bp) == "1";
   for (auto& l : local_) {
     const auto& lt = logical_[size_t(l->world)];
     std::vector<FanTile> fans;
@@ -391,7 +395,12 @@ void Executor::prepare() {
       }
       const uint64_t tb = uint64_t(x.rows) * x.row_bytes;
       bytes += tb * x.n_dst;
-      if (bulk && (bits & 15) == 0 && tb <= cfg_.stage_bytes) {
+      // Cross-GPU tiles use plain st.global through the peer mapping (K2) unless
+      // RESHARD_BULK_PEER=1 lets the TMA engine store to peer addresses too: that variant
+      // has not been validated on a multi-GPU box yet (one GPU in this environment).
+      bool remote = false;
+      for (uint32_t d = 0; d < x.n_dst; ++d) remote |= x.dst_gpu[d] != l->world;
+      if (bulk && (!remote || bulk_peer) && (bits & 15) == 0 && tb <= cfg_.stage_bytes) {
         fans.push_back(f);
         read_bytes += tb;
         continue;
@@ -431,10 +440,24 @@ void Executor::prepare() {
     }
     DeviceGuard g(l->dev);
     if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
+    if (l->d_fan_chunks) cudaFree(l->d_fan_chunks), l->d_fan_chunks = nullptr;
     if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
     if (!fans.empty()) {
+      const int sms = ctx_.sm_count(l->world);
+      auto full = cuda::interleave_for_grid(fans.data(), fans.size(), size_t(cuda::bulk_grid(fans.size(), sms, cfg_)));
       ck(cudaMalloc(&l->d_fan, fans.size() * sizeof(FanTile)), "cudaMalloc tiles");
-      ck(cudaMemcpy(l->d_fan, fans.data(), fans.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
+      ck(cudaMemcpy(l->d_fan, full.data(), full.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
+      if (!l->chunks.empty()) {  // each host chunk is its own launch
+        std::vector<FanTile> per;
+        per.reserve(fans.size());
+        for (const HostChunk& c : l->chunks) {
+          auto v = cuda::interleave_for_grid(fans.data() + c.t0, size_t(c.t1 - c.t0),
+                                             size_t(cuda::bulk_grid(c.t1 - c.t0, sms, cfg_)));
+          per.insert(per.end(), v.begin(), v.end());
+        }
+        ck(cudaMalloc(&l->d_fan_chunks, per.size() * sizeof(FanTile)), "cudaMalloc tiles");
+        ck(cudaMemcpy(l->d_fan_chunks, per.data(), per.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
+      }
     }
     const size_t n = aligned.size() + misc.size();
     if (n) {
@@ -536,7 +559,7 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     for (size_t k = 0; k < K; ++k) {
       ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");
       const uint64_t n = l->chunks[k].t1 - l->chunks[k].t0;
-      if (l->n_fan) cuda::launch_bulk(l->d_fan + l->chunks[k].t0, n, cfg_, sms, s);
+      if (l->n_fan) cuda::launch_bulk(l->d_fan_chunks + l->chunks[k].t0, n, cfg_, sms, s);
       else cuda::launch_copy(l->d_tiles + l->chunks[k].t0, n, cfg_, sms, true, s);
       ck(cudaEventRecord(ec[k], s), "event");
     }

@@ -22,9 +22,11 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("kernel", ["bulk", "ldg"])
+@pytest.mark.parametrize("kernel", ["bulk", "ldg", "bulk-peer"])
 def test_two_ranks_one_gpu_ipc_push(kernel):
-    env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1", RESHARD_COPY_KERNEL=kernel)
+    env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1", RESHARD_COPY_KERNEL=kernel.split("-")[0])
+    if kernel == "bulk-peer":  # TMA bulk stores through the IPC mapping as well
+        env["RESHARD_BULK_PEER"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
            "--workload", "gpt2-small-tp2-to-pp2", "--no-e2e", "--no-cpu-baseline"]
