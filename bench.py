@@ -239,7 +239,8 @@ class ClockSampler:
 
 def copy_kernel_name() -> str:
     k = os.environ.get("RESHARD_COPY_KERNEL", "bulk") or "bulk"
-    return {"bulk": "copy_bulk_kernel", "ldg": "copy_v16_kernel", "ldg8": "copy_v16_kernel"}.get(k, k)
+    return {"bulk": "copy_bulk_kernel", "bulk_strided": "copy_bulk_strided_kernel", "ldg": "copy_v16_kernel",
+            "ldg8": "copy_v16_kernel"}.get(k, k)
 
 
 def ncu_traffic(workload: str, kernel: str):

@@ -261,6 +261,61 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_kernel(const DevFanTile* __re
   bulk_wait_all();
 }
 
+// Variant for A/B measurement (RESHARD_COPY_KERNEL=bulk_strided): the round-1 first bulk
+// kernel's schedule — CTA c takes tiles c, c+grid, ... straight from the natural array — with
+// each descriptor loaded by six independent 16-byte loads when its chunk is issued and
+// parked in shared memory for the store phase.
+__device__ __forceinline__ void load_desc(const DevFanTile* p, DevFanTile& out) {
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&out);
+  uint4 v[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = __ldg(s + k);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) d[k] = v[k];
+}
+
+__global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTile* __restrict__ tiles,
+                                                                  unsigned long long n, int stages, unsigned stage_bytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
+  __shared__ DevFanTile sdesc[kBulkMaxStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const unsigned long long first = blockIdx.x, step = gridDim.x;
+  const unsigned long long mine = first < n ? (n - first + step - 1) / step : 0;
+  const int ahead = stages > 2 ? stages - 2 : 1;
+  int s_load = 0, s_store = 0;
+  unsigned phase = 0;
+  auto issue_load = [&](unsigned long long i) {
+    DevFanTile& t = sdesc[s_load];
+    load_desc(tiles + first + i * step, t);
+    const unsigned bar = smem_u32(&bars[s_load]);
+    const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
+    mbar_expect_tx(bar, t.rows * t.row_bytes);
+    for (unsigned r = 0; r < t.rows; ++r)
+      bulk_g2s(base + r * t.row_bytes, reinterpret_cast<const char*>(t.src) + r * t.src_pitch, t.row_bytes, bar);
+    if (++s_load == stages) s_load = 0;
+  };
+  for (unsigned long long i = 0; i < mine && i < (unsigned long long)ahead; ++i) issue_load(i);
+  for (unsigned long long i = 0; i < mine; ++i) {
+    if (i + ahead < mine) {
+      bulk_wait_read<1>();
+      issue_load(i + ahead);
+    }
+    const DevFanTile& t = sdesc[s_store];
+    mbar_wait(smem_u32(&bars[s_store]), phase);
+    const unsigned base = smem_u32(smem + size_t(s_store) * stage_bytes);
+    for (unsigned d = 0; d < t.n_dst; ++d)
+      for (unsigned r = 0; r < t.rows; ++r)
+        bulk_s2g(reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d], base + r * t.row_bytes, t.row_bytes);
+    bulk_commit();
+    if (++s_store == stages) s_store = 0, phase ^= 1u;
+  }
+  bulk_wait_all();
+}
+
 // ---- synthetic payload ------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -373,13 +428,14 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
   if (n_tiles == 0) return;
   if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
-  const size_t smem = size_t(cfg.stages) * cfg.stage_bytes + kDescRingBytes;
+  const bool strided = cfg.kernel == CopyKernel::BulkStrided;
+  const size_t smem = size_t(cfg.stages) * cfg.stage_bytes + (strided ? 0 : kDescRingBytes);
   if (smem > 227 * 1024) raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
-  check(cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-        "bulk smem attribute");
+  auto kern = strided ? copy_bulk_strided_kernel : copy_bulk_kernel;
+  check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "bulk smem attribute");
   const int grid = bulk_grid(n_tiles, sms, cfg);
-  copy_bulk_kernel<<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTile*>(d_tiles),
-                                                                         n_tiles, cfg.stages, cfg.stage_bytes);
+  kern<<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles,
+                                                             cfg.stages, cfg.stage_bytes);
   check(cudaGetLastError(), "bulk copy launch");
 }
 

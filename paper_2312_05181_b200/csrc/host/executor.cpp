@@ -100,9 +100,10 @@ CopyConfig CopyConfig::from_env() {
     if (s == "ldg") c.kernel = CopyKernel::Ldg;
     else if (s == "ldg8") c.kernel = CopyKernel::Ldg8;
     else if (s == "bulk") c.kernel = CopyKernel::Bulk;
+    else if (s == "bulk_strided") c.kernel = CopyKernel::BulkStrided;
     else if (!s.empty()) raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8 or bulk");
   }
-  c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", c.kernel == CopyKernel::Bulk ? 1 : 3));
+  c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", is_bulk(c.kernel) ? 1 : 3));
   c.stages = env_int("RESHARD_BULK_STAGES", c.stages);
   c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
   return c;
@@ -212,7 +213,7 @@ void Executor::launch_local(Local& l, void* stream) {
 Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu,
                    std::vector<int> dst_gpu, uint64_t tile_bytes, CopyConfig cfg, uint32_t t_begin, uint32_t t_end)
     : ctx_(ctx), plan_(std::move(plan)), src_gpu_(std::move(src_gpu)), dst_gpu_(std::move(dst_gpu)), cfg_(cfg),
-      tile_bytes_(std::max<uint64_t>(4096, std::min<uint64_t>(tile_bytes, cfg.kernel == CopyKernel::Bulk ? cfg.stage_bytes
+      tile_bytes_(std::max<uint64_t>(4096, std::min<uint64_t>(tile_bytes, is_bulk(cfg.kernel) ? cfg.stage_bytes
                                                                                                         : UINT64_MAX) /
                                                16 * 16)),
       t_begin_(t_begin), t_end_(t_end) {
@@ -270,7 +271,7 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
   // the same source box for several destination cells (DP replicas) are grouped; with the
   // bulk kernel their tiles are fused into fan-out tiles (source read once).
   const char* fan_env = std::getenv("RESHARD_FANOUT");
-  const bool fan = cfg_.kernel == CopyKernel::Bulk && !(fan_env && std::string(fan_env) == "0");
+  const bool fan = is_bulk(cfg_.kernel) && !(fan_env && std::string(fan_env) == "0");
   struct Member {
     int32_t dst_gpu;
     uint64_t dst_base;
@@ -373,7 +374,8 @@ void Executor::bind(int gpu, void* src, void* dst) {
 }
 
 void Executor::prepare() {
-  const bool bulk = cfg_.kernel == CopyKernel::Bulk;
+  const bool bulk = is_bulk(cfg_.kernel);
+  const bool interleave = cfg_.kernel == CopyKernel::Bulk;  // bulk_strided walks the natural order
   const char* bp = std::getenv("RESHARD_BULK_PEER");
   const bool bulk_peer = bp && std::string(bp) == "1";
   for (auto& l : local_) {
@@ -444,7 +446,8 @@ void Executor::prepare() {
     if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
     if (!fans.empty()) {
       const int sms = ctx_.sm_count(l->world);
-      auto full = cuda::interleave_for_grid(fans.data(), fans.size(), size_t(cuda::bulk_grid(fans.size(), sms, cfg_)));
+      auto full = cuda::interleave_for_grid(fans.data(), fans.size(),
+                                            interleave ? size_t(cuda::bulk_grid(fans.size(), sms, cfg_)) : 1);
       ck(cudaMalloc(&l->d_fan, fans.size() * sizeof(FanTile)), "cudaMalloc tiles");
       ck(cudaMemcpy(l->d_fan, full.data(), full.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
       if (!l->chunks.empty()) {  // each host chunk is its own launch
@@ -452,7 +455,7 @@ void Executor::prepare() {
         per.reserve(fans.size());
         for (const HostChunk& c : l->chunks) {
           auto v = cuda::interleave_for_grid(fans.data() + c.t0, size_t(c.t1 - c.t0),
-                                             size_t(cuda::bulk_grid(c.t1 - c.t0, sms, cfg_)));
+                                             interleave ? size_t(cuda::bulk_grid(c.t1 - c.t0, sms, cfg_)) : 1);
           per.insert(per.end(), v.begin(), v.end());
         }
         ck(cudaMalloc(&l->d_fan_chunks, per.size() * sizeof(FanTile)), "cudaMalloc tiles");
@@ -588,7 +591,7 @@ uint64_t Executor::copy_bytes_for(int gpu) const {
 }
 uint64_t Executor::read_bytes_for(int gpu) const {
   uint64_t n = 0;
-  const bool bulk = cfg_.kernel == CopyKernel::Bulk;
+  const bool bulk = is_bulk(cfg_.kernel);
   for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes * (bulk ? 1 : x.n_dst);
   return n;
 }

@@ -50,7 +50,8 @@ static_assert(sizeof(FanTile) == 96, "FanTile layout");
 // (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
 // Defaults from the round-1 B200 sweep (profiles/r02_sweep.json): TMA bulk, 1 CTA/SM,
 // 8 stages x 24 KiB reached 6.59 TB/s on GPT-3 1.3B vs 6.17 TB/s for LDG/STG at 3 CTAs/SM.
-enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2 };
+enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2, BulkStrided = 3 };
+inline bool is_bulk(CopyKernel k) { return k == CopyKernel::Bulk || k == CopyKernel::BulkStrided; }
 struct CopyConfig {
   CopyKernel kernel = CopyKernel::Bulk;
   int ctas_per_sm = 1;
