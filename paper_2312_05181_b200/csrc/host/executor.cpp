@@ -174,7 +174,48 @@ int Context::sm_count(int w) const {
 // arena bytes below src_end and writes nothing below dst_min.
 struct HostChunk {
   uint64_t t0, t1, src_end, dst_min;
+  std::vector<std::pair<uint64_t, uint64_t>> uploads;  // src arena [off, off+len) first needed by this chunk
 };
+
+// Src arena byte ranges first read by each chunk (chunks in order): the union of the
+// chunk's tile spans minus everything earlier chunks already uploaded.  Uploading exactly
+// these keeps the H2D stream in the order the kernels consume it, so D2H of early chunks
+// overlaps the rest of the upload whatever the src/dst arena orders are.
+void plan_uploads(std::vector<HostChunk>& chunks, const std::vector<std::vector<std::pair<uint64_t, uint64_t>>>& spans) {
+  std::map<uint64_t, uint64_t> done;  // start -> end, disjoint
+  auto covered_minus = [&](uint64_t a, uint64_t b, std::vector<std::pair<uint64_t, uint64_t>>& out) {
+    auto it = done.upper_bound(a);
+    if (it != done.begin()) --it;
+    uint64_t cur = a;
+    for (; it != done.end() && it->first < b; ++it) {
+      if (it->second <= cur) continue;
+      if (it->first > cur) out.emplace_back(cur, it->first - cur);
+      cur = std::max(cur, it->second);
+      if (cur >= b) break;
+    }
+    if (cur < b) out.emplace_back(cur, b - cur);
+  };
+  for (size_t k = 0; k < chunks.size(); ++k) {
+    auto v = spans[k];
+    std::sort(v.begin(), v.end());
+    std::vector<std::pair<uint64_t, uint64_t>> merged;  // [a, b)
+    for (auto& [a, b] : v) {
+      if (!merged.empty() && a <= merged.back().second) merged.back().second = std::max(merged.back().second, b);
+      else merged.emplace_back(a, b);
+    }
+    for (auto& [a, b] : merged) covered_minus(a, b, chunks[k].uploads);
+    for (auto& [a, b] : merged) {  // insert [a, b) into done, coalescing
+      uint64_t lo = a, hi = b;
+      auto it = done.lower_bound(a);
+      if (it != done.begin() && std::prev(it)->second >= a) --it;
+      while (it != done.end() && it->first <= hi) {
+        lo = std::min(lo, it->first), hi = std::max(hi, it->second);
+        it = done.erase(it);
+      }
+      done[lo] = hi;
+    }
+  }
+}
 
 struct Executor::Local {
   int world = -1, dev = -1;
@@ -423,22 +464,27 @@ void Executor::prepare() {
       const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
       const uint64_t target = std::max<uint64_t>(bytes / kHostChunks, 1);
       const size_t n = fans.empty() ? aligned.size() : fans.size();
-      HostChunk c{0, 0, 0, UINT64_MAX};
+      HostChunk c{0, 0, 0, UINT64_MAX, {}};
+      std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);
       uint64_t acc = 0;
       for (size_t i = 0; i < n; ++i) {
         FanTile f = fans.empty() ? FanTile{aligned[i].src, aligned[i].src_pitch, aligned[i].rows, aligned[i].row_bytes, 1, 0,
                                            {aligned[i].dst}, {aligned[i].dst_pitch}}
                                  : fans[i];
-        c.src_end = std::max(c.src_end, f.src - sb + (f.rows ? (f.rows - 1) * f.src_pitch : 0) + f.row_bytes);
+        const uint64_t s0 = f.src - sb, s1 = s0 + (f.rows ? (f.rows - 1) * f.src_pitch : 0) + f.row_bytes;
+        spans.back().emplace_back(s0, s1);
+        c.src_end = std::max(c.src_end, s1);
         for (uint32_t d = 0; d < f.n_dst; ++d) c.dst_min = std::min(c.dst_min, f.dst[d] - db);
         acc += uint64_t(f.rows) * f.row_bytes * f.n_dst;
         if (acc >= target || i + 1 == n) {
           c.t1 = i + 1;
           l->chunks.push_back(c);
-          c = HostChunk{i + 1, 0, 0, UINT64_MAX};
+          c = HostChunk{i + 1, 0, 0, UINT64_MAX, {}};
+          if (i + 1 < n) spans.emplace_back();
           acc = 0;
         }
       }
+      plan_uploads(l->chunks, spans);
     }
     DeviceGuard g(l->dev);
     if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
@@ -550,14 +596,23 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     ck(cudaStreamWaitEvent(l->s_h2d, l->start, 0), "wait");
     ck(cudaStreamWaitEvent(l->s_d2h, l->start, 0), "wait");
-    uint64_t up = 0, down = 0;
+    uint64_t down = 0;
+    std::vector<std::pair<uint64_t, uint64_t>> all;
     for (size_t k = 0; k < K; ++k) {
-      const uint64_t want = std::max(up, l->chunks[k].src_end);
-      if (want > up) ck(cudaMemcpyAsync(dsrc + up, hsrc + up, want - up, cudaMemcpyHostToDevice, l->s_h2d), "h2d piece");
-      up = want;
+      for (auto [off, len] : l->chunks[k].uploads) {
+        ck(cudaMemcpyAsync(dsrc + off, hsrc + off, len, cudaMemcpyHostToDevice, l->s_h2d), "h2d piece");
+        all.emplace_back(off, off + len);
+      }
       ck(cudaEventRecord(eh[k], l->s_h2d), "event");
     }
-    if (up < ssize) ck(cudaMemcpyAsync(dsrc + up, hsrc + up, ssize - up, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
+    // state no tile reads (kept cells nobody copies) still goes to the device, last
+    std::sort(all.begin(), all.end());
+    uint64_t cur = 0;
+    for (auto [a, b] : all) {
+      if (a > cur) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, a - cur, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
+      cur = std::max(cur, b);
+    }
+    if (cur < ssize) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, ssize - cur, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
     const int sms = ctx_.sm_count(gpu);
     for (size_t k = 0; k < K; ++k) {
       ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");

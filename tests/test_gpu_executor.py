@@ -232,6 +232,7 @@ def test_run_host_pipelined_matches_device_result(rs, ctx):
         hs, hd = rs.host_alloc(s_bytes), rs.host_alloc(max(d_bytes, 1))
         src_ptr, dst_ptr = ex.arenas[0]
         ctx.dtoh(0, hs, src_ptr, s_bytes)
+        ctx.memset(0, src_ptr, 0, s_bytes)  # every source byte must come from the host buffer
         ctx.memset(0, dst_ptr, 0, d_bytes)
         t = ex.run_host(0, hs, hd)
         assert t["launches"] >= 1
