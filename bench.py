@@ -238,7 +238,7 @@ class ClockSampler:
 
 
 def copy_kernel_name() -> str:
-    k = os.environ.get("RESHARD_COPY_KERNEL", "bulk") or "bulk"
+    k = os.environ.get("RESHARD_COPY_KERNEL", "bulk_strided") or "bulk_strided"  # the library default
     return {"bulk": "copy_bulk_kernel", "bulk_strided": "copy_bulk_strided_kernel", "ldg": "copy_v16_kernel",
             "ldg8": "copy_v16_kernel"}.get(k, k)
 

@@ -288,9 +288,14 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
   const int ahead = stages > 2 ? stages - 2 : 1;
   int s_load = 0, s_store = 0;
   unsigned phase = 0;
+  // one-deep register prefetch: the six loads of chunk i+1's descriptor are in flight
+  // while chunk i is issued and stored
+  DevFanTile nxt;
+  if (mine) load_desc(tiles + first, nxt);
   auto issue_load = [&](unsigned long long i) {
-    DevFanTile& t = sdesc[s_load];
-    load_desc(tiles + first + i * step, t);
+    const DevFanTile t = nxt;
+    sdesc[s_load] = t;
+    if (i + 1 < mine) load_desc(tiles + first + (i + 1) * step, nxt);
     const unsigned bar = smem_u32(&bars[s_load]);
     const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
     mbar_expect_tx(bar, t.rows * t.row_bytes);

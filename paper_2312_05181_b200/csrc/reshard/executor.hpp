@@ -53,10 +53,10 @@ static_assert(sizeof(FanTile) == 96, "FanTile layout");
 enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2, BulkStrided = 3 };
 inline bool is_bulk(CopyKernel k) { return k == CopyKernel::Bulk || k == CopyKernel::BulkStrided; }
 struct CopyConfig {
-  CopyKernel kernel = CopyKernel::Bulk;
+  CopyKernel kernel = CopyKernel::BulkStrided;  // r08 same-box A/B: 3-4% faster than Bulk
   int ctas_per_sm = 1;
-  int stages = 7;               // bulk: shared-memory ring depth
-  unsigned stage_bytes = 29696; // bulk: bytes per stage (tiles are cut to fit one stage); r04 sweep
+  int stages = 6;               // bulk: shared-memory ring depth
+  unsigned stage_bytes = 32768; // bulk: bytes per stage (tiles are cut to fit one stage); r08 A/B
   static CopyConfig from_env();
 };
 
