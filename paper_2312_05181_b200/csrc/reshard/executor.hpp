@@ -55,8 +55,8 @@ inline bool is_bulk(CopyKernel k) { return k == CopyKernel::Bulk || k == CopyKer
 struct CopyConfig {
   CopyKernel kernel = CopyKernel::BulkStrided;  // r08 same-box A/B: 3-4% faster than Bulk
   int ctas_per_sm = 1;
-  int stages = 6;               // bulk: shared-memory ring depth
-  unsigned stage_bytes = 32768; // bulk: bytes per stage (tiles are cut to fit one stage); r08 A/B
+  int stages = 7;               // bulk: shared-memory ring depth
+  unsigned stage_bytes = 29696; // bulk: bytes per stage (tiles are cut to fit one stage); r09 A/B
   static CopyConfig from_env();
 };
 
