@@ -468,6 +468,32 @@ def run_ours(args):
         except Exception as exc:  # e.g. not enough pinned host memory
             e2e = {"value": None, "unit": "ms", "h2d_bytes_per_step": s_bytes, "d2h_bytes_per_step": d_bytes,
                    "error": str(exc)[:200]}
+    elif world > 1 and not args.no_e2e:
+        # every rank: H2D of its src arena | barrier | push kernels | barrier | D2H of its dst
+        # arena; CUDA events mark to mark on each rank's stream, max over ranks
+        hs, hd = rs.host_alloc(max(s_bytes, 1)), rs.host_alloc(max(d_bytes, 1))
+        ctx.dtoh(rank, hs, src_ptr, s_bytes)
+        e2e_ms = []
+        for i in range(1 + args.e2e_steps):
+            ex.host_phase(rank, 0, hs)
+            dist.barrier()
+            ex.host_phase(rank, 1)
+            dist.barrier()
+            ex.host_phase(rank, 2, hd)
+            if i:
+                e2e_ms.append(ex.host_elapsed(rank))
+        import torch
+
+        t = torch.tensor([statistics.mean(e2e_ms)], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        totals = torch.tensor([s_bytes, d_bytes], dtype=torch.int64,
+                              device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
+        dist.all_reduce(totals)
+        rs.host_free(hs)
+        rs.host_free(hd)
+        e2e = {"value": round(float(t.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(totals[0].item()),
+               "d2h_bytes_per_step": int(totals[1].item()), "steps": args.e2e_steps,
+               "note": "per rank: H2D | barrier | kernels | barrier | D2H, max over ranks"}
 
     if rank != 0:
         return

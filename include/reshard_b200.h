@@ -206,6 +206,12 @@ int rs_executor_wait(rs_executor* e, int cap, rs_timing* out, int* n); /* per lo
 /* end to end on host buffers (single-GPU world): H2D src arena, copy kernel, D2H dst arena,
  * all on the GPU's stream and bracketed by CUDA events; arenas must be bound */
 int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src_arena, void* host_dst_arena, rs_timing* out);
+/* multi-process end-to-end step in phases separated by the caller's cross-rank barriers:
+ * 0 = start mark + H2D of the GPU's src arena (host_buf = src), 1 = kernels (host_buf
+ * unused), 2 = D2H of its dst arena (host_buf = dst) + stop mark; each phase returns after
+ * its stream work completes.  rs_executor_host_elapsed: event time mark to mark. */
+int rs_executor_host_phase(rs_executor* e, int gpu, int phase, void* host_buf);
+int rs_executor_host_elapsed(rs_executor* e, int gpu, float* ms);
 int rs_executor_fill_sources(rs_executor* e);
 int rs_executor_verify(rs_executor* e, uint64_t* mismatched_bytes);
 /* bindings: src cells in (from-device, tensor, cell) order; dst cells in plan order */

@@ -478,6 +478,14 @@ class Executor:
         _chk(lib.rs_executor_run_host(self.h, gpu, host_src, host_dst, C.byref(t)))
         return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, read_bytes=t.read_bytes)
 
+    def host_phase(self, gpu: int, phase: int, host_buf: int = 0) -> None:
+        _chk(lib.rs_executor_host_phase(self.h, gpu, phase, host_buf))
+
+    def host_elapsed(self, gpu: int) -> float:
+        ms = C.c_float()
+        _chk(lib.rs_executor_host_elapsed(self.h, gpu, C.byref(ms)))
+        return ms.value
+
     def fill_sources(self) -> None:
         _chk(lib.rs_executor_fill_sources(self.h))
 

@@ -510,6 +510,18 @@ int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src, void* ho
     *out = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
   });
 }
+int rs_executor_host_phase(rs_executor* e, int gpu, int phase, void* host_buf) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->host_phase(gpu, phase, host_buf);
+  });
+}
+int rs_executor_host_elapsed(rs_executor* e, int gpu, float* ms) {
+  return guard([&] {
+    need(e, "executor"), need(ms, "ms");
+    *ms = e->e->host_elapsed(gpu);
+  });
+}
 int rs_executor_fill_sources(rs_executor* e) {
   return guard([&] {
     need(e, "executor");

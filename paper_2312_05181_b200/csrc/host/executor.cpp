@@ -549,6 +549,41 @@ std::vector<Timing> Executor::wait() {
   return out;
 }
 
+void Executor::host_phase(int gpu, int phase, void* host_buf) {
+  Local* l = nullptr;
+  for (auto& x : local_)
+    if (x->world == gpu) l = x.get();
+  if (!l) raise(Errc::DeviceUnavailable, "host_phase: GPU " + std::to_string(gpu) + " is not local");
+  DeviceGuard g(l->dev);
+  auto s = static_cast<cudaStream_t>(ctx_.stream(gpu));
+  switch (phase) {
+    case 0:
+      ck(cudaEventRecord(l->start, s), "cudaEventRecord");
+      if (src_size_[size_t(gpu)])
+        ck(cudaMemcpyAsync(src_base_[size_t(gpu)], host_buf, src_size_[size_t(gpu)], cudaMemcpyHostToDevice, s), "h2d");
+      break;
+    case 1: launch_local(*l, s); break;
+    case 2:
+      if (dst_size_[size_t(gpu)])
+        ck(cudaMemcpyAsync(host_buf, dst_base_[size_t(gpu)], dst_size_[size_t(gpu)], cudaMemcpyDeviceToHost, s), "d2h");
+      ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
+      break;
+    default: raise(Errc::InvalidArgument, "host_phase: phase must be 0, 1 or 2");
+  }
+  ck(cudaStreamSynchronize(s), "host_phase sync");
+}
+
+float Executor::host_elapsed(int gpu) {
+  for (auto& x : local_)
+    if (x->world == gpu) {
+      DeviceGuard g(x->dev);
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, x->start, x->stop), "cudaEventElapsedTime");
+      return ms;
+    }
+  raise(Errc::DeviceUnavailable, "host_elapsed: GPU " + std::to_string(gpu) + " is not local");
+}
+
 Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   Local* l = nullptr;
   for (auto& x : local_)

@@ -121,6 +121,12 @@ class Executor {
   // `host_src`, the copy kernel, D2H of the whole dst arena into `host_dst`; CUDA events
   // bracket all three.  Pinned host memory gives full PCIe bandwidth.
   Timing run_host(int gpu, const void* host_src, void* host_dst);
+  // The same end-to-end step for multi-process worlds, in phases the caller separates with
+  // cross-rank barriers: 0 = start mark + H2D of this GPU's src arena, 1 = the kernels,
+  // 2 = D2H of this GPU's dst arena + stop mark.  Each phase is async on the GPU's stream
+  // and synchronized before returning; host_elapsed() is the event time from mark to mark.
+  void host_phase(int gpu, int phase, void* host_buf);
+  float host_elapsed(int gpu);
 
   // Synthetic payload (K6) into the src cells of local GPUs; K7 verification of every
   // destination cell on local GPUs (kept cells included).  Returns mismatching bytes.

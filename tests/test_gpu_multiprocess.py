@@ -22,15 +22,16 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("kernel", ["bulk", "ldg", "bulk-peer"])
+@pytest.mark.parametrize("kernel", ["bulk_strided", "bulk", "ldg", "bulk_strided-peer"])
 def test_two_ranks_one_gpu_ipc_push(kernel):
     env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1", RESHARD_COPY_KERNEL=kernel.split("-")[0])
-    if kernel == "bulk-peer":  # TMA bulk stores through the IPC mapping as well
+    if kernel.endswith("-peer"):  # TMA bulk stores through the IPC mapping as well
         env["RESHARD_BULK_PEER"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
-           "--workload", "gpt2-small-tp2-to-pp2", "--no-e2e", "--no-cpu-baseline"]
+           "--workload", "gpt2-small-tp2-to-pp2", "--no-cpu-baseline", "--e2e-steps", "1"]
     p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["verify_mismatched_bytes"] == 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0  # multi-rank host-buffer path ran
