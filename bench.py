@@ -240,7 +240,7 @@ class ClockSampler:
 def copy_kernel_name() -> str:
     k = os.environ.get("RESHARD_COPY_KERNEL", "bulk_strided") or "bulk_strided"  # the library default
     return {"bulk": "copy_bulk_kernel", "bulk_strided": "copy_bulk_strided_kernel", "ldg": "copy_v16_kernel",
-            "ldg8": "copy_v16_kernel"}.get(k, k)
+            "ldg8": "copy_v16_kernel", "bulk_warp": "copy_bulk_warp_kernel"}.get(k, k)
 
 
 def ncu_traffic(workload: str, kernel: str):
@@ -528,8 +528,6 @@ def run_ours(args):
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
     print(json.dumps(line), flush=True)
-    for p in opened:
-        pass
 
 
 def main():

@@ -29,9 +29,6 @@ ERRC = [
 WIDTH = {0: 4, 1: 2, 2: 8, 3: 1}
 LAYER_PRE, LAYER_POST = -1, -2
 
-u64p = np.ctypeslib.ndpointer(np.uint64, flags="C")
-u32p = np.ctypeslib.ndpointer(np.uint32, flags="C")
-i32p = np.ctypeslib.ndpointer(np.int32, flags="C")
 u8p = np.ctypeslib.ndpointer(np.uint8, flags="C")
 
 

@@ -321,6 +321,61 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
   bulk_wait_all();
 }
 
+// Variant RESHARD_COPY_KERNEL=bulk_warp: the same schedule, but the 32 lanes share the
+// issue work — lane l issues the bulk copies of rows l, l+32, ... of a tile (strided 2-D
+// fragments such as row-parallel TP slices have tens of rows per stage).  Lane 0 owns the
+// mbarriers; every lane commits and drains its own bulk groups before a stage is reused.
+__global__ void __launch_bounds__(32, 1) copy_bulk_warp_kernel(const DevFanTile* __restrict__ tiles, unsigned long long n,
+                                                               int stages, unsigned stage_bytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
+  __shared__ DevFanTile sdesc[kBulkMaxStages];
+  const unsigned lane = threadIdx.x;
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const unsigned long long first = blockIdx.x, step = gridDim.x;
+  const unsigned long long mine = first < n ? (n - first + step - 1) / step : 0;
+  const int ahead = stages > 2 ? stages - 2 : 1;
+  int s_load = 0, s_store = 0;
+  unsigned phase = 0;
+  DevFanTile nxt;
+  if (mine) load_desc(tiles + first, nxt);
+  auto issue_load = [&](unsigned long long i) {
+    const DevFanTile t = nxt;
+    if (i + 1 < mine) load_desc(tiles + first + (i + 1) * step, nxt);
+    const unsigned bar = smem_u32(&bars[s_load]);
+    const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
+    if (lane == 0) {
+      sdesc[s_load] = t;
+      mbar_expect_tx(bar, t.rows * t.row_bytes);
+    }
+    __syncwarp();
+    for (unsigned r = lane; r < t.rows; r += 32)
+      bulk_g2s(base + r * t.row_bytes, reinterpret_cast<const char*>(t.src) + r * t.src_pitch, t.row_bytes, bar);
+    if (++s_load == stages) s_load = 0;
+  };
+  for (unsigned long long i = 0; i < mine && i < (unsigned long long)ahead; ++i) issue_load(i);
+  for (unsigned long long i = 0; i < mine; ++i) {
+    if (i + ahead < mine) {
+      bulk_wait_read<1>();  // this lane's older store groups have read their stage
+      __syncwarp();         // ... and so have every other lane's
+      issue_load(i + ahead);
+    }
+    mbar_wait(smem_u32(&bars[s_store]), phase);
+    const DevFanTile& t = sdesc[s_store];
+    const unsigned base = smem_u32(smem + size_t(s_store) * stage_bytes);
+    for (unsigned d = 0; d < t.n_dst; ++d)
+      for (unsigned r = lane; r < t.rows; r += 32)
+        bulk_s2g(reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d], base + r * t.row_bytes, t.row_bytes);
+    bulk_commit();
+    if (++s_store == stages) s_store = 0, phase ^= 1u;
+  }
+  bulk_wait_all();
+}
+
 // ---- synthetic payload ------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -433,10 +488,12 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
   if (n_tiles == 0) return;
   if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
-  const bool strided = cfg.kernel == CopyKernel::BulkStrided;
+  const bool strided = cfg.kernel == CopyKernel::BulkStrided || cfg.kernel == CopyKernel::BulkWarp;
   const size_t smem = size_t(cfg.stages) * cfg.stage_bytes + (strided ? 0 : kDescRingBytes);
   if (smem > 227 * 1024) raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
-  auto kern = strided ? copy_bulk_strided_kernel : copy_bulk_kernel;
+  auto kern = cfg.kernel == CopyKernel::BulkWarp ? copy_bulk_warp_kernel
+              : strided                          ? copy_bulk_strided_kernel
+                                                 : copy_bulk_kernel;
   check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "bulk smem attribute");
   const int grid = bulk_grid(n_tiles, sms, cfg);
   kern<<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles,

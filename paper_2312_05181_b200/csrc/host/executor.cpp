@@ -101,7 +101,9 @@ CopyConfig CopyConfig::from_env() {
     else if (s == "ldg8") c.kernel = CopyKernel::Ldg8;
     else if (s == "bulk") c.kernel = CopyKernel::Bulk;
     else if (s == "bulk_strided") c.kernel = CopyKernel::BulkStrided;
-    else if (!s.empty()) raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8 or bulk");
+    else if (s == "bulk_warp") c.kernel = CopyKernel::BulkWarp;
+    else if (!s.empty())
+      raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8, bulk, bulk_strided or bulk_warp");
   }
   c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", is_bulk(c.kernel) ? 1 : 3));
   c.stages = env_int("RESHARD_BULK_STAGES", c.stages);

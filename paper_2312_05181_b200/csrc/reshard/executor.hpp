@@ -50,8 +50,10 @@ static_assert(sizeof(FanTile) == 96, "FanTile layout");
 // (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
 // Defaults from the round-1 B200 sweep (profiles/r02_sweep.json): TMA bulk, 1 CTA/SM,
 // 8 stages x 24 KiB reached 6.59 TB/s on GPT-3 1.3B vs 6.17 TB/s for LDG/STG at 3 CTAs/SM.
-enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2, BulkStrided = 3 };
-inline bool is_bulk(CopyKernel k) { return k == CopyKernel::Bulk || k == CopyKernel::BulkStrided; }
+enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2, BulkStrided = 3, BulkWarp = 4 };
+inline bool is_bulk(CopyKernel k) {
+  return k == CopyKernel::Bulk || k == CopyKernel::BulkStrided || k == CopyKernel::BulkWarp;
+}
 struct CopyConfig {
   CopyKernel kernel = CopyKernel::BulkStrided;  // r08 same-box A/B: 3-4% faster than Bulk
   int ctas_per_sm = 1;
@@ -163,7 +165,6 @@ class Executor {
   uint32_t t_begin_, t_end_;
   std::vector<uint64_t> src_size_, dst_size_;
   std::vector<CellBinding> src_bind_, dst_bind_;
-  std::vector<std::vector<size_t>> src_index_;  // [from dev][(t, cell) hosted order] -> src_bind_ index
   std::vector<std::vector<Logical>> logical_;   // per executing (source) world GPU
   std::vector<void*> src_base_, dst_base_;
   std::vector<std::unique_ptr<Local>> local_;   // per local GPU: device tiles, events
