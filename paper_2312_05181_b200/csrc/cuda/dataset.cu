@@ -192,10 +192,143 @@ __global__ void __launch_bounds__(kThreads, 3) repartition_kernel(Params p, Outs
   }
 }
 
+// ---- K5 split variant: gather / scan / finalize -------------------------------------------
+// r05 profile: 27% of the single-pass kernel's stall samples sit behind the block barrier
+// that waits for the decoupled look-back.  The split variant never waits: (a) a pure
+// gather kernel writes pos / entry, parks each sample's length in boff and its class in a
+// byte array, and reduces one aggregate per tile; (b) one CTA scans the tile aggregates;
+// (c) a streaming kernel turns lengths into offsets and fills the locator queues.  Extra
+// traffic: 9 bytes per sample written and read back (~5% of the gather's DRAM bytes).
+__device__ __forceinline__ Agg block_exclusive(const Agg& mine, Agg* warp_tot, Agg& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Agg inc = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Agg up = shfl_up(inc, d);
+    if (lane >= d) inc = inc + up;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  Agg base{0, 0, 0, 0};
+  total = Agg{0, 0, 0, 0};
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) base = base + warp_tot[w];
+    total = total + warp_tot[w];
+  }
+  return base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
+}
+
+__global__ void __launch_bounds__(kThreads) repart_gather_kernel(Params p, Outs o, Agg* agg, unsigned char* cls_out) {
+  __shared__ Agg warp_tot[kWarps];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * kTile + (unsigned long long)threadIdx.x * kItems;
+  unsigned long long batch = 0, r = 0;
+  if (k0 < p.in_full) batch = p.at_step + k0 / p.b, r = k0 % p.b;
+  unsigned long long pos[kItems], idx[kItems], f[kItems], off[kItems], len[kItems];
+  const unsigned nv = p.count > k0 ? unsigned(min(p.count - k0, (unsigned long long)kItems)) : 0u;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long k = k0 + j;
+    if (k < p.in_full) {
+      pos[j] = batch * p.B + p.rank * p.b + r;
+      if (++r == p.b) r = 0, ++batch;
+    } else {
+      pos[j] = p.full * p.B + p.rank * p.b + (k - p.in_full);
+    }
+    idx[j] = j < nv ? __ldg(p.perm + pos[j]) : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long* e = p.samples + 3 * idx[j];
+    if (j < nv) f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
+    else f[j] = 0, off[j] = 0, len[j] = 0;
+  }
+  Agg mine{0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (j >= nv) continue;
+    const unsigned long long k = k0 + j;
+    const unsigned char c = __ldg(p.file_class + f[j]);
+    o.pos[k] = pos[j];
+    o.ent[3 * k] = f[j], o.ent[3 * k + 1] = off[j], o.ent[3 * k + 2] = len[j];
+    o.boff[k] = len[j];  // parked; finalize turns it into the offset
+    cls_out[k] = c;
+    mine.len += len[j];
+    mine.c0 += c == 0, mine.c1 += c == 1, mine.c2 += c == 2;
+  }
+  Agg total;
+  block_exclusive(mine, warp_tot, total);
+  if (threadIdx.x == 0) agg[blockIdx.x] = total;
+}
+
+// One CTA: exclusive scan of the tile aggregates, and the queue totals.
+__global__ void __launch_bounds__(1024) repart_scan_kernel(const Agg* agg, Agg* prefix, unsigned ntiles, Outs o) {
+  __shared__ Agg warp_tot[32];
+  const unsigned per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const unsigned t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
+  Agg mine{0, 0, 0, 0};
+  for (unsigned t = t0; t < t1; ++t) mine = mine + agg[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Agg inc = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Agg up = shfl_up(inc, d);
+    if (lane >= d) inc = inc + up;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  Agg base{0, 0, 0, 0}, total{0, 0, 0, 0};
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+    if (w < warp) base = base + warp_tot[w];
+    total = total + warp_tot[w];
+  }
+  Agg run = base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
+  for (unsigned t = t0; t < t1; ++t) {
+    prefix[t] = run;
+    run = run + agg[t];
+  }
+  if (threadIdx.x == 0) o.qcount[0] = total.c0, o.qcount[1] = total.c1, o.qcount[2] = total.c2;
+}
+
+__global__ void __launch_bounds__(kThreads) repart_finalize_kernel(Params p, Outs o, const Agg* prefix,
+                                                                   const unsigned char* cls_in) {
+  __shared__ Agg warp_tot[kWarps];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * kTile + (unsigned long long)threadIdx.x * kItems;
+  unsigned long long len[kItems];
+  unsigned char cls[kItems];
+  Agg mine{0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long k = k0 + j;
+    len[j] = k < p.count ? o.boff[k] : 0ull;
+    cls[j] = k < p.count ? cls_in[k] : (unsigned char)3;
+    mine.len += len[j];
+    mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
+  }
+  Agg total;
+  const Agg excl = block_exclusive(mine, warp_tot, total);
+  Agg run = prefix[blockIdx.x] + excl;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const unsigned long long k = k0 + j;
+    if (k >= p.count) break;
+    o.boff[k] = run.len;
+    run.len += len[j];
+    if (cls[j] == 0) o.q0[run.c0++] = unsigned(k);
+    else if (cls[j] == 1) o.q1[run.c1++] = unsigned(k);
+    else o.q2[run.c2++] = unsigned(k);
+  }
+}
+
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
+
+bool k5_split() {
+  const char* v = std::getenv("RESHARD_K5");
+  return !(v && std::string(v) == "lookback");
+}
 
 // The dataset kernels are random 8- and 24-byte gathers: with the default L2 fetch
 // granularity every miss pulls a full 128-byte line from HBM (measured 154 DRAM bytes per
@@ -344,7 +477,8 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
 
 uint64_t repartition_scratch_bytes(uint64_t count) {
   const uint64_t tiles = (count + kTile - 1) / kTile;
-  return 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg));
+  // look-back: counter + flags + aggregates + inclusive prefixes; split: + class bytes
+  return 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)) + align256(count);
 }
 
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
@@ -368,9 +502,16 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
            at_step, b, rank, count, full > at_step ? (full - at_step) * b : 0, full};
   Outs o{reinterpret_cast<ull*>(out.pos), reinterpret_cast<ull*>(out.ent), reinterpret_cast<ull*>(out.boff),
          out.queue[0], out.queue[1], out.queue[2], reinterpret_cast<ull*>(out.qcount)};
-  ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
+  const bool split = k5_split();
+  if (!split) ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
   ck(cudaEventRecord(e0, st), "event");
-  if (tiles) {
+  if (tiles && split) {
+    auto* cls = reinterpret_cast<unsigned char*>(sc + 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)));
+    repart_gather_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.agg, cls);
+    repart_scan_kernel<<<1, 1024, 0, st>>>(s.agg, s.inc, unsigned(tiles), o);
+    repart_finalize_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
+    ck(cudaGetLastError(), "repartition launch");
+  } else if (tiles) {
     repartition_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
     ck(cudaGetLastError(), "repartition launch");
   } else {
@@ -384,7 +525,7 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   cudaEventDestroy(e1);
   t.tiles = tiles;
   t.bytes = count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
-  t.launches = tiles ? 1 : 0;
+  t.launches = tiles ? (split ? 3 : 1) : 0;
   return t;
 }
 

@@ -103,7 +103,9 @@ def test_acceptance8_exactly_once_under_dp_changes(rs):
 
 
 @pytest.mark.gpu
-def test_k5_kernel_matches_oracle(rs, orc, ctx):
+@pytest.mark.parametrize("mode", ["split", "lookback"])
+def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, monkeypatch):
+    monkeypatch.setenv("RESHARD_K5", mode)
     rng = random.Random(42)
     for n, nf, B, at, dp in [(50_000, 13, 64, 100, 4), (12_345, 5, 40, 7, 8), (4096, 3, 16, 256, 2),
                              (4096, 3, 16, 0, 1), (300_017, 29, 128, 500, 4)]:
@@ -126,7 +128,7 @@ def test_k5_kernel_matches_oracle(rs, orc, ctx):
             assert np.array_equal(got["boff"], want["boff"])
             assert got["qcount"] == want["qcount"]
             assert np.array_equal(got["qidx"], want["qidx"])
-            assert t["launches"] == (1 if cnt else 0)
+            assert (t["launches"] > 0) == (cnt > 0)
             part.free()
             ctx.free(0, d_fc)
         ctx.free(0, d_perm)
