@@ -122,6 +122,18 @@ int rs_grid_cells(int rank, const uint64_t* shape, const int32_t* npts, const ui
 int rs_grid_refine(int rank_a, const int32_t* npts_a, const uint64_t* pts_a, int rank_b, const int32_t* npts_b,
                    const uint64_t* pts_b, int32_t* npts_out, uint64_t* pts_out);
 int rs_even_split(int rank, const uint64_t* shape, int dim, uint64_t ways, int32_t* npts_out, uint64_t* pts_out);
+/* SplitGrid::cell / cell_index_of (split_grid.hpp:40-44, split_grid.cpp:88-117) */
+int rs_grid_cell(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts, uint64_t index,
+                 rs_range* out);
+int rs_grid_cell_index_of(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts,
+                          const rs_range* r, uint64_t* index);
+/* Range::offset_by / valid_for (range.hpp:45-52, range.cpp:49-90) */
+int rs_range_offset_by(const rs_range* r, const rs_range* outer, rs_range* out);
+int rs_range_valid_for(const rs_range* r, int rank, const uint64_t* shape, int32_t* ok);
+/* RangeSpec::parse + resolve (range.hpp:70-91, range.cpp:146-193): "[:,2:4]" -> box in shape */
+int rs_rangespec_resolve(const char* spec, int rank, const uint64_t* shape, rs_range* out);
+/* dtype_from_name (dtype.hpp:31, dtype.cpp:17-23) plus "bf16"/"BF16" */
+int rs_dtype_from_name(const char* name, int32_t* code);
 
 /* ---- device runtime -------------------------------------------------------------------- */
 int rs_device_count(int* n);

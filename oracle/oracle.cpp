@@ -302,6 +302,59 @@ static std::vector<std::vector<uint64_t>> even_split(const Shape& s, size_t dim,
   for (uint64_t k = 1; k < ways; ++k) g[dim].push_back(k * (s[dim] / ways));
   return g;
 }
+static std::vector<Iv> intervals_of(const std::vector<uint64_t>& pts, uint64_t extent) {
+  std::vector<Iv> v;
+  uint64_t lo = 0;
+  for (auto p : pts) v.push_back({lo, p}), lo = p;
+  v.push_back({lo, extent});
+  return v;
+}
+// SplitGrid::cell (split_grid.cpp:88-101)
+static Box grid_cell(const std::vector<std::vector<uint64_t>>& g, const Shape& s, uint64_t index) {
+  grid_check(g, s);
+  Box b(g.size());
+  uint64_t rest = index;
+  for (size_t d = g.size(); d-- > 0;) {
+    auto iv = intervals_of(g[d], s[d]);
+    b[d] = iv[rest % iv.size()];
+    rest /= iv.size();
+  }
+  if (rest != 0) fail(IndexOutOfRange, "cell index out of range");
+  return b;
+}
+// SplitGrid::cell_index_of (split_grid.cpp:103-117)
+static uint64_t grid_cell_index_of(const std::vector<std::vector<uint64_t>>& g, const Shape& s, const Box& r) {
+  grid_check(g, s);
+  check_box(r, s);
+  uint64_t idx = 0;
+  for (size_t d = 0; d < g.size(); ++d) {
+    auto iv = intervals_of(g[d], s[d]);
+    size_t i = 0;
+    while (i < iv.size() && iv[i].hi <= r[d].lo) ++i;
+    if (i == iv.size() || r[d].lo < iv[i].lo || r[d].hi > iv[i].hi) fail(InvalidSplitPoint, "range crosses a grid boundary");
+    idx = idx * iv.size() + i;
+  }
+  return idx;
+}
+// Range::offset_by (range.cpp:80-90)
+static Box offset_by(const Box& in, const Box& outer) {
+  if (in.size() != outer.size()) fail(RankMismatch, "offset_by rank mismatch");
+  Box r(in.size());
+  for (size_t i = 0; i < in.size(); ++i) {
+    if (in[i].hi + outer[i].lo > outer[i].hi) fail(RangeOutOfBounds, "range exceeds outer");
+    r[i] = {in[i].lo + outer[i].lo, in[i].hi + outer[i].lo};
+  }
+  return r;
+}
+// RangeSpec::resolve (range.cpp:153-164); unconstrained dims are lo = hi = UINT64_MAX
+static Box spec_resolve(const Box& spec, const Shape& s) {
+  if (spec.size() != s.size()) fail(RankMismatch, "range spec rank mismatch");
+  Box r(spec.size());
+  for (size_t i = 0; i < spec.size(); ++i)
+    r[i] = (spec[i].lo == UINT64_MAX && spec[i].hi == UINT64_MAX) ? Iv{0, s[i]} : spec[i];
+  check_box(r, s);
+  return r;
+}
 
 #else  // ---- reference tensor-core (compiled from /root/reference by oracle/Makefile) ----
 
@@ -356,6 +409,24 @@ static std::vector<std::vector<uint64_t>> grid_refine(const std::vector<std::vec
 }
 static std::vector<std::vector<uint64_t>> even_split(const Shape& s, size_t dim, uint64_t ways) {
   return guarded([&] { return reshard::SplitGrid::even_split(s, dim, ways).points(); });
+}
+static Box grid_cell(const std::vector<std::vector<uint64_t>>& g, const Shape& s, uint64_t index) {
+  return guarded([&] { return from_ref(reshard::SplitGrid(g).cell(s, index)); });
+}
+static uint64_t grid_cell_index_of(const std::vector<std::vector<uint64_t>>& g, const Shape& s, const Box& r) {
+  return guarded([&] { return reshard::SplitGrid(g).cell_index_of(s, to_ref(r)); });
+}
+static Box offset_by(const Box& in, const Box& outer) {
+  return guarded([&] { return from_ref(to_ref(in).offset_by(to_ref(outer))); });
+}
+static Box spec_resolve(const Box& spec, const Shape& s) {
+  return guarded([&] {
+    std::vector<std::optional<reshard::Interval>> v;
+    for (auto& i : spec)
+      v.push_back(i.lo == UINT64_MAX && i.hi == UINT64_MAX ? std::optional<reshard::Interval>{}
+                                                           : std::optional<reshard::Interval>{reshard::Interval{i.lo, i.hi}});
+    return from_ref(reshard::RangeSpec(v).resolve(s));
+  });
 }
 static void grid_check(const std::vector<std::vector<uint64_t>>& g, const Shape& s) {
   guarded([&] {
@@ -1063,6 +1134,35 @@ int orc_grid_refine(int rank_a, const int* na, const uint64_t* pa, int rank_b, c
       n_out[d] = int(g[d].size());
       for (auto p : g[d]) pts_out[k++] = p;
     }
+  });
+}
+
+int orc_grid_cell(int rank, const uint64_t* shape, const int* npts, const uint64_t* pts, uint64_t index, uint64_t* lo,
+                  uint64_t* hi) {
+  return guard([&] {
+    Box b = core::grid_cell(grid_from(rank, npts, pts), shape_from(rank, shape), index);
+    for (size_t d = 0; d < b.size(); ++d) lo[d] = b[d].lo, hi[d] = b[d].hi;
+  });
+}
+int orc_grid_cell_index_of(int rank, const uint64_t* shape, const int* npts, const uint64_t* pts, int rrank,
+                           const uint64_t* lo, const uint64_t* hi, uint64_t* index) {
+  return guard([&] {
+    *index = core::grid_cell_index_of(grid_from(rank, npts, pts), shape_from(rank, shape), box_from(rrank, lo, hi));
+  });
+}
+int orc_offset_by(int rank, const uint64_t* lo, const uint64_t* hi, int orank, const uint64_t* olo, const uint64_t* ohi,
+                  uint64_t* out_lo, uint64_t* out_hi) {
+  return guard([&] {
+    Box b = core::offset_by(box_from(rank, lo, hi), box_from(orank, olo, ohi));
+    for (size_t d = 0; d < b.size(); ++d) out_lo[d] = b[d].lo, out_hi[d] = b[d].hi;
+  });
+}
+// spec dims with lo = hi = UINT64_MAX are unconstrained
+int orc_spec_resolve(int rank, const uint64_t* lo, const uint64_t* hi, int srank, const uint64_t* shape, uint64_t* out_lo,
+                     uint64_t* out_hi) {
+  return guard([&] {
+    Box b = core::spec_resolve(box_from(rank, lo, hi), shape_from(srank, shape));
+    for (size_t d = 0; d < b.size(); ++d) out_lo[d] = b[d].lo, out_hi[d] = b[d].hi;
   });
 }
 

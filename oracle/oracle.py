@@ -471,3 +471,55 @@ class State(_Handle):
                                               hi.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p),
                                               C.c_uint64(nb.value), C.byref(nb)))
         return out[: nb.value]
+
+
+def _grid_args(shape, points):
+    sh = np.array(list(shape) + [0], np.uint64)
+    npts = np.array([len(p) for p in points] + [0], np.int32)
+    pts = np.array([x for p in points for x in p] + [0], np.uint64)
+    return sh, npts, pts
+
+
+def _vp(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _oracle_grid_cell(self, shape, points, index):
+    sh, npts, pts = _grid_args(shape, points)
+    lo, hi = np.zeros(MAXR, np.uint64), np.zeros(MAXR, np.uint64)
+    self._chk(self.lib.orc_grid_cell(C.c_int(len(shape)), _vp(sh), _vp(npts), _vp(pts), C.c_uint64(index), _vp(lo), _vp(hi)))
+    return [(int(lo[d]), int(hi[d])) for d in range(len(shape))]
+
+
+def _oracle_grid_cell_index_of(self, shape, points, box):
+    sh, npts, pts = _grid_args(shape, points)
+    lo, hi = _box_arrays([box])
+    out = C.c_uint64()
+    self._chk(self.lib.orc_grid_cell_index_of(C.c_int(len(shape)), _vp(sh), _vp(npts), _vp(pts), C.c_int(len(box)),
+                                              _vp(lo), _vp(hi), C.byref(out)))
+    return out.value
+
+
+def _oracle_offset_by(self, box, outer):
+    lo, hi = _box_arrays([box])
+    olo, ohi = _box_arrays([outer])
+    rl, rh = np.zeros(MAXR, np.uint64), np.zeros(MAXR, np.uint64)
+    self._chk(self.lib.orc_offset_by(C.c_int(len(box)), _vp(lo), _vp(hi), C.c_int(len(outer)), _vp(olo), _vp(ohi),
+                                     _vp(rl), _vp(rh)))
+    return [(int(rl[d]), int(rh[d])) for d in range(len(box))]
+
+
+def _oracle_spec_resolve(self, spec, shape):
+    M = (1 << 64) - 1
+    box = [(M, M) if s is None else s for s in spec]
+    lo, hi = _box_arrays([box])
+    sh = np.array(list(shape) + [0], np.uint64)
+    rl, rh = np.zeros(MAXR, np.uint64), np.zeros(MAXR, np.uint64)
+    self._chk(self.lib.orc_spec_resolve(C.c_int(len(spec)), _vp(lo), _vp(hi), C.c_int(len(shape)), _vp(sh), _vp(rl), _vp(rh)))
+    return [(int(rl[d]), int(rh[d])) for d in range(len(spec))]
+
+
+Oracle.grid_cell = _oracle_grid_cell
+Oracle.grid_cell_index_of = _oracle_grid_cell_index_of
+Oracle.offset_by = _oracle_offset_by
+Oracle.spec_resolve = _oracle_spec_resolve

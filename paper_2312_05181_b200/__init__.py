@@ -143,6 +143,48 @@ def even_split(shape, dim, ways):
     return _grid_out(len(shape), npts, pts)
 
 
+def grid_cell(shape, points, index):
+    """SplitGrid::cell (split_grid.cpp:88-101): the index-th cell, last dim fastest."""
+    r = rs_range()
+    _chk(lib.rs_grid_cell(len(shape), _u64(shape), _i32(len(p) for p in points), _u64(x for p in points for x in p),
+                          int(index), C.byref(r)))
+    return _box(r)
+
+
+def grid_cell_index_of(shape, points, box):
+    """SplitGrid::cell_index_of (split_grid.cpp:103-117): index of the cell holding `box`."""
+    idx = C.c_uint64()
+    _chk(lib.rs_grid_cell_index_of(len(shape), _u64(shape), _i32(len(p) for p in points),
+                                   _u64(x for p in points for x in p), C.byref(_range(box)), C.byref(idx)))
+    return idx.value
+
+
+def range_offset_by(box, outer):
+    """Range::offset_by (range.cpp:80-90): box given relative to `outer`, made absolute."""
+    r = rs_range()
+    _chk(lib.rs_range_offset_by(C.byref(_range(box)), C.byref(_range(outer)), C.byref(r)))
+    return _box(r)
+
+
+def range_valid_for(box, shape) -> bool:
+    ok = C.c_int32()
+    _chk(lib.rs_range_valid_for(C.byref(_range(box)), len(shape), _u64(shape), C.byref(ok)))
+    return bool(ok.value)
+
+
+def rangespec_resolve(spec: str, shape):
+    """RangeSpec::parse(spec).resolve(shape) (range.cpp:153-193): ':' binds the full extent."""
+    r = rs_range()
+    _chk(lib.rs_rangespec_resolve(spec.encode(), len(shape), _u64(shape), C.byref(r)))
+    return _box(r)
+
+
+def dtype_from_name(name: str) -> int:
+    code = C.c_int32()
+    _chk(lib.rs_dtype_from_name(name.encode(), C.byref(code)))
+    return code.value
+
+
 # ---- device runtime ------------------------------------------------------------------------
 def device_count() -> int:
     n = C.c_int()

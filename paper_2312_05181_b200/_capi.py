@@ -67,6 +67,12 @@ SIGNATURES = {
     "rs_grid_cells": (C.c_int, [C.c_int, U64P, I32P, U64P, C.c_int, C.POINTER(rs_range), C.POINTER(C.c_int)]),
     "rs_grid_refine": (C.c_int, [C.c_int, I32P, U64P, C.c_int, I32P, U64P, I32P, U64P]),
     "rs_even_split": (C.c_int, [C.c_int, U64P, C.c_int, C.c_uint64, I32P, U64P]),
+    "rs_grid_cell": (C.c_int, [C.c_int, U64P, I32P, U64P, C.c_uint64, C.POINTER(rs_range)]),
+    "rs_grid_cell_index_of": (C.c_int, [C.c_int, U64P, I32P, U64P, C.POINTER(rs_range), U64P]),
+    "rs_range_offset_by": (C.c_int, [C.POINTER(rs_range), C.POINTER(rs_range), C.POINTER(rs_range)]),
+    "rs_range_valid_for": (C.c_int, [C.POINTER(rs_range), C.c_int, U64P, I32P]),
+    "rs_rangespec_resolve": (C.c_int, [C.c_char_p, C.c_int, U64P, C.POINTER(rs_range)]),
+    "rs_dtype_from_name": (C.c_int, [C.c_char_p, I32P]),
     "rs_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "rs_init": (C.c_int, [C.c_int, C.c_int, I32P, I32P, C.POINTER(P)]),
     "rs_destroy": (None, [P]),

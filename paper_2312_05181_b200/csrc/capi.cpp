@@ -146,6 +146,44 @@ int rs_even_split(int rank, const uint64_t* shape, int dim, uint64_t ways, int32
     from_grid(SplitGrid::even_split(to_shape(rank, shape), size_t(dim), ways), nout, pout);
   });
 }
+int rs_grid_cell(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts, uint64_t index,
+                 rs_range* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = from_range(to_grid(rank, npts, pts).cell(to_shape(rank, shape), index));
+  });
+}
+int rs_grid_cell_index_of(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts,
+                          const rs_range* r, uint64_t* index) {
+  return guard([&] {
+    need(r, "range"), need(index, "index");
+    *index = to_grid(rank, npts, pts).cell_index_of(to_shape(rank, shape), to_range(*r));
+  });
+}
+int rs_range_offset_by(const rs_range* r, const rs_range* outer, rs_range* out) {
+  return guard([&] {
+    need(r, "range"), need(outer, "outer"), need(out, "out");
+    *out = from_range(to_range(*r).offset_by(to_range(*outer)));
+  });
+}
+int rs_range_valid_for(const rs_range* r, int rank, const uint64_t* shape, int32_t* ok) {
+  return guard([&] {
+    need(r, "range"), need(ok, "ok");
+    *ok = to_range(*r).valid_for(to_shape(rank, shape)) ? 1 : 0;
+  });
+}
+int rs_rangespec_resolve(const char* spec, int rank, const uint64_t* shape, rs_range* out) {
+  return guard([&] {
+    need(spec, "spec"), need(out, "out");
+    *out = from_range(RangeSpec::parse(spec).resolve(to_shape(rank, shape)));
+  });
+}
+int rs_dtype_from_name(const char* name, int32_t* code) {
+  return guard([&] {
+    need(name, "name"), need(code, "code");
+    *code = int32_t(dtype_from_name(name));
+  });
+}
 
 // ---- device runtime ------------------------------------------------------------------------
 int rs_device_count(int* n) {

@@ -35,6 +35,14 @@ Dtype dtype_from_code(int code) {
   if (code < 0 || code > 4) raise(Errc::InvalidTensor, "unknown dtype code " + std::to_string(code));
   return static_cast<Dtype>(code);
 }
+Dtype dtype_from_name(std::string_view name) {
+  static constexpr std::pair<const char*, Dtype> names[] = {
+      {"f32", Dtype::F32}, {"F32", Dtype::F32}, {"f16", Dtype::F16}, {"F16", Dtype::F16},   {"i64", Dtype::I64},
+      {"I64", Dtype::I64}, {"u8", Dtype::U8},   {"U8", Dtype::U8},   {"bf16", Dtype::BF16}, {"BF16", Dtype::BF16}};
+  for (auto& [n, d] : names)
+    if (name == n) return d;
+  raise(Errc::MalformedConfig, "unknown dtype '" + std::string(name) + "'");
+}
 const char* dtype_name(Dtype d) {
   static constexpr const char* n[] = {"f32", "f16", "i64", "u8", "bf16"};
   auto i = static_cast<unsigned>(d);
@@ -129,21 +137,84 @@ static uint64_t parse_u64(std::string_view t) {
   if (ec != std::errc() || p != t.data() + t.size()) raise(Errc::MalformedFrame, "bad integer '" + std::string(t) + "'");
   return v;
 }
-Range Range::parse(std::string_view text) {
+// Calls f(item) for every comma-separated item between the brackets; "[]" has none.
+template <class F>
+static void for_each_bracket_item(std::string_view text, F&& f) {
   if (text.size() < 2 || text.front() != '[' || text.back() != ']')
     raise(Errc::MalformedFrame, "range must be bracketed: '" + std::string(text) + "'");
   std::string_view body = text.substr(1, text.size() - 2);
-  std::vector<Interval> dims;
-  while (!body.empty() || !dims.empty()) {
+  if (body.empty()) return;
+  for (;;) {
     size_t comma = body.find(',');
-    std::string_view item = body.substr(0, comma);
-    size_t colon = item.find(':');
-    if (colon == std::string_view::npos) raise(Errc::MalformedFrame, "interval needs ':' in '" + std::string(item) + "'");
-    dims.push_back({parse_u64(item.substr(0, colon)), parse_u64(item.substr(colon + 1))});
-    if (comma == std::string_view::npos) break;
+    f(body.substr(0, comma));
+    if (comma == std::string_view::npos) return;
     body = body.substr(comma + 1);
   }
+}
+static Interval parse_interval(std::string_view item) {
+  size_t colon = item.find(':');
+  if (colon == std::string_view::npos) raise(Errc::MalformedFrame, "interval needs ':' in '" + std::string(item) + "'");
+  return {parse_u64(item.substr(0, colon)), parse_u64(item.substr(colon + 1))};
+}
+Range Range::parse(std::string_view text) {
+  std::vector<Interval> dims;
+  for_each_bracket_item(text, [&](std::string_view item) { dims.push_back(parse_interval(item)); });
   return Range(dims);
+}
+bool Range::valid_for(const Shape& s) const {
+  if (size_t(rank_) != s.size()) return false;
+  for (int i = 0; i < rank_; ++i)
+    if (!(d_[i].lo < d_[i].hi && d_[i].hi <= s[size_t(i)])) return false;
+  return true;
+}
+Range Range::offset_by(const Range& outer) const {
+  if (rank_ != outer.rank_) raise(Errc::RankMismatch, "offset_by rank mismatch");
+  Range r = *this;
+  for (int i = 0; i < rank_; ++i) {
+    if (d_[i].hi + outer.d_[i].lo > outer.d_[i].hi)
+      raise(Errc::RangeOutOfBounds, "range " + to_string() + " exceeds " + outer.to_string());
+    r.d_[i].lo += outer.d_[i].lo;
+    r.d_[i].hi += outer.d_[i].lo;
+  }
+  return r;
+}
+
+// ---- RangeSpec -------------------------------------------------------------------------
+RangeSpec RangeSpec::from_range(const Range& r) {
+  std::vector<std::optional<Interval>> dims;
+  for (int i = 0; i < r.rank(); ++i) dims.emplace_back(r.dim(i));
+  return RangeSpec(std::move(dims));
+}
+Range RangeSpec::resolve(const Shape& s) const {
+  if (dims_.size() != s.size())
+    raise(Errc::RankMismatch, "range spec rank " + std::to_string(dims_.size()) + " vs tensor rank " + std::to_string(s.size()));
+  std::vector<Interval> dims;
+  for (size_t i = 0; i < dims_.size(); ++i) dims.push_back(dims_[i] ? *dims_[i] : Interval{0, s[i]});
+  Range r(dims);
+  r.check_against(s);
+  return r;
+}
+std::string RangeSpec::to_string() const {
+  std::string s(1, '[');
+  for (size_t i = 0; i < dims_.size(); ++i) {
+    if (i) s.push_back(',');
+    if (dims_[i])
+      s += std::to_string(dims_[i]->lo) + ":" + std::to_string(dims_[i]->hi);
+    else
+      s.push_back(':');
+  }
+  s.push_back(']');
+  return s;
+}
+RangeSpec RangeSpec::parse(std::string_view text) {
+  std::vector<std::optional<Interval>> dims;
+  for_each_bracket_item(text, [&](std::string_view item) {
+    if (item == ":")
+      dims.emplace_back(std::nullopt);
+    else
+      dims.emplace_back(parse_interval(item));
+  });
+  return RangeSpec(std::move(dims));
 }
 
 // ---- SplitGrid -------------------------------------------------------------------------
@@ -188,6 +259,39 @@ std::vector<Range> SplitGrid::cells(const Shape& s) const {
   }
   return out;
 }
+bool SplitGrid::valid_for(const Shape& s) const {
+  try {
+    check_against(s);
+    return true;
+  } catch (const Error&) {
+    return false;
+  }
+}
+Range SplitGrid::cell(const Shape& s, uint64_t index) const {
+  check_against(s);
+  std::vector<Interval> dims(pts_.size());
+  uint64_t rest = index;
+  for (size_t d = pts_.size(); d-- > 0;) {
+    const uint64_t m = pts_[d].size() + 1, i = rest % m;
+    rest /= m;
+    dims[d] = {i ? pts_[d][i - 1] : 0, i < pts_[d].size() ? pts_[d][i] : s[d]};
+  }
+  if (rest != 0) raise(Errc::IndexOutOfRange, "cell index " + std::to_string(index) + " out of range");
+  return Range(dims);
+}
+uint64_t SplitGrid::cell_index_of(const Shape& s, const Range& r) const {
+  check_against(s);
+  r.check_against(s);
+  uint64_t index = 0;
+  for (size_t d = 0; d < pts_.size(); ++d) {
+    const Interval& v = r.dim(int(d));
+    const size_t i = interval_of(d, v.lo);
+    const uint64_t hi = i < pts_[d].size() ? pts_[d][i] : s[d];
+    if (v.hi > hi) raise(Errc::InvalidSplitPoint, "range " + r.to_string() + " crosses a grid boundary");
+    index = index * (pts_[d].size() + 1) + i;
+  }
+  return index;
+}
 size_t SplitGrid::interval_of(size_t dim, uint64_t x) const {
   const auto& p = pts_[dim];
   return size_t(std::upper_bound(p.begin(), p.end(), x) - p.begin());
@@ -204,12 +308,17 @@ SplitGrid grid_refine(const SplitGrid& a, const SplitGrid& b) {
   return SplitGrid(std::move(p));
 }
 
-uint64_t fnv1a64(const void* data, size_t n) {
+Fnv1a64& Fnv1a64::update(const void* data, size_t n) {
   const auto* p = static_cast<const uint8_t*>(data);
-  uint64_t h = 0xcbf29ce484222325ull;
-  for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
-  return h;
+  for (size_t i = 0; i < n; ++i) h_ = (h_ ^ p[i]) * 0x100000001b3ull;
+  return *this;
 }
+Fnv1a64& Fnv1a64::update_u64(uint64_t v) {
+  uint8_t le[8];
+  for (int i = 0; i < 8; ++i) le[i] = uint8_t(v >> (8 * i));
+  return update(le, 8);
+}
+uint64_t fnv1a64(const void* data, size_t n) { return Fnv1a64().update(data, n).digest(); }
 uint64_t payload_seed(std::string_view path) { return fnv1a64(path.data(), path.size()) ^ 0x7E9B1E0Cull; }
 
 }  // namespace reshard

@@ -11,6 +11,7 @@
 
 #include <array>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -53,6 +54,7 @@ class Error : public std::runtime_error {
 enum class Dtype : uint8_t { F32 = 0, F16 = 1, I64 = 2, U8 = 3, BF16 = 4 };
 size_t dtype_width(Dtype d);          // InvalidTensor for unknown codes
 Dtype dtype_from_code(int code);      // InvalidTensor for unknown codes
+Dtype dtype_from_name(std::string_view name);  // "f32"/"F32", ... "bf16"; MalformedConfig otherwise
 const char* dtype_name(Dtype d);
 
 // ---- boxes ---------------------------------------------------------------------------
@@ -81,9 +83,11 @@ class Range {
   uint64_t elements() const;
 
   void check_against(const Shape& s) const;  // RankMismatch / RangeOutOfBounds
+  bool valid_for(const Shape& s) const;
   bool contains(const Range& o) const;
   bool overlaps(const Range& o) const;
   Range rebase_into(const Range& outer) const;  // RangeOutOfBounds unless outer.contains(*this)
+  Range offset_by(const Range& outer) const;    // inverse of rebase_into; RankMismatch / RangeOutOfBounds
   std::string to_string() const;
   static Range parse(std::string_view text);  // MalformedFrame
 
@@ -93,6 +97,23 @@ class Range {
  private:
   int rank_ = 0;
   std::array<Interval, kMaxRank> d_{};
+};
+
+// A possibly partial selection `[:,2:4]` (range.hpp:70-91): unconstrained dims are nullopt.
+class RangeSpec {
+ public:
+  RangeSpec() = default;
+  explicit RangeSpec(std::vector<std::optional<Interval>> dims) : dims_(std::move(dims)) {}
+  static RangeSpec from_range(const Range& r);
+  size_t rank() const { return dims_.size(); }
+  const std::vector<std::optional<Interval>>& dims() const { return dims_; }
+  Range resolve(const Shape& s) const;  // RankMismatch / RangeOutOfBounds
+  std::string to_string() const;
+  static RangeSpec parse(std::string_view text);  // MalformedFrame
+  bool operator==(const RangeSpec&) const = default;
+
+ private:
+  std::vector<std::optional<Interval>> dims_;
 };
 
 // Sorted interior split points per dimension; cells in lexicographic order, last dim fastest.
@@ -106,8 +127,11 @@ class SplitGrid {
   size_t rank() const { return pts_.size(); }
   const std::vector<std::vector<uint64_t>>& points() const { return pts_; }
   void check_against(const Shape& s) const;  // RankMismatch / InvalidSplitPoint
+  bool valid_for(const Shape& s) const;
   uint64_t cell_count() const;
   std::vector<Range> cells(const Shape& s) const;
+  Range cell(const Shape& s, uint64_t index) const;               // IndexOutOfRange
+  uint64_t cell_index_of(const Shape& s, const Range& r) const;   // InvalidSplitPoint when r crosses a boundary
   // per-dim index of the grid interval holding coordinate x (binary search)
   size_t interval_of(size_t dim, uint64_t x) const;
   bool operator==(const SplitGrid&) const = default;
@@ -137,6 +161,16 @@ class SplitMix64 {
   uint64_t s_;
 };
 uint64_t fnv1a64(const void* data, size_t n);
+class Fnv1a64 {  // incremental digest (hash.hpp:13-40)
+ public:
+  Fnv1a64& update(const void* data, size_t n);
+  Fnv1a64& update(std::string_view s) { return update(s.data(), s.size()); }
+  Fnv1a64& update_u64(uint64_t v);  // 8 little-endian bytes
+  uint64_t digest() const { return h_; }
+
+ private:
+  uint64_t h_ = 0xcbf29ce484222325ull;
+};
 // Synthetic payload seed of a base tensor: fnv1a64(path) ^ 0x7E9B1E0C.
 uint64_t payload_seed(std::string_view path);
 

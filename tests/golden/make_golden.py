@@ -143,6 +143,43 @@ def main():
     for text in ["[:,2:4]", "[:]", "[:,:]", "[1:2,:]", "[::]", "[]"]:
         kat["parse"].append({"text": text, "spec": True, **call(lambda: ref.range_parse(text, spec=True))})
 
+    # SplitGrid::cell / cell_index_of, Range::offset_by, RangeSpec::resolve
+    kat.update({"grid_cell": [], "cell_index_of": [], "offset_by": [], "spec_resolve": []})
+    for shape, pts in [((6,), [[3]]), ((4, 6), [[], [3]]), ((4, 6), [[1, 3], [2]]), ((5,), [[7]]), ((), [])]:
+        for index in range(8):
+            kat["grid_cell"].append({"shape": list(shape), "points": pts, "index": index,
+                                     **call(lambda: ref.grid_cell(shape, pts, index))})
+    for _ in range(60):
+        rank = rng.randint(1, 3)
+        shape = tuple(rng.randint(1, 9) for _ in range(rank))
+        pts = [sorted(rng.sample(range(1, e), rng.randint(0, min(3, e - 1)))) if e > 1 else [] for e in shape]
+        box = []
+        for e in shape:
+            lo = rng.randint(0, e - 1)
+            box.append((lo, rng.randint(lo + 1, e)))
+        if rng.random() < 0.1:
+            box[0] = (box[0][0], shape[0] + 1)
+        kat["cell_index_of"].append({"shape": list(shape), "points": pts, "box": [list(x) for x in box],
+                                     **call(lambda: ref.grid_cell_index_of(shape, pts, box))})
+        index = rng.randint(0, 12)
+        kat["grid_cell"].append({"shape": list(shape), "points": pts, "index": index,
+                                 **call(lambda: ref.grid_cell(shape, pts, index))})
+        outer = [(rng.randint(0, 4), 0) for _ in range(rank)]
+        outer = [(a, a + rng.randint(1, 6)) for a, _ in outer]
+        inner = []
+        for a, z in outer:
+            lo = rng.randint(0, z - a)
+            inner.append((lo, lo + rng.randint(0, z - a - lo + 1)))
+        if rng.random() < 0.1:
+            outer = outer[:-1]
+        kat["offset_by"].append({"box": [list(x) for x in inner], "outer": [list(x) for x in outer],
+                                 **call(lambda: ref.offset_by(inner, outer))})
+    for text, shape in [("[:,2:4]", (4, 6)), ("[:]", (5,)), ("[1:2,:]", (3, 3)), ("[:,2:7]", (4, 6)),
+                        ("[:]", (4, 6)), ("[]", ()), ("[2:2]", (4,)), ("[0:4,0:6]", (4, 6))]:
+        spec = ref.range_parse(text, spec=True)
+        kat["spec_resolve"].append({"text": text, "shape": list(shape),
+                                    **call(lambda: ref.spec_resolve(spec, shape))})
+
     with open(os.path.join(HERE, "tensor_core_kat.json"), "w") as f:
         json.dump(kat, f, indent=0, sort_keys=True)
 

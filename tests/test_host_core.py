@@ -76,6 +76,43 @@ def test_grid_fixtures(rs):
         assert got == {k: c[k] for k in ("ok", "error") if k in c}, c
 
 
+def _want(c):
+    return {k: c[k] for k in ("ok", "error") if k in c}
+
+
+def _lists(box):
+    return [list(x) for x in box]
+
+
+def test_cell_offset_resolve_fixtures(rs):
+    """SplitGrid::cell / cell_index_of, Range::offset_by, RangeSpec resolve vs the reference."""
+    for c in KAT["grid_cell"]:
+        assert outcome(lambda: _lists(rs.grid_cell(tuple(c["shape"]), c["points"], c["index"]))) == _want(c), c
+    for c in KAT["cell_index_of"]:
+        assert outcome(lambda: rs.grid_cell_index_of(tuple(c["shape"]), c["points"], c["box"])) == _want(c), c
+    for c in KAT["offset_by"]:
+        assert outcome(lambda: _lists(rs.range_offset_by(c["box"], c["outer"]))) == _want(c), c
+    for c in KAT["spec_resolve"]:
+        assert outcome(lambda: _lists(rs.rangespec_resolve(c["text"], tuple(c["shape"])))) == _want(c), c
+    for c in KAT["grid_cells"]:  # cell(i) enumerates cells() in order
+        if "ok" in c:
+            assert [_lists(rs.grid_cell(tuple(c["shape"]), c["points"], i)) for i in range(len(c["ok"]))] == c["ok"]
+            for i, cell in enumerate(c["ok"]):
+                assert rs.grid_cell_index_of(tuple(c["shape"]), c["points"], cell) == i
+
+
+def test_valid_for_and_dtype_names(rs):
+    assert rs.range_valid_for([(0, 4), (2, 4)], (4, 6))
+    assert not rs.range_valid_for([(0, 4), (2, 7)], (4, 6))
+    assert not rs.range_valid_for([(2, 2)], (4,))
+    assert not rs.range_valid_for([(0, 1)], (4, 6))
+    for name, code in [("f32", 0), ("F32", 0), ("f16", 1), ("i64", 2), ("U8", 3), ("bf16", 4), ("BF16", 4)]:
+        assert rs.dtype_from_name(name) == code
+    with pytest.raises(rs.ReshardError) as e:
+        rs.dtype_from_name("fp8")
+    assert e.value.name == "MalformedConfig"
+
+
 def test_fnv_and_seed(rs, orc):
     assert rs.fnv1a64(b"") == 0xCBF29CE484222325
     for s in [b"a", b"param/embedding.word_embeddings.weight", bytes(range(200))]:

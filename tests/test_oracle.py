@@ -62,6 +62,27 @@ def test_grid_refine_split_parse_fixtures(orc):
         assert norm(got) == {k: c[k] for k in ("ok", "error") if k in c}, c
 
 
+def _want(c):
+    return {k: c[k] for k in ("ok", "error") if k in c}
+
+
+def _tup(box):
+    return [tuple(x) for x in box]
+
+
+def test_cell_offset_resolve_fixtures(orc):
+    for c in KAT["grid_cell"]:
+        assert norm(outcome(lambda: orc.grid_cell(tuple(c["shape"]), c["points"], c["index"]))) == _want(c), c
+    for c in KAT["cell_index_of"]:
+        got = outcome(lambda: orc.grid_cell_index_of(tuple(c["shape"]), c["points"], _tup(c["box"])))
+        assert got == _want(c), c
+    for c in KAT["offset_by"]:
+        assert norm(outcome(lambda: orc.offset_by(_tup(c["box"]), _tup(c["outer"])))) == _want(c), c
+    for c in KAT["spec_resolve"]:
+        spec = orc.range_parse(c["text"], True)
+        assert norm(outcome(lambda: orc.spec_resolve(spec, tuple(c["shape"])))) == _want(c), c
+
+
 def test_spec_kats(orc):
     f = np.arange(24, dtype=np.float32).view(np.uint8)
     out = np.frombuffer(orc.slice(0, (4, 6), f, [(0, 4), (2, 4)]).tobytes(), np.float32)
