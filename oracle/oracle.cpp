@@ -911,7 +911,19 @@ static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1
 
   State out;
   for (auto& d : b.devices) out.store[d];  // one store per destination
-  std::vector<Dev> dsts = b.devices;
+  // SPEC.md:504 runs one transformer task per destination device; the cells of one
+  // destination are independent, so the work list is (destination, tensor, cell) and any
+  // number of host threads drain it (the CPU arm uses every core it has).
+  struct Task {
+    const Dev* dst;
+    size_t t, i;
+  };
+  std::vector<Task> tasks;
+  for (auto& r2 : b.devices)
+    for (auto [t, i] : hosted(b, r2))
+      if (in_range(t, t0, t1)) tasks.push_back({&r2, t, i});
+  std::map<Dev, std::mutex> store_mu;
+  for (auto& d : b.devices) store_mu[d];
   std::atomic<size_t> next{0};
   std::atomic<uint64_t> moved{0}, local{0};
   std::vector<Fault> errs;
@@ -922,47 +934,46 @@ static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1
     try {
       for (;;) {
         size_t k = next.fetch_add(1);
-        if (k >= dsts.size()) return;
-        const Dev& r2 = dsts[k];
-        auto& mine = out.store.at(r2);
-        for (auto [t, i] : hosted(b, r2)) {
-          if (!in_range(t, t0, t1)) continue;
-          const Box& c = b.cells[t][i];
-          std::vector<std::pair<Box, core::Tensor>> parts;
-          TensorP whole;
-          for (auto& w : gcells[t]) {
-            if (!box_contains(c, w)) continue;
-            size_t v = cell_containing(a.cells[t], w);
-            const Box& vb = a.cells[t][v];
-            Dev holder;
-            bool resident = hosts(a, t, v, r2) && !plan.failed.count(r2);
-            if (resident) holder = r2;
-            else holder = move_src.at({r2, t, w});
-            const TensorP& stored = src.store.at(holder).at(CellKey{t, vb});
-            if (resident && w == vb && w == c) {  // cell kept as is, no byte moves
-              whole = stored;
-              continue;
-            }
-            // fetch(peer, path, range) == query == slice of the stored cell
-            core::Tensor frag = core::slice(*stored, box_rebase(w, vb));
-            (resident ? local : moved) += core::bytes_of(frag).size();
-            parts.emplace_back(box_rebase(w, c), std::move(frag));
+        if (k >= tasks.size()) return;
+        const Dev& r2 = *tasks[k].dst;
+        const size_t t = tasks[k].t, i = tasks[k].i;
+        const Box& c = b.cells[t][i];
+        std::vector<std::pair<Box, core::Tensor>> parts;
+        TensorP whole, made;
+        for (auto& w : gcells[t]) {
+          if (!box_contains(c, w)) continue;
+          size_t v = cell_containing(a.cells[t], w);
+          const Box& vb = a.cells[t][v];
+          Dev holder;
+          bool resident = hosts(a, t, v, r2) && !plan.failed.count(r2);
+          if (resident) holder = r2;
+          else holder = move_src.at({r2, t, w});
+          const TensorP& stored = src.store.at(holder).at(CellKey{t, vb});
+          if (resident && w == vb && w == c) {  // cell kept as is, no byte moves
+            whole = stored;
+            continue;
           }
-          if (whole) {
-            mine[CellKey{t, c}] = whole;
-          } else if (parts.size() == 1 && parts[0].first == full_box(extents_of(c))) {
-            mine[CellKey{t, c}] = std::make_shared<const core::Tensor>(std::move(parts[0].second));  // merge elided
-          } else {
-            mine[CellKey{t, c}] = std::make_shared<const core::Tensor>(core::merge(std::move(parts), extents_of(c)));
-          }
+          // fetch(peer, path, range) == query == slice of the stored cell
+          core::Tensor frag = core::slice(*stored, box_rebase(w, vb));
+          (resident ? local : moved) += core::bytes_of(frag).size();
+          parts.emplace_back(box_rebase(w, c), std::move(frag));
         }
+        if (whole) {
+          made = whole;
+        } else if (parts.size() == 1 && parts[0].first == full_box(extents_of(c))) {
+          made = std::make_shared<const core::Tensor>(std::move(parts[0].second));  // merge elided
+        } else {
+          made = std::make_shared<const core::Tensor>(core::merge(std::move(parts), extents_of(c)));
+        }
+        std::lock_guard<std::mutex> g(store_mu.at(r2));
+        out.store.at(r2)[CellKey{t, c}] = std::move(made);
       }
     } catch (const Fault& f) {
       std::lock_guard<std::mutex> g(em);
       errs.push_back(f);
     }
   };
-  int nt = std::max(1, std::min<int>(n_threads, int(dsts.size())));
+  int nt = std::max(1, std::min<int>(n_threads, int(tasks.size())));
   std::vector<std::thread> pool;
   for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
   for (auto& th : pool) th.join();  // barrier 2: all fetches and merges done
