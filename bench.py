@@ -237,6 +237,45 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def pcie_probe(nbytes: int = 2 << 30, reps: int = 3) -> dict:
+    """Pinned host <-> device copy rates on this box (off the clock): the link that bounds the
+    host-buffer e2e path.  H2D alone, D2H alone, and both directions at once on two streams."""
+    import torch
+
+    h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(ops):
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            ev = []
+            for stream, fn in ops:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                with torch.cuda.stream(stream):
+                    fn()
+                e1.record(stream)
+                ev.append((e0, e1))
+            torch.cuda.synchronize()
+            best = min(best, max(a.elapsed_time(b) for a, b in ev))
+        return best
+
+    h2d = lambda: d_a.copy_(h_in, non_blocking=True)  # noqa: E731
+    d2h = lambda: h_out.copy_(d_b, non_blocking=True)  # noqa: E731
+    t_h2d = timed([(s1, h2d)])
+    t_d2h = timed([(s2, d2h)])
+    t_both = timed([(s1, h2d), (s2, d2h)])
+    del h_in, h_out, d_a, d_b
+    torch.cuda.empty_cache()
+    gb = nbytes / 1e9
+    return {"h2d_gbs": round(gb / (t_h2d * 1e-3), 1), "d2h_gbs": round(gb / (t_d2h * 1e-3), 1),
+            "bidir_gbs_each": round(gb / (t_both * 1e-3), 1), "probe_bytes": nbytes}
+
+
 def copy_kernel_name() -> str:
     k = os.environ.get("RESHARD_COPY_KERNEL", "bulk_strided") or "bulk_strided"  # the library default
     return {"bulk": "copy_bulk_kernel", "bulk_strided": "copy_bulk_strided_kernel", "ldg": "copy_v16_kernel",
@@ -466,6 +505,14 @@ def run_ours(args):
             rs.host_free(hd)
             e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms", "h2d_bytes_per_step": s_bytes,
                    "d2h_bytes_per_step": d_bytes, "steps": args.e2e_steps, "mismatched_bytes": bad_e2e}
+            try:  # the PCIe bound of this path, measured on the same box
+                link = pcie_probe()
+                bound_ms = max(s_bytes / (link["h2d_gbs"] * 1e9), d_bytes / (link["d2h_gbs"] * 1e9),
+                               max(s_bytes, d_bytes) / (link["bidir_gbs_each"] * 1e9)) * 1e3
+                e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
+                                   "frac": round(bound_ms / e2e["value"], 4)}
+            except Exception as exc:
+                e2e["roofline"] = {"error": str(exc)[:200]}
         except Exception as exc:  # e.g. not enough pinned host memory
             e2e = {"value": None, "unit": "ms", "h2d_bytes_per_step": s_bytes, "d2h_bytes_per_step": d_bytes,
                    "error": str(exc)[:200]}

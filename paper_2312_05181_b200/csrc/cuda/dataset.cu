@@ -59,7 +59,8 @@ __device__ __forceinline__ void stcg(Agg* p, const Agg& v) {
   __stcg(&p->len, v.len), __stcg(&p->c0, v.c0), __stcg(&p->c1, v.c1), __stcg(&p->c2, v.c2);
 }
 
-__global__ void __launch_bounds__(kThreads, 3) repartition_kernel(Params p, Outs o, Scratch s) {
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) repartition_kernel(Params p, Outs o, Scratch s) {
   __shared__ unsigned tile_sh;
   __shared__ Agg warp_tot[kWarps];
   __shared__ Agg tile_prefix;
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 3) repartition_kernel(Params p, Outs
       pos[j] = p.full * p.B + p.rank * p.b + (k - p.in_full);
     }
     idx[j] = j < nv ? __ldg(p.perm + pos[j]) : 0ull;
+    if (j < nv) o.pos[k] = pos[j];  // stored now: pos[] is dead after this loop
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
@@ -101,7 +103,6 @@ __global__ void __launch_bounds__(kThreads, 3) repartition_kernel(Params p, Outs
     cls[j] = j < nv ? __ldg(p.file_class + f[j]) : (unsigned char)3;
     if (j < nv) {
       const unsigned long long k = k0 + j;
-      o.pos[k] = pos[j];
       o.ent[3 * k] = f[j], o.ent[3 * k + 1] = off[j], o.ent[3 * k + 2] = len[j];
       mine.len += len[j];
       mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
@@ -328,7 +329,11 @@ uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 bool k5_split() {
   const char* v = std::getenv("RESHARD_K5");
   return v && std::string(v) == "split";  // r11: split 6.59 ms vs single-pass 6.38 ms per step
-
+}
+// resident CTAs per SM the single-pass kernel is compiled for (RESHARD_K5=lookback4: 4)
+int k5_min_blocks() {
+  const char* v = std::getenv("RESHARD_K5");
+  return v && std::string(v) == "lookback4" ? 4 : 3;
 }
 
 // The dataset kernels are random 8- and 24-byte gathers: with the default L2 fetch
@@ -513,7 +518,8 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
     repart_finalize_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
     ck(cudaGetLastError(), "repartition launch");
   } else if (tiles) {
-    repartition_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
+    if (k5_min_blocks() == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
+    else repartition_kernel<3><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
     ck(cudaGetLastError(), "repartition launch");
   } else {
     ck(cudaMemsetAsync(out.qcount, 0, 3 * sizeof(uint64_t), st), "qcount");

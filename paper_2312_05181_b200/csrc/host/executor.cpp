@@ -20,7 +20,6 @@ void ck(cudaError_t e, const char* what) {
 
 constexpr uint64_t kCellAlign = 256;
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
-constexpr uint64_t kHostChunks = 32;  // pipeline depth of the host-buffer path
 
 struct DeviceGuard {
   int prev = -1;
@@ -108,6 +107,7 @@ CopyConfig CopyConfig::from_env() {
   c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", is_bulk(c.kernel) ? 1 : 3));
   c.stages = env_int("RESHARD_BULK_STAGES", c.stages);
   c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
+  c.host_chunks = std::max(1, env_int("RESHARD_HOST_CHUNKS", c.host_chunks));
   return c;
 }
 
@@ -464,7 +464,7 @@ void Executor::prepare() {
     if (ctx_.world() == 1 && one_list) {
       const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
       const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
-      const uint64_t target = std::max<uint64_t>(bytes / kHostChunks, 1);
+      const uint64_t target = std::max<uint64_t>(bytes / uint64_t(cfg_.host_chunks), 1);
       const size_t n = fans.empty() ? aligned.size() : fans.size();
       HostChunk c{0, 0, 0, UINT64_MAX, {}};
       std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);

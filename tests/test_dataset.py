@@ -1,5 +1,6 @@
 """Dataset index repartitioning: host functions vs the oracle (CPU), the
 SPEC examples and acceptance #8, and the K5 GPU kernel vs the oracle's gather (gpu)."""
+import os
 import random
 
 import numpy as np
@@ -145,3 +146,43 @@ def test_k8_gpu_shuffle_bit_identical(rs, ctx):
         assert np.array_equal(got, rs.shuffle_epoch(n, seed, ep)), n
         assert n < 3 or t["rounds"] >= 1
         ctx.free(0, p)
+
+
+@pytest.mark.gpu
+def test_config5_full_size_matches_oracle(rs, orc, ctx):
+    """BASELINE config 5 at full size (N = 10^8, B = 1280, DP 2 -> 4 -> 8): the K8 GPU epoch
+    permutation equals the host Fisher-Yates, and every rank's K5 output (positions, entries,
+    byte offsets, locator queues) equals the oracle's gather on the same inputs."""
+    n, B, files, per_file, sb = 100_000_000, 1280, 1000, 100_000, 8206
+    k = np.arange(n, dtype=np.uint64)
+    samples = np.empty((n, 3), np.uint64)
+    samples[:, 0] = k // np.uint64(per_file)
+    samples[:, 1] = (k % np.uint64(per_file)) * np.uint64(sb)
+    samples[:, 2] = sb
+    del k
+    perm = rs.shuffle_epoch(n, 0x5EED, 0)
+    d_perm, d_samp = ctx.malloc(0, 8 * n), ctx.malloc(0, 24 * n)
+    ctx.htod(0, d_samp, samples.ctypes.data, 24 * n)
+    rs.shuffle_epoch_device(ctx, 0, n, 0x5EED, 0, d_perm)
+    dev_perm = np.empty(n, np.uint64)
+    ctx.dtoh(0, dev_perm.ctypes.data, d_perm, 8 * n)
+    assert np.array_equal(dev_perm, perm)
+    del dev_perm
+    for at, dp in [(25_000, 4), (50_000, 8)]:
+        for d in range(dp):
+            m = np.arange(files) % (dp + 1)
+            fc = np.where(m == d, 0, np.where(m == dp, 2, 1)).astype(np.uint8)
+            d_fc = ctx.malloc(0, files)
+            ctx.htod(0, d_fc, fc.ctypes.data, files)
+            part = rs.Partition(ctx, 0, rs.repartition_count(n, B, at, dp, d))
+            rs.repartition(ctx, 0, d_perm, d_samp, d_fc, n, B, at, dp, d, part)
+            got = part.fetch()
+            want = orc.dataset_gather(n, B, at, dp, d, perm, samples, fc, n_threads=os.cpu_count() or 1)
+            for key in ("pos", "ent", "boff", "qidx"):
+                assert np.array_equal(got[key], want[key]), (at, dp, d, key)
+            assert got["qcount"] == want["qcount"]
+            del got, want
+            part.free()
+            ctx.free(0, d_fc)
+    ctx.free(0, d_perm)
+    ctx.free(0, d_samp)
