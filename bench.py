@@ -121,6 +121,9 @@ def run_dataset(args, rs):
                  for k in range(0, part.count, max(1, part.count // 1000)))
     ent_ok = bool(np.array_equal(got["ent"][:: max(1, part.count // 1000)],
                                  samples[perm[got["pos"][:: max(1, part.count // 1000)]]]))
+    # the random-read floor of the same step: K5's perm + entry gathers alone (off the clock)
+    floor_ms = sum(rs.repartition_gather_probe(ctx, rank, d_perm, d_samp, n, spec["B"], at, dp, d)["ms"]
+                   for at, dp, d, _, _ in jobs)
     if rank != 0:
         return
     ms = statistics.mean(step_ms)
@@ -136,7 +139,9 @@ def run_dataset(args, rs):
         "samples_per_step": done, "gsamples_per_s": round(done / (ms * 1e-3) / 1e9, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "repartition_kernel", "algorithmic_bytes_per_launch": alg // max(launches, 1)},
+                     "kernel": "repartition_kernel", "algorithmic_bytes_per_launch": alg // max(launches, 1),
+                     "random_gather_floor_ms": round(floor_ms, 4),
+                     "frac_of_gather_floor": round(floor_ms / ms, 4)},
         "gpu_launches": launches * args.steps, "clocks": clocks.summary(), "spot_check": {"pos": pos_ok, "ent": ent_ok},
         "e2e": None,
         "shuffle_epoch_gpu": {"ms": round(shuf["ms"], 3), "rounds": shuf["rounds"], "launches": shuf["launches"],

@@ -280,6 +280,11 @@ int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
 /* K5: gather + scan + compaction for one rank in one kernel launch (timed with events) */
 int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,
                    uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
+/* Diagnostic (no reference counterpart): best-of-`reps` device time of K5's random reads
+ * alone for this rank (perm + 24-byte entry gathers, nothing written) — the floor bench.py
+ * reports K5 against.  idx->file_class is not read. */
+int rs_repartition_gather_probe(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch,
+                                uint64_t at_step, uint64_t new_dp, uint64_t rank, int reps, rs_timing* timing);
 
 #ifdef __cplusplus
 }

@@ -674,6 +674,16 @@ def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_p
     return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches)
 
 
+def repartition_gather_probe(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, n: int, global_batch: int,
+                             at_step: int, new_dp: int, rank: int, reps: int = 3) -> dict:
+    """Diagnostic: device time of K5's random reads alone (the floor for the gather)."""
+    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, 0, n)
+    t = _capi.rs_timing()
+    _chk(lib.rs_repartition_gather_probe(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, reps,
+                                         C.byref(t)))
+    return dict(ms=t.ms, bytes=t.bytes, launches=t.launches)
+
+
 def shuffle_epoch_device(ctx: Context, gpu: int, n: int, seed: int, epoch: int, perm_ptr: int) -> dict:
     """K8: the shuffle_epoch permutation computed on the GPU into perm_ptr (n x u64),
     bit-identical to the host shuffle.  Returns the timing (tiles = rounds)."""

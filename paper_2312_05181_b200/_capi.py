@@ -148,6 +148,8 @@ SIGNATURES = {
                                           C.POINTER(rs_timing)]),
     "rs_repartition": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
                                  P, C.POINTER(rs_timing)]),
+    "rs_repartition_gather_probe": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                              C.c_int, C.POINTER(rs_timing)]),
 }
 
 

@@ -713,5 +713,14 @@ int rs_repartition(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t
     if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
   });
 }
+int rs_repartition_gather_probe(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t B, uint64_t at_step,
+                                uint64_t dp, uint64_t rank, int reps, rs_timing* timing) {
+  return guard([&] {
+    need(idx, "index"), need(timing, "timing");
+    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n};
+    Timing t = repartition_gather_probe(ctx_of(c), gpu, v, B, at_step, dp, rank, reps);
+    *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
+  });
+}
 
 }  // extern "C"

@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(kThreads, MINB) repartition_kernel(Params p, O
       pos[j] = p.full * p.B + p.rank * p.b + (k - p.in_full);
     }
     idx[j] = j < nv ? __ldg(p.perm + pos[j]) : 0ull;
-    if (j < nv) o.pos[k] = pos[j];  // stored now: pos[] is dead after this loop
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
@@ -103,6 +102,7 @@ __global__ void __launch_bounds__(kThreads, MINB) repartition_kernel(Params p, O
     cls[j] = j < nv ? __ldg(p.file_class + f[j]) : (unsigned char)3;
     if (j < nv) {
       const unsigned long long k = k0 + j;
+      o.pos[k] = pos[j];
       o.ent[3 * k] = f[j], o.ent[3 * k + 1] = off[j], o.ent[3 * k + 2] = len[j];
       mine.len += len[j];
       mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
@@ -191,6 +191,42 @@ __global__ void __launch_bounds__(kThreads, MINB) repartition_kernel(Params p, O
     else if (cls[j] == 1) o.q1[run.c1++] = unsigned(k);
     else o.q2[run.c2++] = unsigned(k);
   }
+}
+
+// ---- random-gather ceiling (diagnostic) -----------------------------------------------------
+// K5's two HBM-random levels alone — the rank's perm positions, one 24-byte entry gather per
+// position, nothing written but one word per thread — at the configuration the standalone
+// probe found fastest (4 items per thread, 256 threads; scripts/probe_gather.cu, profiles/r12).
+// Its time is the floor for any kernel that must gather these entries: bench.py reports K5
+// against it next to the streaming-HBM roofline.
+constexpr int kProbeItems = 4;
+__global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsigned long long* sink) {
+  const unsigned long long k0 =
+      ((unsigned long long)blockIdx.x * kThreads + threadIdx.x) * (unsigned long long)kProbeItems;
+  unsigned long long batch = 0, r = 0;
+  if (k0 < p.in_full) batch = p.at_step + k0 / p.b, r = k0 % p.b;
+  unsigned long long idx[kProbeItems], acc = 0;
+#pragma unroll
+  for (int j = 0; j < kProbeItems; ++j) {
+    const unsigned long long k = k0 + j;
+    unsigned long long pos;
+    if (k < p.in_full) {
+      pos = batch * p.B + p.rank * p.b + r;
+      if (++r == p.b) r = 0, ++batch;
+    } else {
+      pos = p.full * p.B + p.rank * p.b + (k - p.in_full);
+    }
+    idx[j] = k < p.count ? __ldg(p.perm + pos) : 0ull;
+  }
+  unsigned long long f[kProbeItems], off[kProbeItems], len[kProbeItems];
+#pragma unroll
+  for (int j = 0; j < kProbeItems; ++j) {
+    const unsigned long long* e = p.samples + 3 * idx[j];
+    f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
+  }
+#pragma unroll
+  for (int j = 0; j < kProbeItems; ++j) acc ^= f[j] + off[j] + len[j];
+  if (acc == 0x9e3779b97f4a7c15ull) *sink = acc;  // keeps the loads; practically never stores
 }
 
 // ---- K5 split variant: gather / scan / finalize -------------------------------------------
@@ -328,7 +364,9 @@ uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 
 bool k5_split() {
   const char* v = std::getenv("RESHARD_K5");
-  return v && std::string(v) == "split";  // r11: split 6.59 ms vs single-pass 6.38 ms per step
+  // r11: split 6.59 ms vs single-pass 6.38 ms per step; r13 (single-pass with pos stored
+  // early, 80 regs and no spills): 6.57 vs 6.78 — that change was reverted
+  return v && std::string(v) == "split";
 }
 // resident CTAs per SM the single-pass kernel is compiled for (RESHARD_K5=lookback4: 4)
 int k5_min_blocks() {
@@ -533,6 +571,40 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   t.tiles = tiles;
   t.bytes = count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
   t.launches = tiles ? (split ? 3 : 1) : 0;
+  return t;
+}
+
+Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
+                                uint64_t new_dp, uint64_t rank, int reps) {
+  const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  const uint64_t b = B / new_dp, full = idx.n / B;
+  using ull = unsigned long long;
+  Params p{reinterpret_cast<const ull*>(idx.perm), reinterpret_cast<const ull*>(idx.samples), idx.file_class, idx.n, B,
+           at_step, b, rank, count, full > at_step ? (full - at_step) * b : 0, full};
+  const uint64_t per = uint64_t(kThreads) * kProbeItems, blocks = (count + per - 1) / per;
+  ull* sink = nullptr;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&sink), sizeof(ull), st), "cudaMallocAsync");
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  Timing t;
+  t.ms = 1e30f;
+  for (int i = 0; i < std::max(1, reps) + 1; ++i) {  // first launch warms up
+    ck(cudaEventRecord(e0, st), "event");
+    if (blocks) gather_probe_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
+    ck(cudaGetLastError(), "probe launch");
+    ck(cudaEventRecord(e1, st), "event");
+    ck(cudaEventSynchronize(e1), "sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    if (i > 0) t.ms = std::min(t.ms, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ck(cudaFreeAsync(sink, st), "cudaFreeAsync");
+  t.tiles = blocks, t.launches = blocks ? 1 : 0, t.bytes = count * (8 + 24);
   return t;
 }
 

@@ -54,5 +54,9 @@ uint64_t repartition_scratch_bytes(uint64_t count);
 // memory; it is cleared on the stream before the launch.
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch);
+// Diagnostic: best-of-`reps` time of K5's random reads alone (perm + entry gathers of the
+// rank's positions, nothing written) — the floor for any kernel that must gather them.
+Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
+                                uint64_t new_dp, uint64_t rank, int reps);
 
 }  // namespace reshard

@@ -59,7 +59,7 @@ struct CopyConfig {
   int ctas_per_sm = 1;
   int stages = 7;               // bulk: shared-memory ring depth
   unsigned stage_bytes = 29696; // bulk: bytes per stage (tiles are cut to fit one stage); r09 A/B
-  int host_chunks = 32;         // pipeline depth of the host-buffer path (run_host)
+  int host_chunks = 64;         // pipeline depth of the host-buffer path (run_host); r13 sweep
   static CopyConfig from_env();
 };
 
