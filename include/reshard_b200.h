@@ -209,6 +209,14 @@ int rs_executor_create(rs_context* ctx, const rs_plan* plan, const int32_t* src_
  * run as several windows (waves) over reused arenas */
 int rs_executor_create_window(rs_context* ctx, const rs_plan* plan, const int32_t* src_gpu, const int32_t* dst_gpu,
                               uint64_t tile_bytes, uint32_t t_begin, uint32_t t_end, rs_executor** out);
+/* apply_plan(plan, central) (the paper's §6.3 baseline): every moved
+ * fragment goes source -> staging region on `central_gpu` -> destination, in two dependent
+ * phases; same final state as distributed mode.  The staging region is the tail of the
+ * central GPU's dst arena (rs_executor_arena_bytes includes it).  Every GPU of the world
+ * must be local to the context. */
+int rs_executor_create_central(rs_context* ctx, const rs_plan* plan, const int32_t* src_gpu, const int32_t* dst_gpu,
+                               uint64_t tile_bytes, int central_gpu, rs_executor** out);
+int rs_executor_staging_bytes(const rs_executor* e, uint64_t* bytes);
 void rs_executor_destroy(rs_executor* e);
 int rs_executor_arena_bytes(const rs_executor* e, int gpu, uint64_t* src_bytes, uint64_t* dst_bytes);
 int rs_executor_bind(rs_executor* e, int gpu, void* src_arena, void* dst_arena);

@@ -458,9 +458,16 @@ class Executor:
     """apply_plan data plane: arenas per GPU, one tile-copy kernel per source GPU."""
 
     def __init__(self, ctx: Context, plan: Plan, src_gpu: Sequence[int], dst_gpu: Sequence[int],
-                 tile_bytes: int = 256 << 10, window: tuple[int, int] | None = None):
+                 tile_bytes: int = 256 << 10, window: tuple[int, int] | None = None, central: int | None = None):
+        """central=g: apply_plan's central mode, every moved fragment staged
+        on GPU g; otherwise distributed mode (push from each source GPU)."""
         h = C.c_void_p()
-        if window is None:
+        if central is not None:
+            if window is not None:
+                raise ValueError("central mode runs the whole catalog (no window)")
+            _chk(lib.rs_executor_create_central(ctx.h, plan.h, _i32(src_gpu), _i32(dst_gpu), tile_bytes, int(central),
+                                                C.byref(h)))
+        elif window is None:
             _chk(lib.rs_executor_create(ctx.h, plan.h, _i32(src_gpu), _i32(dst_gpu), tile_bytes, C.byref(h)))
         else:
             _chk(lib.rs_executor_create_window(ctx.h, plan.h, _i32(src_gpu), _i32(dst_gpu), tile_bytes,
@@ -484,6 +491,11 @@ class Executor:
         s, d = C.c_uint64(), C.c_uint64()
         _chk(lib.rs_executor_arena_bytes(self.h, gpu, C.byref(s), C.byref(d)))
         return s.value, d.value
+
+    def staging_bytes(self) -> int:
+        b = C.c_uint64()
+        _chk(lib.rs_executor_staging_bytes(self.h, C.byref(b)))
+        return b.value
 
     def bind(self, gpu: int, src_ptr: int, dst_ptr: int) -> None:
         _chk(lib.rs_executor_bind(self.h, gpu, src_ptr, dst_ptr))

@@ -117,6 +117,8 @@ SIGNATURES = {
     "rs_choose_source": (C.c_int, [C.c_int, C.POINTER(rs_device), U64P, rs_device, C.POINTER(rs_device)]),
     "rs_executor_create": (C.c_int, [P, P, I32P, I32P, C.c_uint64, C.POINTER(P)]),
     "rs_executor_create_window": (C.c_int, [P, P, I32P, I32P, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(P)]),
+    "rs_executor_create_central": (C.c_int, [P, P, I32P, I32P, C.c_uint64, C.c_int, C.POINTER(P)]),
+    "rs_executor_staging_bytes": (C.c_int, [P, U64P]),
     "rs_executor_destroy": (None, [P]),
     "rs_executor_arena_bytes": (C.c_int, [P, C.c_int, U64P, U64P]),
     "rs_executor_bind": (C.c_int, [P, C.c_int, P, P]),

@@ -508,6 +508,23 @@ int rs_executor_create_window(rs_context* c, const rs_plan* p, const int32_t* sr
                                                       CopyConfig::from_env(), t_begin, t_end)};
   });
 }
+int rs_executor_create_central(rs_context* c, const rs_plan* p, const int32_t* src_gpu, const int32_t* dst_gpu,
+                               uint64_t tile_bytes, int central_gpu, rs_executor** out) {
+  return guard([&] {
+    need(p, "plan"), need(out, "out");
+    if (central_gpu < 0) raise(Errc::InvalidArgument, "central GPU must be >= 0");
+    std::vector<int> s(src_gpu, src_gpu + p->p->from->devices.size());
+    std::vector<int> d(dst_gpu, dst_gpu + p->p->to->devices.size());
+    *out = new rs_executor{std::make_unique<Executor>(ctx_of(c), p->p, s, d, tile_bytes ? tile_bytes : (256u << 10),
+                                                      CopyConfig::from_env(), 0, UINT32_MAX, central_gpu)};
+  });
+}
+int rs_executor_staging_bytes(const rs_executor* e, uint64_t* bytes) {
+  return guard([&] {
+    need(e, "executor"), need(bytes, "bytes");
+    *bytes = e->e->staging_bytes();
+  });
+}
 void rs_executor_destroy(rs_executor* e) { delete e; }
 int rs_executor_arena_bytes(const rs_executor* e, int gpu, uint64_t* s, uint64_t* d) {
   return guard([&] {

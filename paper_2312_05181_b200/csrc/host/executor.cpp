@@ -230,6 +230,7 @@ struct Executor::Local {
   std::vector<HostChunk> chunks;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev;
+  std::unique_ptr<Local> phase_b;  // central mode, on the central GPU: staging -> destination tiles
   uint64_t launches() const { return (n_fan ? 1 : 0) + (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
   ~Local() {
     if (dev < 0) return;
@@ -254,12 +255,13 @@ void Executor::launch_local(Local& l, void* stream) {
 }
 
 Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu,
-                   std::vector<int> dst_gpu, uint64_t tile_bytes, CopyConfig cfg, uint32_t t_begin, uint32_t t_end)
+                   std::vector<int> dst_gpu, uint64_t tile_bytes, CopyConfig cfg, uint32_t t_begin, uint32_t t_end,
+                   int central_gpu)
     : ctx_(ctx), plan_(std::move(plan)), src_gpu_(std::move(src_gpu)), dst_gpu_(std::move(dst_gpu)), cfg_(cfg),
       tile_bytes_(std::max<uint64_t>(4096, std::min<uint64_t>(tile_bytes, is_bulk(cfg.kernel) ? cfg.stage_bytes
                                                                                                         : UINT64_MAX) /
                                                16 * 16)),
-      t_begin_(t_begin), t_end_(t_end) {
+      t_begin_(t_begin), t_end_(t_end), central_(central_gpu) {
   auto in = [&](uint32_t t) { return t >= t_begin_ && t < t_end_; };
   const PTC& a = *plan_->from;
   const PTC& b = *plan_->to;
@@ -270,13 +272,17 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     if (g < 0 || g >= G) raise(Errc::InvalidArgument, "src GPU out of range");
   for (int g : dst_gpu_)
     if (g < 0 || g >= G) raise(Errc::InvalidArgument, "dst GPU out of range");
+  if (central_ >= G) raise(Errc::InvalidArgument, "central GPU out of range");
+  // (a planning-only context, with no local GPU, may still compute central layouts)
+  if (central_ >= 0 && !ctx_.local_world_ids().empty() && int(ctx_.local_world_ids().size()) != G)
+    raise(Errc::InvalidArgument, "central mode needs every GPU of the world in this process");
   src_size_.assign(size_t(G), 0);
   dst_size_.assign(size_t(G), 0);
   src_base_.assign(size_t(G), nullptr);
   dst_base_.assign(size_t(G), nullptr);
 
   // src arena layout
-  std::vector<std::unordered_map<uint64_t, size_t>> src_lookup(a.devices.size());
+  SrcLookup src_lookup(a.devices.size());
   for (uint32_t i = 0; i < a.devices.size(); ++i)
     for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
       if (!in(t)) {  // outside this executor's tensor window: no storage, no work
@@ -310,9 +316,85 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     dst_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
     dst_bind_.push_back(bnd);
   }
-  // fragments -> logical tiles, grouped by the executing (source) GPU.  Fragments that read
-  // the same source box for several destination cells (DP replicas) are grouped; with the
-  // bulk kernel their tiles are fused into fan-out tiles (source read once).
+  logical_.assign(size_t(G), {});
+  if (central_ >= 0) build_central(src_lookup);
+  else build_distributed(src_lookup);
+  for (int w : ctx_.local_world_ids()) {
+    auto l = std::make_unique<Local>();
+    l->world = w;
+    l->dev = ctx_.cuda_device(w);
+    DeviceGuard g(l->dev);
+    ck(cudaEventCreate(&l->start), "cudaEventCreate");
+    ck(cudaEventCreate(&l->stop), "cudaEventCreate");
+    ck(cudaMalloc(&l->d_count, sizeof(unsigned long long)), "cudaMalloc");
+    if (w == central_) {
+      l->phase_b = std::make_unique<Local>();
+      l->phase_b->world = w, l->phase_b->dev = l->dev;
+    }
+    local_.push_back(std::move(l));
+  }
+}
+
+// apply_plan central mode: each Move's fragment is fetched into the
+// central GPU's staging region (dense box, one slot per Move as plan_cost_central counts
+// it), then written from there into its destination cell.  Resident fragments are copied
+// locally as in distributed mode.
+void Executor::build_central(const SrcLookup& src_lookup) {
+  const PTC& a = *plan_->from;
+  const PTC& b = *plan_->to;
+  const uint64_t stage_base = dst_size_[size_t(central_)];
+  uint64_t stage = 0;
+  for (size_t j = 0; j < plan_->dst_cells.size(); ++j) {
+    const PlanDstCell& dc = plan_->dst_cells[j];
+    const CellBinding& db = dst_bind_[j];
+    if (db.arena == 0 || db.gpu < 0) continue;  // kept in place / outside the tensor window
+    const Range& dbox = b.cells[dc.tensor][dc.cell];
+    const uint64_t w = dtype_width(a.catalog.tensors[dc.tensor].dtype);
+    for (uint32_t k = dc.first; k < dc.first + dc.count; ++k) {
+      const PlanFragment& f = plan_->fragments[k];
+      const CellBinding& sb = src_bind_[src_lookup[f.src_device].at((uint64_t(dc.tensor) << 32) | f.src_cell)];
+      const Range& sbox = a.cells[dc.tensor][f.src_cell];
+      const Range rs = f.box.rebase_into(sbox), rd = f.box.rebase_into(dbox);
+      Shape sl, dl, ext = f.box.extents();
+      for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo), dl.push_back(rd.dim(d).lo);
+      const Shape zero(ext.size(), 0);
+      auto tile = [](int32_t sg, uint32_t sa, uint64_t so, uint64_t sp, int32_t dg, uint64_t dof, uint64_t dp,
+                     uint64_t rows, uint64_t run) {
+        Logical x{};
+        x.src_gpu = sg, x.src_arena = sa, x.n_dst = 1, x.src_off = so, x.src_pitch = sp;
+        x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
+        x.dst_gpu[0] = dg, x.dst_off[0] = dof, x.dst_pitch[0] = dp;
+        return x;
+      };
+      if (f.resident) {
+        lower_box(ext, sl, sbox.extents(), dl, dbox.extents(), w, tile_bytes_,
+                  [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+                    logical_[size_t(sb.gpu)].push_back(tile(sb.gpu, 0, sb.offset + so, sp, db.gpu, db.offset + dof, dp, rows, run));
+                  });
+        continue;
+      }
+      const uint64_t slot = stage_base + stage;
+      stage = align_up(stage + f.box.elements() * w, kCellAlign);
+      lower_box(ext, sl, sbox.extents(), zero, ext, w, tile_bytes_,  // fetch: source cell -> staging slot
+                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+                  logical_[size_t(sb.gpu)].push_back(tile(sb.gpu, 0, sb.offset + so, sp, central_, slot + dof, dp, rows, run));
+                });
+      lower_box(ext, zero, ext, dl, dbox.extents(), w, tile_bytes_,  // re-upload: staging slot -> destination
+                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+                  logical_b_.push_back(tile(central_, 1, slot + so, sp, db.gpu, db.offset + dof, dp, rows, run));
+                });
+    }
+  }
+  staging_bytes_ = stage;
+  dst_size_[size_t(central_)] = stage_base + stage;
+}
+
+// fragments -> logical tiles, grouped by the executing (source) GPU.  Fragments that read
+// the same source box for several destination cells (DP replicas) are grouped; with the
+// bulk kernel their tiles are fused into fan-out tiles (source read once).
+void Executor::build_distributed(const SrcLookup& src_lookup) {
+  const PTC& a = *plan_->from;
+  const PTC& b = *plan_->to;
   const char* fan_env = std::getenv("RESHARD_FANOUT");
   const bool fan = is_bulk(cfg_.kernel) && !(fan_env && std::string(fan_env) == "0");
   struct Member {
@@ -349,7 +431,6 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
       groups[fan ? it->second : groups.size() - 1].members.push_back(Member{db.gpu, db.offset, dl, dbox.extents()});
     }
   }
-  logical_.assign(size_t(G), {});
   for (const Group& grp : groups) {
     const CellBinding& sb = src_bind_[grp.src_bind];
     const Range& sbox = a.cells[grp.tensor][grp.src_cell];
@@ -393,16 +474,6 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
         out.push_back(x);
       }
   }
-  for (int w : ctx_.local_world_ids()) {
-    auto l = std::make_unique<Local>();
-    l->world = w;
-    l->dev = ctx_.cuda_device(w);
-    DeviceGuard g(l->dev);
-    ck(cudaEventCreate(&l->start), "cudaEventCreate");
-    ck(cudaEventCreate(&l->stop), "cudaEventCreate");
-    ck(cudaMalloc(&l->d_count, sizeof(unsigned long long)), "cudaMalloc");
-    local_.push_back(std::move(l));
-  }
 }
 
 Executor::~Executor() = default;
@@ -417,17 +488,25 @@ void Executor::bind(int gpu, void* src, void* dst) {
 }
 
 void Executor::prepare() {
+  for (auto& l : local_) {
+    lower_tiles(*l, logical_[size_t(l->world)], central_ < 0);
+    if (l->phase_b) lower_tiles(*l->phase_b, logical_b_, false);
+  }
+}
+
+// Logical tiles -> device descriptors of one local GPU (bases known after bind()).
+void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool host_chunks) {
   const bool bulk = is_bulk(cfg_.kernel);
   const bool interleave = cfg_.kernel == CopyKernel::Bulk;  // bulk_strided walks the natural order
   const char* bp = std::getenv("RESHARD_BULK_PEER");
   const bool bulk_peer = bp && std::string(bp) == "1";
-  for (auto& l : local_) {
-    const auto& lt = logical_[size_t(l->world)];
+  Local* l = &local;
+  {
     std::vector<FanTile> fans;
     std::vector<CopyTile> aligned, misc;
     uint64_t bytes = 0, read_bytes = 0;
     for (const Logical& x : lt) {
-      char* s = static_cast<char*>(src_base_[size_t(x.src_gpu)]);
+      char* s = static_cast<char*>(x.src_arena ? dst_base_[size_t(x.src_gpu)] : src_base_[size_t(x.src_gpu)]);
       if (!s) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.src_gpu) + " not bound");
       FanTile f{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), x.src_pitch, x.rows, x.row_bytes, x.n_dst, 0, {}, {}};
       uint64_t bits = f.src | f.row_bytes | (x.rows > 1 ? x.src_pitch : 0);
@@ -461,7 +540,7 @@ void Executor::prepare() {
     std::sort(aligned.begin(), aligned.end(), [](const CopyTile& p, const CopyTile& q) { return p.dst < q.dst; });
     l->chunks.clear();
     const bool one_list = misc.empty() && (fans.empty() != aligned.empty());
-    if (ctx_.world() == 1 && one_list) {
+    if (host_chunks && ctx_.world() == 1 && one_list) {
       const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
       const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
       const uint64_t target = std::max<uint64_t>(bytes / uint64_t(cfg_.host_chunks), 1);
@@ -526,12 +605,22 @@ void Executor::prepare() {
 }
 
 void Executor::run() {
+  Local* central = nullptr;
   for (auto& l : local_) {
     DeviceGuard g(l->dev);
     auto s = static_cast<cudaStream_t>(ctx_.stream(l->world));
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     launch_local(*l, s);
     ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
+    if (l->phase_b) central = l.get();
+  }
+  if (central) {  // central mode, phase 2: once every GPU's fetch into the staging region landed
+    DeviceGuard g(central->dev);
+    auto s = static_cast<cudaStream_t>(ctx_.stream(central->world));
+    for (auto& l : local_)
+      if (l.get() != central) ck(cudaStreamWaitEvent(s, l->stop, 0), "cudaStreamWaitEvent");
+    launch_local(*central->phase_b, s);
+    ck(cudaEventRecord(central->stop, s), "cudaEventRecord");
   }
 }
 
@@ -546,6 +635,10 @@ std::vector<Timing> Executor::wait() {
     t.bytes = l->bytes;
     t.read_bytes = l->read_bytes;
     t.launches = l->launches();
+    if (const Local* p = l->phase_b.get()) {
+      t.tiles += p->n_fan + p->n_aligned + p->n_misc;
+      t.bytes += p->bytes, t.read_bytes += p->read_bytes, t.launches += p->launches();
+    }
     out.push_back(t);
   }
   return out;
@@ -564,7 +657,10 @@ void Executor::host_phase(int gpu, int phase, void* host_buf) {
       if (src_size_[size_t(gpu)])
         ck(cudaMemcpyAsync(src_base_[size_t(gpu)], host_buf, src_size_[size_t(gpu)], cudaMemcpyHostToDevice, s), "h2d");
       break;
-    case 1: launch_local(*l, s); break;
+    case 1:
+      launch_local(*l, s);
+      if (l->phase_b) launch_local(*l->phase_b, s);  // central mode (single-process worlds only)
+      break;
     case 2:
       if (dst_size_[size_t(gpu)])
         ck(cudaMemcpyAsync(host_buf, dst_base_[size_t(gpu)], dst_size_[size_t(gpu)], cudaMemcpyDeviceToHost, s), "d2h");
@@ -605,8 +701,11 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     ck(cudaMemcpyAsync(dsrc, hsrc, ssize, cudaMemcpyHostToDevice, s), "h2d src arena");
     launch_local(*l, s);
-    ck(cudaMemcpyAsync(hdst, ddst, dsize, cudaMemcpyDeviceToHost, s), "d2h dst arena");
-    t.launches = l->launches();
+    if (l->phase_b) launch_local(*l->phase_b, s);  // central mode: staging -> destinations
+    // the staging region (central mode) sits at the end of the dst arena and is not state
+    ck(cudaMemcpyAsync(hdst, ddst, dsize - (l->phase_b ? staging_bytes_ : 0), cudaMemcpyDeviceToHost, s),
+       "d2h dst arena");
+    t.launches = l->launches() + (l->phase_b ? l->phase_b->launches() : 0);
   } else {
     // Pipelined over destination-ordered chunks: H2D of src pieces (copy engine 1), the
     // chunk's kernel once the src bytes it reads have landed, D2H of the dst bytes that no
@@ -675,16 +774,22 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   return t;
 }
 
-uint64_t Executor::tiles_for(int gpu) const { return logical_[size_t(gpu)].size(); }
+uint64_t Executor::tiles_for(int gpu) const {
+  return logical_[size_t(gpu)].size() + (gpu == central_ ? logical_b_.size() : 0);
+}
 uint64_t Executor::copy_bytes_for(int gpu) const {
   uint64_t n = 0;
   for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes * x.n_dst;
+  if (gpu == central_)
+    for (auto& x : logical_b_) n += uint64_t(x.rows) * x.row_bytes * x.n_dst;
   return n;
 }
 uint64_t Executor::read_bytes_for(int gpu) const {
   uint64_t n = 0;
   const bool bulk = is_bulk(cfg_.kernel);
   for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes * (bulk ? 1 : x.n_dst);
+  if (gpu == central_)
+    for (auto& x : logical_b_) n += uint64_t(x.rows) * x.row_bytes * (bulk ? 1 : x.n_dst);
   return n;
 }
 

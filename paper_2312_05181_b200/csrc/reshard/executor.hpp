@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <unordered_map>
 #include <vector>
 
 #include "reshard/planner.hpp"
@@ -105,10 +106,16 @@ class Executor {
   // src_gpu[i]: world GPU of from->devices[i]; dst_gpu[j]: world GPU of to->devices[j].
   // [t_begin, t_end): only the tensors of this catalog window get storage and work — a plan
   // too large for the world's HBM is executed as several windows (waves) over the same arenas.
+  // central_gpu >= 0 selects apply_plan's central mode (the paper's §6.3
+  // baseline): every moved fragment is first fetched into a staging region at the end of
+  // that GPU's dst arena, then re-uploaded from there to its destination cell (two
+  // dependent phases); resident fragments stay local.  Same final state as distributed mode.
   Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu, std::vector<int> dst_gpu,
            uint64_t tile_bytes = 256 << 10, CopyConfig cfg = CopyConfig::from_env(), uint32_t t_begin = 0,
-           uint32_t t_end = UINT32_MAX);
+           uint32_t t_end = UINT32_MAX, int central_gpu = -1);
   const CopyConfig& copy_config() const { return cfg_; }
+  int central_gpu() const { return central_; }        // -1: distributed mode
+  uint64_t staging_bytes() const { return staging_bytes_; }  // central mode: part of dst_arena_bytes(central)
   ~Executor();
 
   uint64_t src_arena_bytes(int gpu) const { return src_size_[size_t(gpu)]; }
@@ -149,6 +156,7 @@ class Executor {
   struct Logical {  // a tile before arena bases are known; n_dst > 1: fan-out (DP replicas)
     int32_t src_gpu;
     uint32_t n_dst;
+    uint32_t src_arena;  // 0: src arena of src_gpu, 1: its dst arena (central mode's staging)
     uint64_t src_off, src_pitch;
     uint32_t rows, row_bytes;
     int32_t dst_gpu[kMaxFan];
@@ -156,6 +164,10 @@ class Executor {
   };
   struct Local;
   void launch_local(Local& l, void* stream);
+  using SrcLookup = std::vector<std::unordered_map<uint64_t, size_t>>;  // (tensor<<32|cell) -> src_bind_ index
+  void build_distributed(const SrcLookup& src_lookup);
+  void build_central(const SrcLookup& src_lookup);
+  void lower_tiles(Local& l, const std::vector<Logical>& lt, bool host_chunks);
   uint64_t payload_pass(const std::vector<std::vector<cuda::PayloadTask>>& per_local, bool verify);
 
   Context& ctx_;
@@ -167,6 +179,9 @@ class Executor {
   std::vector<uint64_t> src_size_, dst_size_;
   std::vector<CellBinding> src_bind_, dst_bind_;
   std::vector<std::vector<Logical>> logical_;   // per executing (source) world GPU
+  int central_ = -1;
+  std::vector<Logical> logical_b_;              // central mode: staging -> destinations (on central_)
+  uint64_t staging_bytes_ = 0;
   std::vector<void*> src_base_, dst_base_;
   std::vector<std::unique_ptr<Local>> local_;   // per local GPU: device tiles, events
 };

@@ -309,3 +309,27 @@ def test_identity_transition_moves_nothing(rs, orc, ctx):
     ex, t = _run(rs, ctx, plan, 4, 4)
     assert t[0]["bytes"] == 0
     assert ex.verify() == 0
+
+
+def test_central_mode_same_final_state(rs, orc, ctx):
+    """apply_plan(plan, central): every moved fragment staged on the
+    central GPU, then re-uploaded — the destination cells equal the oracle's (and therefore
+    distributed mode's) byte for byte; the executed bytes are 2 x moved + relayout."""
+    entries = [("param/w", 0, (12, 8), 0, 0), ("param/v", 1, (6, 8), 1, 1), ("exp_avg/w", 0, (12, 8), 0, 0),
+               ("param/b", 3, (5,), -1, -1)]
+    for a_cfg, b_cfg, failed in [((2, 1, 1, DEV(2)), (1, 2, 1, DEV(2)), ()),
+                                 ((2, 1, 1, DEV(2)), (2, 1, 2, DEV(4)), ()),
+                                 ((2, 2, 1, DEV(4)), (4, 1, 1, DEV(4)), ()),
+                                 ((2, 1, 2, DEV(4)), (2, 1, 1, [(0, 0), (0, 1)]), [(0, 2), (0, 3)])]:
+        a, b, plan, oa, ob, oplan = _pair(rs, orc, entries, a_cfg, b_cfg, failed)
+        n_src, n_dst = len(a_cfg[3]), len(b_cfg[3])
+        ex = rs.Executor(ctx, plan, [0] * n_src, [0] * n_dst, 4096, central=0)
+        ex.allocate_local()
+        ex.prepare()
+        ex.fill_sources()
+        t = ex.apply()
+        st = plan.stats()
+        assert t[0]["bytes"] == 2 * st["moved_bytes"] + st["relayout_bytes"]
+        assert ex.verify() == 0
+        ostate = oplan.apply(oa.fill())[0]
+        assert _compare_with_oracle(rs, ctx, ex, b, ostate, [d for d in b_cfg[3]]) > 0

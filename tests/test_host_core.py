@@ -145,3 +145,31 @@ def test_planning_only_context_lowers_tiles(rs):
     t1, b1 = ex.tiles(1)
     assert b0 + b1 == st["moved_bytes"] + st["relayout_bytes"]
     assert t0 > 0 and t1 > 0
+
+
+def test_central_mode_layout_and_traffic(rs):
+    """apply_plan(central): the central GPU stages every Move once, so its
+    executed bytes are 2 x moved bytes (fetch + re-upload) plus local relayouts, its dst arena
+    grows by the staging region, and the per-GPU traffic matches plan_cost_central."""
+    cat = rs.Catalog.gpt(64, 4, 16, 128, rs.MIXED_ADAM)
+    for (a_cfg, b_cfg) in [((2, 1, 1, 2), (1, 2, 1, 2)), ((2, 1, 1, 2), (2, 1, 2, 4)), ((4, 2, 1, 8), (2, 2, 2, 8))]:
+        a = cat.build_strategy([(0, i) for i in range(a_cfg[3])], *a_cfg[:3])
+        b = cat.build_strategy([(0, i) for i in range(b_cfg[3])], *b_cfg[:3])
+        plan = rs.generate_plan(a, b)
+        st = plan.stats()
+        G = max(a_cfg[3], b_cfg[3])
+        ctx = rs.Context(G, [], [])
+        dist = rs.Executor(ctx, plan, list(range(a_cfg[3])), list(range(b_cfg[3])), 4096)
+        cen = rs.Executor(ctx, plan, list(range(a_cfg[3])), list(range(b_cfg[3])), 4096, central=0)
+        assert cen.staging_bytes() >= st["moved_bytes"]
+        assert dist.staging_bytes() == 0
+        assert cen.arena_bytes(0)[1] == dist.arena_bytes(0)[1] + cen.staging_bytes()
+        total = sum(cen.tiles(g)[1] for g in range(G))
+        assert total == 2 * st["moved_bytes"] + st["relayout_bytes"]
+        # central GPU 0 re-uploads every moved byte; the others only fetch theirs
+        fetch = sum(dist.tiles(g)[1] for g in range(G)) - st["relayout_bytes"]
+        assert fetch == st["moved_bytes"]
+        assert cen.tiles(0)[1] >= st["moved_bytes"]
+    with pytest.raises(rs.ReshardError) as e:
+        rs.Executor(rs.Context(2, [], []), plan, list(range(8)), list(range(8)), 4096, central=8)
+    assert e.value.name == "InvalidArgument"
