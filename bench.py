@@ -421,8 +421,13 @@ def run_ours(args):
             bounds.append(t + 1)
     bounds.append(len(ent))
     windows = [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
-    exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10, window=w if len(windows) > 1 else None)
-           for w in windows]
+    if args.mode == "central":  # apply_plan(central): one process drives the world, staging on GPU 0
+        if world > 1 or len(windows) > 1:
+            raise SystemExit("--mode central: single-process, single-wave workloads only")
+        exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10, central=0)]
+    else:
+        exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10, window=w if len(windows) > 1 else None)
+               for w in windows]
     s_bytes = max(e.arena_bytes(rank)[0] for e in exs)
     d_bytes = max(e.arena_bytes(rank)[1] for e in exs)
     src_ptr, dst_ptr = ctx.malloc(rank, max(s_bytes, 256)), ctx.malloc(rank, max(d_bytes, 256))
@@ -509,7 +514,8 @@ def run_ours(args):
             rs.host_free(hs)
             rs.host_free(hd)
             e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms", "h2d_bytes_per_step": s_bytes,
-                   "d2h_bytes_per_step": d_bytes, "steps": args.e2e_steps, "mismatched_bytes": bad_e2e}
+                   "d2h_bytes_per_step": d_bytes - ex.staging_bytes(), "steps": args.e2e_steps,
+                   "mismatched_bytes": bad_e2e}
             try:  # the PCIe bound of this path, measured on the same box
                 link = pcie_probe()
                 bound_ms = max(s_bytes / (link["h2d_gbs"] * 1e9), d_bytes / (link["d2h_gbs"] * 1e9),
@@ -562,7 +568,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 payload of the model shapes)",
         "config": {"workload": args.workload, "parallelism": f"{N} GPU" + ("s" if N > 1 else "") +
                    (" (1-GPU emulation of all logical devices)" if N == 1 else ", logical device d on GPU d%N"),
-                   "l2": "inputs larger than L2 (no flush)", "tile_kib": args.tile_kib},
+                   "l2": "inputs larger than L2 (no flush)", "tile_kib": args.tile_kib, "mode": args.mode},
         "effective_gbs": round((stats["moved_bytes"] + stats["relayout_bytes"]) / (ms * 1e-3) / 1e9, 1),
         "moved_bytes": stats["moved_bytes"], "relayout_bytes": stats["relayout_bytes"],
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
@@ -591,6 +597,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS) + sorted(DATASET))
     ap.add_argument("--tile-kib", type=int, default=256)
+    ap.add_argument("--mode", choices=["distributed", "central"], default="distributed",
+                    help="apply_plan mode (SPEC.md:466): central stages every moved fragment on GPU 0")
     ap.add_argument("--waves", type=int, default=0, help="catalog windows run one after another (0: automatic)")
     ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--e2e-steps", type=int, default=3)
