@@ -561,7 +561,8 @@ def run_ours(args):
     alg_bytes = read_bytes + copy_bytes
     achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
     kname = copy_kernel_name()
-    traffic = ncu_traffic(args.workload, kname)
+    # the committed ncu capture is of the distributed-mode launch
+    traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" else None
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",

@@ -193,6 +193,186 @@ __global__ void __launch_bounds__(kThreads, MINB) repartition_kernel(Params p, O
   }
 }
 
+// ---- K5 persistent variant: tiles software-pipelined across the look-back ---------------------
+// r13 profile of the single-pass kernel: 41 % of warp samples wait at the barrier behind the
+// look-back while no gather of that CTA is in flight.  Here each CTA keeps pulling tiles in
+// order and runs two tiles ahead: while tile T is scanned (look-back, offsets, queues), the
+// entry gathers of T+1 and the permutation reads of T+2 are already in flight.  Tiles are
+// 1024 samples (4 per thread) so three tiles' worth of loads fit the register budget.
+constexpr int kPItems = 4, kPTile = kThreads * kPItems;
+
+// Warp 0: publish this tile's aggregate, walk back over predecessors (warp-parallel), publish
+// the inclusive prefix.  Returns the exclusive prefix of the tile (every lane).
+__device__ __forceinline__ Agg decoupled_lookback(unsigned tile, const Agg& total, const Scratch& s, int lane) {
+  Agg prefix{0, 0, 0, 0};
+  if (tile == 0) {
+    if (lane == 0) {
+      stcg(&s.inc[0], total);
+      __threadfence();
+      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[0]).store(2u, ::cuda::memory_order_release);
+    }
+    return prefix;
+  }
+  if (lane == 0) {
+    stcg(&s.agg[tile], total);
+    __threadfence();
+    ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(1u, ::cuda::memory_order_release);
+  }
+  for (long long base = (long long)tile - 1;; base -= 32) {
+    const long long j = base - lane;
+    unsigned f = 2u;
+    Agg v{0, 0, 0, 0};
+    if (j >= 0) {
+      ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device> fl(s.flags[j]);
+      while ((f = fl.load(::cuda::memory_order_acquire)) == 0u) {
+      }
+      v = f == 2u ? ldcg(&s.inc[j]) : ldcg(&s.agg[j]);
+    }
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, f == 2u);
+    const int stop = inc_mask ? __ffs(inc_mask) - 1 : 31;
+    if (lane > stop) v = Agg{0, 0, 0, 0};
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      v.len += __shfl_xor_sync(0xffffffffu, v.len, d);
+      v.c0 += __shfl_xor_sync(0xffffffffu, v.c0, d);
+      v.c1 += __shfl_xor_sync(0xffffffffu, v.c1, d);
+      v.c2 += __shfl_xor_sync(0xffffffffu, v.c2, d);
+    }
+    prefix = prefix + v;
+    if (inc_mask) break;
+  }
+  if (lane == 0) {
+    stcg(&s.inc[tile], prefix + total);
+    __threadfence();
+    ::cuda::atomic_ref<unsigned, ::cuda::thread_scope_device>(s.flags[tile]).store(2u, ::cuda::memory_order_release);
+  }
+  return prefix;
+}
+
+// Position (in the epoch order) of the rank's k-th remaining sample and the cursor after it.
+struct PosCursor {
+  unsigned long long batch, r;
+};
+__device__ __forceinline__ PosCursor pos_cursor(const Params& p, unsigned long long k) {
+  return k < p.in_full ? PosCursor{p.at_step + k / p.b, k % p.b} : PosCursor{0, 0};
+}
+__device__ __forceinline__ unsigned long long next_pos(const Params& p, PosCursor& c, unsigned long long k) {
+  if (k < p.in_full) {
+    const unsigned long long pos = c.batch * p.B + p.rank * p.b + c.r;
+    if (++c.r == p.b) c.r = 0, ++c.batch;
+    return pos;
+  }
+  return p.full * p.B + p.rank * p.b + (k - p.in_full);
+}
+
+__device__ __forceinline__ void load_perm(const Params& p, unsigned tile, unsigned long long (&idx)[kPItems]) {
+  const unsigned long long k0 = (unsigned long long)tile * kPTile + (unsigned long long)threadIdx.x * kPItems;
+  PosCursor c = pos_cursor(p, k0);
+#pragma unroll
+  for (int j = 0; j < kPItems; ++j) {
+    const unsigned long long k = k0 + j;
+    const unsigned long long pos = next_pos(p, c, k);
+    idx[j] = k < p.count ? __ldg(p.perm + pos) : 0ull;
+  }
+}
+struct Entries {
+  unsigned long long f[kPItems], off[kPItems], len[kPItems];
+};
+__device__ __forceinline__ void load_entries(const Params& p, const unsigned long long (&idx)[kPItems], Entries& e) {
+#pragma unroll
+  for (int j = 0; j < kPItems; ++j) {
+    const unsigned long long* q = p.samples + 3 * idx[j];
+    e.f[j] = __ldg(q), e.off[j] = __ldg(q + 1), e.len[j] = __ldg(q + 2);
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) repartition_persistent_kernel(Params p, Outs o, Scratch s) {
+  __shared__ unsigned next_sh;
+  __shared__ Agg warp_tot[kWarps];
+  __shared__ Agg tile_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) next_sh = atomicAdd(s.counter, 1u);
+  __syncthreads();
+  unsigned cur = next_sh;
+  __syncthreads();
+  if (threadIdx.x == 0) next_sh = atomicAdd(s.counter, 1u);
+  __syncthreads();
+  unsigned nxt = next_sh;
+  __syncthreads();  // everyone has read nxt before thread 0 overwrites next_sh in the loop
+  unsigned long long idx[kPItems];
+  Entries ec, en;
+  if (cur < s.ntiles) {
+    load_perm(p, cur, idx);
+    load_entries(p, idx, ec);
+  }
+  if (nxt < s.ntiles) load_perm(p, nxt, idx);
+  while (cur < s.ntiles) {
+    // (1) gathers of the next tile, (2) permutation reads of the one after, both in flight
+    // while the current tile is scanned
+    if (nxt < s.ntiles) load_entries(p, idx, en);
+    if (threadIdx.x == 0) next_sh = atomicAdd(s.counter, 1u);
+    // (3) the current tile: class lookups, pos / entry stores, block scan, look-back
+    const unsigned long long k0 = (unsigned long long)cur * kPTile + (unsigned long long)threadIdx.x * kPItems;
+    unsigned char cls[kPItems];
+    Agg mine{0, 0, 0, 0};
+    PosCursor c = pos_cursor(p, k0);
+#pragma unroll
+    for (int j = 0; j < kPItems; ++j) {
+      const unsigned long long k = k0 + j;
+      const unsigned long long pos = next_pos(p, c, k);
+      cls[j] = 3;
+      if (k < p.count) {
+        cls[j] = __ldg(p.file_class + ec.f[j]);
+        o.pos[k] = pos;
+        o.ent[3 * k] = ec.f[j], o.ent[3 * k + 1] = ec.off[j], o.ent[3 * k + 2] = ec.len[j];
+        mine.len += ec.len[j];
+        mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
+      }
+    }
+    Agg inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      Agg up = shfl_up(inc, d);
+      if (lane >= d) inc = inc + up;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();  // barrier 1: warp totals and next_sh visible
+    const unsigned after = next_sh;
+    Agg warp_base{0, 0, 0, 0}, total{0, 0, 0, 0};
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      if (w < warp) warp_base = warp_base + warp_tot[w];
+      total = total + warp_tot[w];
+    }
+    if (after < s.ntiles) load_perm(p, after, idx);
+    if (warp == 0) {
+      const Agg prefix = decoupled_lookback(cur, total, s, lane);
+      if (lane == 0) {
+        tile_prefix = prefix;
+        if (cur == s.ntiles - 1) {
+          const Agg all = prefix + total;
+          o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
+        }
+      }
+    }
+    __syncthreads();  // barrier 2: tile prefix visible
+    Agg run = tile_prefix + warp_base +
+              Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
+#pragma unroll
+    for (int j = 0; j < kPItems; ++j) {
+      const unsigned long long k = k0 + j;
+      if (k >= p.count) break;
+      o.boff[k] = run.len;
+      run.len += ec.len[j];
+      if (cls[j] == 0) o.q0[run.c0++] = unsigned(k);
+      else if (cls[j] == 1) o.q1[run.c1++] = unsigned(k);
+      else o.q2[run.c2++] = unsigned(k);
+    }
+    cur = nxt, nxt = after, ec = en;
+  }
+}
+
 // ---- random-gather ceiling (diagnostic) -----------------------------------------------------
 // K5's two HBM-random levels alone — the rank's perm positions, one 24-byte entry gather per
 // position, nothing written but one word per thread — at the configuration the standalone
@@ -519,8 +699,16 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
   return t;
 }
 
+// RESHARD_K5=persistent: 2 CTAs per SM (no spills); persistent3: 3 CTAs per SM (spills)
+int k5_persistent() {
+  const char* v = std::getenv("RESHARD_K5");
+  if (!v) return 0;
+  const std::string s(v);
+  return s == "persistent" ? 2 : s == "persistent3" ? 3 : 0;
+}
+
 uint64_t repartition_scratch_bytes(uint64_t count) {
-  const uint64_t tiles = (count + kTile - 1) / kTile;
+  const uint64_t tiles = (count + kPTile - 1) / kPTile;  // the smallest tile of the variants
   // look-back: counter + flags + aggregates + inclusive prefixes; split: + class bytes
   return 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)) + align256(count);
 }
@@ -529,7 +717,9 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch) {
   const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
   if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
-  const uint64_t tiles = (count + kTile - 1) / kTile;
+  const int persistent = k5_persistent();  // resident CTAs per SM, 0: not persistent
+  const uint64_t tile = persistent ? kPTile : kTile;
+  const uint64_t tiles = (count + tile - 1) / tile;
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
@@ -554,6 +744,11 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
     repart_gather_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.agg, cls);
     repart_scan_kernel<<<1, 1024, 0, st>>>(s.agg, s.inc, unsigned(tiles), o);
     repart_finalize_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
+    ck(cudaGetLastError(), "repartition launch");
+  } else if (tiles && persistent) {
+    const uint64_t grid = std::min<uint64_t>(tiles, uint64_t(ctx.sm_count(gpu)) * uint64_t(persistent));
+    if (persistent == 3) repartition_persistent_kernel<3><<<unsigned(grid), kThreads, 0, st>>>(p, o, s);
+    else repartition_persistent_kernel<2><<<unsigned(grid), kThreads, 0, st>>>(p, o, s);
     ck(cudaGetLastError(), "repartition launch");
   } else if (tiles) {
     if (k5_min_blocks() == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);

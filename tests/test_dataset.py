@@ -104,7 +104,7 @@ def test_acceptance8_exactly_once_under_dp_changes(rs):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["split", "lookback"])
+@pytest.mark.parametrize("mode", ["split", "lookback", "persistent", "persistent3"])
 def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, monkeypatch):
     monkeypatch.setenv("RESHARD_K5", mode)
     rng = random.Random(42)
