@@ -90,6 +90,8 @@ typedef struct rs_timing {
   uint64_t bytes;          /* algorithmic bytes written by this GPU */
   uint64_t launches;       /* kernels launched in the timed region */
   uint64_t read_bytes;     /* algorithmic bytes read (fan-out tiles read their source once) */
+  float main_ms;           /* CUDA-event time of the dominant kernel alone, 0 if not timed
+                              separately (rs_repartition: the gather pass) */
 } rs_timing;
 
 typedef struct rs_cell_binding {

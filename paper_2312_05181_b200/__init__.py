@@ -683,12 +683,14 @@ def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_p
     out = part.c()
     _chk(lib.rs_repartition(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, C.byref(out),
                             part.scratch, C.byref(t)))
-    return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches)
+    return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, gather_ms=t.main_ms)
 
 
 def repartition_gather_probe(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, n: int, global_batch: int,
                              at_step: int, new_dp: int, rank: int, reps: int = 3) -> dict:
-    """Diagnostic: device time of K5's random reads alone (the floor for the gather)."""
+    """Diagnostic: device time of K5's gathers plus its 44 output bytes per sample, coalesced and
+    with no scan (the floor for any kernel producing the partition); RESHARD_PROBE=read times
+    the gathers alone."""
     idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, 0, n)
     t = _capi.rs_timing()
     _chk(lib.rs_repartition_gather_probe(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, reps,

@@ -43,7 +43,7 @@ class rs_plan_stats(C.Structure):
 
 class rs_timing(C.Structure):
     _fields_ = [("ms", C.c_float), ("tiles", C.c_uint64), ("bytes", C.c_uint64), ("launches", C.c_uint64),
-                ("read_bytes", C.c_uint64)]
+                ("read_bytes", C.c_uint64), ("main_ms", C.c_float)]
 
 
 class rs_cell_binding(C.Structure):

@@ -556,14 +556,14 @@ int rs_executor_wait(rs_executor* e, int cap, rs_timing* out, int* n) {
     auto t = e->e->wait();
     *n = int(t.size());
     for (int i = 0; i < *n && i < cap; ++i)
-      out[i] = rs_timing{t[size_t(i)].ms, t[size_t(i)].tiles, t[size_t(i)].bytes, t[size_t(i)].launches, t[size_t(i)].read_bytes};
+      out[i] = rs_timing{t[size_t(i)].ms, t[size_t(i)].tiles, t[size_t(i)].bytes, t[size_t(i)].launches, t[size_t(i)].read_bytes, t[size_t(i)].main_ms};
   });
 }
 int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src, void* host_dst, rs_timing* out) {
   return guard([&] {
     need(e, "executor"), need(out, "out");
     Timing t = e->e->run_host(gpu, host_src, host_dst);
-    *out = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
+    *out = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
 int rs_executor_host_phase(rs_executor* e, int gpu, int phase, void* host_buf) {
@@ -711,7 +711,7 @@ int rs_shuffle_epoch_device(rs_context* c, int gpu, uint64_t n, uint64_t seed, u
   return guard([&] {
     need(perm, "perm"), need(scratch, "scratch");
     Timing t = shuffle_epoch_device(ctx_of(c), gpu, n, seed, epoch, perm, scratch);
-    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes) {
@@ -727,7 +727,7 @@ int rs_repartition(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t
     DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n};
     PartitionOut o{out->pos, out->ent, out->boff, {out->queue[0], out->queue[1], out->queue[2]}, out->qcount};
     Timing t = repartition_device(ctx_of(c), gpu, v, B, at_step, dp, rank, o, scratch);
-    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
 int rs_repartition_gather_probe(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t B, uint64_t at_step,
@@ -736,7 +736,7 @@ int rs_repartition_gather_probe(rs_context* c, int gpu, const rs_dataset_index* 
     need(idx, "index"), need(timing, "timing");
     DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n};
     Timing t = repartition_gather_probe(ctx_of(c), gpu, v, B, at_step, dp, rank, reps);
-    *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes};
+    *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
 

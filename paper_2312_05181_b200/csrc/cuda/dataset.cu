@@ -1,14 +1,15 @@
-// K5 dataset_repartition (sm_100a): for one new DP rank, in ONE pass over its remaining
-// samples —
+// K5 dataset_repartition (sm_100a): for one new DP rank, over its remaining samples k —
 //   pos[k]  = closed-form global position,
 //   ent[k]  = samples[perm[pos[k]]]                (24-byte gather through the permutation),
 //   boff[k] = exclusive prefix sum of lengths       (the sample's offset in the read buffer),
 //   queue[class] += k                               (stable compaction by locator class,
 //                                                    local > peer > remote).
-// The scan is a single-pass decoupled look-back: each CTA takes the next tile from an
-// atomic counter (so it only ever waits on tiles already owned by running CTAs), scans its
-// 2048 items with warp shuffles, publishes its aggregate, looks back over predecessors'
-// aggregates / inclusive prefixes, and publishes its inclusive prefix.
+// Default (split2): a register-light gather pass at full occupancy writes pos / entries,
+// parks each length in boff and each class in a byte, and reduces one aggregate per
+// 1024-sample tile; a few-CTA tile scan (decoupled look-back over 1024-tile blocks) turns
+// the aggregates into prefixes; a finalize pass turns the parked lengths into offsets in
+// place and fills the class queues.  The single-pass decoupled look-back kernel
+// (repartition_kernel) stays selectable (RESHARD_K5=lookback).
 // Replaces the CPU loops of oracle.cpp orc_dataset_gather (SPEC restatement).
 #include <cuda/atomic>
 #include <cuda_runtime.h>
@@ -193,13 +194,7 @@ __global__ void __launch_bounds__(kThreads, MINB) repartition_kernel(Params p, O
   }
 }
 
-// ---- K5 persistent variant: tiles software-pipelined across the look-back ---------------------
-// r13 profile of the single-pass kernel: 41 % of warp samples wait at the barrier behind the
-// look-back while no gather of that CTA is in flight.  Here each CTA keeps pulling tiles in
-// order and runs two tiles ahead: while tile T is scanned (look-back, offsets, queues), the
-// entry gathers of T+1 and the permutation reads of T+2 are already in flight.  Tiles are
-// 1024 samples (4 per thread) so three tiles' worth of loads fit the register budget.
-constexpr int kPItems = 4, kPTile = kThreads * kPItems;
+// ---- shared helpers ---------------------------------------------------------------------
 
 // Warp 0: publish this tile's aggregate, walk back over predecessors (warp-parallel), publish
 // the inclusive prefix.  Returns the exclusive prefix of the tile (every lane).
@@ -249,136 +244,22 @@ __device__ __forceinline__ Agg decoupled_lookback(unsigned tile, const Agg& tota
   return prefix;
 }
 
-// Position (in the epoch order) of the rank's k-th remaining sample and the cursor after it.
-struct PosCursor {
-  unsigned long long batch, r;
-};
-__device__ __forceinline__ PosCursor pos_cursor(const Params& p, unsigned long long k) {
-  return k < p.in_full ? PosCursor{p.at_step + k / p.b, k % p.b} : PosCursor{0, 0};
-}
-__device__ __forceinline__ unsigned long long next_pos(const Params& p, PosCursor& c, unsigned long long k) {
+// count < 2^32 (checked by the host), so k and the in-batch arithmetic are 32-bit
+__device__ __forceinline__ unsigned long long sample_pos(const Params& p, unsigned k) {
   if (k < p.in_full) {
-    const unsigned long long pos = c.batch * p.B + p.rank * p.b + c.r;
-    if (++c.r == p.b) c.r = 0, ++c.batch;
-    return pos;
+    const unsigned b = unsigned(p.b), q = k / b;
+    return (p.at_step + q) * p.B + p.rank * p.b + (k - q * b);
   }
   return p.full * p.B + p.rank * p.b + (k - p.in_full);
 }
 
-__device__ __forceinline__ void load_perm(const Params& p, unsigned tile, unsigned long long (&idx)[kPItems]) {
-  const unsigned long long k0 = (unsigned long long)tile * kPTile + (unsigned long long)threadIdx.x * kPItems;
-  PosCursor c = pos_cursor(p, k0);
-#pragma unroll
-  for (int j = 0; j < kPItems; ++j) {
-    const unsigned long long k = k0 + j;
-    const unsigned long long pos = next_pos(p, c, k);
-    idx[j] = k < p.count ? __ldg(p.perm + pos) : 0ull;
-  }
-}
-struct Entries {
-  unsigned long long f[kPItems], off[kPItems], len[kPItems];
-};
-__device__ __forceinline__ void load_entries(const Params& p, const unsigned long long (&idx)[kPItems], Entries& e) {
-#pragma unroll
-  for (int j = 0; j < kPItems; ++j) {
-    const unsigned long long* q = p.samples + 3 * idx[j];
-    e.f[j] = __ldg(q), e.off[j] = __ldg(q + 1), e.len[j] = __ldg(q + 2);
-  }
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) repartition_persistent_kernel(Params p, Outs o, Scratch s) {
-  __shared__ unsigned next_sh;
-  __shared__ Agg warp_tot[kWarps];
-  __shared__ Agg tile_prefix;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) next_sh = atomicAdd(s.counter, 1u);
-  __syncthreads();
-  unsigned cur = next_sh;
-  __syncthreads();
-  if (threadIdx.x == 0) next_sh = atomicAdd(s.counter, 1u);
-  __syncthreads();
-  unsigned nxt = next_sh;
-  __syncthreads();  // everyone has read nxt before thread 0 overwrites next_sh in the loop
-  unsigned long long idx[kPItems];
-  Entries ec, en;
-  if (cur < s.ntiles) {
-    load_perm(p, cur, idx);
-    load_entries(p, idx, ec);
-  }
-  if (nxt < s.ntiles) load_perm(p, nxt, idx);
-  while (cur < s.ntiles) {
-    // (1) gathers of the next tile, (2) permutation reads of the one after, both in flight
-    // while the current tile is scanned
-    if (nxt < s.ntiles) load_entries(p, idx, en);
-    if (threadIdx.x == 0) next_sh = atomicAdd(s.counter, 1u);
-    // (3) the current tile: class lookups, pos / entry stores, block scan, look-back
-    const unsigned long long k0 = (unsigned long long)cur * kPTile + (unsigned long long)threadIdx.x * kPItems;
-    unsigned char cls[kPItems];
-    Agg mine{0, 0, 0, 0};
-    PosCursor c = pos_cursor(p, k0);
-#pragma unroll
-    for (int j = 0; j < kPItems; ++j) {
-      const unsigned long long k = k0 + j;
-      const unsigned long long pos = next_pos(p, c, k);
-      cls[j] = 3;
-      if (k < p.count) {
-        cls[j] = __ldg(p.file_class + ec.f[j]);
-        o.pos[k] = pos;
-        o.ent[3 * k] = ec.f[j], o.ent[3 * k + 1] = ec.off[j], o.ent[3 * k + 2] = ec.len[j];
-        mine.len += ec.len[j];
-        mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
-      }
-    }
-    Agg inc = mine;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      Agg up = shfl_up(inc, d);
-      if (lane >= d) inc = inc + up;
-    }
-    if (lane == 31) warp_tot[warp] = inc;
-    __syncthreads();  // barrier 1: warp totals and next_sh visible
-    const unsigned after = next_sh;
-    Agg warp_base{0, 0, 0, 0}, total{0, 0, 0, 0};
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      if (w < warp) warp_base = warp_base + warp_tot[w];
-      total = total + warp_tot[w];
-    }
-    if (after < s.ntiles) load_perm(p, after, idx);
-    if (warp == 0) {
-      const Agg prefix = decoupled_lookback(cur, total, s, lane);
-      if (lane == 0) {
-        tile_prefix = prefix;
-        if (cur == s.ntiles - 1) {
-          const Agg all = prefix + total;
-          o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
-        }
-      }
-    }
-    __syncthreads();  // barrier 2: tile prefix visible
-    Agg run = tile_prefix + warp_base +
-              Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
-#pragma unroll
-    for (int j = 0; j < kPItems; ++j) {
-      const unsigned long long k = k0 + j;
-      if (k >= p.count) break;
-      o.boff[k] = run.len;
-      run.len += ec.len[j];
-      if (cls[j] == 0) o.q0[run.c0++] = unsigned(k);
-      else if (cls[j] == 1) o.q1[run.c1++] = unsigned(k);
-      else o.q2[run.c2++] = unsigned(k);
-    }
-    cur = nxt, nxt = after, ec = en;
-  }
-}
-
-// ---- random-gather ceiling (diagnostic) -----------------------------------------------------
-// K5's two HBM-random levels alone — the rank's perm positions, one 24-byte entry gather per
-// position, nothing written but one word per thread — at the configuration the standalone
-// probe found fastest (4 items per thread, 256 threads; scripts/probe_gather.cu, profiles/r12).
-// Its time is the floor for any kernel that must gather these entries: bench.py reports K5
-// against it next to the streaming-HBM roofline.
+// ---- random-gather floors (diagnostic) --------------------------------------------------------
+// gather_probe_kernel: K5's two HBM-random levels alone — the rank's perm positions, one
+// 24-byte entry gather per position, nothing written but one word per thread — at the
+// configuration the standalone probe found fastest (4 items per thread, 256 threads;
+// scripts/probe_gather.cu, profiles/r12).  gather_write_probe_kernel (below, the default of
+// repartition_gather_probe): the same gathers plus every output byte K5 must write.  bench.py
+// reports K5 against the latter next to the streaming-HBM roofline.
 constexpr int kProbeItems = 4;
 __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsigned long long* sink) {
   const unsigned long long k0 =
@@ -409,131 +290,185 @@ __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsign
   if (acc == 0x9e3779b97f4a7c15ull) *sink = acc;  // keeps the loads; practically never stores
 }
 
-// ---- K5 split variant: gather / scan / finalize -------------------------------------------
-// r05 profile: 27% of the single-pass kernel's stall samples sit behind the block barrier
-// that waits for the decoupled look-back.  The split variant never waits: (a) a pure
-// gather kernel writes pos / entry, parks each sample's length in boff and its class in a
-// byte array, and reduces one aggregate per tile; (b) one CTA scans the tile aggregates;
-// (c) a streaming kernel turns lengths into offsets and fills the locator queues.  Extra
-// traffic: 9 bytes per sample written and read back (~5% of the gather's DRAM bytes).
-__device__ __forceinline__ Agg block_exclusive(const Agg& mine, Agg* warp_tot, Agg& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Agg inc = mine;
+// The same gathers plus K5's 44 output bytes per sample (pos, entry, a length word, a u32
+// queue word), warp-striped so every store is coalesced, and no scan: the floor of any
+// kernel that must both gather the entries and write the partition (RESHARD_PROBE=write).
+__global__ void __launch_bounds__(kThreads) gather_write_probe_kernel(Params p, Outs o) {
+  unsigned long long idx[kProbeItems], pos[kProbeItems];
+  const unsigned long long base = (unsigned long long)blockIdx.x * (kThreads * kProbeItems) + threadIdx.x;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    Agg up = shfl_up(inc, d);
-    if (lane >= d) inc = inc + up;
+  for (int j = 0; j < kProbeItems; ++j) {
+    const unsigned long long k = base + j * kThreads;
+    pos[j] = k < p.count ? sample_pos(p, unsigned(k)) : 0ull;
+    idx[j] = k < p.count ? __ldg(p.perm + pos[j]) : 0ull;
   }
-  if (lane == 31) warp_tot[warp] = inc;
-  __syncthreads();
-  Agg base{0, 0, 0, 0};
-  total = Agg{0, 0, 0, 0};
+  unsigned long long f[kProbeItems], off[kProbeItems], len[kProbeItems];
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    if (w < warp) base = base + warp_tot[w];
-    total = total + warp_tot[w];
-  }
-  return base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
-}
-
-__global__ void __launch_bounds__(kThreads) repart_gather_kernel(Params p, Outs o, Agg* agg, unsigned char* cls_out) {
-  __shared__ Agg warp_tot[kWarps];
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * kTile + (unsigned long long)threadIdx.x * kItems;
-  unsigned long long batch = 0, r = 0;
-  if (k0 < p.in_full) batch = p.at_step + k0 / p.b, r = k0 % p.b;
-  unsigned long long pos[kItems], idx[kItems], f[kItems], off[kItems], len[kItems];
-  const unsigned nv = p.count > k0 ? unsigned(min(p.count - k0, (unsigned long long)kItems)) : 0u;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const unsigned long long k = k0 + j;
-    if (k < p.in_full) {
-      pos[j] = batch * p.B + p.rank * p.b + r;
-      if (++r == p.b) r = 0, ++batch;
-    } else {
-      pos[j] = p.full * p.B + p.rank * p.b + (k - p.in_full);
-    }
-    idx[j] = j < nv ? __ldg(p.perm + pos[j]) : 0ull;
-  }
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < kProbeItems; ++j) {
     const unsigned long long* e = p.samples + 3 * idx[j];
-    if (j < nv) f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
-    else f[j] = 0, off[j] = 0, len[j] = 0;
+    f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
   }
-  Agg mine{0, 0, 0, 0};
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    if (j >= nv) continue;
-    const unsigned long long k = k0 + j;
-    const unsigned char c = __ldg(p.file_class + f[j]);
+  for (int j = 0; j < kProbeItems; ++j) {
+    const unsigned long long k = base + j * kThreads;
+    if (k >= p.count) break;
     o.pos[k] = pos[j];
     o.ent[3 * k] = f[j], o.ent[3 * k + 1] = off[j], o.ent[3 * k + 2] = len[j];
-    o.boff[k] = len[j];  // parked; finalize turns it into the offset
-    cls_out[k] = c;
-    mine.len += len[j];
-    mine.c0 += c == 0, mine.c1 += c == 1, mine.c2 += c == 2;
+    o.boff[k] = len[j];
+    o.q0[k] = unsigned(f[j]);
   }
-  Agg total;
-  block_exclusive(mine, warp_tot, total);
-  if (threadIdx.x == 0) agg[blockIdx.x] = total;
 }
 
-// One CTA: exclusive scan of the tile aggregates, and the queue totals.
-__global__ void __launch_bounds__(1024) repart_scan_kernel(const Agg* agg, Agg* prefix, unsigned ntiles, Outs o) {
-  __shared__ Agg warp_tot[32];
-  const unsigned per = (ntiles + blockDim.x - 1) / blockDim.x;
-  const unsigned t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
-  Agg mine{0, 0, 0, 0};
-  for (unsigned t = t0; t < t1; ++t) mine = mine + agg[t];
+// ---- K5 split2: register-light gather at full occupancy / scan / finalize ------------------
+// r16 probes: the entry gathers plus every output store of K5 (44 B / sample, coalesced) run
+// in 3.50 ms per step when nothing waits (gather_write_probe_kernel), against 6.36 ms for the
+// single-pass kernel, whose 80-register threads (3 CTAs / SM) hold 8 entries each and then
+// stall behind the look-back.  split2 keeps the probe's shape for the heavy pass: 4 items per
+// thread, 32 registers, 8 CTAs / SM (8192 gathers in flight per SM), warp-contiguous items so
+// every store is coalesced, and a register-only tile reduction instead of a scan.  Lengths are
+// parked in boff and classes in a byte array (9 B / sample written and re-read); one CTA scans
+// the tile aggregates; the finalize pass turns the parked lengths into offsets in place and
+// fills the class queues with ballots.
+constexpr int kGItems = 4, kGTile = kThreads * kGItems, kGWarpItems = 32 * kGItems;
+constexpr int kClsBits = 21;  // per-class counts packed into one u64 (a tile has <= 1024 items)
+constexpr unsigned long long kClsMask = (1ull << kClsBits) - 1;
+
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p, Outs o, Scratch sc,
+                                                                         unsigned char* cls_out) {
+  __shared__ unsigned long long warp_len[kWarps], warp_cnt[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * kGTile + warp * kGWarpItems + lane;
+  unsigned long long idx[kGItems];
+#pragma unroll
+  for (int j = 0; j < kGItems; ++j) {
+    const unsigned long long k = k0 + 32 * j;
+    idx[j] = k < p.count ? __ldg(p.perm + sample_pos(p, unsigned(k))) : 0ull;
+  }
+  unsigned long long f[kGItems], off[kGItems], len[kGItems];
+#pragma unroll
+  for (int j = 0; j < kGItems; ++j) {
+    const unsigned long long* e = p.samples + 3 * idx[j];
+    const bool v = k0 + 32 * j < p.count;
+    f[j] = v ? __ldg(e) : 0ull, off[j] = v ? __ldg(e + 1) : 0ull, len[j] = v ? __ldg(e + 2) : 0ull;
+  }
+  unsigned long long lsum = 0, cnt = 0;
+#pragma unroll
+  for (int j = 0; j < kGItems; ++j) {
+    const unsigned long long k = k0 + 32 * j;
+    if (k < p.count) {
+      const unsigned char c = min(__ldg(p.file_class + f[j]), (unsigned char)2);  // 0 local, 1 peer, 2 remote
+      o.pos[k] = sample_pos(p, unsigned(k));
+      o.ent[3 * k] = f[j], o.ent[3 * k + 1] = off[j], o.ent[3 * k + 2] = len[j];
+      o.boff[k] = len[j];  // parked; finalize turns it into the offset
+      cls_out[k] = c;
+      lsum += len[j];
+      cnt += 1ull << (kClsBits * c);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, d);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+  }
+  if (lane == 0) warp_len[warp] = lsum, warp_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long L = 0, C = 0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) L += warp_len[q], C += warp_cnt[q];
+    sc.agg[blockIdx.x] = Agg{L, C & kClsMask, (C >> kClsBits) & kClsMask, C >> (2 * kClsBits)};
+  }
+  if (blockIdx.x == 0)  // the tile scan's look-back flags (one per 1024 tiles), consumed after this launch
+    for (unsigned i = threadIdx.x; i < (sc.ntiles + 1023) / 1024; i += kThreads) sc.flags[i] = 0u;
+}
+
+// Exclusive scan of the tile aggregates: one 1024-thread CTA per 1024 tiles (coalesced loads,
+// block scan in registers and shared memory), chained by a decoupled look-back over the few
+// block aggregates (the flags were cleared by the gather pass).  Writes prefix[t] (s.inc)
+// and the queue totals.
+__global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg* blk_agg, Agg* blk_inc, Outs o) {
+  __shared__ Agg warp_tot[32];
+  __shared__ Agg blk_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned t = blockIdx.x * 1024u + threadIdx.x;
+  const Agg mine = t < sc.ntiles ? sc.agg[t] : Agg{0, 0, 0, 0};
   Agg inc = mine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    Agg up = shfl_up(inc, d);
+    const Agg up = shfl_up(inc, d);
     if (lane >= d) inc = inc + up;
   }
   if (lane == 31) warp_tot[warp] = inc;
   __syncthreads();
   Agg base{0, 0, 0, 0}, total{0, 0, 0, 0};
-  for (int w = 0; w < int(blockDim.x >> 5); ++w) {
-    if (w < warp) base = base + warp_tot[w];
-    total = total + warp_tot[w];
+  for (int q = 0; q < 32; ++q) {
+    if (q < warp) base = base + warp_tot[q];
+    total = total + warp_tot[q];
   }
-  Agg run = base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
-  for (unsigned t = t0; t < t1; ++t) {
-    prefix[t] = run;
-    run = run + agg[t];
+  if (warp == 0) {
+    const Scratch bs{nullptr, sc.flags, blk_agg, blk_inc, gridDim.x};
+    const Agg prefix = decoupled_lookback(blockIdx.x, total, bs, lane);
+    if (lane == 0) {
+      blk_prefix = prefix;
+      if (blockIdx.x == gridDim.x - 1) {
+        const Agg all = prefix + total;
+        o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
+      }
+    }
   }
-  if (threadIdx.x == 0) o.qcount[0] = total.c0, o.qcount[1] = total.c1, o.qcount[2] = total.c2;
+  __syncthreads();
+  if (t < sc.ntiles)
+    sc.inc[t] = blk_prefix + base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
 }
 
-__global__ void __launch_bounds__(kThreads) repart_finalize_kernel(Params p, Outs o, const Agg* prefix,
-                                                                   const unsigned char* cls_in) {
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
+                                                                     const unsigned char* cls_in) {
   __shared__ Agg warp_tot[kWarps];
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * kTile + (unsigned long long)threadIdx.x * kItems;
-  unsigned long long len[kItems];
-  unsigned char cls[kItems];
-  Agg mine{0, 0, 0, 0};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * kGTile + warp * kGWarpItems + lane;
+  unsigned long long len[kGItems];
+  unsigned char cls[kGItems];
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const unsigned long long k = k0 + j;
+  for (int j = 0; j < kGItems; ++j) {
+    const unsigned long long k = k0 + 32 * j;
     len[j] = k < p.count ? o.boff[k] : 0ull;
     cls[j] = k < p.count ? cls_in[k] : (unsigned char)3;
-    mine.len += len[j];
-    mine.c0 += cls[j] == 0, mine.c1 += cls[j] == 1, mine.c2 += cls[j] == 2;
   }
-  Agg total;
-  const Agg excl = block_exclusive(mine, warp_tot, total);
-  Agg run = prefix[blockIdx.x] + excl;
+  unsigned long long lenx[kGItems];
+  Agg w{0, 0, 0, 0};
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const unsigned long long k = k0 + j;
-    if (k >= p.count) break;
-    o.boff[k] = run.len;
-    run.len += len[j];
-    if (cls[j] == 0) o.q0[run.c0++] = unsigned(k);
-    else if (cls[j] == 1) o.q1[run.c1++] = unsigned(k);
-    else o.q2[run.c2++] = unsigned(k);
+  for (int j = 0; j < kGItems; ++j) {
+    unsigned long long inc = len[j];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long up = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += up;
+    }
+    lenx[j] = w.len + inc - len[j];
+    w.len += __shfl_sync(0xffffffffu, inc, 31);
+    w.c0 += __popc(__ballot_sync(0xffffffffu, cls[j] == 0));
+    w.c1 += __popc(__ballot_sync(0xffffffffu, cls[j] == 1));
+    w.c2 += __popc(__ballot_sync(0xffffffffu, cls[j] == 2));
+  }
+  if (lane == 0) warp_tot[warp] = w;
+  __syncthreads();
+  Agg run = prefix[blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < kWarps; ++q)
+    if (q < warp) run = run + warp_tot[q];
+#pragma unroll
+  for (int j = 0; j < kGItems; ++j) {
+    const unsigned long long k = k0 + 32 * j;
+    if (k < p.count) o.boff[k] = run.len + lenx[j];
+    const unsigned m0 = __ballot_sync(0xffffffffu, cls[j] == 0), m1 = __ballot_sync(0xffffffffu, cls[j] == 1),
+                   m2 = __ballot_sync(0xffffffffu, cls[j] == 2);
+    if (cls[j] == 0) o.q0[run.c0 + __popc(m0 & lt)] = unsigned(k);
+    else if (cls[j] == 1) o.q1[run.c1 + __popc(m1 & lt)] = unsigned(k);
+    else if (cls[j] == 2) o.q2[run.c2 + __popc(m2 & lt)] = unsigned(k);
+    run.c0 += __popc(m0), run.c1 += __popc(m1), run.c2 += __popc(m2);
   }
 }
 
@@ -542,16 +477,27 @@ void ck(cudaError_t e, const char* what) {
 }
 uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 
-bool k5_split() {
+// K5 variant (RESHARD_K5): "split2" (default: gather pass at 5 resident CTAs / SM, tile
+// scan, finalize), "split2_6" / "split2_8" (gather pass at 6 / 8 CTAs / SM), "lookback" /
+// "lookback4" (the single-pass decoupled look-back kernel at 3 / 4 CTAs / SM).  r16 same-box
+// A/B (profiles/r16): split2 4.25 ms, split2_6 4.31, split2_8 4.88, lookback 6.34 per step.
+struct K5Mode {
+  bool lookback = false;
+  int minb = 5;  // resident CTAs per SM the chosen gather kernel is compiled for
+  int fin_minb = 0;
+};
+K5Mode k5_mode() {
+  K5Mode m;
   const char* v = std::getenv("RESHARD_K5");
-  // r11: split 6.59 ms vs single-pass 6.38 ms per step; r13 (single-pass with pos stored
-  // early, 80 regs and no spills): 6.57 vs 6.78 — that change was reverted
-  return v && std::string(v) == "split";
-}
-// resident CTAs per SM the single-pass kernel is compiled for (RESHARD_K5=lookback4: 4)
-int k5_min_blocks() {
-  const char* v = std::getenv("RESHARD_K5");
-  return v && std::string(v) == "lookback4" ? 4 : 3;
+  const std::string s = v ? v : "";
+  if (s == "lookback") m.lookback = true, m.minb = 3;
+  else if (s == "lookback4") m.lookback = true, m.minb = 4;
+  else if (s == "split2_6") m.minb = 6;
+  else if (s == "split2_8") m.minb = 8;
+  else if (!s.empty() && s != "split2") raise(Errc::InvalidArgument, "RESHARD_K5: unknown variant " + s);
+  const char* f = std::getenv("RESHARD_K5_FIN");
+  m.fin_minb = f && std::string(f) == "8" ? 8 : 0;
+  return m;
 }
 
 // The dataset kernels are random 8- and 24-byte gathers: with the default L2 fetch
@@ -699,33 +645,28 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
   return t;
 }
 
-// RESHARD_K5=persistent: 2 CTAs per SM (no spills); persistent3: 3 CTAs per SM (spills)
-int k5_persistent() {
-  const char* v = std::getenv("RESHARD_K5");
-  if (!v) return 0;
-  const std::string s(v);
-  return s == "persistent" ? 2 : s == "persistent3" ? 3 : 0;
-}
-
 uint64_t repartition_scratch_bytes(uint64_t count) {
-  const uint64_t tiles = (count + kPTile - 1) / kPTile;  // the smallest tile of the variants
-  // look-back: counter + flags + aggregates + inclusive prefixes; split: + class bytes
-  return 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)) + align256(count);
+  const uint64_t tiles = (count + kGTile - 1) / kGTile;  // the smaller tile of the variants
+  // counter + flags + tile aggregates + tile prefixes; split2: + class bytes + the tile
+  // scan's block aggregates / inclusive prefixes
+  return 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)) + align256(count) +
+         2 * align256((tiles + 1023) / 1024 * sizeof(Agg));
 }
 
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch) {
   const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
   if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
-  const int persistent = k5_persistent();  // resident CTAs per SM, 0: not persistent
-  const uint64_t tile = persistent ? kPTile : kTile;
+  const K5Mode mode = k5_mode();
+  const uint64_t tile = mode.lookback ? kTile : kGTile;
   const uint64_t tiles = (count + tile - 1) / tile;
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
-  cudaEvent_t e0, e1;
+  cudaEvent_t e0, e1, em;  // em: end of the gather pass (the dominant kernel)
   ck(cudaEventCreate(&e0), "event");
   ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventCreate(&em), "event");
   char* sc = static_cast<char*>(scratch);
   Scratch s{reinterpret_cast<unsigned*>(sc), reinterpret_cast<unsigned*>(sc + 256),
             reinterpret_cast<Agg*>(sc + 256 + align256(tiles * 4)),
@@ -736,22 +677,22 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
            at_step, b, rank, count, full > at_step ? (full - at_step) * b : 0, full};
   Outs o{reinterpret_cast<ull*>(out.pos), reinterpret_cast<ull*>(out.ent), reinterpret_cast<ull*>(out.boff),
          out.queue[0], out.queue[1], out.queue[2], reinterpret_cast<ull*>(out.qcount)};
-  const bool split = k5_split();
-  if (!split) ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
+  if (mode.lookback) ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
   ck(cudaEventRecord(e0, st), "event");
-  if (tiles && split) {
+  if (tiles && !mode.lookback) {
     auto* cls = reinterpret_cast<unsigned char*>(sc + 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)));
-    repart_gather_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.agg, cls);
-    repart_scan_kernel<<<1, 1024, 0, st>>>(s.agg, s.inc, unsigned(tiles), o);
-    repart_finalize_kernel<<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
-    ck(cudaGetLastError(), "repartition launch");
-  } else if (tiles && persistent) {
-    const uint64_t grid = std::min<uint64_t>(tiles, uint64_t(ctx.sm_count(gpu)) * uint64_t(persistent));
-    if (persistent == 3) repartition_persistent_kernel<3><<<unsigned(grid), kThreads, 0, st>>>(p, o, s);
-    else repartition_persistent_kernel<2><<<unsigned(grid), kThreads, 0, st>>>(p, o, s);
+    if (mode.minb == 6) repart_gather2_kernel<6><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s, cls);
+    else if (mode.minb == 8) repart_gather2_kernel<8><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s, cls);
+    else repart_gather2_kernel<5><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s, cls);
+    ck(cudaEventRecord(em, st), "event");
+    const uint64_t sblocks = (tiles + 1023) / 1024;
+    Agg* blk = reinterpret_cast<Agg*>(cls + align256(count));
+    repart_tile_scan_kernel<<<unsigned(sblocks), 1024, 0, st>>>(s, blk, blk + sblocks, o);
+    if (mode.fin_minb == 8) repart_finalize2_kernel<8><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
+    else repart_finalize2_kernel<1><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
     ck(cudaGetLastError(), "repartition launch");
   } else if (tiles) {
-    if (k5_min_blocks() == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
+    if (mode.minb == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
     else repartition_kernel<3><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
     ck(cudaGetLastError(), "repartition launch");
   } else {
@@ -761,11 +702,14 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   ck(cudaEventSynchronize(e1), "sync");
   Timing t;
   ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  if (tiles && !mode.lookback) ck(cudaEventElapsedTime(&t.main_ms, e0, em), "elapsed");
+  else t.main_ms = t.ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaEventDestroy(em);
   t.tiles = tiles;
   t.bytes = count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
-  t.launches = tiles ? (split ? 3 : 1) : 0;
+  t.launches = tiles ? (mode.lookback ? 1 : 3) : 0;
   return t;
 }
 
@@ -781,6 +725,18 @@ Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& i
   const uint64_t per = uint64_t(kThreads) * kProbeItems, blocks = (count + per - 1) / per;
   ull* sink = nullptr;
   ck(cudaMallocAsync(reinterpret_cast<void**>(&sink), sizeof(ull), st), "cudaMallocAsync");
+  // default: the gather + write floor (scratch outputs of 44 B / sample); RESHARD_PROBE=read:
+  // the gathers alone
+  const bool wr = !(std::getenv("RESHARD_PROBE") && std::string(std::getenv("RESHARD_PROBE")) == "read");
+  void* wbuf = nullptr;
+  Outs wo{};
+  if (wr && count) {
+    ck(cudaMallocAsync(&wbuf, count * 44 + 256, st), "cudaMallocAsync");
+    char* w = static_cast<char*>(wbuf);
+    wo.pos = reinterpret_cast<ull*>(w), wo.ent = reinterpret_cast<ull*>(w + 8 * count);
+    wo.boff = reinterpret_cast<ull*>(w + 32 * count), wo.q0 = reinterpret_cast<unsigned*>(w + 40 * count);
+  }
+  L2FetchScope l2fetch;
   cudaEvent_t e0, e1;
   ck(cudaEventCreate(&e0), "event");
   ck(cudaEventCreate(&e1), "event");
@@ -788,7 +744,8 @@ Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& i
   t.ms = 1e30f;
   for (int i = 0; i < std::max(1, reps) + 1; ++i) {  // first launch warms up
     ck(cudaEventRecord(e0, st), "event");
-    if (blocks) gather_probe_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
+    if (blocks && wr) gather_write_probe_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
+    else if (blocks) gather_probe_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
     ck(cudaGetLastError(), "probe launch");
     ck(cudaEventRecord(e1, st), "event");
     ck(cudaEventSynchronize(e1), "sync");
@@ -799,6 +756,7 @@ Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& i
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   ck(cudaFreeAsync(sink, st), "cudaFreeAsync");
+  if (wbuf) ck(cudaFreeAsync(wbuf, st), "cudaFreeAsync");
   t.tiles = blocks, t.launches = blocks ? 1 : 0, t.bytes = count * (8 + 24);
   return t;
 }

@@ -77,6 +77,7 @@ struct Timing {
   uint64_t bytes = 0;       // algorithmic bytes written (each destination byte once)
   uint64_t launches = 0;
   uint64_t read_bytes = 0;  // algorithmic bytes read (a fan-out tile reads its source once)
+  float main_ms = 0;        // device time of the dominant kernel alone, when timed separately (K5: gather pass)
 };
 
 // The GPUs this process drives.  World GPU w is local iff local_of(w) >= 0.

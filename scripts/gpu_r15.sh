@@ -1,10 +1,12 @@
 #!/bin/bash
-# r15: K5 persistent (software-pipelined) variants: parity + same-box A/B + ncu.
+# r15: full GPU suite, default bench, K5 persistent (software-pipelined) variants:
+# same-box A/B + ncu.  Usage: gpurun -- 'bash scripts/gpu_r15.sh'
 set -u
 TAG=${1:-r15}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
-timeout 900 python -m pytest tests/test_dataset.py -m gpu -x -q > "$OUT/pytest_dataset.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_dataset.log"
+timeout 1500 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_gpu.log"
+timeout 600 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
 : > "$OUT/k5.jsonl"
 for rep in 1 2; do
 for m in lookback split persistent persistent3; do

@@ -28,15 +28,22 @@ def launches(path: str) -> dict:
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    per = defaultdict(list)
+    ki, vi, mi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
+    per = defaultdict(lambda: defaultdict(list))
     for r in rows[hdr + 1:]:
         if len(r) > vi and r[vi]:
             name = r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", "")
-            per[name].append(float(r[vi].replace(",", "")))
-    total = sum(sum(v) for v in per.values())
-    return {k: {"launches": len(v), "total_ns": sum(v), "mean_ns": sum(v) / len(v), "share": sum(v) / total}
-            for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]))}
+            per[name][r[mi]].append(float(r[vi].replace(",", "")))
+    t = "gpu__time_duration.sum"
+    total = sum(sum(m[t]) for m in per.values())
+    out = {}
+    for k, m in sorted(per.items(), key=lambda kv: -sum(kv[1][t])):
+        v = m[t]
+        out[k] = {"launches": len(v), "total_ns": sum(v), "mean_ns": sum(v) / len(v), "share": sum(v) / total}
+        for metric, vals in m.items():  # any other metric captured with the launch list: mean per launch
+            if metric != t:
+                out[k][f"mean_{metric}"] = sum(vals) / len(vals)
+    return out
 
 
 def report(path: str) -> dict:

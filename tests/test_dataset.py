@@ -104,9 +104,11 @@ def test_acceptance8_exactly_once_under_dp_changes(rs):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["split", "lookback", "persistent", "persistent3"])
-def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, monkeypatch):
+@pytest.mark.parametrize("mode,fin", [("split2", ""), ("split2", "8"), ("split2_6", ""), ("split2_8", ""),
+                                      ("lookback", ""), ("lookback4", "")])
+def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, fin, monkeypatch):
     monkeypatch.setenv("RESHARD_K5", mode)
+    monkeypatch.setenv("RESHARD_K5_FIN", fin)
     rng = random.Random(42)
     for n, nf, B, at, dp in [(50_000, 13, 64, 100, 4), (12_345, 5, 40, 7, 8), (4096, 3, 16, 256, 2),
                              (4096, 3, 16, 0, 1), (300_017, 29, 128, 500, 4)]:
