@@ -84,6 +84,13 @@ def run_dataset(args, rs):
     ctx = rs.Context(world, [rank], [local])
     d_perm, d_samp = ctx.malloc(rank, 8 * n), ctx.malloc(rank, 24 * n)
     ctx.htod(rank, d_samp, samples.ctypes.data, 24 * n)
+    # device layout of the static index: padded 32-byte records (one per sector), written once
+    # per index load by rs_dataset_index_pad; RESHARD_INDEX=packed keeps the 24-byte records
+    eb = 24 if os.environ.get("RESHARD_INDEX", "padded") == "packed" else 32
+    d_idx, pad_ms = d_samp, None
+    if eb == 32:
+        d_idx = ctx.malloc(rank, 32 * n)
+        pad_ms = rs.dataset_index_pad(ctx, rank, d_samp, d_idx, n)["ms"]
     # K8: the epoch permutation on the GPU (bit-identical to the host shuffle, checked here)
     shuf = [rs.shuffle_epoch_device(ctx, rank, n, spec["seed"], spec["epoch"], d_perm) for _ in range(2)][-1]
     dev_perm = np.empty(n, np.uint64)
@@ -103,7 +110,7 @@ def run_dataset(args, rs):
     def step():
         ms, gms, samples_done, launches = 0.0, 0.0, 0, 0
         for at, dp, d, p_fc, part in jobs:
-            t = rs.repartition(ctx, rank, d_perm, d_samp, p_fc, n, spec["B"], at, dp, d, part)
+            t = rs.repartition(ctx, rank, d_perm, d_idx, p_fc, n, spec["B"], at, dp, d, part, entry_bytes=eb)
             ms += t["ms"]
             gms += t["gather_ms"]
             samples_done += part.count
@@ -126,7 +133,7 @@ def run_dataset(args, rs):
     ent_ok = bool(np.array_equal(got["ent"][:: max(1, part.count // 1000)],
                                  samples[perm[got["pos"][:: max(1, part.count // 1000)]]]))
     # the floor of the same step: K5's gathers plus its output stores, no scan (off the clock)
-    floor_ms = sum(rs.repartition_gather_probe(ctx, rank, d_perm, d_samp, n, spec["B"], at, dp, d)["ms"]
+    floor_ms = sum(rs.repartition_gather_probe(ctx, rank, d_perm, d_idx, n, spec["B"], at, dp, d, entry_bytes=eb)["ms"]
                    for at, dp, d, _, _ in jobs)
     if rank != 0:
         return
@@ -143,7 +150,9 @@ def run_dataset(args, rs):
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (100M-sample index, 1000 files)",
         "config": {"workload": args.workload, "events": spec["events"], "B": spec["B"], "n": n,
-                   "l2": "inputs larger than L2 (no flush)"},
+                   "l2": "inputs larger than L2 (no flush)",
+                   "index_layout": "padded 32-byte records" if eb == 32 else "packed 24-byte records"},
+        "index_pad_ms_once": None if pad_ms is None else round(pad_ms, 3),
         "samples_per_step": done, "gsamples_per_s": round(done / (ms * 1e-3) / 1e9, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,

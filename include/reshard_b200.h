@@ -270,6 +270,8 @@ typedef struct rs_dataset_index {  /* device pointers */
   const uint64_t* samples;       /* N x {file, offset, length} */
   const uint8_t* file_class;     /* per file: 0 local, 1 peer, 2 remote for the calling rank */
   uint64_t n;
+  uint64_t entry_bytes;          /* 0 or 24: packed records as the reference stores them;
+                                    32: padded device layout from rs_dataset_index_pad */
 } rs_dataset_index;
 
 typedef struct rs_partition_out {  /* device pointers, capacity = the rank's count */
@@ -286,13 +288,22 @@ int rs_shuffle_scratch_bytes(uint64_t n, uint64_t* bytes);
 int rs_shuffle_epoch_device(rs_context* ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm_dev,
                             void* scratch, rs_timing* timing);
 
+/* Device layout of the index (no reference counterpart; the index is static across epochs
+ * and DP changes, so this runs once per index load): packed 24-byte records -> padded
+ * 32-byte records (padded: n x 32 bytes, 16-byte aligned).  rs_repartition's outputs are
+ * identical for either layout; the padded one never straddles a DRAM line. */
+int rs_dataset_index_pad(rs_context* ctx, int gpu, const uint64_t* packed_dev, uint64_t* padded_dev, uint64_t n,
+                         rs_timing* timing);
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
-/* K5: gather + scan + compaction for one rank in one kernel launch (timed with events) */
+/* K5: gather pass + tile scan + finalize for one rank (three launches, timed with events;
+ * timing->main_ms = the gather pass alone).  Replaces the SPEC's per-rank repartition +
+ * locate_sample loops. */
 int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,
                    uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
-/* Diagnostic (no reference counterpart): best-of-`reps` device time of K5's random reads
- * alone for this rank (perm + 24-byte entry gathers, nothing written) — the floor bench.py
- * reports K5 against.  idx->file_class is not read. */
+/* Diagnostic (no reference counterpart): best-of-`reps` device time of K5's perm + entry
+ * gathers for this rank plus all 44 output bytes per sample written coalesced, no scan
+ * (env RESHARD_PROBE=read: nothing written) — the floor bench.py reports K5 against.
+ * idx->file_class is not read. */
 int rs_repartition_gather_probe(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch,
                                 uint64_t at_step, uint64_t new_dp, uint64_t rank, int reps, rs_timing* timing);
 

@@ -677,8 +677,10 @@ class Partition:
 
 
 def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_ptr: int, n: int, global_batch: int,
-                at_step: int, new_dp: int, rank: int, part: "Partition") -> dict:
-    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, class_ptr, n)
+                at_step: int, new_dp: int, rank: int, part: "Partition", entry_bytes: int = 24) -> dict:
+    """K5 for one rank.  entry_bytes 24: samples_ptr holds the packed reference records;
+    32: the padded device layout from dataset_index_pad (same outputs)."""
+    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, class_ptr, n, entry_bytes)
     t = _capi.rs_timing()
     out = part.c()
     _chk(lib.rs_repartition(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, C.byref(out),
@@ -686,12 +688,19 @@ def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_p
     return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, gather_ms=t.main_ms)
 
 
+def dataset_index_pad(ctx: Context, gpu: int, packed_ptr: int, padded_ptr: int, n: int) -> dict:
+    """Packed 24-byte index records -> padded 32-byte device layout (padded_ptr: 32 n bytes)."""
+    t = _capi.rs_timing()
+    _chk(lib.rs_dataset_index_pad(ctx.h, gpu, packed_ptr, padded_ptr, n, C.byref(t)))
+    return dict(ms=t.ms, bytes=t.bytes, read_bytes=t.read_bytes, launches=t.launches)
+
+
 def repartition_gather_probe(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, n: int, global_batch: int,
-                             at_step: int, new_dp: int, rank: int, reps: int = 3) -> dict:
+                             at_step: int, new_dp: int, rank: int, reps: int = 3, entry_bytes: int = 24) -> dict:
     """Diagnostic: device time of K5's gathers plus its 44 output bytes per sample, coalesced and
     with no scan (the floor for any kernel producing the partition); RESHARD_PROBE=read times
     the gathers alone."""
-    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, 0, n)
+    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, 0, n, entry_bytes)
     t = _capi.rs_timing()
     _chk(lib.rs_repartition_gather_probe(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, reps,
                                          C.byref(t)))

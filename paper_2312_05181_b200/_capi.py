@@ -145,6 +145,7 @@ SIGNATURES = {
     "rs_repartition_position": (C.c_int, [C.c_uint64] * 6 + [U64P]),
     "rs_locate_sample": (C.c_int, [C.c_uint64] * 6 + [P, P, P, U64P]),
     "rs_repartition_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
+    "rs_dataset_index_pad": (C.c_int, [P, C.c_int, P, P, C.c_uint64, P]),
     "rs_shuffle_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
     "rs_shuffle_epoch_device": (C.c_int, [P, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, P, P,
                                           C.POINTER(rs_timing)]),
@@ -156,7 +157,8 @@ SIGNATURES = {
 
 
 class rs_dataset_index(C.Structure):
-    _fields_ = [("perm", C.c_void_p), ("samples", C.c_void_p), ("file_class", C.c_void_p), ("n", C.c_uint64)]
+    _fields_ = [("perm", C.c_void_p), ("samples", C.c_void_p), ("file_class", C.c_void_p), ("n", C.c_uint64),
+                ("entry_bytes", C.c_uint64)]
 
 
 class rs_partition_out(C.Structure):

@@ -714,6 +714,14 @@ int rs_shuffle_epoch_device(rs_context* c, int gpu, uint64_t n, uint64_t seed, u
     if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
+int rs_dataset_index_pad(rs_context* c, int gpu, const uint64_t* packed, uint64_t* padded, uint64_t n,
+                         rs_timing* timing) {
+  return guard([&] {
+    need(packed, "packed"), need(padded, "padded");
+    Timing t = dataset_index_pad(ctx_of(c), gpu, packed, padded, n);
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
+  });
+}
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes) {
   return guard([&] {
     need(bytes, "bytes");
@@ -724,7 +732,7 @@ int rs_repartition(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t
                    uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing) {
   return guard([&] {
     need(idx, "index"), need(out, "out"), need(scratch, "scratch");
-    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n};
+    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n, idx->entry_bytes};
     PartitionOut o{out->pos, out->ent, out->boff, {out->queue[0], out->queue[1], out->queue[2]}, out->qcount};
     Timing t = repartition_device(ctx_of(c), gpu, v, B, at_step, dp, rank, o, scratch);
     if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
@@ -734,7 +742,7 @@ int rs_repartition_gather_probe(rs_context* c, int gpu, const rs_dataset_index* 
                                 uint64_t dp, uint64_t rank, int reps, rs_timing* timing) {
   return guard([&] {
     need(idx, "index"), need(timing, "timing");
-    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n};
+    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n, idx->entry_bytes};
     Timing t = repartition_gather_probe(ctx_of(c), gpu, v, B, at_step, dp, rank, reps);
     *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });

@@ -253,6 +253,35 @@ __device__ __forceinline__ unsigned long long sample_pos(const Params& p, unsign
   return p.full * p.B + p.rank * p.b + (k - p.in_full);
 }
 
+// One index entry {file, offset, length}: the reference's packed 24-byte record (PAD false:
+// three 8-byte loads, one record in 8 straddles a 128-byte line), or the padded 32-byte
+// device layout of dataset_index_pad (PAD true: one 16-byte and one 8-byte load from a single
+// 32-byte sector).
+template <bool PAD>
+__device__ __forceinline__ void load_entry(const unsigned long long* samples, unsigned long long idx,
+                                           unsigned long long& f, unsigned long long& off, unsigned long long& len) {
+  if (PAD) {
+    const unsigned long long* e = samples + 4 * idx;
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(e));
+    f = a.x, off = a.y, len = __ldg(e + 2);
+  } else {
+    const unsigned long long* e = samples + 3 * idx;
+    f = __ldg(e), off = __ldg(e + 1), len = __ldg(e + 2);
+  }
+}
+
+// dataset_index_pad: packed 24-byte records -> padded 32-byte records (pad word zero); one
+// streaming pass, coalesced 8-byte loads and 16-byte stores.
+__global__ void __launch_bounds__(kThreads) index_pad_kernel(const unsigned long long* __restrict__ src,
+                                                             unsigned long long* __restrict__ dst, unsigned long long n) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * kThreads) {
+    const unsigned long long f = __ldg(src + 3 * i), off = __ldg(src + 3 * i + 1), len = __ldg(src + 3 * i + 2);
+    reinterpret_cast<ulonglong2*>(dst + 4 * i)[0] = make_ulonglong2(f, off);
+    reinterpret_cast<ulonglong2*>(dst + 4 * i)[1] = make_ulonglong2(len, 0ull);
+  }
+}
+
 // ---- random-gather floors (diagnostic) --------------------------------------------------------
 // gather_probe_kernel: K5's two HBM-random levels alone — the rank's perm positions, one
 // 24-byte entry gather per position, nothing written but one word per thread — at the
@@ -261,6 +290,7 @@ __device__ __forceinline__ unsigned long long sample_pos(const Params& p, unsign
 // repartition_gather_probe): the same gathers plus every output byte K5 must write.  bench.py
 // reports K5 against the latter next to the streaming-HBM roofline.
 constexpr int kProbeItems = 4;
+template <bool PAD>
 __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsigned long long* sink) {
   const unsigned long long k0 =
       ((unsigned long long)blockIdx.x * kThreads + threadIdx.x) * (unsigned long long)kProbeItems;
@@ -282,8 +312,7 @@ __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsign
   unsigned long long f[kProbeItems], off[kProbeItems], len[kProbeItems];
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) {
-    const unsigned long long* e = p.samples + 3 * idx[j];
-    f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
+    load_entry<PAD>(p.samples, idx[j], f[j], off[j], len[j]);
   }
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) acc ^= f[j] + off[j] + len[j];
@@ -293,6 +322,7 @@ __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsign
 // The same gathers plus K5's 44 output bytes per sample (pos, entry, a length word, a u32
 // queue word), warp-striped so every store is coalesced, and no scan: the floor of any
 // kernel that must both gather the entries and write the partition (RESHARD_PROBE=write).
+template <bool PAD>
 __global__ void __launch_bounds__(kThreads) gather_write_probe_kernel(Params p, Outs o) {
   unsigned long long idx[kProbeItems], pos[kProbeItems];
   const unsigned long long base = (unsigned long long)blockIdx.x * (kThreads * kProbeItems) + threadIdx.x;
@@ -305,8 +335,7 @@ __global__ void __launch_bounds__(kThreads) gather_write_probe_kernel(Params p, 
   unsigned long long f[kProbeItems], off[kProbeItems], len[kProbeItems];
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) {
-    const unsigned long long* e = p.samples + 3 * idx[j];
-    f[j] = __ldg(e), off[j] = __ldg(e + 1), len[j] = __ldg(e + 2);
+    load_entry<PAD>(p.samples, idx[j], f[j], off[j], len[j]);
   }
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) {
@@ -333,7 +362,7 @@ constexpr int kGItems = 4, kGTile = kThreads * kGItems, kGWarpItems = 32 * kGIte
 constexpr int kClsBits = 21;  // per-class counts packed into one u64 (a tile has <= 1024 items)
 constexpr unsigned long long kClsMask = (1ull << kClsBits) - 1;
 
-template <int MINB>
+template <int MINB, bool PAD>
 __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p, Outs o, Scratch sc,
                                                                          unsigned char* cls_out) {
   __shared__ unsigned long long warp_len[kWarps], warp_cnt[kWarps];
@@ -348,9 +377,8 @@ __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p
   unsigned long long f[kGItems], off[kGItems], len[kGItems];
 #pragma unroll
   for (int j = 0; j < kGItems; ++j) {
-    const unsigned long long* e = p.samples + 3 * idx[j];
-    const bool v = k0 + 32 * j < p.count;
-    f[j] = v ? __ldg(e) : 0ull, off[j] = v ? __ldg(e + 1) : 0ull, len[j] = v ? __ldg(e + 2) : 0ull;
+    f[j] = 0, off[j] = 0, len[j] = 0;
+    if (k0 + 32 * j < p.count) load_entry<PAD>(p.samples, idx[j], f[j], off[j], len[j]);
   }
   unsigned long long lsum = 0, cnt = 0;
 #pragma unroll
@@ -422,25 +450,29 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
     sc.inc[t] = blk_prefix + base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
 }
 
-template <int MINB>
+// IT items per thread (4 or 8): a CTA covers IT / 4 aggregate tiles; warp w owns 32 IT
+// consecutive samples, inside aggregate tile (CTA * IT / 4 + w * IT / 32).
+template <int MINB, int IT>
 __global__ void __launch_bounds__(kThreads, MINB) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
-                                                                     const unsigned char* cls_in) {
+                                                                          const unsigned char* cls_in) {
+  static_assert(IT == 4 || IT == 8, "IT");
+  constexpr int kWarpsPerTile = kWarps * kGItems / IT;
   __shared__ Agg warp_tot[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * kGTile + warp * kGWarpItems + lane;
-  unsigned long long len[kGItems];
-  unsigned char cls[kGItems];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * (kThreads * IT) + warp * (32 * IT) + lane;
+  unsigned long long len[IT];
+  unsigned char cls[IT];
 #pragma unroll
-  for (int j = 0; j < kGItems; ++j) {
+  for (int j = 0; j < IT; ++j) {
     const unsigned long long k = k0 + 32 * j;
     len[j] = k < p.count ? o.boff[k] : 0ull;
     cls[j] = k < p.count ? cls_in[k] : (unsigned char)3;
   }
-  unsigned long long lenx[kGItems];
+  unsigned long long lenx[IT];
   Agg w{0, 0, 0, 0};
 #pragma unroll
-  for (int j = 0; j < kGItems; ++j) {
+  for (int j = 0; j < IT; ++j) {
     unsigned long long inc = len[j];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -455,12 +487,14 @@ __global__ void __launch_bounds__(kThreads, MINB) repart_finalize2_kernel(Params
   }
   if (lane == 0) warp_tot[warp] = w;
   __syncthreads();
-  Agg run = prefix[blockIdx.x];
+  const int first = warp / kWarpsPerTile * kWarpsPerTile;  // first warp of this warp's aggregate tile
+  const unsigned long long tile = (unsigned long long)blockIdx.x * (IT / kGItems) + warp / kWarpsPerTile;
+  Agg run = tile < (p.count + kGTile - 1) / kGTile ? prefix[tile] : Agg{0, 0, 0, 0};
 #pragma unroll
   for (int q = 0; q < kWarps; ++q)
-    if (q < warp) run = run + warp_tot[q];
+    if (q >= first && q < warp) run = run + warp_tot[q];
 #pragma unroll
-  for (int j = 0; j < kGItems; ++j) {
+  for (int j = 0; j < IT; ++j) {
     const unsigned long long k = k0 + 32 * j;
     if (k < p.count) o.boff[k] = run.len + lenx[j];
     const unsigned m0 = __ballot_sync(0xffffffffu, cls[j] == 0), m1 = __ballot_sync(0xffffffffu, cls[j] == 1),
@@ -480,11 +514,12 @@ uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 // K5 variant (RESHARD_K5): "split2" (default: gather pass at 5 resident CTAs / SM, tile
 // scan, finalize), "split2_6" / "split2_8" (gather pass at 6 / 8 CTAs / SM), "lookback" /
 // "lookback4" (the single-pass decoupled look-back kernel at 3 / 4 CTAs / SM).  r16 same-box
-// A/B (profiles/r16): split2 4.25 ms, split2_6 4.31, split2_8 4.88, lookback 6.34 per step.
+// A/B (profiles/r16): split2 4.25 ms, split2_6 4.31, split2_8 4.88, lookback 6.34 per step
+// (packed index).  Finalize at 6 / 8 CTAs per SM or 8 items per thread: within +-1 % or 5 %
+// slower (r18b), not kept.
 struct K5Mode {
   bool lookback = false;
   int minb = 5;  // resident CTAs per SM the chosen gather kernel is compiled for
-  int fin_minb = 0;
 };
 K5Mode k5_mode() {
   K5Mode m;
@@ -495,8 +530,6 @@ K5Mode k5_mode() {
   else if (s == "split2_6") m.minb = 6;
   else if (s == "split2_8") m.minb = 8;
   else if (!s.empty() && s != "split2") raise(Errc::InvalidArgument, "RESHARD_K5: unknown variant " + s);
-  const char* f = std::getenv("RESHARD_K5_FIN");
-  m.fin_minb = f && std::string(f) == "8" ? 8 : 0;
   return m;
 }
 
@@ -645,6 +678,38 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
   return t;
 }
 
+// entry_bytes 0 / 24: the packed reference records; 32: the padded device layout
+bool entry_padded(const DatasetIndexView& idx) {
+  if (idx.entry_bytes != 0 && idx.entry_bytes != 24 && idx.entry_bytes != 32)
+    raise(Errc::InvalidArgument, "entry_bytes must be 24 (packed) or 32 (padded), got " + std::to_string(idx.entry_bytes));
+  if (idx.entry_bytes == 32 && (reinterpret_cast<uintptr_t>(idx.samples) & 15))
+    raise(Errc::InvalidArgument, "padded index must be 16-byte aligned");
+  return idx.entry_bytes == 32;
+}
+
+Timing dataset_index_pad(Context& ctx, int gpu, const uint64_t* packed, uint64_t* padded, uint64_t n) {
+  if ((reinterpret_cast<uintptr_t>(padded) & 15) || (reinterpret_cast<uintptr_t>(packed) & 7))
+    raise(Errc::InvalidArgument, "dataset_index_pad: misaligned buffers");
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventRecord(e0, st), "event");
+  const uint64_t grid = std::min<uint64_t>((n + kThreads - 1) / kThreads, uint64_t(ctx.sm_count(gpu)) * 8);
+  if (grid) index_pad_kernel<<<unsigned(grid), kThreads, 0, st>>>(reinterpret_cast<const unsigned long long*>(packed),
+                                                                 reinterpret_cast<unsigned long long*>(padded), n);
+  ck(cudaGetLastError(), "index pad launch");
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  Timing t;
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t.launches = grid ? 1 : 0, t.bytes = 32 * n, t.read_bytes = 24 * n;
+  return t;
+}
+
 uint64_t repartition_scratch_bytes(uint64_t count) {
   const uint64_t tiles = (count + kGTile - 1) / kGTile;  // the smaller tile of the variants
   // counter + flags + tile aggregates + tile prefixes; split2: + class bytes + the tile
@@ -657,6 +722,7 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch) {
   const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
   if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
+  const bool pad = entry_padded(idx);
   const K5Mode mode = k5_mode();
   const uint64_t tile = mode.lookback ? kTile : kGTile;
   const uint64_t tiles = (count + tile - 1) / tile;
@@ -677,19 +743,26 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
            at_step, b, rank, count, full > at_step ? (full - at_step) * b : 0, full};
   Outs o{reinterpret_cast<ull*>(out.pos), reinterpret_cast<ull*>(out.ent), reinterpret_cast<ull*>(out.boff),
          out.queue[0], out.queue[1], out.queue[2], reinterpret_cast<ull*>(out.qcount)};
+  if (mode.lookback && pad) raise(Errc::InvalidArgument, "RESHARD_K5=lookback reads the packed index only");
   if (mode.lookback) ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
   ck(cudaEventRecord(e0, st), "event");
   if (tiles && !mode.lookback) {
     auto* cls = reinterpret_cast<unsigned char*>(sc + 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)));
-    if (mode.minb == 6) repart_gather2_kernel<6><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s, cls);
-    else if (mode.minb == 8) repart_gather2_kernel<8><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s, cls);
-    else repart_gather2_kernel<5><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s, cls);
+    const unsigned g = unsigned(tiles);
+    if (pad) {
+      if (mode.minb == 6) repart_gather2_kernel<6, true><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else if (mode.minb == 8) repart_gather2_kernel<8, true><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else repart_gather2_kernel<5, true><<<g, kThreads, 0, st>>>(p, o, s, cls);
+    } else {
+      if (mode.minb == 6) repart_gather2_kernel<6, false><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else if (mode.minb == 8) repart_gather2_kernel<8, false><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else repart_gather2_kernel<5, false><<<g, kThreads, 0, st>>>(p, o, s, cls);
+    }
     ck(cudaEventRecord(em, st), "event");
     const uint64_t sblocks = (tiles + 1023) / 1024;
     Agg* blk = reinterpret_cast<Agg*>(cls + align256(count));
     repart_tile_scan_kernel<<<unsigned(sblocks), 1024, 0, st>>>(s, blk, blk + sblocks, o);
-    if (mode.fin_minb == 8) repart_finalize2_kernel<8><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
-    else repart_finalize2_kernel<1><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s.inc, cls);
+    repart_finalize2_kernel<1, 4><<<g, kThreads, 0, st>>>(p, o, s.inc, cls);
     ck(cudaGetLastError(), "repartition launch");
   } else if (tiles) {
     if (mode.minb == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
@@ -716,6 +789,7 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
 Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                                 uint64_t new_dp, uint64_t rank, int reps) {
   const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
+  const bool pad = entry_padded(idx);
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
   const uint64_t b = B / new_dp, full = idx.n / B;
@@ -744,8 +818,10 @@ Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& i
   t.ms = 1e30f;
   for (int i = 0; i < std::max(1, reps) + 1; ++i) {  // first launch warms up
     ck(cudaEventRecord(e0, st), "event");
-    if (blocks && wr) gather_write_probe_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
-    else if (blocks) gather_probe_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
+    if (blocks && wr && pad) gather_write_probe_kernel<true><<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
+    else if (blocks && wr) gather_write_probe_kernel<false><<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
+    else if (blocks && pad) gather_probe_kernel<true><<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
+    else if (blocks) gather_probe_kernel<false><<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
     ck(cudaGetLastError(), "probe launch");
     ck(cudaEventRecord(e1, st), "event");
     ck(cudaEventSynchronize(e1), "sync");

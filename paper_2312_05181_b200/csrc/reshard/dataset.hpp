@@ -21,15 +21,21 @@ void repartition_check(uint64_t n, uint64_t B, uint64_t at_step, uint64_t new_dp
 uint64_t repartition_count(uint64_t n, uint64_t B, uint64_t at_step, uint64_t new_dp, uint64_t rank);
 uint64_t repartition_position(uint64_t n, uint64_t B, uint64_t at_step, uint64_t new_dp, uint64_t rank, uint64_t k);
 
-// Device-resident dataset index.  samples: N x {file, offset, length} (u64 each);
-// file_class: the calling rank's locator class per file, 0 local / 1 peer / 2 remote
-// (priority order of SPEC.md:357).
+// Device-resident dataset index.  samples: N x {file, offset, length} (u64 each), packed
+// 24-byte records as the reference stores them (entry_bytes 0 or 24) or the padded 32-byte
+// device layout written by dataset_index_pad (entry_bytes 32: one record per 32-byte
+// sector, so a random gather never straddles a DRAM line); file_class: the calling rank's
+// locator class per file, 0 local / 1 peer / 2 remote (priority order of SPEC.md:357).
 struct DatasetIndexView {
   const uint64_t* perm;
   const uint64_t* samples;
   const uint8_t* file_class;
   uint64_t n;
+  uint64_t entry_bytes = 24;
 };
+// Packed -> padded index records on the device (one streaming pass; padded: 32 n bytes,
+// 16-byte aligned).  The outputs of repartition are identical for either layout.
+Timing dataset_index_pad(Context& ctx, int gpu, const uint64_t* packed, uint64_t* padded, uint64_t n);
 // Outputs of one rank (device).  For the rank's k-th remaining sample: pos[k],
 // ent[3k..3k+2] = samples[perm[pos[k]]], boff[k] = exclusive prefix sum of lengths (the
 // sample's offset in the rank's read buffer); queue[c] lists the k with locator class c in
@@ -50,12 +56,14 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
                             void* scratch);
 
 uint64_t repartition_scratch_bytes(uint64_t count);
-// K5: one launch for one rank.  `scratch` (repartition_scratch_bytes) must be device
-// memory; it is cleared on the stream before the launch.
+// K5 for one rank: gather pass, tile scan, finalize (three launches; RESHARD_K5=lookback:
+// one).  `scratch` (repartition_scratch_bytes) must be device memory.  Timing.main_ms is
+// the gather pass alone.
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch);
-// Diagnostic: best-of-`reps` time of K5's random reads alone (perm + entry gathers of the
-// rank's positions, nothing written) — the floor for any kernel that must gather them.
+// Diagnostic: best-of-`reps` time of K5's perm + entry gathers for the rank's positions
+// plus all 44 output bytes per sample written coalesced, no scan (RESHARD_PROBE=read:
+// nothing written) — the floor for any kernel that must produce the partition.
 Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                                 uint64_t new_dp, uint64_t rank, int reps);
 

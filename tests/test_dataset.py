@@ -104,11 +104,13 @@ def test_acceptance8_exactly_once_under_dp_changes(rs):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode,fin", [("split2", ""), ("split2", "8"), ("split2_6", ""), ("split2_8", ""),
-                                      ("lookback", ""), ("lookback4", "")])
-def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, fin, monkeypatch):
+@pytest.mark.parametrize("mode,eb", [("split2", 24), ("split2", 32), ("split2_6", 32), ("split2_8", 24),
+                                     ("lookback", 24), ("lookback4", 24)])
+def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, eb, monkeypatch):
+    """K5 against the oracle's restated repartition + locate on ragged
+    partitions, trailing partial batches and at_step 0, for every variant and both device
+    layouts of the index (packed 24-byte reference records, padded 32-byte)."""
     monkeypatch.setenv("RESHARD_K5", mode)
-    monkeypatch.setenv("RESHARD_K5_FIN", fin)
     rng = random.Random(42)
     for n, nf, B, at, dp in [(50_000, 13, 64, 100, 4), (12_345, 5, 40, 7, 8), (4096, 3, 16, 256, 2),
                              (4096, 3, 16, 0, 1), (300_017, 29, 128, 500, 4)]:
@@ -117,13 +119,17 @@ def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, fin, monkeypatch):
         d_perm, d_samp = ctx.malloc(0, 8 * n), ctx.malloc(0, 24 * n)
         ctx.htod(0, d_perm, perm.ctypes.data, 8 * n)
         ctx.htod(0, d_samp, samples.ctypes.data, 24 * n)
+        d_idx = d_samp
+        if eb == 32:
+            d_idx = ctx.malloc(0, 32 * n)
+            rs.dataset_index_pad(ctx, 0, d_samp, d_idx, n)
         for d in range(dp):
             fc = classes(nf, dp, d)
             d_fc = ctx.malloc(0, nf)
             ctx.htod(0, d_fc, fc.ctypes.data, nf)
             cnt = rs.repartition_count(n, B, at, dp, d)
             part = rs.Partition(ctx, 0, cnt)
-            t = rs.repartition(ctx, 0, d_perm, d_samp, d_fc, n, B, at, dp, d, part)
+            t = rs.repartition(ctx, 0, d_perm, d_idx, d_fc, n, B, at, dp, d, part, entry_bytes=eb)
             got = part.fetch()
             want = orc.dataset_gather(n, B, at, dp, d, perm, samples, fc, n_threads=3)
             assert np.array_equal(got["pos"], want["pos"])
@@ -136,6 +142,38 @@ def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, fin, monkeypatch):
             ctx.free(0, d_fc)
         ctx.free(0, d_perm)
         ctx.free(0, d_samp)
+        if eb == 32:
+            ctx.free(0, d_idx)
+
+
+@pytest.mark.gpu
+def test_index_pad_layout_and_errors(rs, ctx, monkeypatch):
+    """rs_dataset_index_pad writes {file, offset, length, 0} per record; bad entry_bytes and
+    the look-back variant on a padded index fail with InvalidArgument."""
+    rng = random.Random(5)
+    n = 100_003
+    samples = corpus(n, 7, rng)
+    d_samp, d_pad = ctx.malloc(0, 24 * n), ctx.malloc(0, 32 * n)
+    ctx.htod(0, d_samp, samples.ctypes.data, 24 * n)
+    t = rs.dataset_index_pad(ctx, 0, d_samp, d_pad, n)
+    assert t["launches"] == 1 and t["bytes"] == 32 * n
+    got = np.empty((n, 4), np.uint64)
+    ctx.dtoh(0, got.ctypes.data, d_pad, 32 * n)
+    assert np.array_equal(got[:, :3], samples) and not got[:, 3].any()
+    perm = rs.shuffle_epoch(n, 1, 0)
+    d_perm, d_fc = ctx.malloc(0, 8 * n), ctx.malloc(0, 7)
+    ctx.htod(0, d_perm, perm.ctypes.data, 8 * n)
+    fc = classes(7, 2, 0)
+    ctx.htod(0, d_fc, fc.ctypes.data, 7)
+    part = rs.Partition(ctx, 0, rs.repartition_count(n, 64, 3, 2, 0))
+    with pytest.raises(rs.ReshardError, match="InvalidArgument"):
+        rs.repartition(ctx, 0, d_perm, d_pad, d_fc, n, 64, 3, 2, 0, part, entry_bytes=16)
+    monkeypatch.setenv("RESHARD_K5", "lookback")
+    with pytest.raises(rs.ReshardError, match="InvalidArgument"):
+        rs.repartition(ctx, 0, d_perm, d_pad, d_fc, n, 64, 3, 2, 0, part, entry_bytes=32)
+    part.free()
+    for p in (d_samp, d_pad, d_perm, d_fc):
+        ctx.free(0, p)
 
 
 @pytest.mark.gpu
