@@ -135,6 +135,9 @@ def run_dataset(args, rs):
     # the floor of the same step: K5's gathers plus its output stores, no scan (off the clock)
     floor_ms = sum(rs.repartition_gather_probe(ctx, rank, d_perm, d_idx, n, spec["B"], at, dp, d, entry_bytes=eb)["ms"]
                    for at, dp, d, _, _ in jobs)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        e2e = dataset_e2e(args, rs, ctx, rank, spec, perm, samples, d_perm, d_samp, d_idx if eb == 32 else 0, eb, jobs)
     if rank != 0:
         return
     ms = statistics.mean(step_ms)
@@ -167,7 +170,7 @@ def run_dataset(args, rs):
                                    "bytes per sample, coalesced, no scan; random 24-B gathers cost whole DRAM "
                                    "lines, so the streaming-HBM frac is not reachable"},
         "gpu_launches": launches * args.steps, "clocks": clocks.summary(), "spot_check": {"pos": pos_ok, "ent": ent_ok},
-        "e2e": None,
+        "e2e": e2e,
         "shuffle_epoch_gpu": {"ms": round(shuf["ms"], 3), "rounds": shuf["rounds"], "launches": shuf["launches"],
                               "bit_identical_to_host": shuffle_identical,
                               "host_shuffle_ms_1thread": round(host_shuffle_ms, 1)},
@@ -188,6 +191,57 @@ def run_dataset(args, rs):
                                 "sample": "full workload (all ranks of both DP events), restated gather with "
                                           f"{threads} threads"}
     print(json.dumps(line), flush=True)
+
+
+def dataset_e2e(args, rs, ctx, rank, spec, perm, samples, d_perm, d_samp, d_pad, eb, jobs):
+    """The dataset step through the C ABI with host buffers: every step uploads the epoch
+    permutation and the packed index from pinned memory (and pads it on the device), runs
+    every rank's K5, and reads every rank's outputs back into pinned buffers.  Wall clock
+    around the whole step (each call returns after its stream work)."""
+    import ctypes
+
+    import numpy as np
+
+    n = spec["n"]
+    h_perm, h_samp = rs.host_alloc(8 * n), rs.host_alloc(24 * n)
+    ctypes.memmove(h_perm, perm.ctypes.data, 8 * n)
+    ctypes.memmove(h_samp, samples.ctypes.data, 24 * n)
+    hosts = [rs.HostPartition(part.count) for *_, part in jobs]
+    try:
+        step_ms, d2h = [], 0
+        for i in range(1 + args.e2e_steps):  # the first pass warms up the pinned pages
+            t0 = time.perf_counter()
+            up = rs.dataset_index_upload(ctx, rank, h_perm, h_samp, n, d_perm, d_samp, d_pad)
+            d2h = 0
+            for (at, dp, d, p_fc, part), host in zip(jobs, hosts):
+                r = rs.repartition_to_host(ctx, rank, d_perm, d_pad or d_samp, p_fc, n, spec["B"], at, dp, d, part,
+                                           host, entry_bytes=eb)
+                d2h += r["d2h_bytes"]
+            if i:
+                step_ms.append((time.perf_counter() - t0) * 1e3)
+        # the host copies agree with the device outputs
+        at, dp, d, _, part = jobs[-1]
+        got, want = hosts[-1].arrays(), part.fetch()
+        same = all(np.array_equal(got[k], want[k]) for k in ("pos", "ent", "boff", "qidx")) and \
+            got["qcount"] == want["qcount"]
+        line = {"value": round(statistics.mean(step_ms), 3), "unit": "ms", "h2d_bytes_per_step": up["bytes"],
+                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "host_matches_device": bool(same),
+                "path": "rs_dataset_index_upload + rs_repartition_to_host per rank, pinned host buffers"}
+        try:
+            link = pcie_probe()
+            bound = up["bytes"] / (link["h2d_gbs"] * 1e9) * 1e3 + d2h / (link["d2h_gbs"] * 1e9) * 1e3
+            line["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound, 2),
+                                "frac": round(bound / line["value"], 4),
+                                "note": "H2D then D2H at the measured one-way rates (the gathers need the whole "
+                                        "index before any output exists)"}
+        except Exception as exc:  # noqa: BLE001
+            line["roofline"] = {"error": str(exc)[:200]}
+        return line
+    finally:
+        for h in hosts:
+            h.free()
+        rs.host_free(h_perm)
+        rs.host_free(h_samp)
 
 
 DIST_BACKEND = os.environ.get("RESHARD_DIST_BACKEND", "nccl")

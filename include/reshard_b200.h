@@ -282,6 +282,14 @@ typedef struct rs_partition_out {  /* device pointers, capacity = the rank's cou
   uint64_t* qcount;              /* 3 counts, written by the kernel */
 } rs_partition_out;
 
+typedef struct rs_partition_host {  /* host pointers (pinned for full PCIe rate) */
+  uint64_t* pos;
+  uint64_t* ent;
+  uint64_t* boff;
+  uint32_t* queue[3];            /* receives exactly qcount[c] entries */
+  uint64_t* qcount;
+} rs_partition_host;
+
 /* K8: shuffle_epoch on the GPU, bit-identical to rs_shuffle_epoch (deterministic
  * reservations); perm_dev: n x u64 device buffer; scratch: rs_shuffle_scratch_bytes(n) */
 int rs_shuffle_scratch_bytes(uint64_t n, uint64_t* bytes);
@@ -294,12 +302,25 @@ int rs_shuffle_epoch_device(rs_context* ctx, int gpu, uint64_t n, uint64_t seed,
  * identical for either layout; the padded one never straddles a DRAM line. */
 int rs_dataset_index_pad(rs_context* ctx, int gpu, const uint64_t* packed_dev, uint64_t* padded_dev, uint64_t n,
                          rs_timing* timing);
+/* Host-buffer path (the SPEC's dataset module works on host-resident indexes):
+ * upload perm (8n B) and the packed records (24n B) into perm_dev / samples_dev on the GPU's
+ * stream; with padded_dev non-null also rewrite them padded (rs_dataset_index_pad).  timing->ms:
+ * event time of the upload. */
+int rs_dataset_index_upload(rs_context* ctx, int gpu, const uint64_t* host_perm, const uint64_t* host_samples,
+                            uint64_t n, uint64_t* perm_dev, uint64_t* samples_dev, uint64_t* padded_dev,
+                            rs_timing* timing);
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
 /* K5: gather pass + tile scan + finalize for one rank (three launches, timed with events;
  * timing->main_ms = the gather pass alone).  Replaces the SPEC's per-rank repartition +
  * locate_sample loops. */
 int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,
                    uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
+/* rs_repartition, then the rank's outputs back to host buffers on the same stream (count
+ * entries of pos / ent / boff, qcount[c] entries of queue c).  timing->ms: kernels + D2H,
+ * timing->main_ms: the gather pass, timing->bytes: D2H bytes. */
+int rs_repartition_to_host(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch,
+                           uint64_t at_step, uint64_t new_dp, uint64_t rank, const rs_partition_out* out,
+                           void* scratch, const rs_partition_host* host, rs_timing* timing);
 /* Diagnostic (no reference counterpart): best-of-`reps` device time of K5's perm + entry
  * gathers for this rank plus all 44 output bytes per sample written coalesced, no scan
  * (env RESHARD_PROBE=read: nothing written) — the floor bench.py reports K5 against.

@@ -688,6 +688,62 @@ def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_p
     return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, gather_ms=t.main_ms)
 
 
+def dataset_index_upload(ctx: Context, gpu: int, host_perm: int, host_samples: int, n: int, perm_ptr: int,
+                         samples_ptr: int, padded_ptr: int = 0) -> dict:
+    """Host -> device upload of an index (pinned host pointers; padded_ptr: also pad it)."""
+    t = _capi.rs_timing()
+    _chk(lib.rs_dataset_index_upload(ctx.h, gpu, host_perm, host_samples, n, perm_ptr, samples_ptr, padded_ptr or None,
+                                     C.byref(t)))
+    return dict(ms=t.ms, bytes=t.bytes, launches=t.launches)
+
+
+class HostPartition:
+    """Pinned host buffers receiving one rank's repartition output."""
+
+    def __init__(self, count: int):
+        self.count = count
+        n = max(count, 1)
+        self.pos, self.ent, self.boff = host_alloc(8 * n), host_alloc(24 * n), host_alloc(8 * n)
+        self.queue = [host_alloc(4 * n) for _ in range(3)]
+        self.qcount = host_alloc(24)
+
+    def c(self):
+        h = _capi.rs_partition_host()
+        h.pos, h.ent, h.boff, h.qcount = self.pos, self.ent, self.boff, self.qcount
+        for i in range(3):
+            h.queue[i] = self.queue[i]
+        return h
+
+    def arrays(self) -> dict:
+        import numpy as np
+
+        n = self.count
+
+        def view(ptr, dt, k):
+            return np.ctypeslib.as_array((C.c_uint8 * max(k * np.dtype(dt).itemsize, 1)).from_address(ptr)).view(dt)[:k]
+
+        qc = [int(x) for x in view(self.qcount, np.uint64, 3)]
+        return {"pos": view(self.pos, np.uint64, n), "ent": view(self.ent, np.uint64, 3 * n).reshape(n, 3),
+                "boff": view(self.boff, np.uint64, n), "qcount": qc,
+                "qidx": np.concatenate([view(self.queue[c], np.uint32, qc[c]) for c in range(3)])}
+
+    def free(self):
+        for p in [self.pos, self.ent, self.boff, self.qcount, *self.queue]:
+            host_free(p)
+
+
+def repartition_to_host(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_ptr: int, n: int,
+                        global_batch: int, at_step: int, new_dp: int, rank: int, part: "Partition",
+                        host: HostPartition, entry_bytes: int = 24) -> dict:
+    """K5 for one rank with its outputs read back into `host` (kernels + D2H, event-timed)."""
+    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, class_ptr, n, entry_bytes)
+    t = _capi.rs_timing()
+    out, h = part.c(), host.c()
+    _chk(lib.rs_repartition_to_host(ctx.h, gpu, C.byref(idx), global_batch, at_step, new_dp, rank, C.byref(out),
+                                    part.scratch, C.byref(h), C.byref(t)))
+    return dict(ms=t.ms, gather_ms=t.main_ms, d2h_bytes=t.bytes, launches=t.launches)
+
+
 def dataset_index_pad(ctx: Context, gpu: int, packed_ptr: int, padded_ptr: int, n: int) -> dict:
     """Packed 24-byte index records -> padded 32-byte device layout (padded_ptr: 32 n bytes)."""
     t = _capi.rs_timing()

@@ -146,6 +146,9 @@ SIGNATURES = {
     "rs_locate_sample": (C.c_int, [C.c_uint64] * 6 + [P, P, P, U64P]),
     "rs_repartition_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
     "rs_dataset_index_pad": (C.c_int, [P, C.c_int, P, P, C.c_uint64, P]),
+    "rs_dataset_index_upload": (C.c_int, [P, C.c_int, P, P, C.c_uint64, P, P, P, P]),
+    "rs_repartition_to_host": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                         C.c_void_p, P, C.c_void_p, P]),
     "rs_shuffle_scratch_bytes": (C.c_int, [C.c_uint64, U64P]),
     "rs_shuffle_epoch_device": (C.c_int, [P, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, P, P,
                                           C.POINTER(rs_timing)]),
@@ -159,6 +162,11 @@ SIGNATURES = {
 class rs_dataset_index(C.Structure):
     _fields_ = [("perm", C.c_void_p), ("samples", C.c_void_p), ("file_class", C.c_void_p), ("n", C.c_uint64),
                 ("entry_bytes", C.c_uint64)]
+
+
+class rs_partition_host(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("ent", C.c_void_p), ("boff", C.c_void_p), ("queue", C.c_void_p * 3),
+                ("qcount", C.c_void_p)]
 
 
 class rs_partition_out(C.Structure):

@@ -722,6 +722,28 @@ int rs_dataset_index_pad(rs_context* c, int gpu, const uint64_t* packed, uint64_
     if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
+int rs_dataset_index_upload(rs_context* c, int gpu, const uint64_t* host_perm, const uint64_t* host_samples,
+                            uint64_t n, uint64_t* perm, uint64_t* samples, uint64_t* padded, rs_timing* timing) {
+  return guard([&] {
+    need(host_perm, "host_perm"), need(host_samples, "host_samples"), need(perm, "perm"), need(samples, "samples");
+    Timing t = dataset_index_upload(ctx_of(c), gpu, host_perm, host_samples, n, perm, samples, padded);
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
+  });
+}
+int rs_repartition_to_host(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t B, uint64_t at_step,
+                           uint64_t dp, uint64_t rank, const rs_partition_out* out, void* scratch,
+                           const rs_partition_host* host, rs_timing* timing) {
+  return guard([&] {
+    need(idx, "index"), need(out, "out"), need(scratch, "scratch"), need(host, "host");
+    need(host->pos, "host pos"), need(host->ent, "host ent"), need(host->boff, "host boff"), need(host->qcount, "host qcount");
+    for (int q = 0; q < 3; ++q) need(host->queue[q], "host queue");
+    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n, idx->entry_bytes};
+    PartitionOut o{out->pos, out->ent, out->boff, {out->queue[0], out->queue[1], out->queue[2]}, out->qcount};
+    PartitionHost h{host->pos, host->ent, host->boff, {host->queue[0], host->queue[1], host->queue[2]}, host->qcount};
+    Timing t = repartition_to_host(ctx_of(c), gpu, v, B, at_step, dp, rank, o, scratch, h);
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
+  });
+}
 int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes) {
   return guard([&] {
     need(bytes, "bytes");

@@ -710,6 +710,33 @@ Timing dataset_index_pad(Context& ctx, int gpu, const uint64_t* packed, uint64_t
   return t;
 }
 
+Timing dataset_index_upload(Context& ctx, int gpu, const uint64_t* host_perm, const uint64_t* host_samples,
+                            uint64_t n, uint64_t* perm, uint64_t* samples, uint64_t* padded) {
+  if (padded && (reinterpret_cast<uintptr_t>(padded) & 15))
+    raise(Errc::InvalidArgument, "dataset_index_upload: padded index must be 16-byte aligned");
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventRecord(e0, st), "event");
+  ck(cudaMemcpyAsync(perm, host_perm, 8 * n, cudaMemcpyHostToDevice, st), "H2D perm");
+  ck(cudaMemcpyAsync(samples, host_samples, 24 * n, cudaMemcpyHostToDevice, st), "H2D samples");
+  const uint64_t grid = std::min<uint64_t>((n + kThreads - 1) / kThreads, uint64_t(ctx.sm_count(gpu)) * 8);
+  if (padded && grid)
+    index_pad_kernel<<<unsigned(grid), kThreads, 0, st>>>(reinterpret_cast<const unsigned long long*>(samples),
+                                                          reinterpret_cast<unsigned long long*>(padded), n);
+  ck(cudaGetLastError(), "index pad launch");
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  Timing t;
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t.launches = padded && grid ? 1 : 0, t.bytes = 32 * n;
+  return t;
+}
+
 uint64_t repartition_scratch_bytes(uint64_t count) {
   const uint64_t tiles = (count + kGTile - 1) / kGTile;  // the smaller tile of the variants
   // counter + flags + tile aggregates + tile prefixes; split2: + class bytes + the tile
@@ -783,6 +810,39 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   t.tiles = tiles;
   t.bytes = count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
   t.launches = tiles ? (mode.lookback ? 1 : 3) : 0;
+  return t;
+}
+
+Timing repartition_to_host(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
+                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch,
+                           const PartitionHost& host) {
+  const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  cudaEvent_t e0, e1;
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventRecord(e0, st), "event");
+  Timing t = repartition_device(ctx, gpu, idx, B, at_step, new_dp, rank, out, scratch);
+  // the queue lengths decide how much of each queue comes back: read them first
+  ck(cudaMemcpyAsync(host.qcount, out.qcount, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "D2H qcount");
+  ck(cudaMemcpyAsync(host.pos, out.pos, 8 * count, cudaMemcpyDeviceToHost, st), "D2H pos");
+  ck(cudaMemcpyAsync(host.ent, out.ent, 24 * count, cudaMemcpyDeviceToHost, st), "D2H ent");
+  ck(cudaMemcpyAsync(host.boff, out.boff, 8 * count, cudaMemcpyDeviceToHost, st), "D2H boff");
+  ck(cudaStreamSynchronize(st), "sync");
+  uint64_t qbytes = 0;
+  for (int c = 0; c < 3; ++c) {
+    if (host.qcount[c] > count) raise(Errc::CudaError, "repartition_to_host: queue length above the count");
+    if (host.qcount[c])
+      ck(cudaMemcpyAsync(host.queue[c], out.queue[c], 4 * host.qcount[c], cudaMemcpyDeviceToHost, st), "D2H queue");
+    qbytes += 4 * host.qcount[c];
+  }
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t.bytes = 24 + 40 * count + qbytes;  // D2H bytes
   return t;
 }
 

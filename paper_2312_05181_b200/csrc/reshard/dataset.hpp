@@ -48,6 +48,16 @@ struct PartitionOut {
   uint64_t* qcount;
 };
 
+// Host copies of one rank's outputs (pinned memory for full PCIe rate), same layout as
+// PartitionOut; queue[c] receives exactly qcount[c] entries.
+struct PartitionHost {
+  uint64_t* pos;
+  uint64_t* ent;
+  uint64_t* boff;
+  uint32_t* queue[3];
+  uint64_t* qcount;
+};
+
 // K8: the same permutation as shuffle_epoch, computed on the GPU (bit-identical; parallel
 // Fisher-Yates by deterministic reservations).  perm: device, n entries; scratch:
 // shuffle_scratch_bytes(n) of device memory.  Timing.tiles = rounds.
@@ -55,12 +65,24 @@ uint64_t shuffle_scratch_bytes(uint64_t n);
 Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm,
                             void* scratch);
 
+// Host -> device upload of an index (perm, packed samples) on the GPU's stream; with
+// `padded` non-null the packed records are also rewritten there (dataset_index_pad).
+// Timing.ms: event time of the whole upload; bytes: H2D bytes.
+Timing dataset_index_upload(Context& ctx, int gpu, const uint64_t* host_perm, const uint64_t* host_samples,
+                            uint64_t n, uint64_t* perm, uint64_t* samples, uint64_t* padded);
+
 uint64_t repartition_scratch_bytes(uint64_t count);
 // K5 for one rank: gather pass, tile scan, finalize (three launches; RESHARD_K5=lookback:
 // one).  `scratch` (repartition_scratch_bytes) must be device memory.  Timing.main_ms is
 // the gather pass alone.
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch);
+// repartition_device, then the rank's outputs device -> host (exactly count entries of
+// pos / ent / boff and qcount[c] of each queue) on the same stream.  Timing.ms: kernels +
+// D2H (events), main_ms: the gather pass, bytes: D2H bytes.
+Timing repartition_to_host(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
+                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch,
+                           const PartitionHost& host);
 // Diagnostic: best-of-`reps` time of K5's perm + entry gathers for the rank's positions
 // plus all 44 output bytes per sample written coalesced, no scan (RESHARD_PROBE=read:
 // nothing written) — the floor for any kernel that must produce the partition.

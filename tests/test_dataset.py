@@ -177,6 +177,46 @@ def test_index_pad_layout_and_errors(rs, ctx, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("eb", [24, 32])
+def test_host_buffer_path_matches_oracle(rs, orc, ctx, eb):
+    """rs_dataset_index_upload + rs_repartition_to_host: pinned host index in, pinned host
+    outputs back, equal to the oracle for every rank of a DP change."""
+    import ctypes
+
+    rng = random.Random(11)
+    n, nf, B, at, dp = 77_777, 11, 96, 40, 4
+    samples = corpus(n, nf, rng)
+    perm = rs.shuffle_epoch(n, 3, 2)
+    h_perm, h_samp = rs.host_alloc(8 * n), rs.host_alloc(24 * n)
+    ctypes.memmove(h_perm, perm.ctypes.data, 8 * n)
+    ctypes.memmove(h_samp, samples.ctypes.data, 24 * n)
+    d_perm, d_samp = ctx.malloc(0, 8 * n), ctx.malloc(0, 24 * n)
+    d_pad = ctx.malloc(0, 32 * n) if eb == 32 else 0
+    up = rs.dataset_index_upload(ctx, 0, h_perm, h_samp, n, d_perm, d_samp, d_pad)
+    assert up["bytes"] == 32 * n and up["launches"] == (1 if eb == 32 else 0)
+    for d in range(dp):
+        fc = classes(nf, dp, d)
+        d_fc = ctx.malloc(0, nf)
+        ctx.htod(0, d_fc, fc.ctypes.data, nf)
+        cnt = rs.repartition_count(n, B, at, dp, d)
+        part, host = rs.Partition(ctx, 0, cnt), rs.HostPartition(cnt)
+        r = rs.repartition_to_host(ctx, 0, d_perm, d_pad or d_samp, d_fc, n, B, at, dp, d, part, host, entry_bytes=eb)
+        got = host.arrays()
+        want = orc.dataset_gather(n, B, at, dp, d, perm, samples, fc, n_threads=2)
+        assert np.array_equal(got["pos"], want["pos"]) and np.array_equal(got["ent"], want["ent"])
+        assert np.array_equal(got["boff"], want["boff"]) and got["qcount"] == want["qcount"]
+        assert np.array_equal(got["qidx"], want["qidx"])
+        assert r["d2h_bytes"] == 24 + 40 * cnt + 4 * sum(want["qcount"])
+        host.free()
+        part.free()
+        ctx.free(0, d_fc)
+    for p in (d_perm, d_samp) + ((d_pad,) if d_pad else ()):
+        ctx.free(0, p)
+    rs.host_free(h_perm)
+    rs.host_free(h_samp)
+
+
+@pytest.mark.gpu
 def test_k8_gpu_shuffle_bit_identical(rs, ctx):
     for n, seed, ep in [(1, 3, 0), (2, 3, 1), (1000, 0x5EED, 0), (123_457, 9, 4), (3_000_000, 0x5EED, 2)]:
         p = ctx.malloc(0, 8 * n)
