@@ -450,59 +450,76 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
     sc.inc[t] = blk_prefix + base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
 }
 
-// IT items per thread (4 or 8): a CTA covers IT / 4 aggregate tiles; warp w owns 32 IT
-// consecutive samples, inside aggregate tile (CTA * IT / 4 + w * IT / 32).
-template <int MINB, int IT>
-__global__ void __launch_bounds__(kThreads, MINB) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
-                                                                          const unsigned char* cls_in) {
-  static_assert(IT == 4 || IT == 8, "IT");
-  constexpr int kWarpsPerTile = kWarps * kGItems / IT;
+// Finalize: thread t of tile T owns the 4 consecutive samples T*1024 + 4t .. 4t+3 (16-byte
+// vector loads / stores of the parked lengths, one 4-byte load of the classes), so the scan
+// is a sequential sum in registers plus ONE warp scan of (length total, packed class counts)
+// per thread instead of one per item (r21 ncu: the warp-striped version was issue-bound,
+// 61 % SM throughput, 107 us per launch).
+constexpr int kCntBits = 10;  // per-class counts of one warp (<= 128) packed into a u32
+__global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
+                                                                     const unsigned char* cls_in) {
   __shared__ Agg warp_tot[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * (kThreads * IT) + warp * (32 * IT) + lane;
-  unsigned long long len[IT];
-  unsigned char cls[IT];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * kGTile + (unsigned long long)threadIdx.x * kGItems;
+  unsigned long long len[kGItems];
+  unsigned cls4;  // 4 class bytes, item j in byte j
+  const bool full = k0 + kGItems <= p.count && (reinterpret_cast<uintptr_t>(o.boff) & 15) == 0;
+  if (full) {
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(o.boff + k0);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(o.boff + k0 + 2);
+    len[0] = a.x, len[1] = a.y, len[2] = b.x, len[3] = b.y;
+    cls4 = *reinterpret_cast<const unsigned*>(cls_in + k0);
+  } else {
+    cls4 = 0x03030303u;
 #pragma unroll
-  for (int j = 0; j < IT; ++j) {
-    const unsigned long long k = k0 + 32 * j;
-    len[j] = k < p.count ? o.boff[k] : 0ull;
-    cls[j] = k < p.count ? cls_in[k] : (unsigned char)3;
-  }
-  unsigned long long lenx[IT];
-  Agg w{0, 0, 0, 0};
-#pragma unroll
-  for (int j = 0; j < IT; ++j) {
-    unsigned long long inc = len[j];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned long long up = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc += up;
+    for (int j = 0; j < kGItems; ++j) {
+      len[j] = k0 + j < p.count ? o.boff[k0 + j] : 0ull;
+      if (k0 + j < p.count) cls4 = (cls4 & ~(0xffu << (8 * j))) | (unsigned(cls_in[k0 + j]) << (8 * j));
     }
-    lenx[j] = w.len + inc - len[j];
-    w.len += __shfl_sync(0xffffffffu, inc, 31);
-    w.c0 += __popc(__ballot_sync(0xffffffffu, cls[j] == 0));
-    w.c1 += __popc(__ballot_sync(0xffffffffu, cls[j] == 1));
-    w.c2 += __popc(__ballot_sync(0xffffffffu, cls[j] == 2));
   }
-  if (lane == 0) warp_tot[warp] = w;
+  unsigned long long tl = 0;
+  unsigned tc = 0;
+#pragma unroll
+  for (int j = 0; j < kGItems; ++j) {
+    const unsigned c = (cls4 >> (8 * j)) & 0xffu;
+    tl += len[j];
+    if (c < 3) tc += 1u << (kCntBits * c);
+  }
+  unsigned long long il = tl;
+  unsigned ic = tc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long ul = __shfl_up_sync(0xffffffffu, il, d);
+    const unsigned uc = __shfl_up_sync(0xffffffffu, ic, d);
+    if (lane >= d) il += ul, ic += uc;
+  }
+  constexpr unsigned m = (1u << kCntBits) - 1u;
+  if (lane == 31) warp_tot[warp] = Agg{il, ic & m, (ic >> kCntBits) & m, ic >> (2 * kCntBits)};
   __syncthreads();
-  const int first = warp / kWarpsPerTile * kWarpsPerTile;  // first warp of this warp's aggregate tile
-  const unsigned long long tile = (unsigned long long)blockIdx.x * (IT / kGItems) + warp / kWarpsPerTile;
-  Agg run = tile < (p.count + kGTile - 1) / kGTile ? prefix[tile] : Agg{0, 0, 0, 0};
+  Agg run = prefix[blockIdx.x];
 #pragma unroll
   for (int q = 0; q < kWarps; ++q)
-    if (q >= first && q < warp) run = run + warp_tot[q];
+    if (q < warp) run = run + warp_tot[q];
+  const unsigned ex = ic - tc;  // exclusive class counts within the warp
+  unsigned long long off = run.len + il - tl;
+  unsigned long long qi[3] = {run.c0 + (ex & m), run.c1 + ((ex >> kCntBits) & m), run.c2 + (ex >> (2 * kCntBits))};
+  unsigned long long out[kGItems];
 #pragma unroll
-  for (int j = 0; j < IT; ++j) {
-    const unsigned long long k = k0 + 32 * j;
-    if (k < p.count) o.boff[k] = run.len + lenx[j];
-    const unsigned m0 = __ballot_sync(0xffffffffu, cls[j] == 0), m1 = __ballot_sync(0xffffffffu, cls[j] == 1),
-                   m2 = __ballot_sync(0xffffffffu, cls[j] == 2);
-    if (cls[j] == 0) o.q0[run.c0 + __popc(m0 & lt)] = unsigned(k);
-    else if (cls[j] == 1) o.q1[run.c1 + __popc(m1 & lt)] = unsigned(k);
-    else if (cls[j] == 2) o.q2[run.c2 + __popc(m2 & lt)] = unsigned(k);
-    run.c0 += __popc(m0), run.c1 += __popc(m1), run.c2 += __popc(m2);
+  for (int j = 0; j < kGItems; ++j) {
+    out[j] = off;
+    off += len[j];
+    const unsigned c = (cls4 >> (8 * j)) & 0xffu;
+    if (c == 0) o.q0[qi[0]++] = unsigned(k0 + j);
+    else if (c == 1) o.q1[qi[1]++] = unsigned(k0 + j);
+    else if (c == 2) o.q2[qi[2]++] = unsigned(k0 + j);
+  }
+  if (full) {
+    *reinterpret_cast<ulonglong2*>(o.boff + k0) = make_ulonglong2(out[0], out[1]);
+    *reinterpret_cast<ulonglong2*>(o.boff + k0 + 2) = make_ulonglong2(out[2], out[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kGItems; ++j)
+      if (k0 + j < p.count) o.boff[k0 + j] = out[j];
   }
 }
 
@@ -789,7 +806,7 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
     const uint64_t sblocks = (tiles + 1023) / 1024;
     Agg* blk = reinterpret_cast<Agg*>(cls + align256(count));
     repart_tile_scan_kernel<<<unsigned(sblocks), 1024, 0, st>>>(s, blk, blk + sblocks, o);
-    repart_finalize2_kernel<1, 4><<<g, kThreads, 0, st>>>(p, o, s.inc, cls);
+    repart_finalize2_kernel<<<g, kThreads, 0, st>>>(p, o, s.inc, cls);
     ck(cudaGetLastError(), "repartition launch");
   } else if (tiles) {
     if (mode.minb == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
