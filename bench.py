@@ -640,7 +640,8 @@ def run_ours(args):
     achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
     kname = copy_kernel_name()
     # the committed ncu capture is of the distributed-mode launch
-    traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" else None
+    # the committed ncu capture is of the one-GPU launch; a rank of a larger world launches a share of it
+    traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" and world == 1 else None
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
