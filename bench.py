@@ -639,7 +639,6 @@ def run_ours(args):
     alg_bytes = read_bytes + copy_bytes
     achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
     kname = copy_kernel_name()
-    # the committed ncu capture is of the distributed-mode launch
     # the committed ncu capture is of the one-GPU launch; a rank of a larger world launches a share of it
     traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" and world == 1 else None
     line = {
