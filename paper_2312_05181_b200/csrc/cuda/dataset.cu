@@ -407,8 +407,10 @@ __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p
     for (int q = 0; q < kWarps; ++q) L += warp_len[q], C += warp_cnt[q];
     sc.agg[blockIdx.x] = Agg{L, C & kClsMask, (C >> kClsBits) & kClsMask, C >> (2 * kClsBits)};
   }
-  if (blockIdx.x == 0)  // the tile scan's look-back flags (one per 1024 tiles), consumed after this launch
+  if (blockIdx.x == 0) {  // the tile scan's ticket counter and look-back flags, consumed after this launch
+    if (threadIdx.x == 0) *sc.counter = 0u;
     for (unsigned i = threadIdx.x; i < (sc.ntiles + 1023) / 1024; i += kThreads) sc.flags[i] = 0u;
+  }
 }
 
 // Exclusive scan of the tile aggregates: one 1024-thread CTA per 1024 tiles (coalesced loads,
@@ -418,8 +420,14 @@ __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p
 __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg* blk_agg, Agg* blk_inc, Outs o) {
   __shared__ Agg warp_tot[32];
   __shared__ Agg blk_prefix;
+  __shared__ unsigned ticket;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned t = blockIdx.x * 1024u + threadIdx.x;
+  // block order from an atomic ticket, not blockIdx: a block only ever waits on blocks that
+  // already run, whatever order the hardware schedules them in
+  if (threadIdx.x == 0) ticket = atomicAdd(sc.counter, 1u);
+  __syncthreads();
+  const unsigned b = ticket;
+  const unsigned t = b * 1024u + threadIdx.x;
   const Agg mine = t < sc.ntiles ? sc.agg[t] : Agg{0, 0, 0, 0};
   Agg inc = mine;
 #pragma unroll
@@ -436,10 +444,10 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
   }
   if (warp == 0) {
     const Scratch bs{nullptr, sc.flags, blk_agg, blk_inc, gridDim.x};
-    const Agg prefix = decoupled_lookback(blockIdx.x, total, bs, lane);
+    const Agg prefix = decoupled_lookback(b, total, bs, lane);
     if (lane == 0) {
       blk_prefix = prefix;
-      if (blockIdx.x == gridDim.x - 1) {
+      if (b == gridDim.x - 1) {
         const Agg all = prefix + total;
         o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
       }

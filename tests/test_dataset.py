@@ -232,7 +232,8 @@ def test_k8_gpu_shuffle_bit_identical(rs, ctx):
 def test_config5_full_size_matches_oracle(rs, orc, ctx):
     """BASELINE config 5 at full size (N = 10^8, B = 1280, DP 2 -> 4 -> 8): the K8 GPU epoch
     permutation equals the host Fisher-Yates, and every rank's K5 output (positions, entries,
-    byte offsets, locator queues) equals the oracle's gather on the same inputs."""
+    byte offsets, locator queues) equals the oracle's gather on the same inputs (17 tile-scan
+    blocks per rank; the 2 -> 4 event reads the packed index, 4 -> 8 the padded one)."""
     n, B, files, per_file, sb = 100_000_000, 1280, 1000, 100_000, 8206
     k = np.arange(n, dtype=np.uint64)
     samples = np.empty((n, 3), np.uint64)
@@ -248,14 +249,16 @@ def test_config5_full_size_matches_oracle(rs, orc, ctx):
     ctx.dtoh(0, dev_perm.ctypes.data, d_perm, 8 * n)
     assert np.array_equal(dev_perm, perm)
     del dev_perm
-    for at, dp in [(25_000, 4), (50_000, 8)]:
+    d_pad = ctx.malloc(0, 32 * n)
+    rs.dataset_index_pad(ctx, 0, d_samp, d_pad, n)
+    for (at, dp), eb in [((25_000, 4), 24), ((50_000, 8), 32)]:  # packed then padded index
         for d in range(dp):
             m = np.arange(files) % (dp + 1)
             fc = np.where(m == d, 0, np.where(m == dp, 2, 1)).astype(np.uint8)
             d_fc = ctx.malloc(0, files)
             ctx.htod(0, d_fc, fc.ctypes.data, files)
             part = rs.Partition(ctx, 0, rs.repartition_count(n, B, at, dp, d))
-            rs.repartition(ctx, 0, d_perm, d_samp, d_fc, n, B, at, dp, d, part)
+            rs.repartition(ctx, 0, d_perm, d_pad if eb == 32 else d_samp, d_fc, n, B, at, dp, d, part, entry_bytes=eb)
             got = part.fetch()
             want = orc.dataset_gather(n, B, at, dp, d, perm, samples, fc, n_threads=os.cpu_count() or 1)
             for key in ("pos", "ent", "boff", "qidx"):
@@ -266,3 +269,4 @@ def test_config5_full_size_matches_oracle(rs, orc, ctx):
             ctx.free(0, d_fc)
     ctx.free(0, d_perm)
     ctx.free(0, d_samp)
+    ctx.free(0, d_pad)
