@@ -151,6 +151,26 @@ __device__ __forceinline__ void bulk_s2g(void* dst, unsigned src_smem, unsigned 
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
                : "memory");
 }
+// The same copies with an L2 cache policy (bulk_*_hint): HINT bit 0 = loads evict_first,
+// bit 1 = stores evict_first (the state streams through once; RESHARD_BULK_HINT A/B).
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(unsigned dst_smem, const void* src, unsigned bytes, unsigned bar,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* dst, unsigned src_smem, unsigned bytes, unsigned long long pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst), "r"(src_smem),
+               "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -275,6 +295,7 @@ __device__ __forceinline__ void load_desc(const DevFanTile* p, DevFanTile& out) 
   for (int k = 0; k < 6; ++k) d[k] = v[k];
 }
 
+template <int HINT>
 __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTile* __restrict__ tiles,
                                                                   unsigned long long n, int stages, unsigned stage_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -283,6 +304,7 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
   if (threadIdx.x != 0) return;
   for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const unsigned long long pol = HINT ? policy_evict_first() : 0ull;
   const unsigned long long first = blockIdx.x, step = gridDim.x;
   const unsigned long long mine = first < n ? (n - first + step - 1) / step : 0;
   const int ahead = stages > 2 ? stages - 2 : 1;
@@ -299,8 +321,11 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
     const unsigned bar = smem_u32(&bars[s_load]);
     const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
     mbar_expect_tx(bar, t.rows * t.row_bytes);
-    for (unsigned r = 0; r < t.rows; ++r)
-      bulk_g2s(base + r * t.row_bytes, reinterpret_cast<const char*>(t.src) + r * t.src_pitch, t.row_bytes, bar);
+    for (unsigned r = 0; r < t.rows; ++r) {
+      const char* src = reinterpret_cast<const char*>(t.src) + r * t.src_pitch;
+      if (HINT & 1) bulk_g2s_hint(base + r * t.row_bytes, src, t.row_bytes, bar, pol);
+      else bulk_g2s(base + r * t.row_bytes, src, t.row_bytes, bar);
+    }
     if (++s_load == stages) s_load = 0;
   };
   for (unsigned long long i = 0; i < mine && i < (unsigned long long)ahead; ++i) issue_load(i);
@@ -313,8 +338,11 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
     mbar_wait(smem_u32(&bars[s_store]), phase);
     const unsigned base = smem_u32(smem + size_t(s_store) * stage_bytes);
     for (unsigned d = 0; d < t.n_dst; ++d)
-      for (unsigned r = 0; r < t.rows; ++r)
-        bulk_s2g(reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d], base + r * t.row_bytes, t.row_bytes);
+      for (unsigned r = 0; r < t.rows; ++r) {
+        char* dst = reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d];
+        if (HINT & 2) bulk_s2g_hint(dst, base + r * t.row_bytes, t.row_bytes, pol);
+        else bulk_s2g(dst, base + r * t.row_bytes, t.row_bytes);
+      }
     bulk_commit();
     if (++s_store == stages) s_store = 0, phase ^= 1u;
   }
@@ -491,8 +519,12 @@ void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg
   const bool strided = cfg.kernel == CopyKernel::BulkStrided || cfg.kernel == CopyKernel::BulkWarp;
   const size_t smem = size_t(cfg.stages) * cfg.stage_bytes + (strided ? 0 : kDescRingBytes);
   if (smem > 227 * 1024) raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
+  auto strided_kern = cfg.l2_hint == 1   ? copy_bulk_strided_kernel<1>
+                      : cfg.l2_hint == 2 ? copy_bulk_strided_kernel<2>
+                      : cfg.l2_hint == 3 ? copy_bulk_strided_kernel<3>
+                                         : copy_bulk_strided_kernel<0>;
   auto kern = cfg.kernel == CopyKernel::BulkWarp ? copy_bulk_warp_kernel
-              : strided                          ? copy_bulk_strided_kernel
+              : strided                          ? strided_kern
                                                  : copy_bulk_kernel;
   check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "bulk smem attribute");
   const int grid = bulk_grid(n_tiles, sms, cfg);

@@ -106,6 +106,7 @@ CopyConfig CopyConfig::from_env() {
   }
   c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", is_bulk(c.kernel) ? 1 : 3));
   c.stages = env_int("RESHARD_BULK_STAGES", c.stages);
+  c.l2_hint = env_int("RESHARD_BULK_HINT", c.l2_hint) & 3;
   c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
   c.host_chunks = std::max(1, env_int("RESHARD_HOST_CHUNKS", c.host_chunks));
   return c;
