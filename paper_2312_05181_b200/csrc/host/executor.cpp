@@ -230,6 +230,8 @@ struct Executor::Local {
   unsigned long long* d_count = nullptr;
   std::vector<HostChunk> chunks;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaStream_t s_aux = nullptr;                       // LDG/STG tiles beside the bulk kernel
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> ev;
   std::unique_ptr<Local> phase_b;  // central mode, on the central GPU: staging -> destination tiles
   uint64_t launches() const { return (n_fan ? 1 : 0) + (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
@@ -245,14 +247,38 @@ struct Executor::Local {
     for (auto e : ev) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
+    if (s_aux) cudaStreamDestroy(s_aux);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
   }
 };
 
+// The bulk kernel (one 32-thread CTA per SM, TMA-driven) and the LDG/STG kernels (tiles
+// with a peer destination, or not 16-byte aligned) run concurrently on two streams: they
+// co-reside on every SM (32 + 3 x 512 threads, the LDG kernels use no shared memory), so a
+// GPU's local relayout (HBM) overlaps its NVLink pushes instead of preceding them.
 void Executor::launch_local(Local& l, void* stream) {
   const int sms = ctx_.sm_count(l.world);
-  cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, stream);
-  cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, stream);
-  cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, stream);
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool both = l.n_fan && (l.n_aligned || l.n_misc);
+  cudaStream_t side = s;
+  if (both) {
+    if (!l.s_aux) {
+      ck(cudaStreamCreateWithFlags(&l.s_aux, cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming), "event");
+    }
+    ck(cudaEventRecord(l.fork, s), "fork");
+    ck(cudaStreamWaitEvent(l.s_aux, l.fork, 0), "fork wait");
+    side = l.s_aux;
+  }
+  cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, s);
+  cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, side);
+  cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, side);
+  if (both) {
+    ck(cudaEventRecord(l.join, side), "join");
+    ck(cudaStreamWaitEvent(s, l.join, 0), "join wait");
+  }
 }
 
 Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::vector<int> src_gpu,
