@@ -173,3 +173,30 @@ def test_central_mode_layout_and_traffic(rs):
     with pytest.raises(rs.ReshardError) as e:
         rs.Executor(rs.Context(2, [], []), plan, list(range(8)), list(range(8)), 4096, central=8)
     assert e.value.name == "InvalidArgument"
+
+
+def test_dataset_abi_argument_errors(rs):
+    """The dataset entry points validate their arguments before touching a device: null
+    pointers and an unknown index layout fail with InvalidArgument (no exception crosses
+    the C ABI; the message carries the Errc name like reshard::Error::what())."""
+    import ctypes as C
+
+    from paper_2312_05181_b200 import _capi
+
+    lib = rs.lib
+    ctx = rs.Context(1, [], [])
+    t = _capi.rs_timing()
+    inv = 1 + rs._capi.ERRC.index("InvalidArgument")
+    assert lib.rs_dataset_index_upload(ctx.h, 0, None, None, 10, None, None, None, C.byref(t)) == inv
+    assert "InvalidArgument" in lib.rs_last_error().decode()
+    assert lib.rs_dataset_index_pad(ctx.h, 0, None, None, 10, C.byref(t)) == inv
+    idx = _capi.rs_dataset_index(8, 8, 8, 100, 24)
+    out = _capi.rs_partition_out()
+    assert lib.rs_repartition_to_host(ctx.h, 0, C.byref(idx), 10, 0, 2, 0, C.byref(out), None, None, C.byref(t)) == inv
+    host = _capi.rs_partition_host()
+    out.pos = out.ent = out.boff = out.qcount = 8
+    assert lib.rs_repartition_to_host(ctx.h, 0, C.byref(idx), 10, 0, 2, 0, C.byref(out), 8, C.byref(host),
+                                      C.byref(t)) == inv  # null host buffers
+    bad = _capi.rs_dataset_index(8, 8, 8, 100, 16)
+    assert lib.rs_repartition(ctx.h, 0, C.byref(bad), 10, 0, 2, 0, C.byref(out), 8, C.byref(t)) == inv
+    assert "entry_bytes" in lib.rs_last_error().decode()
