@@ -1,6 +1,7 @@
 // Executor: lowers a ReconfigPlan to copy tiles and runs them (see reshard/executor.hpp).
 #include "reshard/executor.hpp"
 
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -742,11 +743,24 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
       ck(cudaStreamCreateWithFlags(&l->s_h2d, cudaStreamNonBlocking), "stream");
       ck(cudaStreamCreateWithFlags(&l->s_d2h, cudaStreamNonBlocking), "stream");
     }
+    // RESHARD_HOST_TRACE=1 (diagnostic): timing-enabled events and a per-chunk timeline
+    // (H2D landed / kernel done / D2H done, ms from the start) on stderr
+    const bool trace = std::getenv("RESHARD_HOST_TRACE") && std::string(std::getenv("RESHARD_HOST_TRACE")) == "1";
+    if (trace)
+      for (auto e : l->ev) cudaEventDestroy(e);
+    if (trace) l->ev.clear();
     while (l->ev.size() < 2 * K + 1) {
       cudaEvent_t e;
-      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming), "event");
       l->ev.push_back(e);
     }
+    std::vector<cudaEvent_t> ed;  // trace: D2H done per chunk
+    if (trace)
+      for (size_t k = 0; k < K; ++k) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "event");
+        ed.push_back(e);
+      }
     cudaEvent_t* eh = l->ev.data();
     cudaEvent_t* ec = l->ev.data() + K;
     cudaEvent_t done = l->ev[2 * K];
@@ -788,12 +802,32 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
       ck(cudaStreamWaitEvent(l->s_d2h, ec[k], 0), "wait");
       if (safe[k] > down) ck(cudaMemcpyAsync(hdst + down, ddst + down, safe[k] - down, cudaMemcpyDeviceToHost, l->s_d2h), "d2h piece");
       down = std::max(down, safe[k]);
+      if (trace) ck(cudaEventRecord(ed[k], l->s_d2h), "event");
     }
     ck(cudaEventRecord(done, l->s_d2h), "event");
     ck(cudaStreamWaitEvent(s, done, 0), "wait");
     ck(cudaEventRecord(done, l->s_h2d), "event");  // the H2D tail must land too
     ck(cudaStreamWaitEvent(s, done, 0), "wait");
     t.launches = K;
+    if (trace) {
+      ck(cudaEventSynchronize(done), "sync");
+      uint64_t up = 0, dn = 0, pieces = 0;
+      for (size_t k = 0; k < K; ++k) {
+        float a = 0, b = 0, c = 0;
+        ck(cudaEventElapsedTime(&a, l->start, eh[k]), "elapsed");
+        ck(cudaEventElapsedTime(&b, l->start, ec[k]), "elapsed");
+        ck(cudaEventElapsedTime(&c, l->start, ed[k]), "elapsed");
+        uint64_t ub = 0;
+        for (auto [off, len] : l->chunks[k].uploads) ub += len, ++pieces;
+        up += ub;
+        std::fprintf(stderr, "host-trace chunk %zu: up %.2f MB (%zu pieces) h2d@%.3f kern@%.3f d2h@%.3f safe %.2f MB\n", k,
+                     ub / 1e6, l->chunks[k].uploads.size(), a, b, c, safe[k] / 1e6);
+      }
+      dn = down;
+      std::fprintf(stderr, "host-trace total: %zu chunks, %llu pieces, %.2f GB up in chunks (of %.2f), %.2f GB down\n", K,
+                   (unsigned long long)pieces, up / 1e9, ssize / 1e9, dn / 1e9);
+      for (auto e : ed) cudaEventDestroy(e);
+    }
   }
   ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
   ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
