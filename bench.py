@@ -455,8 +455,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(leg["value"], 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(leg["value"], 3),
-        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (splitmix64 payload of the model shapes)",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64" if args.workload in DATASET else "u8",
+        "data": "synthetic (100M-sample index, 1000 files)" if args.workload in DATASET
+        else "synthetic (splitmix64 payload of the model shapes)",
         "config": {"workload": args.workload, "parallelism": "cpu"},
         "cpu_baseline": {"value": round(leg["value"], 3), "unit": "ms", "cores": leg["cores"], "kind": leg["kind"],
                          "sample": leg["sample"]},
