@@ -18,6 +18,7 @@
 #include <string>
 
 #include "reshard/dataset.hpp"
+#include "reshard/trace.hpp"
 
 namespace reshard {
 
@@ -656,6 +657,7 @@ __global__ void shuffle_commit_kernel(const unsigned long long* __restrict__ lis
 uint64_t shuffle_scratch_bytes(uint64_t n) { return 256 + 3 * align256(n * 8); }
 
 Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm, void* scratch) {
+  TraceRange trace_("shuffle_epoch_device");
   if (n >= (1ull << 32)) raise(Errc::InvalidArgument, "GPU shuffle supports N < 2^32");
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   L2FetchScope l2fetch;
@@ -713,6 +715,7 @@ bool entry_padded(const DatasetIndexView& idx) {
 }
 
 Timing dataset_index_pad(Context& ctx, int gpu, const uint64_t* packed, uint64_t* padded, uint64_t n) {
+  TraceRange trace_("dataset_index_pad");
   if ((reinterpret_cast<uintptr_t>(padded) & 15) || (reinterpret_cast<uintptr_t>(packed) & 7))
     raise(Errc::InvalidArgument, "dataset_index_pad: misaligned buffers");
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
@@ -737,6 +740,7 @@ Timing dataset_index_pad(Context& ctx, int gpu, const uint64_t* packed, uint64_t
 
 Timing dataset_index_upload(Context& ctx, int gpu, const uint64_t* host_perm, const uint64_t* host_samples,
                             uint64_t n, uint64_t* perm, uint64_t* samples, uint64_t* padded) {
+  TraceRange trace_("dataset_index_upload");
   if (padded && (reinterpret_cast<uintptr_t>(padded) & 15))
     raise(Errc::InvalidArgument, "dataset_index_upload: padded index must be 16-byte aligned");
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
@@ -772,6 +776,7 @@ uint64_t repartition_scratch_bytes(uint64_t count) {
 
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch) {
+  TraceRange trace_("repartition_device");
   const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
   if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
   const bool pad = entry_padded(idx);
@@ -841,6 +846,7 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
 Timing repartition_to_host(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                            uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch,
                            const PartitionHost& host) {
+  TraceRange trace_("repartition_to_host");
   const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
   cudaEvent_t e0, e1;

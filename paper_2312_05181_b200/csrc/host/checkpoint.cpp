@@ -2,6 +2,7 @@
 // Device <-> file traffic is staged through two pinned buffers so the D2H (H2D) of one
 // chunk overlaps the write (read) of the previous one.
 #include "reshard/checkpoint.hpp"
+#include "reshard/trace.hpp"
 
 #include <cuda_runtime.h>
 
@@ -148,6 +149,7 @@ PtxHeader ptx_decode_header(const uint8_t* p, size_t n) {
 }
 
 IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
+  TraceRange trace_("checkpoint_save");
   const auto t0 = std::chrono::steady_clock::now();
   const ReconfigPlan& plan = ex.plan();
   Context& ctx = ex.context();
@@ -189,6 +191,7 @@ IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
 }
 
 IoStats checkpoint_load(Executor& ex, const std::string& dir) {
+  TraceRange trace_("checkpoint_load");
   const auto t0 = std::chrono::steady_clock::now();
   const PTC& a = *ex.plan().from;
   Context& ctx = ex.context();

@@ -10,6 +10,7 @@
 #include <unordered_map>
 
 #include "cuda/kernels.hpp"
+#include "reshard/trace.hpp"
 
 namespace reshard {
 
@@ -516,6 +517,7 @@ void Executor::bind(int gpu, void* src, void* dst) {
 }
 
 void Executor::prepare() {
+  TraceRange trace_("Executor::prepare");
   for (auto& l : local_) {
     lower_tiles(*l, logical_[size_t(l->world)], central_ < 0);
     if (l->phase_b) lower_tiles(*l->phase_b, logical_b_, false);
@@ -633,6 +635,7 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
 }
 
 void Executor::run() {
+  TraceRange trace_("Executor::run");
   Local* central = nullptr;
   for (auto& l : local_) {
     DeviceGuard g(l->dev);
@@ -653,6 +656,7 @@ void Executor::run() {
 }
 
 std::vector<Timing> Executor::wait() {
+  TraceRange trace_("Executor::wait");
   std::vector<Timing> out;
   for (auto& l : local_) {
     DeviceGuard g(l->dev);
@@ -673,6 +677,7 @@ std::vector<Timing> Executor::wait() {
 }
 
 void Executor::host_phase(int gpu, int phase, void* host_buf) {
+  TraceRange trace_("Executor::host_phase");
   Local* l = nullptr;
   for (auto& x : local_)
     if (x->world == gpu) l = x.get();
@@ -711,6 +716,7 @@ float Executor::host_elapsed(int gpu) {
 }
 
 Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
+  TraceRange trace_("Executor::run_host");
   Local* l = nullptr;
   for (auto& x : local_)
     if (x->world == gpu) l = x.get();
@@ -857,6 +863,7 @@ uint64_t Executor::read_bytes_for(int gpu) const {
 // Upload a batch of payload tasks per local GPU and run K6 (fill) or K7 (verify) in one
 // launch each; returns the mismatch count (verify).
 uint64_t Executor::payload_pass(const std::vector<std::vector<cuda::PayloadTask>>& per_local, bool verify) {
+  TraceRange trace_("Executor::payload_pass");
   uint64_t bad = 0;
   for (size_t li = 0; li < local_.size(); ++li) {
     Local& l = *local_[li];

@@ -14,6 +14,7 @@
 #include <sstream>
 
 #include "reshard/planner.hpp"
+#include "reshard/trace.hpp"
 
 namespace reshard {
 
@@ -144,6 +145,7 @@ std::shared_ptr<const ReconfigPlan> plan_impl(std::shared_ptr<const PTC> from, s
 }  // namespace
 
 std::shared_ptr<const ReconfigPlan> generate_plan(std::shared_ptr<const PTC> from, std::shared_ptr<const PTC> to) {
+  TraceRange trace_("reshard::generate_plan");
   return plan_impl(std::move(from), std::move(to), {});
 }
 

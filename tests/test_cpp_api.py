@@ -40,3 +40,24 @@ def test_cpp_plan_equals_c_abi_plan(plan_cli, rs):
 def test_cpp_error_code(plan_cli):
     p = subprocess.run([plan_cli, "gpt", "3", "1", "1", "1", "1", "1"], capture_output=True, text=True)
     assert p.returncode == 1 + 9 and p.stderr.startswith("IndivisibleSliceDim")  # 64 % 3 != 0
+
+
+def test_planner_clean_under_asan_ubsan(plan_cli, tmp_path):
+    """The host planner (core / ptc / planner sources, no CUDA) built with AddressSanitizer
+    and UndefinedBehaviorSanitizer: the Fig. 6 plan, the BASELINE 6.7B transitions and an
+    error path run without a sanitizer report and print exactly what the normal build
+    prints (host ASan/UBSan)."""
+    asan = str(tmp_path / "plan_cli_asan")
+    host = os.path.join(PKG, "csrc", "host")
+    subprocess.run([CXX, "-std=c++20", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+                    "-fno-omit-frame-pointer", "-I", os.path.join(PKG, "csrc"),
+                    os.path.join(ROOT, "examples", "plan_cli.cpp"),
+                    *[os.path.join(host, f) for f in ("core.cpp", "ptc.cpp", "planner.cpp")], "-o", asan], check=True)
+    env = dict(os.environ, ASAN_OPTIONS="detect_leaks=1:abort_on_error=0", UBSAN_OPTIONS="print_stacktrace=1")
+    for args in (["fig6"], ["gpt", "4", "2", "1", "2", "2", "2", "4096", "32", "2048", "50304"],
+                 ["gpt", "2", "2", "2", "2", "2", "1"], ["gpt", "2", "1", "1", "1", "2", "1", "768", "12", "1024", "50304"],
+                 ["gpt", "3", "1", "1", "1", "1", "1"]):
+        want = subprocess.run([plan_cli, *args], capture_output=True, text=True)
+        got = subprocess.run([asan, *args], capture_output=True, text=True, env=env)
+        assert "Sanitizer" not in got.stderr and "runtime error" not in got.stderr, got.stderr[-2000:]
+        assert (got.returncode, got.stdout) == (want.returncode, want.stdout)
