@@ -11,7 +11,6 @@
 // place and fills the class queues.  The single-pass decoupled look-back kernel
 // (repartition_kernel) stays selectable (RESHARD_K5=lookback).
 // Replaces the CPU loops of oracle.cpp orc_dataset_gather (SPEC restatement).
-#include <cooperative_groups.h>
 #include <cuda/atomic>
 #include <cuda_runtime.h>
 
@@ -653,62 +652,6 @@ __global__ void shuffle_commit_kernel(const unsigned long long* __restrict__ lis
   }
 }
 
-// All rounds in ONE cooperative launch (default): a resident grid runs reserve / grid sync /
-// commit / grid sync until no iteration is pending, so the ~72 rounds need no kernel launches
-// and no host round trip for the pending count.  perm / list traffic goes through L2
-// (ld/st.cg): L1 is not coherent across the grid-wide barriers.  r30 same-box A/B: 32.9 ms vs
-// 33.0 ms for RESHARD_K8=rounds (two launches per round) — the first five rounds' random
-// reservations and swaps over the 800 MB arrays are the whole cost, not the launches.
-__global__ void __launch_bounds__(256) shuffle_rounds_kernel(unsigned long long* list0, unsigned long long* list1,
-                                                             unsigned* counts, unsigned long long* resv,
-                                                             unsigned long long* perm, unsigned* rounds_out) {
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  unsigned long long* lists[2] = {list0, list1};
-  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x, lane = threadIdx.x & 31;
-  for (unsigned long long round = 1;; ++round) {
-    const int cur = int((round - 1) & 1);
-    const unsigned n = *reinterpret_cast<volatile unsigned*>(counts + cur);
-    if (n == 0) {
-      if (tid == 0) *rounds_out = unsigned(round - 1);
-      return;
-    }
-    if (tid == 0) counts[cur ^ 1] = 0u;
-    const unsigned long long* list = lists[cur];
-    for (unsigned k = tid; k < n; k += nth) {
-      const unsigned long long e = __ldcg(list + k), i = e >> 32, h = e & 0xffffffffull;
-      const unsigned long long key = (round << 32) | i;
-      atomicMax(resv + i, key);
-      if (h != i) atomicMax(resv + h, key);
-    }
-    grid.sync();
-    unsigned long long* next = lists[cur ^ 1];
-    for (unsigned base = tid & ~31u; base < n; base += nth) {
-      const unsigned k = base + lane;
-      bool pending = false;
-      unsigned long long e = 0;
-      if (k < n) {
-        e = __ldcg(list + k);
-        const unsigned long long i = e >> 32, h = e & 0xffffffffull, key = (round << 32) | i;
-        if (__ldcg(resv + i) == key && __ldcg(resv + h) == key) {
-          if (h != i) {
-            const unsigned long long a = __ldcg(perm + i), b = __ldcg(perm + h);
-            __stcg(perm + i, b);
-            __stcg(perm + h, a);
-          }
-        } else {
-          pending = true;
-        }
-      }
-      const unsigned mask = __ballot_sync(0xffffffffu, pending);
-      unsigned slot = 0;
-      if (lane == 0 && mask) slot = atomicAdd(counts + (cur ^ 1), unsigned(__popc(mask)));
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      if (pending) __stcg(next + slot + __popc(mask & ((1u << lane) - 1u)), e);
-    }
-    grid.sync();
-  }
-}
-
 }  // namespace
 
 uint64_t shuffle_scratch_bytes(uint64_t n) { return 256 + 3 * align256(n * 8); }
@@ -738,25 +681,7 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
                                                  seed ^ epoch);
   ck(cudaGetLastError(), "shuffle init");
   t.launches = 1;
-  const char* k8 = std::getenv("RESHARD_K8");
-  if (!(k8 && std::string(k8) == "rounds") && init > 0) {
-    static int coop_blocks = 0;  // resident 256-thread CTAs per SM of the rounds kernel
-    if (!coop_blocks) {
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_blocks, shuffle_rounds_kernel, 256, 0), "occupancy");
-      coop_blocks = std::max(1, coop_blocks);
-    }
-    const unsigned grid = unsigned(std::min<uint64_t>(uint64_t(ctx.sm_count(gpu)) * uint64_t(coop_blocks),
-                                                      (uint64_t(init) + 255) / 256));
-    unsigned* d_rounds = counts + 2;  // the scratch head has room for it
-    void* args[] = {&lists[0], &lists[1], &counts, &resv, &perm, &d_rounds};
-    ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(shuffle_rounds_kernel), dim3(grid), dim3(256), args, 0, st),
-       "shuffle rounds (cooperative)");
-    t.launches += 1;
-    ck(cudaMemcpyAsync(pinned, d_rounds, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "rounds d2h");
-    ck(cudaStreamSynchronize(st), "shuffle sync");
-    t.tiles = *pinned;
-  }
-  unsigned pending = k8 && std::string(k8) == "rounds" ? init : 0u;
+  unsigned pending = init;
   for (unsigned long long round = 1, cur = 0; pending > 0; ++round, cur ^= 1) {
     const int grid = int(std::min<unsigned long long>(grid_full, (pending + 255) / 256));
     ck(cudaMemsetAsync(counts + (cur ^ 1), 0, sizeof(unsigned), st), "reset count");

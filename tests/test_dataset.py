@@ -217,11 +217,7 @@ def test_host_buffer_path_matches_oracle(rs, orc, ctx, eb):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k8", ["", "rounds"])
-def test_k8_gpu_shuffle_bit_identical(rs, ctx, k8, monkeypatch):
-    """K8 (one cooperative launch for all rounds, or RESHARD_K8=rounds: two launches per
-    round) equals the host Fisher-Yates bit for bit."""
-    monkeypatch.setenv("RESHARD_K8", k8)
+def test_k8_gpu_shuffle_bit_identical(rs, ctx):
     for n, seed, ep in [(1, 3, 0), (2, 3, 1), (1000, 0x5EED, 0), (123_457, 9, 4), (3_000_000, 0x5EED, 2)]:
         p = ctx.malloc(0, 8 * n)
         t = rs.shuffle_epoch_device(ctx, 0, n, seed, ep, p)
