@@ -71,7 +71,21 @@ def dataset_classes(files, dp, d):
     return np.where(m == d, 0, np.where(m == dp, 2, 1)).astype(np.uint8)
 
 
-def run_dataset(args, rs):
+def _reduce(dist, local, vals, op):
+    """All-reduce a list of floats over the ranks (max or sum); identity for one process."""
+    if dist is None:
+        return vals
+    import torch
+
+    t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]
+
+
+def run_dataset(args, rs, dist=None):
+    """configs[4]: every new DP rank's repartition of both events; rank d of an event runs on
+    GPU d % N (each GPU independent, no data-path collective: scaling "weak" in ranks per
+    GPU, the time is the max over GPUs of their ranks' device time)."""
     import numpy as np
 
     rank, world, local = dist_env()
@@ -119,12 +133,18 @@ def run_dataset(args, rs):
 
     for _ in range(args.warmup):
         step()
+    ctx.sync(rank)
+    if dist is not None:
+        dist.barrier()
     step_ms, gather_ms = [], []
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             ms, gms, done, launches = step()
             step_ms.append(ms)
             gather_ms.append(gms)
+    ctx.sync(rank)
+    if dist is not None:
+        dist.barrier()
     # parity spot check of the last step against the host restatement of one rank
     at, dp, d, _, part = jobs[-1]
     got = part.fetch()
@@ -136,18 +156,32 @@ def run_dataset(args, rs):
     floor_ms = sum(rs.repartition_gather_probe(ctx, rank, d_perm, d_idx, n, spec["B"], at, dp, d, entry_bytes=eb)["ms"]
                    for at, dp, d, _, _ in jobs)
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if not args.no_e2e:
         e2e = dataset_e2e(args, rs, ctx, rank, spec, perm, samples, d_perm, d_samp, d_idx if eb == 32 else 0, eb, jobs)
+    # step time: max over GPUs of each GPU's device time; samples / launches summed.  The
+    # dominant kernel's achieved GB/s is per GPU: all GPUs' gather bytes over all GPUs'
+    # gather-pass time (the average launch of the dominant kernel).
+    split2 = os.environ.get("RESHARD_K5", "split2").startswith("split2")
+    per_sample = DATASET_GATHER_BYTES_PER_SAMPLE if split2 else DATASET_BYTES_PER_SAMPLE
+    ms, floor_ms = _reduce(dist, local, [statistics.mean(step_ms), floor_ms], "max")
+    done_r = done
+    done, launches, g_sum, b_sum = _reduce(dist, local, [done, launches, statistics.mean(gather_ms), done_r * per_sample],
+                                           "sum")
+    done, launches = int(done), int(launches)
+    if e2e is not None and dist is not None:
+        e2e["value"] = round(_reduce(dist, local, [e2e["value"]], "max")[0], 3)
+        h2d, d2h = _reduce(dist, local, [e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]], "sum")
+        e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"] = int(h2d), int(d2h)
+        e2e["note"] = "per GPU: upload of the whole index, its ranks' K5 + D2H; max over GPUs"
+        e2e.pop("roofline", None)
     if rank != 0:
         return
-    ms = statistics.mean(step_ms)
     peak, peak_kind = measured_peaks()
     alg = done * DATASET_BYTES_PER_SAMPLE
-    gms = statistics.mean(gather_ms)
-    split2 = os.environ.get("RESHARD_K5", "split2").startswith("split2")
-    galg = done * (DATASET_GATHER_BYTES_PER_SAMPLE if split2 else DATASET_BYTES_PER_SAMPLE)
-    achieved = galg / (gms * 1e-3) / 1e9  # the dominant kernel (gather pass) over its own event time
-    n_gather = len(jobs)
+    gms = g_sum / world  # mean over GPUs of the gather-pass time per step
+    galg = done * per_sample
+    achieved = b_sum / (g_sum * 1e-3) / 1e9  # the dominant kernel (gather pass) over its own event time
+    n_gather = sum(dp for _, dp in spec["events"])
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
@@ -164,7 +198,7 @@ def run_dataset(args, rs):
                      "kernel_ms_per_step": round(gms, 4),
                      "step_achieved_gbs": round(alg / (ms * 1e-3) / 1e9, 1),
                      "gather_write_floor_ms": round(floor_ms, 4),
-                     "kernel_frac_of_floor": round(floor_ms / gms, 4),
+                     "kernel_frac_of_floor": round(floor_ms / gms, 4) if world == 1 else None,
                      "step_frac_of_floor": round(floor_ms / ms, 4),
                      "floor_note": "gather_write_probe_kernel: the same perm + entry gathers and the 44 output "
                                    "bytes per sample, coalesced, no scan; random 24-B gathers cost whole DRAM "
@@ -228,6 +262,8 @@ def dataset_e2e(args, rs, ctx, rank, spec, perm, samples, d_perm, d_samp, d_pad,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "host_matches_device": bool(same),
                 "path": "rs_dataset_index_upload + rs_repartition_to_host per rank, pinned host buffers"}
         try:
+            if dist_env()[1] > 1:
+                raise RuntimeError("PCIe roofline measured in one-GPU runs only")
             link = pcie_probe()
             bound = up["bytes"] / (link["h2d_gbs"] * 1e9) * 1e3 + d2h / (link["d2h_gbs"] * 1e9) * 1e3
             line["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound, 2),
@@ -485,8 +521,6 @@ def run_ours(args):
     N = args.gpus
     if world > 1 and world != N:
         raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}")
-    if args.workload in DATASET:
-        return run_dataset(args, rs)
     dist = None
     if world > 1:
         import torch
@@ -497,6 +531,8 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:  # gloo plumbing: lets several ranks share one GPU (multi-process correctness runs)
             dist.init_process_group("gloo")
+    if args.workload in DATASET:
+        return run_dataset(args, rs, dist)
     cat, a, b, plan, src_gpu, dst_gpu = build_plan(rs, args.workload, N)
     ctx = rs.Context(N, [rank], [local])
     # waves: catalog windows of ~equal bytes executed one after another over reused arenas
