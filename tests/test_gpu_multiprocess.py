@@ -35,3 +35,19 @@ def test_two_ranks_one_gpu_ipc_push(kernel):
     line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["verify_mismatched_bytes"] == 0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0  # multi-rank host-buffer path ran
+
+
+def test_two_ranks_dataset_repartition():
+    """configs[4] through torchrun with 2 ranks sharing cuda:0: new DP rank d of each event
+    runs on GPU d % 2, the line aggregates every rank's samples (10^8 x 1.04) and each
+    rank's spot check of positions / entries against the host restatement passes."""
+    env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--workload", "dataset-100m-dp2to4to8", "--no-cpu-baseline", "--no-e2e"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["samples_per_step"] == 104_000_000
+    assert line["spot_check"] == {"pos": True, "ent": True}
+    assert line["shuffle_epoch_gpu"]["bit_identical_to_host"]
