@@ -644,8 +644,12 @@ def run_ours(args):
                    "mismatched_bytes": bad_e2e}
             try:  # the PCIe bound of this path, measured on the same box
                 link = pcie_probe()
-                bound_ms = max(s_bytes / (link["h2d_gbs"] * 1e9), d_bytes / (link["d2h_gbs"] * 1e9),
-                               max(s_bytes, d_bytes) / (link["bidir_gbs_each"] * 1e9)) * 1e3
+                d_eff = d_bytes - ex.staging_bytes()
+                if args.mode == "central":  # H2D, both phases, D2H in sequence (no chunk pipeline)
+                    bound_ms = (s_bytes / (link["h2d_gbs"] * 1e9) + d_eff / (link["d2h_gbs"] * 1e9)) * 1e3
+                else:  # chunk pipeline: both directions at once
+                    bound_ms = max(s_bytes / (link["h2d_gbs"] * 1e9), d_eff / (link["d2h_gbs"] * 1e9),
+                                   max(s_bytes, d_eff) / (link["bidir_gbs_each"] * 1e9)) * 1e3
                 e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
                                    "frac": round(bound_ms / e2e["value"], 4)}
             except Exception as exc:
