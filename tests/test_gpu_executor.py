@@ -333,3 +333,31 @@ def test_central_mode_same_final_state(rs, orc, ctx):
         assert ex.verify() == 0
         ostate = oplan.apply(oa.fill())[0]
         assert _compare_with_oracle(rs, ctx, ex, b, ostate, [d for d in b_cfg[3]]) > 0
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_single_process_multi_gpu_world_on_one_device(rs, orc, world):
+    """One process driving a `world`-GPU world whose GPUs all map to cuda:0 (per-GPU streams,
+    arenas and launches): logical device d runs on world GPU d % world, so most fragments
+    have a destination on another world GPU (LDG/STG peer tiles beside the bulk kernel on
+    a second stream, fan-out tiles with mixed local / remote replicas).  Every destination
+    cell equals the oracle's."""
+    ctx = rs.Context(world, list(range(world)), [0] * world)
+    entries = [("param/w", 1, (16, 8), 0, 0), ("param/d", 1, (8, 16), 1, 0), ("exp_avg/w", 2, (16, 8), 0, 1),
+               ("param/b", 3, (24,), 0, 1), ("param/ln", 2, (8,), -1, -1)]
+    for a_cfg, b_cfg in [((2, 1, 1, DEV(2)), (2, 1, 2, DEV(4))),
+                         ((4, 2, 1, DEV(8)), (2, 2, 2, DEV(8))),
+                         ((2, 2, 2, DEV(8)), (4, 1, 1, DEV(4))),
+                         ((1, 2, 1, DEV(2)), (2, 1, 4, DEV(8)))]:
+        a, b, plan, oa, ob, oplan = _pair(rs, orc, entries, a_cfg, b_cfg)
+        n_src, n_dst = len(a_cfg[3]), len(b_cfg[3])
+        ex = rs.Executor(ctx, plan, [d % world for d in range(n_src)], [d % world for d in range(n_dst)], 4096)
+        ex.allocate_local()
+        ex.prepare()
+        ex.fill_sources()
+        t = ex.apply()
+        assert len(t) == world
+        assert ex.verify() == 0
+        ostate = oplan.apply(oa.fill())[0]
+        assert _compare_with_oracle(rs, ctx, ex, b, ostate, list(b_cfg[3])) > 0
+        del ex
