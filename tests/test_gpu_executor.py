@@ -335,13 +335,14 @@ def test_central_mode_same_final_state(rs, orc, ctx):
         assert _compare_with_oracle(rs, ctx, ex, b, ostate, [d for d in b_cfg[3]]) > 0
 
 
-@pytest.mark.parametrize("world", [4, 8])
-def test_single_process_multi_gpu_world_on_one_device(rs, orc, world):
+@pytest.mark.parametrize("world,bulk_peer", [(4, "0"), (8, "0"), (8, "1")])
+def test_single_process_multi_gpu_world_on_one_device(rs, orc, world, bulk_peer, monkeypatch):
     """One process driving a `world`-GPU world whose GPUs all map to cuda:0 (per-GPU streams,
     arenas and launches): logical device d runs on world GPU d % world, so most fragments
     have a destination on another world GPU (LDG/STG peer tiles beside the bulk kernel on
     a second stream, fan-out tiles with mixed local / remote replicas).  Every destination
-    cell equals the oracle's."""
+    cell equals the oracle's.  RESHARD_BULK_PEER=1: TMA bulk stores to the other GPUs too."""
+    monkeypatch.setenv("RESHARD_BULK_PEER", bulk_peer)
     ctx = rs.Context(world, list(range(world)), [0] * world)
     entries = [("param/w", 1, (16, 8), 0, 0), ("param/d", 1, (8, 16), 1, 0), ("exp_avg/w", 2, (16, 8), 0, 1),
                ("param/b", 3, (24,), 0, 1), ("param/ln", 2, (8,), -1, -1)]
