@@ -676,7 +676,7 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
   ck(cudaMallocHost(&pinned, sizeof(unsigned)), "pinned");
   const unsigned init = n ? unsigned(n - 1) : 0u;
   ck(cudaMemcpyAsync(counts, &init, sizeof(unsigned), cudaMemcpyHostToDevice, st), "count");
-  const int grid_full = 148 * 8;
+  const int grid_full = ctx.sm_count(gpu) * 8;  // 8 resident 256-thread CTAs per SM
   shuffle_init_kernel<<<grid_full, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(perm), resv, lists[0], n,
                                                  seed ^ epoch);
   ck(cudaGetLastError(), "shuffle init");
