@@ -4,9 +4,9 @@
  * namespace `reshard`, with no FFI of its own.  These entry points are the flat C binding a
  * maintainer would put in front of it (ctypes / cgo / JNI), one per reference operation:
  *
- *   rs_slice                 reshard::slice             proj/include/reshard/tensor/tensor.hpp:42
+ *   rs_slice / _host         reshard::slice             proj/include/reshard/tensor/tensor.hpp:42
  *                                                        proj/src/tensor/tensor.cpp:61-78
- *   rs_merge                 reshard::merge             tensor.hpp:47, tensor.cpp:80-114
+ *   rs_merge / _host         reshard::merge             tensor.hpp:47, tensor.cpp:80-114
  *   rs_range_parse/_format   Range::parse / to_string   range.hpp:59-60, range.cpp:92-144
  *   rs_grid_cells            SplitGrid::cells           split_grid.hpp:37, split_grid.cpp:62-86
  *   rs_grid_refine           grid_refine                split_grid.hpp:55, split_grid.cpp:119-130
@@ -160,6 +160,13 @@ int rs_ipc_close_handle(rs_context* ctx, int gpu, void* ptr);
 int rs_slice(rs_context* ctx, int gpu, const rs_tensor* t, const rs_range* r, void* out);
 int rs_merge(rs_context* ctx, int gpu, int n_parts, const rs_range* ranges, const rs_tensor* parts, int rank,
              const uint64_t* target_shape, void* out);
+/* The same on HOST buffers (t->data / parts[i].data / out are host pointers): the reference's
+ * value-level slice / merge (tensor.hpp:40-47) — validated first, in the reference's order,
+ * then staged through the context's GPU.  C++ callers get the reference's own value type
+ * instead: reshard::Tensor, reshard::slice, reshard::merge (reshard/tensor.hpp). */
+int rs_slice_host(rs_context* ctx, int gpu, const rs_tensor* t, const rs_range* r, void* out);
+int rs_merge_host(rs_context* ctx, int gpu, int n_parts, const rs_range* ranges, const rs_tensor* parts, int rank,
+                  const uint64_t* target_shape, void* out);
 
 /* ---- collection description ------------------------------------------------------------- */
 int rs_catalog_create(rs_catalog** out);

@@ -275,6 +275,36 @@ def merge(ctx: Context, gpu: int, parts: Sequence[tuple], target_shape, out: int
     _chk(lib.rs_merge(ctx.h, gpu, n, rngs, ts, len(target_shape), _u64(target_shape), out))
 
 
+def slice_host(ctx: Context, gpu: int, dtype: int, shape, payload: bytes, box) -> bytes:
+    """The reference's value-level slice (tensor.hpp:40-42) on host bytes, through the GPU."""
+    import numpy as np
+
+    src = np.frombuffer(payload, np.uint8).copy() if len(payload) else np.zeros(1, np.uint8)
+    w = WIDTH.get(dtype, 1)
+    n = int(np.prod([b - a for a, b in box])) * w if box else w
+    out = np.zeros(max(n, 1), np.uint8)
+    t = DeviceTensor(dtype, tuple(shape), src.ctypes.data)
+    _chk(lib.rs_slice_host(ctx.h, gpu, C.byref(t.c()), C.byref(_range(box)), out.ctypes.data))
+    return out[:n].tobytes()
+
+
+def merge_host(ctx: Context, gpu: int, parts: Sequence[tuple], target_shape, dtype_hint: int = 0) -> bytes:
+    """The reference's value-level merge (tensor.hpp:44-47) on host bytes:
+    parts = [(box, dtype, shape, payload bytes), ...]."""
+    import numpy as np
+
+    keep = [np.frombuffer(p, np.uint8).copy() if len(p) else np.zeros(1, np.uint8) for _, _, _, p in parts]
+    n = len(parts)
+    rngs = (rs_range * max(n, 1))(*[_range(b) for b, _, _, _ in parts])
+    ts = (rs_tensor * max(n, 1))(*[DeviceTensor(dt, tuple(sh), k.ctypes.data).c() for (_, dt, sh, _), k in zip(parts, keep)])
+    dt = parts[0][1] if parts else dtype_hint
+    w = WIDTH.get(dt, 1)
+    nbytes = int(np.prod(target_shape)) * w if len(target_shape) else w
+    out = np.zeros(max(nbytes, 1), np.uint8)
+    _chk(lib.rs_merge_host(ctx.h, gpu, n, rngs, ts, len(target_shape), _u64(target_shape), out.ctypes.data))
+    return out[:nbytes].tobytes()
+
+
 # ---- collection description ------------------------------------------------------------------
 class Catalog:
     def __init__(self, handle=None):

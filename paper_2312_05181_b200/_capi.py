@@ -89,6 +89,8 @@ SIGNATURES = {
     "rs_ipc_close_handle": (C.c_int, [P, C.c_int, P]),
     "rs_slice": (C.c_int, [P, C.c_int, C.POINTER(rs_tensor), C.POINTER(rs_range), P]),
     "rs_merge": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(rs_range), C.POINTER(rs_tensor), C.c_int, U64P, P]),
+    "rs_slice_host": (C.c_int, [P, C.c_int, C.POINTER(rs_tensor), C.POINTER(rs_range), P]),
+    "rs_merge_host": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(rs_range), C.POINTER(rs_tensor), C.c_int, U64P, P]),
     "rs_catalog_create": (C.c_int, [C.POINTER(P)]),
     "rs_catalog_gpt": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(P)]),
     "rs_catalog_add": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int, U64P, C.c_int, C.c_int]),

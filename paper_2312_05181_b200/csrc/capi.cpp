@@ -11,6 +11,7 @@
 #include "reshard/config.hpp"
 #include "reshard/dataset.hpp"
 #include "reshard/executor.hpp"
+#include "reshard/tensor.hpp"
 
 using namespace reshard;
 
@@ -295,6 +296,25 @@ int rs_merge(rs_context* c, int gpu, int n, const rs_range* ranges, const rs_ten
     std::vector<std::pair<Range, DeviceTensorView>> v;
     for (int i = 0; i < n; ++i) v.emplace_back(to_range(ranges[i]), to_view(parts[i]));
     device_merge(ctx_of(c), gpu, v, to_shape(rank, target), out);
+  });
+}
+
+int rs_slice_host(rs_context* c, int gpu, const rs_tensor* t, const rs_range* r, void* out) {
+  return guard([&] {
+    need(t, "tensor"), need(r, "range");
+    const DeviceTensorView v = to_view(*t);
+    host_slice(ctx_of(c), gpu, HostTensorView{v.dtype, v.shape, v.data}, to_range(*r), out);
+  });
+}
+int rs_merge_host(rs_context* c, int gpu, int n, const rs_range* ranges, const rs_tensor* parts, int rank,
+                  const uint64_t* target, void* out) {
+  return guard([&] {
+    std::vector<std::pair<Range, HostTensorView>> v;
+    for (int i = 0; i < n; ++i) {
+      const DeviceTensorView d = to_view(parts[i]);
+      v.emplace_back(to_range(ranges[i]), HostTensorView{d.dtype, d.shape, d.data});
+    }
+    host_merge(ctx_of(c), gpu, v, to_shape(rank, target), out);
   });
 }
 

@@ -954,26 +954,34 @@ void device_slice(Context& ctx, int gpu, const DeviceTensorView& t, const Range&
   run_tiles_once(ctx, gpu, tiles);
 }
 
-void device_merge(Context& ctx, int gpu, const std::vector<std::pair<Range, DeviceTensorView>>& parts, const Shape& target,
-                  void* out) {
+void validate_merge(const std::vector<MergePartSpec>& parts, const Shape& target) {
   // validation order of the reference merge (tensor.cpp:81-98)
   if (parts.empty()) raise(Errc::TilingGap, "no parts");
-  const Dtype dt = parts.front().second.dtype;
+  const Dtype dt = parts.front().dtype;
   uint64_t covered = 0;
-  for (const auto& [r, p] : parts) {
-    r.check_against(target);
+  for (const MergePartSpec& p : parts) {
+    p.range->check_against(target);
     if (p.dtype != dt) raise(Errc::DtypeMismatch, "parts disagree on dtype");
-    if (p.shape != r.extents()) raise(Errc::ShapeMismatch, "part shape does not match its range " + r.to_string());
-    covered += r.elements();
+    if (*p.shape != p.range->extents()) raise(Errc::ShapeMismatch, "part shape does not match its range " + p.range->to_string());
+    covered += p.range->elements();
   }
   for (size_t i = 0; i < parts.size(); ++i)
     for (size_t j = i + 1; j < parts.size(); ++j)
-      if (parts[i].first.overlaps(parts[j].first))
-        raise(Errc::TilingOverlap, parts[i].first.to_string() + " overlaps " + parts[j].first.to_string());
+      if (parts[i].range->overlaps(*parts[j].range))
+        raise(Errc::TilingOverlap, parts[i].range->to_string() + " overlaps " + parts[j].range->to_string());
   if (covered != shape_elements(target))
     raise(Errc::TilingGap, "parts cover " + std::to_string(covered) + " of " + std::to_string(shape_elements(target)) + " elements");
   for (auto e : target)
     if (e == 0) raise(Errc::InvalidTensor, "zero extent");
+}
+
+void device_merge(Context& ctx, int gpu, const std::vector<std::pair<Range, DeviceTensorView>>& parts, const Shape& target,
+                  void* out) {
+  std::vector<MergePartSpec> spec;
+  spec.reserve(parts.size());
+  for (const auto& [r, p] : parts) spec.push_back({&r, p.dtype, &p.shape});
+  validate_merge(spec, target);
+  const Dtype dt = parts.front().second.dtype;
   const uint64_t w = dtype_width(dt);
   std::vector<CopyTile> tiles;
   for (const auto& [r, p] : parts) {

@@ -196,6 +196,14 @@ struct DeviceTensorView {
   const void* data;
 };
 void device_slice(Context& ctx, int gpu, const DeviceTensorView& t, const Range& r, void* out);
+// The reference merge's checks alone, in its order (tensor.cpp:81-98), for callers that
+// validate before staging data (host_merge).
+struct MergePartSpec {
+  const Range* range;
+  Dtype dtype;
+  const Shape* shape;
+};
+void validate_merge(const std::vector<MergePartSpec>& parts, const Shape& target);
 void device_merge(Context& ctx, int gpu, const std::vector<std::pair<Range, DeviceTensorView>>& parts,
                   const Shape& target, void* out);
 

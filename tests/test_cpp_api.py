@@ -61,3 +61,38 @@ def test_planner_clean_under_asan_ubsan(plan_cli, tmp_path):
         got = subprocess.run([asan, *args], capture_output=True, text=True, env=env)
         assert "Sanitizer" not in got.stderr and "runtime error" not in got.stderr, got.stderr[-2000:]
         assert (got.returncode, got.stdout) == (want.returncode, want.stdout)
+
+
+@pytest.fixture(scope="module")
+def tensor_values(rs, tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("cpp") / "tensor_values")
+    subprocess.run([CXX, "-std=c++20", "-O1", "-I", os.path.join(PKG, "csrc"),
+                    os.path.join(ROOT, "examples", "tensor_values.cpp"), "-L", PKG, "-lreshard_b200",
+                    f"-Wl,-rpath,{PKG}", "-o", out], check=True)
+    return out
+
+
+EXPECTED_ERRORS = ["zero extent: InvalidTensor", "payload size: InvalidTensor", "slice out of bounds: RangeOutOfBounds",
+                   "merge gap: TilingGap", "merge overlap: TilingOverlap"]
+
+
+def test_reference_tensor_value_api_validation(tensor_values, rs):
+    """reshard::Tensor / slice / merge with the reference's signatures (tensor.hpp:16-47):
+    construction and argument errors come out with the reference's Errc before any device
+    work; without a GPU the first data operation fails with DeviceUnavailable."""
+    p = subprocess.run([tensor_values], capture_output=True, text=True)
+    assert p.stdout.splitlines()[:5] == EXPECTED_ERRORS
+    if rs.device_count() == 0:
+        assert p.returncode == 1 + rs._capi.ERRC.index("DeviceUnavailable")
+        assert p.stderr.startswith("DeviceUnavailable")
+
+
+@pytest.mark.gpu
+def test_reference_tensor_value_api_on_gpu(tensor_values):
+    """The same program on a B200: SPEC.md:60-62's slice and the quadrant round trip."""
+    p = subprocess.run([tensor_values], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    lines = p.stdout.splitlines()
+    assert lines[:5] == EXPECTED_ERRORS
+    assert lines[5] == "slice [0:4,2:4]: 2 3 8 9 14 15 20 21"
+    assert lines[6] == "quadrant round trip: equal"

@@ -362,3 +362,24 @@ def test_single_process_multi_gpu_world_on_one_device(rs, orc, world, bulk_peer,
         ostate = oplan.apply(oa.fill())[0]
         assert _compare_with_oracle(rs, ctx, ex, b, ostate, list(b_cfg[3])) > 0
         del ex
+
+
+def test_reference_fixtures_through_host_value_api(rs, ctx):
+    """The reference fixtures replayed through rs_slice_host / rs_merge_host (host buffers in
+    and out, bytes moved on the GPU): same bytes, same error names."""
+    kat = _kat()
+
+    def outcome(fn):
+        try:
+            return {"ok": fn().hex()}
+        except rs.ReshardError as e:
+            return {"error": e.name}
+
+    for c in kat["slice"]:
+        got = outcome(lambda: rs.slice_host(ctx, 0, c["dtype"], c["shape"], bytes.fromhex(c["payload"]),
+                                            [tuple(b) for b in c["box"]]))
+        assert got == {k: c[k] for k in ("ok", "error") if k in c}, c["shape"]
+    for c in kat["merge"]:
+        parts = [([tuple(b) for b in p["box"]], p["dtype"], p["shape"], bytes.fromhex(p["payload"])) for p in c["parts"]]
+        got = outcome(lambda: rs.merge_host(ctx, 0, parts, tuple(c["target"])))
+        assert got == {k: c[k] for k in ("ok", "error") if k in c}, c["target"]

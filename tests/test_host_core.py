@@ -200,3 +200,34 @@ def test_dataset_abi_argument_errors(rs):
     bad = _capi.rs_dataset_index(8, 8, 8, 100, 16)
     assert lib.rs_repartition(ctx.h, 0, C.byref(bad), 10, 0, 2, 0, C.byref(out), 8, C.byref(t)) == inv
     assert "entry_bytes" in lib.rs_last_error().decode()
+
+
+def _kat():
+    import json
+
+    return json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "tensor_core_kat.json")))
+
+
+def test_host_value_slice_merge_validate_before_device(rs):
+    """rs_slice_host / rs_merge_host (the reference's value-level slice / merge) check their
+    arguments exactly like the reference before touching a device: every error case of the
+    reference fixtures gives the reference's error name with no GPU present, and a valid call
+    then fails with DeviceUnavailable (no CPU path)."""
+    ctx = rs.Context(1, [], [])
+
+    def outcome(fn):
+        try:
+            fn()
+            return "ok"
+        except rs.ReshardError as e:
+            return e.name
+
+    kat = _kat()
+    for c in kat["slice"]:
+        got = outcome(lambda: rs.slice_host(ctx, 0, c["dtype"], c["shape"], bytes.fromhex(c["payload"]),
+                                            [tuple(b) for b in c["box"]]))
+        assert got == (c["error"] if "error" in c else "DeviceUnavailable"), c
+    for c in kat["merge"]:
+        parts = [([tuple(b) for b in p["box"]], p["dtype"], p["shape"], bytes.fromhex(p["payload"])) for p in c["parts"]]
+        got = outcome(lambda: rs.merge_host(ctx, 0, parts, tuple(c["target"])))
+        assert got == (c["error"] if "error" in c else "DeviceUnavailable"), c
