@@ -43,6 +43,8 @@ int main() {
     expect_error("merge overlap", Errc::TilingOverlap, [&] {
       merge({{Range::parse("[0:4]"), iota_f32({4})}, {Range::parse("[2:6]"), iota_f32({4})}}, Shape{6});
     });
+    // the per-base-tensor digest the SPEC verifies against (hash.hpp:42)
+    std::printf("digest %016llx\n", (unsigned long long)fnv1a64(t.bytes()));
     // data: SPEC.md:60-62 and the quadrant round trip
     const Tensor s = slice(t, Range::parse("[0:4,2:4]"));
     std::printf("slice [0:4,2:4]:");

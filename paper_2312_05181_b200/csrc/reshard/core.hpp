@@ -14,6 +14,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <span>
 #include <string_view>
 #include <vector>
 
@@ -161,9 +162,13 @@ class SplitMix64 {
   uint64_t s_;
 };
 uint64_t fnv1a64(const void* data, size_t n);
+inline uint64_t fnv1a64(std::span<const uint8_t> bytes) { return fnv1a64(bytes.data(), bytes.size()); }  // hash.hpp:42
 class Fnv1a64 {  // incremental digest (hash.hpp:13-40)
  public:
+  static constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
+  static constexpr uint64_t kPrime = 0x100000001b3ull;
   Fnv1a64& update(const void* data, size_t n);
+  Fnv1a64& update(std::span<const uint8_t> bytes) { return update(bytes.data(), bytes.size()); }
   Fnv1a64& update(std::string_view s) { return update(s.data(), s.size()); }
   Fnv1a64& update_u64(uint64_t v);  // 8 little-endian bytes
   uint64_t digest() const { return h_; }
