@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 
+#include "reshard/checkpoint.hpp"  // ptx_encode / ptx_decode (ptx_io.hpp:13-20)
 #include "reshard/tensor.hpp"
 
 using namespace reshard;
@@ -45,6 +46,10 @@ int main() {
     });
     // the per-base-tensor digest the SPEC verifies against (hash.hpp:42)
     std::printf("digest %016llx\n", (unsigned long long)fnv1a64(t.bytes()));
+    // PTX1 container: header 6 + 8 x rank bytes, then the payload
+    const std::vector<uint8_t> enc = ptx_encode(t);
+    std::printf("ptx round trip: %s (%zu bytes, encoded_size %zu)\n", ptx_decode(enc) == t ? "equal" : "DIFFERENT",
+                enc.size(), ptx_encoded_size(t));
     // data: SPEC.md:60-62 and the quadrant round trip
     const Tensor s = slice(t, Range::parse("[0:4,2:4]"));
     std::printf("slice [0:4,2:4]:");

@@ -148,6 +148,39 @@ PtxHeader ptx_decode_header(const uint8_t* p, size_t n) {
   return PtxHeader{d, s, hb, payload};
 }
 
+std::vector<uint8_t> ptx_encode(const Tensor& t) {
+  std::vector<uint8_t> out = ptx_encode_header(t.dtype(), t.shape());
+  out.insert(out.end(), t.payload().begin(), t.payload().end());
+  return out;
+}
+
+Tensor ptx_decode(std::span<const uint8_t> bytes) {
+  const PtxHeader h = ptx_decode_header(bytes.data(), bytes.size());
+  return Tensor(h.dtype, h.shape,
+                std::vector<uint8_t>(bytes.begin() + std::ptrdiff_t(h.header_bytes), bytes.end()));
+}
+
+size_t ptx_encoded_size(const Tensor& t) { return ptx_encoded_size(t.dtype(), t.shape()); }
+
+void ptx_write_file(const std::string& path, const Tensor& t) {
+  const std::vector<uint8_t> b = ptx_encode(t);
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) raise(Errc::InvalidArgument, "cannot open " + path + " for writing");
+  const size_t w = std::fwrite(b.data(), 1, b.size(), f);
+  const bool ok = std::fclose(f) == 0 && w == b.size();
+  if (!ok) raise(Errc::InvalidArgument, "short write to " + path);
+}
+
+Tensor ptx_read_file(const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) raise(Errc::InvalidTensor, "cannot open " + path);
+  std::vector<uint8_t> b;
+  uint8_t buf[1 << 16];
+  for (size_t n; (n = std::fread(buf, 1, sizeof buf, f)) > 0;) b.insert(b.end(), buf, buf + n);
+  std::fclose(f);
+  return ptx_decode(b);
+}
+
 IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
   TraceRange trace_("checkpoint_save");
   const auto t0 = std::chrono::steady_clock::now();

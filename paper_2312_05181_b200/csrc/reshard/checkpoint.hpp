@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "reshard/executor.hpp"
+#include "reshard/tensor.hpp"
 
 namespace reshard {
 
@@ -29,6 +30,13 @@ struct PtxHeader {
 // Parses and validates a PTX1 buffer of `n` bytes (header + payload): InvalidTensor on a
 // bad magic, truncated header, unknown dtype code, zero extent or payload size mismatch.
 PtxHeader ptx_decode_header(const uint8_t* bytes, size_t n);
+
+// The reference's value-level PTX1 functions, same signatures as ptx_io.hpp:13-20.
+std::vector<uint8_t> ptx_encode(const Tensor& t);
+Tensor ptx_decode(std::span<const uint8_t> bytes);  // InvalidTensor
+void ptx_write_file(const std::string& path, const Tensor& t);
+Tensor ptx_read_file(const std::string& path);      // InvalidTensor on a bad file
+size_t ptx_encoded_size(const Tensor& t);
 
 struct IoStats {
   uint64_t files = 0, bytes = 0;
