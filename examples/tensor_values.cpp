@@ -1,14 +1,21 @@
-// examples/tensor_values.cpp — the reference's tensor-core value API (proj/include/reshard/
-// tensor/tensor.hpp:16-47) used unchanged from C++: reshard::Tensor, slice, merge.  The
-// validation errors come first and need no GPU; the data operations run on the GPU.
+// examples/tensor_values.cpp — a translation unit written against the reference's own headers
+// (the include paths of proj/include/reshard/...: error.hpp, tensor/{dtype,range,split_grid,
+// tensor,ptx_io}.hpp, util/hash.hpp) compiled unchanged against this library: Tensor, slice,
+// merge, SplitGrid, grid_refine, Range, PTX1, FNV-1a, splitmix64.  The validation errors and
+// the host-only calls need no GPU; slice / merge move their bytes on the GPU.
 //
 //   g++ -std=c++20 -I paper_2312_05181_b200/csrc examples/tensor_values.cpp \
 //       -L paper_2312_05181_b200 -lreshard_b200 -Wl,-rpath,$PWD/paper_2312_05181_b200 -o tensor_values
 #include <cstdio>
 #include <cstring>
 
-#include "reshard/checkpoint.hpp"  // ptx_encode / ptx_decode (ptx_io.hpp:13-20)
-#include "reshard/tensor.hpp"
+#include "reshard/error.hpp"
+#include "reshard/tensor/dtype.hpp"
+#include "reshard/tensor/ptx_io.hpp"
+#include "reshard/tensor/range.hpp"
+#include "reshard/tensor/split_grid.hpp"
+#include "reshard/tensor/tensor.hpp"
+#include "reshard/util/hash.hpp"
 
 using namespace reshard;
 
@@ -44,6 +51,12 @@ int main() {
     expect_error("merge overlap", Errc::TilingOverlap, [&] {
       merge({{Range::parse("[0:4]"), iota_f32({4})}, {Range::parse("[2:6]"), iota_f32({4})}}, Shape{6});
     });
+    // SURVEY §4 KATs: grid_refine({3}, {2,4}) on [6]; the first splitmix64 output from state 0
+    const SplitGrid g = grid_refine(SplitGrid({{3}}), SplitGrid({{2, 4}}));
+    std::printf("refine:");
+    for (const Range& c : g.cells(Shape{6})) std::printf("%s", c.to_string().c_str());
+    std::printf(" splitmix64(0) %016llx dtype %s\n", (unsigned long long)SplitMix64(0).next(),
+                dtype_name(dtype_from_code(uint8_t(0))));
     // the per-base-tensor digest the SPEC verifies against (hash.hpp:42)
     std::printf("digest %016llx\n", (unsigned long long)fnv1a64(t.bytes()));
     // PTX1 container: header 6 + 8 x rank bytes, then the payload

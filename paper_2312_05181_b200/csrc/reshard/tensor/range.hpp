@@ -1,0 +1,6 @@
+// reshard/tensor/range.hpp — the reference include path, forwarded: a reference translation unit compiles
+// unchanged against this library with -I paper_2312_05181_b200/csrc.  Declares what
+// proj/include/reshard/tensor/range.hpp (Shape, Interval, Range, RangeSpec) declares.
+#pragma once
+
+#include "reshard/core.hpp"

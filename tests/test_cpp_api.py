@@ -85,8 +85,9 @@ def test_reference_tensor_value_api_validation(tensor_values, rs):
     import struct
 
     iota = b"".join(struct.pack("<f", float(i)) for i in range(24))
-    assert p.stdout.splitlines()[5] == f"digest {rs.fnv1a64(iota):016x}"  # reshard::fnv1a64(std::span)
-    assert p.stdout.splitlines()[6] == "ptx round trip: equal (118 bytes, encoded_size 118)"  # 4+1+1+2*8 + 96
+    assert p.stdout.splitlines()[5] == "refine:[0:2][2:3][3:4][4:6] splitmix64(0) e220a8397b1dcdaf dtype f32"
+    assert p.stdout.splitlines()[6] == f"digest {rs.fnv1a64(iota):016x}"  # reshard::fnv1a64(std::span)
+    assert p.stdout.splitlines()[7] == "ptx round trip: equal (118 bytes, encoded_size 118)"  # 4+1+1+2*8 + 96
     if rs.device_count() == 0:
         assert p.returncode == 1 + rs._capi.ERRC.index("DeviceUnavailable")
         assert p.stderr.startswith("DeviceUnavailable")
@@ -99,5 +100,5 @@ def test_reference_tensor_value_api_on_gpu(tensor_values):
     assert p.returncode == 0, p.stderr
     lines = p.stdout.splitlines()
     assert lines[:5] == EXPECTED_ERRORS
-    assert lines[7] == "slice [0:4,2:4]: 2 3 8 9 14 15 20 21"
-    assert lines[8] == "quadrant round trip: equal"
+    assert lines[8] == "slice [0:4,2:4]: 2 3 8 9 14 15 20 21"
+    assert lines[9] == "quadrant round trip: equal"
