@@ -157,7 +157,11 @@ def run_dataset(args, rs, dist=None):
                    for at, dp, d, _, _ in jobs)
     e2e = None
     if not args.no_e2e:
-        e2e = dataset_e2e(args, rs, ctx, rank, spec, perm, samples, d_perm, d_samp, d_idx if eb == 32 else 0, eb, jobs)
+        try:
+            e2e = dataset_e2e(args, rs, ctx, rank, spec, perm, samples, d_perm, d_samp, d_idx if eb == 32 else 0, eb,
+                              jobs)
+        except Exception as exc:  # e.g. not enough pinned host memory on this box
+            e2e = {"value": None, "unit": "ms", "error": str(exc)[:200], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     # step time: max over GPUs of each GPU's device time; samples / launches summed.  The
     # dominant kernel's achieved GB/s is per GPU: all GPUs' gather bytes over all GPUs'
     # gather-pass time (the average launch of the dominant kernel).
