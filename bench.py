@@ -172,12 +172,18 @@ def run_dataset(args, rs, dist=None):
     done, launches, g_sum, b_sum = _reduce(dist, local, [done, launches, statistics.mean(gather_ms), done_r * per_sample],
                                            "sum")
     done, launches = int(done), int(launches)
-    if e2e is not None and dist is not None:
-        e2e["value"] = round(_reduce(dist, local, [e2e["value"]], "max")[0], 3)
+    if e2e is not None and dist is not None:  # every rank takes part in the same collectives
+        ok = e2e["value"] is not None
+        failed, v = _reduce(dist, local, [0.0 if ok else 1.0, e2e["value"] if ok else 0.0], "max")
         h2d, d2h = _reduce(dist, local, [e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]], "sum")
-        e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"] = int(h2d), int(d2h)
-        e2e["note"] = "per GPU: upload of the whole index, its ranks' K5 + D2H; max over GPUs"
-        e2e.pop("roofline", None)
+        if failed:
+            e2e = {"value": None, "unit": "ms", "error": e2e.get("error", "failed on another rank"),
+                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+        else:
+            e2e["value"] = round(v, 3)
+            e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"] = int(h2d), int(d2h)
+            e2e["note"] = "per GPU: upload of the whole index, its ranks' K5 + D2H; max over GPUs"
+            e2e.pop("roofline", None)
     if rank != 0:
         return
     peak, peak_kind = measured_peaks()
