@@ -722,7 +722,7 @@ def run_ours(args):
     }
     if N == 1 and not args.no_cpu_baseline:
         try:
-            leg = cpu_reference_leg(args.workload, args.sample_frac, 1, 0)
+            leg = cpu_reference_leg(args.workload, args.sample_frac, 3, 1)
             line["cpu_baseline"] = {"value": round(leg["value"], 3), "unit": "ms", "cores": leg["cores"],
                                     "kind": leg["kind"], "sample": leg["sample"]}
         except Exception as exc:
