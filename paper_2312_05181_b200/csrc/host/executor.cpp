@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <unordered_map>
@@ -91,6 +92,7 @@ int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
 }
+
 
 }  // namespace
 
@@ -460,26 +462,38 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
       groups[fan ? it->second : groups.size() - 1].members.push_back(Member{db.gpu, db.offset, dl, dbox.extents()});
     }
   }
-  for (const Group& grp : groups) {
+  // one fragment group -> logical tiles of its executing GPU (fan-out tiles when every
+  // member lowers to the same source tiles)
+  auto lower_group = [&](const Group& grp, std::vector<std::vector<Logical>>& outs) {
     const CellBinding& sb = src_bind_[grp.src_bind];
     const Range& sbox = a.cells[grp.tensor][grp.src_cell];
     const Range rs = grp.box.rebase_into(sbox);
     Shape sl;
     for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo);
     const uint64_t w = dtype_width(a.catalog.tensors[grp.tensor].dtype);
+    auto& out = outs[size_t(sb.gpu)];
+    if (grp.members.size() == 1) {  // the common case: tiles straight into the executing GPU's list
+      const Member& mem = grp.members[0];
+      lower_box(grp.box.extents(), sl, sbox.extents(), mem.dl, mem.dshape, w, tile_bytes_,
+                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+                  Logical& x = out.emplace_back();
+                  x.src_gpu = sb.gpu, x.src_arena = 0, x.n_dst = 1, x.src_off = sb.offset + so, x.src_pitch = sp;
+                  x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
+                  x.dst_gpu[0] = mem.dst_gpu, x.dst_off[0] = mem.dst_base + dof, x.dst_pitch[0] = dp;
+                });
+      return;
+    }
     std::vector<std::vector<Logical>> per(grp.members.size());
     for (size_t m = 0; m < grp.members.size(); ++m) {
       const Member& mem = grp.members[m];
       lower_box(grp.box.extents(), sl, sbox.extents(), mem.dl, mem.dshape, w, tile_bytes_,
                 [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                  Logical x{};
+                  Logical& x = per[m].emplace_back();
                   x.src_gpu = sb.gpu, x.n_dst = 1, x.src_off = sb.offset + so, x.src_pitch = sp;
                   x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
                   x.dst_gpu[0] = mem.dst_gpu, x.dst_off[0] = mem.dst_base + dof, x.dst_pitch[0] = dp;
-                  per[m].push_back(x);
                 });
     }
-    auto& out = logical_[size_t(sb.gpu)];
     bool same = per.size() > 1;
     for (size_t m = 1; same && m < per.size(); ++m) {
       same = per[m].size() == per[0].size();
@@ -489,7 +503,7 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
     }
     if (!same) {
       for (auto& v : per) out.insert(out.end(), v.begin(), v.end());
-      continue;
+      return;
     }
     for (size_t m0 = 0; m0 < per.size(); m0 += kMaxFan)
       for (size_t t = 0; t < per[0].size(); ++t) {
@@ -502,7 +516,15 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
         }
         out.push_back(x);
       }
+  };
+  {  // capacity: about one tile per tile_bytes_ of each executing GPU's copies
+    std::vector<uint64_t> est(logical_.size(), 0);
+    for (const Group& grp : groups)
+      est[size_t(src_bind_[grp.src_bind].gpu)] +=
+          grp.members.size() * (grp.box.elements() * dtype_width(a.catalog.tensors[grp.tensor].dtype) / tile_bytes_ + 1);
+    for (size_t g = 0; g < est.size(); ++g) logical_[g].reserve(logical_[g].size() + est[g] + 16);
   }
+  for (const Group& grp : groups) lower_group(grp, logical_);
 }
 
 Executor::~Executor() = default;
@@ -528,12 +550,20 @@ void Executor::prepare() {
 void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool host_chunks) {
   const bool bulk = is_bulk(cfg_.kernel);
   const bool interleave = cfg_.kernel == CopyKernel::Bulk;  // bulk_strided walks the natural order
+  using clk = std::chrono::steady_clock;
+  const bool trace = std::getenv("RESHARD_HOST_TRACE") && std::string(std::getenv("RESHARD_HOST_TRACE")) == "1";
+  auto t_mark = clk::now();
+  auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
   const char* bp = std::getenv("RESHARD_BULK_PEER");
   const bool bulk_peer = bp && std::string(bp) == "1";
   Local* l = &local;
   {
+    // Logical tiles -> descriptors with arena bases, classified: bulk fan tiles / 16-byte
+    // aligned LDG tiles / misaligned LDG tiles
     std::vector<FanTile> fans;
     std::vector<CopyTile> aligned, misc;
+    if (bulk) fans.reserve(lt.size());
+    else aligned.reserve(lt.size());
     uint64_t bytes = 0, read_bytes = 0;
     for (const Logical& x : lt) {
       char* s = static_cast<char*>(x.src_arena ? dst_base_[size_t(x.src_gpu)] : src_base_[size_t(x.src_gpu)]);
@@ -565,9 +595,24 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
         read_bytes += tb;
       }
     }
-    // destination order: sequential writes, and monotone destinations per host chunk
-    std::sort(fans.begin(), fans.end(), [](const FanTile& p, const FanTile& q) { return p.dst[0] < q.dst[0]; });
-    std::sort(aligned.begin(), aligned.end(), [](const CopyTile& p, const CopyTile& q) { return p.dst < q.dst; });
+    // destination order: sequential writes, and monotone destinations per host chunk (the
+    // tiles usually arrive sorted already; otherwise sort 16-byte keys and permute once)
+    auto by_dst = [](auto& v, auto dst_of) {
+      bool sorted = true;
+      for (size_t i = 1; sorted && i < v.size(); ++i) sorted = dst_of(v[i - 1]) <= dst_of(v[i]);
+      if (sorted) return;
+      std::vector<std::pair<uint64_t, uint32_t>> key(v.size());
+      for (size_t i = 0; i < v.size(); ++i) key[i] = {dst_of(v[i]), uint32_t(i)};
+      std::stable_sort(key.begin(), key.end(), [](const auto& p, const auto& q) { return p.first < q.first; });
+      std::remove_reference_t<decltype(v)> out;
+      out.reserve(v.size());
+      for (const auto& k : key) out.push_back(v[k.second]);
+      v.swap(out);
+    };
+    if (trace) std::fprintf(stderr, "prepare-trace convert %.1f ms (%zu tiles)\n", ms_since(t_mark), lt.size()), t_mark = clk::now();
+    by_dst(fans, [](const FanTile& t) { return t.dst[0]; });
+    if (trace) std::fprintf(stderr, "prepare-trace sort %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
+    by_dst(aligned, [](const CopyTile& t) { return t.dst; });
     l->chunks.clear();
     const bool one_list = misc.empty() && (fans.empty() != aligned.empty());
     if (host_chunks && ctx_.world() == 1 && one_list) {
@@ -579,14 +624,17 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
       std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);
       uint64_t acc = 0;
       for (size_t i = 0; i < n; ++i) {
-        FanTile f = fans.empty() ? FanTile{aligned[i].src, aligned[i].src_pitch, aligned[i].rows, aligned[i].row_bytes, 1, 0,
-                                           {aligned[i].dst}, {aligned[i].dst_pitch}}
-                                 : fans[i];
-        const uint64_t s0 = f.src - sb, s1 = s0 + (f.rows ? (f.rows - 1) * f.src_pitch : 0) + f.row_bytes;
-        spans.back().emplace_back(s0, s1);
+        const bool fan = !fans.empty();
+        const uint64_t src = fan ? fans[i].src : aligned[i].src, sp = fan ? fans[i].src_pitch : aligned[i].src_pitch;
+        const uint32_t rows = fan ? fans[i].rows : aligned[i].rows, rb = fan ? fans[i].row_bytes : aligned[i].row_bytes;
+        const uint32_t nd = fan ? fans[i].n_dst : 1;
+        const uint64_t s0 = src - sb, s1 = s0 + (rows ? (rows - 1) * sp : 0) + rb;
+        auto& sv = spans.back();  // consecutive tiles usually continue the previous source run
+        if (!sv.empty() && s0 >= sv.back().first && s0 <= sv.back().second) sv.back().second = std::max(sv.back().second, s1);
+        else sv.emplace_back(s0, s1);
         c.src_end = std::max(c.src_end, s1);
-        for (uint32_t d = 0; d < f.n_dst; ++d) c.dst_min = std::min(c.dst_min, f.dst[d] - db);
-        acc += uint64_t(f.rows) * f.row_bytes * f.n_dst;
+        for (uint32_t d = 0; d < nd; ++d) c.dst_min = std::min(c.dst_min, (fan ? fans[i].dst[d] : aligned[i].dst) - db);
+        acc += uint64_t(rows) * rb * nd;
         if (acc >= target || i + 1 == n) {
           c.t1 = i + 1;
           l->chunks.push_back(c);
@@ -597,17 +645,29 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
       }
       plan_uploads(l->chunks, spans);
     }
+    if (trace) std::fprintf(stderr, "prepare-trace chunks %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
     DeviceGuard g(l->dev);
     if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
     if (l->d_fan_chunks) cudaFree(l->d_fan_chunks), l->d_fan_chunks = nullptr;
     if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
     if (!fans.empty()) {
       const int sms = ctx_.sm_count(l->world);
-      auto full = cuda::interleave_for_grid(fans.data(), fans.size(),
-                                            interleave ? size_t(cuda::bulk_grid(fans.size(), sms, cfg_)) : 1);
-      ck(cudaMalloc(&l->d_fan, fans.size() * sizeof(FanTile)), "cudaMalloc tiles");
-      ck(cudaMemcpy(l->d_fan, full.data(), full.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
-      if (!l->chunks.empty()) {  // each host chunk is its own launch
+      // stream-ordered pool allocation: a plain cudaMalloc of the descriptor array took 62 ms
+      // after the arenas were allocated (r47b)
+      auto s = static_cast<cudaStream_t>(ctx_.stream(l->world));
+      ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan), fans.size() * sizeof(FanTile), s), "cudaMallocAsync tiles");
+      ck(cudaStreamSynchronize(s), "sync");
+      if (trace) std::fprintf(stderr, "prepare-trace malloc %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
+      if (interleave) {
+        auto full = cuda::interleave_for_grid(fans.data(), fans.size(), size_t(cuda::bulk_grid(fans.size(), sms, cfg_)));
+        ck(cudaMemcpy(l->d_fan, full.data(), full.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
+      } else {  // bulk_strided walks the natural (destination) order
+        ck(cudaMemcpy(l->d_fan, fans.data(), fans.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
+      }
+      if (trace) std::fprintf(stderr, "prepare-trace memcpy %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
+      if (!l->chunks.empty() && !interleave) {  // natural order: the chunks are slices of d_fan
+        l->d_fan_chunks = nullptr;
+      } else if (!l->chunks.empty()) {  // each host chunk is its own launch
         std::vector<FanTile> per;
         per.reserve(fans.size());
         for (const HostChunk& c : l->chunks) {
@@ -626,6 +686,7 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
       ck(cudaMemcpy(l->d_tiles + aligned.size(), misc.data(), misc.size() * sizeof(CopyTile), cudaMemcpyHostToDevice),
          "upload tiles");
     }
+    if (trace) std::fprintf(stderr, "prepare-trace upload %.1f ms\n", ms_since(t_mark));
     l->n_fan = fans.size();
     l->n_aligned = aligned.size();
     l->n_misc = misc.size();
@@ -800,7 +861,7 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     for (size_t k = 0; k < K; ++k) {
       ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");
       const uint64_t n = l->chunks[k].t1 - l->chunks[k].t0;
-      if (l->n_fan) cuda::launch_bulk(l->d_fan_chunks + l->chunks[k].t0, n, cfg_, sms, s);
+      if (l->n_fan) cuda::launch_bulk((l->d_fan_chunks ? l->d_fan_chunks : l->d_fan) + l->chunks[k].t0, n, cfg_, sms, s);
       else cuda::launch_copy(l->d_tiles + l->chunks[k].t0, n, cfg_, sms, true, s);
       ck(cudaEventRecord(ec[k], s), "event");
     }
