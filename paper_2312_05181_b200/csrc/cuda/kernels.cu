@@ -533,6 +533,74 @@ void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg
   check(cudaGetLastError(), "bulk copy launch");
 }
 
+// ---- schedule expansion: pieces -> tiles, on the device ---------------------------------------
+// One thread per output tile: binary search of its piece by `first`, then the same tile math
+// the host lowering uses (piece_tile, reshard/executor.hpp).  The host uploads only the
+// pieces (one per fragment and outer index: thousands), not the tiles (~10^5-10^6).
+__device__ __forceinline__ uint32_t piece_of(const DevPiece* __restrict__ p, uint32_t n, uint64_t t) {
+  uint32_t lo = 0, hi = n;  // last piece with first <= t
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (__ldg(&p[mid].first) <= t) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+// position of tile i of n in interleave_for_grid(., n, grid) order
+__device__ __forceinline__ uint64_t interleaved(uint64_t i, uint64_t n, uint64_t grid) {
+  const uint64_t q = n / grid, r = n % grid, c = i % grid;
+  return c * q + (c < r ? c : r) + i / grid;
+}
+
+__global__ void __launch_bounds__(256) expand_fan_kernel(const DevPiece* __restrict__ p, uint32_t np, uint64_t t0,
+                                                         uint64_t t1, FanTile* __restrict__ out, unsigned grid) {
+  const uint64_t n = t1 - t0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = t0 + i;
+    const DevPiece& q = p[piece_of(p, np, t)];
+    uint64_t r0, c;
+    uint32_t rows, bytes;
+    piece_tile(q.rows, q.row_bytes, q.per, q.tile, t - q.first, r0, c, rows, bytes);
+    FanTile f;
+    f.src = q.src + r0 * q.src_pitch + c, f.src_pitch = q.src_pitch;
+    f.rows = rows, f.row_bytes = bytes, f.n_dst = q.n_dst, f.pad = 0;
+#pragma unroll
+    for (int d = 0; d < kMaxFan; ++d) {
+      f.dst[d] = d < int(q.n_dst) ? q.dst[d] + r0 * q.dst_pitch[d] + c : 0ull;
+      f.dst_pitch[d] = d < int(q.n_dst) ? q.dst_pitch[d] : 0ull;
+    }
+    out[grid ? interleaved(i, n, grid) : i] = f;
+  }
+}
+
+__global__ void __launch_bounds__(256) expand_copy_kernel(const DevPiece* __restrict__ p, uint32_t np, uint64_t n,
+                                                          CopyTile* __restrict__ out) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+    const DevPiece& q = p[piece_of(p, np, t)];
+    uint64_t r0, c;
+    uint32_t rows, bytes;
+    piece_tile(q.rows, q.row_bytes, q.per, q.tile, t - q.first, r0, c, rows, bytes);
+    out[t] = CopyTile{q.src + r0 * q.src_pitch + c, q.dst[0] + r0 * q.dst_pitch[0] + c, q.src_pitch, q.dst_pitch[0],
+                      rows, bytes};
+  }
+}
+
+void launch_expand_fan(const DevPiece* d_pieces, uint32_t n_pieces, uint64_t t0, uint64_t t1, FanTile* out,
+                       unsigned grid, int sms, void* stream) {
+  if (t1 <= t0 || n_pieces == 0) return;
+  const uint64_t blocks = std::min<uint64_t>((t1 - t0 + 255) / 256, uint64_t(sms) * 8);
+  expand_fan_kernel<<<unsigned(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(d_pieces, n_pieces, t0, t1, out,
+                                                                                      grid);
+  check(cudaGetLastError(), "expand launch");
+}
+void launch_expand_copy(const DevPiece* d_pieces, uint32_t n_pieces, uint64_t n_tiles, CopyTile* out, int sms,
+                        void* stream) {
+  if (n_tiles == 0 || n_pieces == 0) return;
+  const uint64_t blocks = std::min<uint64_t>((n_tiles + 255) / 256, uint64_t(sms) * 8);
+  expand_copy_kernel<<<unsigned(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(d_pieces, n_pieces, n_tiles, out);
+  check(cudaGetLastError(), "expand launch");
+}
+
 void launch_payload(const PayloadTask* d_tasks, uint64_t n_tasks, uint64_t max_bytes, bool verify,
                     unsigned long long* d_count, void* stream) {
   if (n_tasks == 0) return;

@@ -40,6 +40,14 @@ std::vector<T> interleave_for_grid(const T* tiles, size_t n, size_t grid) {
     for (size_t i = c; i < n; i += grid) out.push_back(tiles[i]);
   return out;
 }
+// Expand pieces (device array, `first` = tile prefix) into tiles: tiles [t0, t1) of the
+// concatenated schedule go to out[0 .. t1-t0), in natural order (grid == 0) or in
+// interleave_for_grid order for a `grid`-CTA bulk launch.  FanTile for the bulk kernel;
+// CopyTile (n_dst == 1 pieces) for the LDG/STG kernels.
+void launch_expand_fan(const DevPiece* d_pieces, uint32_t n_pieces, uint64_t t0, uint64_t t1, FanTile* out,
+                       unsigned grid, int sms, void* stream);
+void launch_expand_copy(const DevPiece* d_pieces, uint32_t n_pieces, uint64_t n_tiles, CopyTile* out, int sms,
+                        void* stream);
 // K6 / K7 over a batch of cells (device array of tasks): write the splitmix64 payload, or
 // count the bytes that differ from it into *d_count (atomic add).  One launch per 65535 cells.
 struct PayloadTask {

@@ -38,16 +38,22 @@ struct DeviceGuard {
 // Emit the copy of box `ext` from (src cell shape ss, origin sl) to (dst cell shape ds,
 // origin dl), collapsing dimensions that are full on both sides into one contiguous run
 // and cutting the rest into tiles of about `tile` bytes.
+// One strided box copy (extents `ext`, source origin/shape sl/ss, destination origin/shape
+// dl/ds, element width w) as pieces: dims full on both sides collapse into one contiguous
+// run; for every index of the dims outside (row dim, run) one piece of `rows` rows, cut into
+// tiles of ~`tile` bytes — several rows per tile (row mode, in-tile byte offsets < 2^31 for
+// the kernels) or, when a run is longer than a tile, `tile`-byte slices of each row (split
+// mode).  emit(src_off, dst_off, src_pitch, dst_pitch, rows, run, per, split_tile).
 template <class Emit>
-void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& dl, const Shape& ds, uint64_t w,
-               uint64_t tile, Emit&& emit) {
+void lower_box_pieces(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& dl, const Shape& ds, uint64_t w,
+                      uint64_t tile, Emit&& emit) {
   const int r = int(ext.size());
   std::vector<uint64_t> sst(size_t(r), w), dst(size_t(r), w);
   for (int d = r - 1; d > 0; --d) sst[size_t(d - 1)] = sst[size_t(d)] * ss[size_t(d)], dst[size_t(d - 1)] = dst[size_t(d)] * ds[size_t(d)];
   uint64_t soff = 0, doff = 0;
   for (int d = 0; d < r; ++d) soff += sl[size_t(d)] * sst[size_t(d)], doff += dl[size_t(d)] * dst[size_t(d)];
   if (r == 0) {
-    emit(soff, doff, 0, 0, 1, w);
+    emit(soff, doff, uint64_t(0), uint64_t(0), uint64_t(1), w, uint32_t(1), uint32_t(0));
     return;
   }
   // innermost run: dims k..r-1, where every dim > k is full on both sides
@@ -61,20 +67,15 @@ void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& 
   const uint64_t rows = k > 0 ? ext[size_t(k - 1)] : 1;
   const uint64_t sp = k > 0 ? sst[size_t(k - 1)] : run, dp = k > 0 ? dst[size_t(k - 1)] : run;
   const int outer = std::max(k - 1, 0);
+  const bool split = run >= tile;
+  // rows per tile: ~tile bytes, and in-tile byte offsets must fit 31 bits (kernel math)
+  const uint64_t span = std::max<uint64_t>(std::max(sp, dp), 1);
+  const uint32_t per = split ? 0u : uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(tile / run, ((1ull << 31) - run) / span + 1)));
   std::vector<uint64_t> idx(size_t(outer), 0);
   for (;;) {
     uint64_t so = soff, dof = doff;
     for (int d = 0; d < outer; ++d) so += idx[size_t(d)] * sst[size_t(d)], dof += idx[size_t(d)] * dst[size_t(d)];
-    if (run >= tile) {
-      for (uint64_t row = 0; row < rows; ++row)
-        for (uint64_t c = 0; c < run; c += tile) emit(so + row * sp + c, dof + row * dp + c, 0, 0, 1, std::min(tile, run - c));
-    } else {
-      // rows per tile: ~tile bytes, and in-tile byte offsets must fit 31 bits (kernel math)
-      const uint64_t span = std::max<uint64_t>(std::max(sp, dp), 1);
-      const uint64_t per = std::max<uint64_t>(1, std::min<uint64_t>(tile / run, ((1ull << 31) - run) / span + 1));
-      for (uint64_t row = 0; row < rows; row += per)
-        emit(so + row * sp, dof + row * dp, sp, dp, std::min(per, rows - row), run);
-    }
+    emit(so, dof, sp, dp, rows, run, per, split ? uint32_t(tile) : uint32_t(0));
     int d = outer - 1;
     for (; d >= 0; --d) {
       if (++idx[size_t(d)] < ext[size_t(d)]) break;
@@ -82,6 +83,25 @@ void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& 
     }
     if (d < 0) return;
   }
+}
+
+// The same copy as tiles: emit(src_off, dst_off, src_pitch, dst_pitch, rows, bytes) — the
+// host expansion of lower_box_pieces, with the device expansion's tile math.
+template <class Emit>
+void lower_box(const Shape& ext, const Shape& sl, const Shape& ss, const Shape& dl, const Shape& ds, uint64_t w,
+               uint64_t tile, Emit&& emit) {
+  lower_box_pieces(ext, sl, ss, dl, ds, w, tile,
+                   [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run, uint32_t per,
+                       uint32_t tl) {
+                     const uint64_t n = piece_tile_count(uint32_t(rows), run, per, tl);
+                     for (uint64_t t = 0; t < n; ++t) {
+                       uint64_t r0, c;
+                       uint32_t nr, nb;
+                       piece_tile(uint32_t(rows), run, per, tl, t, r0, c, nr, nb);
+                       emit(so + r0 * sp + c, dof + r0 * dp + c, per ? sp : uint64_t(0), per ? dp : uint64_t(0),
+                            uint64_t(nr), uint64_t(nb));
+                     }
+                   });
 }
 
 bool aligned16(const CopyTile& t) {
@@ -389,31 +409,37 @@ void Executor::build_central(const SrcLookup& src_lookup) {
       Shape sl, dl, ext = f.box.extents();
       for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo), dl.push_back(rd.dim(d).lo);
       const Shape zero(ext.size(), 0);
-      auto tile = [](int32_t sg, uint32_t sa, uint64_t so, uint64_t sp, int32_t dg, uint64_t dof, uint64_t dp,
-                     uint64_t rows, uint64_t run) {
+      auto piece = [](int32_t sg, uint32_t sa, uint64_t so, uint64_t sp, int32_t dg, uint64_t dof, uint64_t dp,
+                      uint64_t rows, uint64_t run, uint32_t per, uint32_t tl) {
         Logical x{};
         x.src_gpu = sg, x.src_arena = sa, x.n_dst = 1, x.src_off = so, x.src_pitch = sp;
-        x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
+        x.rows = uint32_t(rows), x.row_bytes = run, x.per = per, x.tile = tl;
+        x.n_tiles = piece_tile_count(x.rows, run, per, tl);
         x.dst_gpu[0] = dg, x.dst_off[0] = dof, x.dst_pitch[0] = dp;
         return x;
       };
       if (f.resident) {
-        lower_box(ext, sl, sbox.extents(), dl, dbox.extents(), w, tile_bytes_,
-                  [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                    logical_[size_t(sb.gpu)].push_back(tile(sb.gpu, 0, sb.offset + so, sp, db.gpu, db.offset + dof, dp, rows, run));
-                  });
+        lower_box_pieces(ext, sl, sbox.extents(), dl, dbox.extents(), w, tile_bytes_,
+                         [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run, uint32_t per,
+                             uint32_t tl) {
+                           logical_[size_t(sb.gpu)].push_back(
+                               piece(sb.gpu, 0, sb.offset + so, sp, db.gpu, db.offset + dof, dp, rows, run, per, tl));
+                         });
         continue;
       }
       const uint64_t slot = stage_base + stage;
       stage = align_up(stage + f.box.elements() * w, kCellAlign);
-      lower_box(ext, sl, sbox.extents(), zero, ext, w, tile_bytes_,  // fetch: source cell -> staging slot
-                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                  logical_[size_t(sb.gpu)].push_back(tile(sb.gpu, 0, sb.offset + so, sp, central_, slot + dof, dp, rows, run));
-                });
-      lower_box(ext, zero, ext, dl, dbox.extents(), w, tile_bytes_,  // re-upload: staging slot -> destination
-                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                  logical_b_.push_back(tile(central_, 1, slot + so, sp, db.gpu, db.offset + dof, dp, rows, run));
-                });
+      lower_box_pieces(ext, sl, sbox.extents(), zero, ext, w, tile_bytes_,  // fetch: source cell -> staging slot
+                       [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run, uint32_t per,
+                           uint32_t tl) {
+                         logical_[size_t(sb.gpu)].push_back(
+                             piece(sb.gpu, 0, sb.offset + so, sp, central_, slot + dof, dp, rows, run, per, tl));
+                       });
+      lower_box_pieces(ext, zero, ext, dl, dbox.extents(), w, tile_bytes_,  // re-upload: staging slot -> destination
+                       [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run, uint32_t per,
+                           uint32_t tl) {
+                         logical_b_.push_back(piece(central_, 1, slot + so, sp, db.gpu, db.offset + dof, dp, rows, run, per, tl));
+                       });
     }
   }
   staging_bytes_ = stage;
@@ -472,34 +498,32 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
     for (int d = 0; d < rs.rank(); ++d) sl.push_back(rs.dim(d).lo);
     const uint64_t w = dtype_width(a.catalog.tensors[grp.tensor].dtype);
     auto& out = outs[size_t(sb.gpu)];
-    if (grp.members.size() == 1) {  // the common case: tiles straight into the executing GPU's list
-      const Member& mem = grp.members[0];
-      lower_box(grp.box.extents(), sl, sbox.extents(), mem.dl, mem.dshape, w, tile_bytes_,
-                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                  Logical& x = out.emplace_back();
-                  x.src_gpu = sb.gpu, x.src_arena = 0, x.n_dst = 1, x.src_off = sb.offset + so, x.src_pitch = sp;
-                  x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
-                  x.dst_gpu[0] = mem.dst_gpu, x.dst_off[0] = mem.dst_base + dof, x.dst_pitch[0] = dp;
-                });
+    auto lower_member = [&](const Member& mem, std::vector<Logical>& dst) {
+      lower_box_pieces(grp.box.extents(), sl, sbox.extents(), mem.dl, mem.dshape, w, tile_bytes_,
+                       [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run, uint32_t per,
+                           uint32_t tl) {
+                         Logical& x = dst.emplace_back();
+                         x.src_gpu = sb.gpu, x.src_arena = 0, x.n_dst = 1, x.src_off = sb.offset + so, x.src_pitch = sp;
+                         x.rows = uint32_t(rows), x.row_bytes = run, x.per = per, x.tile = tl;
+                         x.n_tiles = piece_tile_count(x.rows, run, per, tl);
+                         x.dst_gpu[0] = mem.dst_gpu, x.dst_off[0] = mem.dst_base + dof, x.dst_pitch[0] = dp;
+                       });
+    };
+    if (grp.members.size() == 1) {  // the common case: pieces straight into the executing GPU's list
+      lower_member(grp.members[0], out);
       return;
     }
     std::vector<std::vector<Logical>> per(grp.members.size());
-    for (size_t m = 0; m < grp.members.size(); ++m) {
-      const Member& mem = grp.members[m];
-      lower_box(grp.box.extents(), sl, sbox.extents(), mem.dl, mem.dshape, w, tile_bytes_,
-                [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
-                  Logical& x = per[m].emplace_back();
-                  x.src_gpu = sb.gpu, x.n_dst = 1, x.src_off = sb.offset + so, x.src_pitch = sp;
-                  x.rows = uint32_t(rows), x.row_bytes = uint32_t(run);
-                  x.dst_gpu[0] = mem.dst_gpu, x.dst_off[0] = mem.dst_base + dof, x.dst_pitch[0] = dp;
-                });
-    }
+    for (size_t m = 0; m < grp.members.size(); ++m) lower_member(grp.members[m], per[m]);
+    // fan-out needs the same source tiles for every member: same pieces with the same cut
     bool same = per.size() > 1;
     for (size_t m = 1; same && m < per.size(); ++m) {
       same = per[m].size() == per[0].size();
       for (size_t t = 0; same && t < per[0].size(); ++t)
         same = per[m][t].src_off == per[0][t].src_off && per[m][t].rows == per[0][t].rows &&
-               per[m][t].row_bytes == per[0][t].row_bytes && (per[0][t].rows == 1 || per[m][t].src_pitch == per[0][t].src_pitch);
+               per[m][t].row_bytes == per[0][t].row_bytes && per[m][t].per == per[0][t].per &&
+               per[m][t].tile == per[0][t].tile &&
+               (per[0][t].rows == 1 || per[m][t].src_pitch == per[0][t].src_pitch);
     }
     if (!same) {
       for (auto& v : per) out.insert(out.end(), v.begin(), v.end());
@@ -517,13 +541,6 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
         out.push_back(x);
       }
   };
-  {  // capacity: about one tile per tile_bytes_ of each executing GPU's copies
-    std::vector<uint64_t> est(logical_.size(), 0);
-    for (const Group& grp : groups)
-      est[size_t(src_bind_[grp.src_bind].gpu)] +=
-          grp.members.size() * (grp.box.elements() * dtype_width(a.catalog.tensors[grp.tensor].dtype) / tile_bytes_ + 1);
-    for (size_t g = 0; g < est.size(); ++g) logical_[g].reserve(logical_[g].size() + est[g] + 16);
-  }
   for (const Group& grp : groups) lower_group(grp, logical_);
 }
 
@@ -546,7 +563,10 @@ void Executor::prepare() {
   }
 }
 
-// Logical tiles -> device descriptors of one local GPU (bases known after bind()).
+// Pieces -> the device-resident copy schedule of one local GPU (bases known after bind()):
+// the host binds the arena bases into the few pieces, classifies them (bulk fan tiles /
+// 16-byte aligned LDG tiles / misaligned LDG tiles), orders them by destination and uploads
+// them; the expansion kernels write the tile arrays in device memory.
 void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool host_chunks) {
   const bool bulk = is_bulk(cfg_.kernel);
   const bool interleave = cfg_.kernel == CopyKernel::Bulk;  // bulk_strided walks the natural order
@@ -557,84 +577,87 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   const char* bp = std::getenv("RESHARD_BULK_PEER");
   const bool bulk_peer = bp && std::string(bp) == "1";
   Local* l = &local;
-  {
-    // Logical tiles -> descriptors with arena bases, classified: bulk fan tiles / 16-byte
-    // aligned LDG tiles / misaligned LDG tiles
-    std::vector<FanTile> fans;
-    std::vector<CopyTile> aligned, misc;
-    if (bulk) fans.reserve(lt.size());
-    else aligned.reserve(lt.size());
-    uint64_t bytes = 0, read_bytes = 0;
-    for (const Logical& x : lt) {
-      char* s = static_cast<char*>(x.src_arena ? dst_base_[size_t(x.src_gpu)] : src_base_[size_t(x.src_gpu)]);
-      if (!s) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.src_gpu) + " not bound");
-      FanTile f{uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), x.src_pitch, x.rows, x.row_bytes, x.n_dst, 0, {}, {}};
-      uint64_t bits = f.src | f.row_bytes | (x.rows > 1 ? x.src_pitch : 0);
-      for (uint32_t d = 0; d < x.n_dst; ++d) {
-        char* dp = static_cast<char*>(dst_base_[size_t(x.dst_gpu[d])]);
-        if (!dp) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.dst_gpu[d]) + " not bound");
-        f.dst[d] = uint64_t(reinterpret_cast<uintptr_t>(dp + x.dst_off[d]));
-        f.dst_pitch[d] = x.dst_pitch[d];
-        bits |= f.dst[d] | (x.rows > 1 ? x.dst_pitch[d] : 0);
-      }
-      const uint64_t tb = uint64_t(x.rows) * x.row_bytes;
-      bytes += tb * x.n_dst;
-      // Cross-GPU tiles use plain st.global through the peer mapping (K2) unless
-      // RESHARD_BULK_PEER=1 lets the TMA engine store to peer addresses too: that variant
-      // has not been validated on a multi-GPU box yet (one GPU in this environment).
-      bool remote = false;
-      for (uint32_t d = 0; d < x.n_dst; ++d) remote |= x.dst_gpu[d] != l->world;
-      if (bulk && (!remote || bulk_peer) && (bits & 15) == 0 && tb <= cfg_.stage_bytes) {
-        fans.push_back(f);
-        read_bytes += tb;
-        continue;
-      }
-      for (uint32_t d = 0; d < x.n_dst; ++d) {
-        CopyTile t{f.src, f.dst[d], x.src_pitch, f.dst_pitch[d], x.rows, x.row_bytes};
-        (aligned16(t) ? aligned : misc).push_back(t);
-        read_bytes += tb;
-      }
+  std::vector<DevPiece> fanp, alignedp, miscp;
+  uint64_t bytes = 0, read_bytes = 0;
+  for (const Logical& x : lt) {
+    char* s = static_cast<char*>(x.src_arena ? dst_base_[size_t(x.src_gpu)] : src_base_[size_t(x.src_gpu)]);
+    if (!s) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.src_gpu) + " not bound");
+    DevPiece q{};
+    q.src = uint64_t(reinterpret_cast<uintptr_t>(s + x.src_off)), q.src_pitch = x.src_pitch;
+    q.row_bytes = x.row_bytes, q.rows = x.rows, q.per = x.per, q.tile = x.tile, q.n_dst = x.n_dst;
+    // every tile is 16-byte aligned iff the base, the pitch (several rows), the run and the
+    // split stride are
+    const uint64_t common = x.row_bytes | (x.per ? 0 : x.tile);
+    uint64_t bits = q.src | common | (x.rows > 1 ? x.src_pitch : 0);
+    bool remote = false;
+    for (uint32_t d = 0; d < x.n_dst; ++d) {
+      char* dp = static_cast<char*>(dst_base_[size_t(x.dst_gpu[d])]);
+      if (!dp) raise(Errc::InvalidArgument, "prepare: GPU " + std::to_string(x.dst_gpu[d]) + " not bound");
+      q.dst[d] = uint64_t(reinterpret_cast<uintptr_t>(dp + x.dst_off[d]));
+      q.dst_pitch[d] = x.dst_pitch[d];
+      bits |= q.dst[d] | (x.rows > 1 ? x.dst_pitch[d] : 0);
+      remote |= x.dst_gpu[d] != l->world;
     }
-    // destination order: sequential writes, and monotone destinations per host chunk (the
-    // tiles usually arrive sorted already; otherwise sort 16-byte keys and permute once)
-    auto by_dst = [](auto& v, auto dst_of) {
-      bool sorted = true;
-      for (size_t i = 1; sorted && i < v.size(); ++i) sorted = dst_of(v[i - 1]) <= dst_of(v[i]);
-      if (sorted) return;
-      std::vector<std::pair<uint64_t, uint32_t>> key(v.size());
-      for (size_t i = 0; i < v.size(); ++i) key[i] = {dst_of(v[i]), uint32_t(i)};
-      std::stable_sort(key.begin(), key.end(), [](const auto& p, const auto& q) { return p.first < q.first; });
-      std::remove_reference_t<decltype(v)> out;
-      out.reserve(v.size());
-      for (const auto& k : key) out.push_back(v[k.second]);
-      v.swap(out);
-    };
-    if (trace) std::fprintf(stderr, "prepare-trace convert %.1f ms (%zu tiles)\n", ms_since(t_mark), lt.size()), t_mark = clk::now();
-    by_dst(fans, [](const FanTile& t) { return t.dst[0]; });
-    if (trace) std::fprintf(stderr, "prepare-trace sort %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
-    by_dst(aligned, [](const CopyTile& t) { return t.dst; });
-    l->chunks.clear();
-    const bool one_list = misc.empty() && (fans.empty() != aligned.empty());
-    if (host_chunks && ctx_.world() == 1 && one_list) {
-      const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
-      const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
-      const uint64_t target = std::max<uint64_t>(bytes / uint64_t(cfg_.host_chunks), 1);
-      const size_t n = fans.empty() ? aligned.size() : fans.size();
-      HostChunk c{0, 0, 0, UINT64_MAX, {}};
-      std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);
-      uint64_t acc = 0;
-      for (size_t i = 0; i < n; ++i) {
-        const bool fan = !fans.empty();
-        const uint64_t src = fan ? fans[i].src : aligned[i].src, sp = fan ? fans[i].src_pitch : aligned[i].src_pitch;
-        const uint32_t rows = fan ? fans[i].rows : aligned[i].rows, rb = fan ? fans[i].row_bytes : aligned[i].row_bytes;
-        const uint32_t nd = fan ? fans[i].n_dst : 1;
-        const uint64_t s0 = src - sb, s1 = s0 + (rows ? (rows - 1) * sp : 0) + rb;
+    const uint64_t pb = uint64_t(x.rows) * x.row_bytes;  // the piece's bytes per destination
+    const uint64_t max_tile = x.per ? uint64_t(x.per) * x.row_bytes : x.tile;
+    bytes += pb * x.n_dst;
+    // Cross-GPU tiles use plain st.global through the peer mapping (K2) unless
+    // RESHARD_BULK_PEER=1 lets the TMA engine store to peer addresses too: that variant
+    // has not been validated on a multi-GPU box yet (one GPU in this environment).
+    if (bulk && (!remote || bulk_peer) && (bits & 15) == 0 && max_tile <= cfg_.stage_bytes) {
+      fanp.push_back(q);
+      read_bytes += pb;
+      continue;
+    }
+    for (uint32_t d = 0; d < x.n_dst; ++d) {  // one single-destination piece per destination
+      DevPiece one = q;
+      one.n_dst = 1, one.dst[0] = q.dst[d], one.dst_pitch[0] = q.dst_pitch[d];
+      for (int e = 1; e < kMaxFan; ++e) one.dst[e] = 0, one.dst_pitch[e] = 0;
+      const uint64_t b1 = q.src | common | (x.rows > 1 ? (x.src_pitch | q.dst_pitch[d]) : 0) | q.dst[d];
+      ((b1 & 15) == 0 ? alignedp : miscp).push_back(one);
+      read_bytes += pb;
+    }
+  }
+  // destination order (sequential writes; monotone destinations per host chunk when the
+  // pieces do not interleave), then each piece's first tile
+  auto by_dst = [](std::vector<DevPiece>& v) {
+    std::stable_sort(v.begin(), v.end(), [](const DevPiece& p, const DevPiece& q) { return p.dst[0] < q.dst[0]; });
+  };
+  by_dst(fanp), by_dst(alignedp);
+  auto number = [](std::vector<DevPiece>& v) {
+    uint64_t n = 0;
+    for (DevPiece& q : v) q.first = n, n += piece_tile_count(q.rows, q.row_bytes, q.per, q.tile);
+    return n;
+  };
+  const uint64_t nf = number(fanp), na = number(alignedp), nm = number(miscp);
+  if (trace) std::fprintf(stderr, "prepare-trace pieces %.1f ms (%zu pieces -> %llu tiles)\n", ms_since(t_mark), lt.size(),
+                          (unsigned long long)(nf + na + nm)), t_mark = clk::now();
+  l->chunks.clear();
+  const bool one_list = nm == 0 && ((nf == 0) != (na == 0));
+  if (host_chunks && ctx_.world() == 1 && one_list) {
+    // host-buffer pipeline: chunks of ~bytes / host_chunks in tile order, each with the
+    // source spans its tiles read and the lowest destination it writes (tile math on the host)
+    const std::vector<DevPiece>& pv = nf ? fanp : alignedp;
+    const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
+    const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
+    const uint64_t target = std::max<uint64_t>(bytes / uint64_t(cfg_.host_chunks), 1);
+    const uint64_t n = nf ? nf : na;
+    HostChunk c{0, 0, 0, UINT64_MAX, {}};
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);
+    uint64_t acc = 0, i = 0;
+    for (const DevPiece& q : pv) {
+      const uint64_t nt = piece_tile_count(q.rows, q.row_bytes, q.per, q.tile);
+      for (uint64_t t = 0; t < nt; ++t, ++i) {
+        uint64_t r0, cc;
+        uint32_t nr, nb;
+        piece_tile(q.rows, q.row_bytes, q.per, q.tile, t, r0, cc, nr, nb);
+        const uint64_t s0 = q.src + r0 * q.src_pitch + cc - sb, s1 = s0 + (nr ? (nr - 1) * q.src_pitch : 0) + nb;
         auto& sv = spans.back();  // consecutive tiles usually continue the previous source run
         if (!sv.empty() && s0 >= sv.back().first && s0 <= sv.back().second) sv.back().second = std::max(sv.back().second, s1);
         else sv.emplace_back(s0, s1);
         c.src_end = std::max(c.src_end, s1);
-        for (uint32_t d = 0; d < nd; ++d) c.dst_min = std::min(c.dst_min, (fan ? fans[i].dst[d] : aligned[i].dst) - db);
-        acc += uint64_t(rows) * rb * nd;
+        for (uint32_t d = 0; d < q.n_dst; ++d) c.dst_min = std::min(c.dst_min, q.dst[d] + r0 * q.dst_pitch[d] + cc - db);
+        acc += uint64_t(nr) * nb * q.n_dst;
         if (acc >= target || i + 1 == n) {
           c.t1 = i + 1;
           l->chunks.push_back(c);
@@ -643,56 +666,52 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
           acc = 0;
         }
       }
-      plan_uploads(l->chunks, spans);
     }
-    if (trace) std::fprintf(stderr, "prepare-trace chunks %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
-    DeviceGuard g(l->dev);
-    if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
-    if (l->d_fan_chunks) cudaFree(l->d_fan_chunks), l->d_fan_chunks = nullptr;
-    if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
-    if (!fans.empty()) {
-      const int sms = ctx_.sm_count(l->world);
-      // stream-ordered pool allocation: a plain cudaMalloc of the descriptor array took 62 ms
-      // after the arenas were allocated (r47b)
-      auto s = static_cast<cudaStream_t>(ctx_.stream(l->world));
-      ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan), fans.size() * sizeof(FanTile), s), "cudaMallocAsync tiles");
-      ck(cudaStreamSynchronize(s), "sync");
-      if (trace) std::fprintf(stderr, "prepare-trace malloc %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
-      if (interleave) {
-        auto full = cuda::interleave_for_grid(fans.data(), fans.size(), size_t(cuda::bulk_grid(fans.size(), sms, cfg_)));
-        ck(cudaMemcpy(l->d_fan, full.data(), full.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
-      } else {  // bulk_strided walks the natural (destination) order
-        ck(cudaMemcpy(l->d_fan, fans.data(), fans.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
-      }
-      if (trace) std::fprintf(stderr, "prepare-trace memcpy %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
-      if (!l->chunks.empty() && !interleave) {  // natural order: the chunks are slices of d_fan
-        l->d_fan_chunks = nullptr;
-      } else if (!l->chunks.empty()) {  // each host chunk is its own launch
-        std::vector<FanTile> per;
-        per.reserve(fans.size());
-        for (const HostChunk& c : l->chunks) {
-          auto v = cuda::interleave_for_grid(fans.data() + c.t0, size_t(c.t1 - c.t0),
-                                             interleave ? size_t(cuda::bulk_grid(c.t1 - c.t0, sms, cfg_)) : 1);
-          per.insert(per.end(), v.begin(), v.end());
-        }
-        ck(cudaMalloc(&l->d_fan_chunks, per.size() * sizeof(FanTile)), "cudaMalloc tiles");
-        ck(cudaMemcpy(l->d_fan_chunks, per.data(), per.size() * sizeof(FanTile), cudaMemcpyHostToDevice), "upload tiles");
-      }
-    }
-    const size_t n = aligned.size() + misc.size();
-    if (n) {
-      ck(cudaMalloc(&l->d_tiles, n * sizeof(CopyTile)), "cudaMalloc tiles");
-      ck(cudaMemcpy(l->d_tiles, aligned.data(), aligned.size() * sizeof(CopyTile), cudaMemcpyHostToDevice), "upload tiles");
-      ck(cudaMemcpy(l->d_tiles + aligned.size(), misc.data(), misc.size() * sizeof(CopyTile), cudaMemcpyHostToDevice),
-         "upload tiles");
-    }
-    if (trace) std::fprintf(stderr, "prepare-trace upload %.1f ms\n", ms_since(t_mark));
-    l->n_fan = fans.size();
-    l->n_aligned = aligned.size();
-    l->n_misc = misc.size();
-    l->bytes = bytes;
-    l->read_bytes = read_bytes;
+    plan_uploads(l->chunks, spans);
   }
+  if (trace) std::fprintf(stderr, "prepare-trace chunks %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
+  DeviceGuard g(l->dev);
+  auto st = static_cast<cudaStream_t>(ctx_.stream(l->world));
+  const int sms = ctx_.sm_count(l->world);
+  if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
+  if (l->d_fan_chunks) cudaFree(l->d_fan_chunks), l->d_fan_chunks = nullptr;
+  if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
+  // stream-ordered pool allocations (a plain cudaMalloc after the arenas took 62 ms, r47b)
+  auto upload = [&](const std::vector<DevPiece>& v) -> DevPiece* {
+    if (v.empty()) return nullptr;
+    DevPiece* d = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&d), v.size() * sizeof(DevPiece), st), "cudaMallocAsync pieces");
+    ck(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(DevPiece), cudaMemcpyHostToDevice, st), "upload pieces");
+    return d;
+  };
+  DevPiece* dfan = upload(fanp);
+  DevPiece* dal = upload(alignedp);
+  DevPiece* dmi = upload(miscp);
+  if (nf) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan), nf * sizeof(FanTile), st), "cudaMallocAsync tiles");
+    cuda::launch_expand_fan(dfan, uint32_t(fanp.size()), 0, nf, l->d_fan,
+                            interleave ? unsigned(cuda::bulk_grid(nf, sms, cfg_)) : 0u, sms, st);
+    if (!l->chunks.empty() && interleave) {  // each host chunk is its own launch, interleaved for its grid
+      ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan_chunks), nf * sizeof(FanTile), st), "cudaMallocAsync tiles");
+      for (const HostChunk& c : l->chunks)
+        cuda::launch_expand_fan(dfan, uint32_t(fanp.size()), c.t0, c.t1, l->d_fan_chunks + c.t0,
+                                unsigned(cuda::bulk_grid(c.t1 - c.t0, sms, cfg_)), sms, st);
+    }  // natural order: the chunks are slices of d_fan
+  }
+  if (na + nm) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_tiles), (na + nm) * sizeof(CopyTile), st), "cudaMallocAsync tiles");
+    cuda::launch_expand_copy(dal, uint32_t(alignedp.size()), na, l->d_tiles, sms, st);
+    cuda::launch_expand_copy(dmi, uint32_t(miscp.size()), nm, l->d_tiles + na, sms, st);
+  }
+  for (DevPiece* d : {dfan, dal, dmi})
+    if (d) ck(cudaFreeAsync(d, st), "cudaFreeAsync pieces");
+  ck(cudaStreamSynchronize(st), "expand schedule");
+  if (trace) std::fprintf(stderr, "prepare-trace expand %.1f ms\n", ms_since(t_mark));
+  l->n_fan = nf;
+  l->n_aligned = na;
+  l->n_misc = nm;
+  l->bytes = bytes;
+  l->read_bytes = read_bytes;
 }
 
 void Executor::run() {
@@ -903,7 +922,11 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
 }
 
 uint64_t Executor::tiles_for(int gpu) const {
-  return logical_[size_t(gpu)].size() + (gpu == central_ ? logical_b_.size() : 0);
+  uint64_t n = 0;
+  for (auto& x : logical_[size_t(gpu)]) n += x.n_tiles;
+  if (gpu == central_)
+    for (auto& x : logical_b_) n += x.n_tiles;
+  return n;
 }
 uint64_t Executor::copy_bytes_for(int gpu) const {
   uint64_t n = 0;

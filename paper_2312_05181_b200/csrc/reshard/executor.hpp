@@ -46,6 +46,41 @@ struct FanTile {
 };
 static_assert(sizeof(FanTile) == 96, "FanTile layout");
 
+#if defined(__CUDACC__)
+#define RS_HD __host__ __device__ __forceinline__
+#else
+#define RS_HD inline
+#endif
+
+// A piece of one strided box copy, i.e. the tiles one lower_box step produces, kept as one
+// record until the bases are known and expanded into tiles on the GPU (the device-resident
+// copy schedule): row mode (per > 0) — tile t covers rows [t per, min(rows, (t+1) per)) of
+// row_bytes each; split mode (per == 0) — each row is cut into `tile`-byte tiles, row-major.
+struct DevPiece {
+  uint64_t src, src_pitch;
+  uint64_t dst[kMaxFan], dst_pitch[kMaxFan];
+  uint64_t first;       // index of the piece's first tile in the expanded array
+  uint64_t row_bytes;   // split mode: a whole contiguous run (may exceed 4 GiB)
+  uint32_t rows, per, tile, n_dst;
+};
+static_assert(sizeof(DevPiece) == 112, "DevPiece layout");
+
+RS_HD uint64_t piece_tile_count(uint32_t rows, uint64_t row_bytes, uint32_t per, uint32_t tile) {
+  return per ? (uint64_t(rows) + per - 1) / per : uint64_t(rows) * ((row_bytes + tile - 1) / tile);
+}
+// Tile t of a piece: first row r0, byte offset c within the row, rows and bytes per row.
+RS_HD void piece_tile(uint32_t rows, uint64_t row_bytes, uint32_t per, uint32_t tile, uint64_t t, uint64_t& r0,
+                      uint64_t& c, uint32_t& n_rows, uint32_t& n_bytes) {
+  if (per) {
+    r0 = t * per, c = 0;
+    n_rows = uint32_t(rows - r0 < per ? rows - r0 : per), n_bytes = uint32_t(row_bytes);
+  } else {
+    const uint64_t cpr = (row_bytes + tile - 1) / tile;
+    r0 = t / cpr, c = (t % cpr) * tile;
+    n_rows = 1, n_bytes = uint32_t(row_bytes - c < tile ? row_bytes - c : tile);
+  }
+}
+
 // Which copy kernel moves the 16-byte-aligned tiles (misaligned ones always take the
 // generic-width LDG/STG kernel).  Defaults can be overridden by RESHARD_COPY_KERNEL
 // (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
@@ -155,12 +190,14 @@ class Executor {
   uint64_t read_bytes_for(int gpu) const;  // bytes they read (fan-out reads once)
 
  private:
-  struct Logical {  // a tile before arena bases are known; n_dst > 1: fan-out (DP replicas)
+  struct Logical {  // a piece (DevPiece geometry) before arena bases are known; n_dst > 1: fan-out
     int32_t src_gpu;
     uint32_t n_dst;
     uint32_t src_arena;  // 0: src arena of src_gpu, 1: its dst arena (central mode's staging)
     uint64_t src_off, src_pitch;
-    uint32_t rows, row_bytes;
+    uint64_t row_bytes;       // the contiguous run (split mode: may exceed one tile)
+    uint32_t rows, per, tile;  // per == 0: split mode, `tile` bytes per tile
+    uint64_t n_tiles;
     int32_t dst_gpu[kMaxFan];
     uint64_t dst_off[kMaxFan], dst_pitch[kMaxFan];
   };
