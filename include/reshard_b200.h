@@ -160,6 +160,12 @@ int rs_ipc_close_handle(rs_context* ctx, int gpu, void* ptr);
 int rs_slice(rs_context* ctx, int gpu, const rs_tensor* t, const rs_range* r, void* out);
 int rs_merge(rs_context* ctx, int gpu, int n_parts, const rs_range* ranges, const rs_tensor* parts, int rank,
              const uint64_t* target_shape, void* out);
+/* SURVEY §8(b) rs_broadcast, without NCCL: `bytes` at `src` (device memory of world GPU `gpu`)
+ * to every pointer of dsts[0..n_dst) (local or peer / IPC mappings) by one kernel on that GPU:
+ * the source is read once per kMaxFan destinations and stored to each (TMA bulk fan-out tiles
+ * when all pointers and `bytes` are 16-byte aligned).  DP replication as one push. */
+int rs_broadcast(rs_context* ctx, int gpu, const void* src, int n_dst, void* const* dsts, uint64_t bytes,
+                 rs_timing* timing);
 /* The same on HOST buffers (t->data / parts[i].data / out are host pointers): the reference's
  * value-level slice / merge (tensor.hpp:40-47) — validated first, in the reference's order,
  * then staged through the context's GPU.  C++ callers get the reference's own value type

@@ -275,6 +275,16 @@ def merge(ctx: Context, gpu: int, parts: Sequence[tuple], target_shape, out: int
     _chk(lib.rs_merge(ctx.h, gpu, n, rngs, ts, len(target_shape), _u64(target_shape), out))
 
 
+def broadcast(ctx: Context, gpu: int, src_ptr: int, dst_ptrs: Sequence[int], nbytes: int) -> dict:
+    """DP replication as one push (rs_broadcast): src -> every dst pointer, source read once
+    per 4 destinations (TMA fan-out tiles when aligned)."""
+    n = len(dst_ptrs)
+    arr = (C.c_void_p * max(n, 1))(*dst_ptrs)
+    t = _capi.rs_timing()
+    _chk(lib.rs_broadcast(ctx.h, gpu, src_ptr, n, arr, nbytes, C.byref(t)))
+    return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, read_bytes=t.read_bytes, launches=t.launches)
+
+
 def slice_host(ctx: Context, gpu: int, dtype: int, shape, payload: bytes, box) -> bytes:
     """The reference's value-level slice (tensor.hpp:40-42) on host bytes, through the GPU."""
     import numpy as np

@@ -90,6 +90,7 @@ SIGNATURES = {
     "rs_slice": (C.c_int, [P, C.c_int, C.POINTER(rs_tensor), C.POINTER(rs_range), P]),
     "rs_merge": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(rs_range), C.POINTER(rs_tensor), C.c_int, U64P, P]),
     "rs_slice_host": (C.c_int, [P, C.c_int, C.POINTER(rs_tensor), C.POINTER(rs_range), P]),
+    "rs_broadcast": (C.c_int, [P, C.c_int, P, C.c_int, C.POINTER(C.c_void_p), C.c_uint64, P]),
     "rs_merge_host": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(rs_range), C.POINTER(rs_tensor), C.c_int, U64P, P]),
     "rs_catalog_create": (C.c_int, [C.POINTER(P)]),
     "rs_catalog_gpt": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(P)]),

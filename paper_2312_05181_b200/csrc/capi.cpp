@@ -299,6 +299,14 @@ int rs_merge(rs_context* c, int gpu, int n, const rs_range* ranges, const rs_ten
   });
 }
 
+int rs_broadcast(rs_context* c, int gpu, const void* src, int n_dst, void* const* dsts, uint64_t bytes, rs_timing* timing) {
+  return guard([&] {
+    if (n_dst < 0 || (n_dst > 0 && !dsts)) raise(Errc::InvalidArgument, "broadcast: bad destination list");
+    std::vector<void*> d(dsts, dsts + n_dst);
+    Timing t = broadcast(ctx_of(c), gpu, src, d, bytes);
+    if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
+  });
+}
 int rs_slice_host(rs_context* c, int gpu, const rs_tensor* t, const rs_range* r, void* out) {
   return guard([&] {
     need(t, "tensor"), need(r, "range");

@@ -1003,6 +1003,77 @@ uint64_t Executor::verify_destinations() {
   return payload_pass(per, true);
 }
 
+// ---- broadcast (fan-out push) ----------------------------------------------------------------
+Timing broadcast(Context& ctx, int gpu, const void* src, const std::vector<void*>& dsts, uint64_t bytes) {
+  TraceRange trace_("broadcast");
+  if (!src) raise(Errc::InvalidArgument, "broadcast: null source");
+  if (dsts.empty()) raise(Errc::InvalidArgument, "broadcast: no destinations");
+  for (void* d : dsts)
+    if (!d) raise(Errc::InvalidArgument, "broadcast: null destination");
+  const CopyConfig cfg = CopyConfig::from_env();
+  DeviceGuard g(ctx.cuda_device(gpu));
+  auto s = static_cast<cudaStream_t>(ctx.stream(gpu));
+  const int sms = ctx.sm_count(gpu);
+  uint64_t bits = reinterpret_cast<uintptr_t>(src) | bytes;
+  for (void* d : dsts) bits |= reinterpret_cast<uintptr_t>(d);
+  const bool bulk = is_bulk(cfg.kernel) && (bits & 15) == 0;
+  const uint32_t tile = bulk ? cfg.stage_bytes / 16 * 16 : 256u << 10;
+  Timing t;
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  if (bytes == 0) {
+    t.ms = 0;
+  } else if (bulk) {
+    std::vector<DevPiece> pieces;
+    for (size_t i = 0; i < dsts.size(); i += kMaxFan) {
+      DevPiece q{};
+      q.src = reinterpret_cast<uintptr_t>(src), q.row_bytes = bytes, q.rows = 1, q.per = 0, q.tile = tile;
+      for (size_t d = i; d < dsts.size() && d < i + kMaxFan; ++d) q.dst[q.n_dst++] = reinterpret_cast<uintptr_t>(dsts[d]);
+      q.first = uint64_t(pieces.size()) * piece_tile_count(1, bytes, 0, tile);
+      pieces.push_back(q);
+    }
+    const uint64_t n = uint64_t(pieces.size()) * piece_tile_count(1, bytes, 0, tile);
+    DevPiece* dp = nullptr;
+    FanTile* dt = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&dp), pieces.size() * sizeof(DevPiece), s), "cudaMallocAsync");
+    ck(cudaMemcpyAsync(dp, pieces.data(), pieces.size() * sizeof(DevPiece), cudaMemcpyHostToDevice, s), "pieces h2d");
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&dt), n * sizeof(FanTile), s), "cudaMallocAsync");
+    const bool interleave = cfg.kernel == CopyKernel::Bulk;
+    cuda::launch_expand_fan(dp, uint32_t(pieces.size()), 0, n, dt, interleave ? unsigned(cuda::bulk_grid(n, sms, cfg)) : 0u,
+                            sms, s);
+    ck(cudaEventRecord(e0, s), "event");
+    cuda::launch_bulk(dt, n, cfg, sms, s);
+    ck(cudaEventRecord(e1, s), "event");
+    ck(cudaFreeAsync(dp, s), "cudaFreeAsync");
+    ck(cudaFreeAsync(dt, s), "cudaFreeAsync");
+    t.tiles = n, t.launches = 1, t.read_bytes = bytes * pieces.size();
+  } else {
+    std::vector<CopyTile> tiles;
+    for (void* d : dsts)
+      for (uint64_t c = 0; c < bytes; c += tile)
+        tiles.push_back(CopyTile{uint64_t(reinterpret_cast<uintptr_t>(src)) + c, uint64_t(reinterpret_cast<uintptr_t>(d)) + c,
+                                 0, 0, 1, uint32_t(std::min<uint64_t>(tile, bytes - c))});
+    CopyTile* dt = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&dt), tiles.size() * sizeof(CopyTile), s), "cudaMallocAsync");
+    ck(cudaMemcpyAsync(dt, tiles.data(), tiles.size() * sizeof(CopyTile), cudaMemcpyHostToDevice, s), "tiles h2d");
+    ck(cudaEventRecord(e0, s), "event");
+    cuda::launch_copy(dt, tiles.size(), cfg, sms, false, s);
+    ck(cudaEventRecord(e1, s), "event");
+    ck(cudaFreeAsync(dt, s), "cudaFreeAsync");
+    t.tiles = tiles.size(), t.launches = 1, t.read_bytes = bytes * dsts.size();
+  }
+  if (bytes) {
+    ck(cudaEventSynchronize(e1), "sync");
+    ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ck(cudaStreamSynchronize(s), "broadcast sync");
+  t.bytes = bytes * dsts.size();
+  return t;
+}
+
 // ---- device slice / merge ----------------------------------------------------------------
 namespace {
 void run_tiles_once(Context& ctx, int gpu, const std::vector<CopyTile>& tiles) {

@@ -225,6 +225,13 @@ class Executor {
   std::vector<std::unique_ptr<Local>> local_;   // per local GPU: device tiles, events
 };
 
+// DP replication as a single push (SURVEY §8(b) rs_broadcast): `bytes` at `src` on world GPU
+// `gpu` copied to every pointer in `dsts` (local memory or peer mappings) by one kernel on
+// that GPU — fan-out tiles read the source once per group of kMaxFan destinations and store
+// it to each (TMA bulk when everything is 16-byte aligned, LDG/STG otherwise).  No NCCL
+// ring on the data path; this is what the executor's fan-out tiles do inside a reshard.
+Timing broadcast(Context& ctx, int gpu, const void* src, const std::vector<void*>& dsts, uint64_t bytes);
+
 // Device-side slice / merge on one GPU (reference slice tensor.cpp:61-78, merge :80-114):
 // same validation and error precedence, bytes moved by the tile kernel.
 struct DeviceTensorView {

@@ -383,3 +383,26 @@ def test_reference_fixtures_through_host_value_api(rs, ctx):
         parts = [([tuple(b) for b in p["box"]], p["dtype"], p["shape"], bytes.fromhex(p["payload"])) for p in c["parts"]]
         got = outcome(lambda: rs.merge_host(ctx, 0, parts, tuple(c["target"])))
         assert got == {k: c[k] for k in ("ok", "error") if k in c}, c["target"]
+
+
+@pytest.mark.parametrize("kernel", ["bulk_strided", "bulk", "ldg"])
+def test_broadcast_fan_out_push(rs, ctx, kernel, monkeypatch):
+    """rs_broadcast: one source to 1, 4, 6 destinations (fan-out groups of 4), aligned (TMA
+    fan-out tiles) and misaligned (LDG/STG), every destination byte equal to the source."""
+    monkeypatch.setenv("RESHARD_COPY_KERNEL", kernel)
+    rng = np.random.default_rng(3)
+    for nbytes, n_dst, skew in [(10 << 20, 6, 0), (1 << 20, 1, 0), (3 * 29696 + 48, 4, 0), (777_777, 3, 8), (96, 5, 0)]:
+        src_h = rng.integers(0, 256, nbytes, dtype=np.uint8)
+        src = ctx.malloc(0, nbytes + 64)
+        ctx.htod(0, src + skew, src_h.ctypes.data, nbytes)
+        dsts = [ctx.malloc(0, nbytes + 64) for _ in range(n_dst)]
+        t = rs.broadcast(ctx, 0, src + skew, [d + skew for d in dsts], nbytes)
+        assert t["bytes"] == nbytes * n_dst and t["launches"] == 1
+        for d in dsts:
+            got = np.empty(nbytes, np.uint8)
+            ctx.dtoh(0, got.ctypes.data, d + skew, nbytes)
+            assert np.array_equal(got, src_h)
+            ctx.free(0, d)
+        ctx.free(0, src)
+    with pytest.raises(rs.ReshardError, match="InvalidArgument"):
+        rs.broadcast(ctx, 0, 0, [1 << 20], 16)

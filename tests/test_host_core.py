@@ -231,3 +231,13 @@ def test_host_value_slice_merge_validate_before_device(rs):
         parts = [([tuple(b) for b in p["box"]], p["dtype"], p["shape"], bytes.fromhex(p["payload"])) for p in c["parts"]]
         got = outcome(lambda: rs.merge_host(ctx, 0, parts, tuple(c["target"])))
         assert got == (c["error"] if "error" in c else "DeviceUnavailable"), c
+
+
+def test_broadcast_argument_errors(rs):
+    """rs_broadcast rejects a null source / empty or null destination list before any device
+    work (InvalidArgument)."""
+    ctx = rs.Context(1, [], [])
+    for src, dsts in [(0, [4096]), (4096, []), (4096, [0])]:
+        with pytest.raises(rs.ReshardError) as e:
+            rs.broadcast(ctx, 0, src, dsts, 64)
+        assert e.value.name == "InvalidArgument"
