@@ -721,7 +721,9 @@ def run_ours(args):
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind, "peak_how": peak_how(),
-                     "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes},
+                     "kernel": kname,
+                     "algorithmic_bytes_per_launch": alg_bytes // max(1, launches_total // max(args.steps, 1)),
+                     "launches_per_step": launches_total // max(args.steps, 1)},
         "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs),
         "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "wall_s": round(wall, 4),
         "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4), "tiles": tiles,
