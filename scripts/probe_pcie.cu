@@ -58,6 +58,39 @@ int main(int argc, char** argv) {
     if (op == 3) h2d_sm(s);
     if (op == 4) d2h_sm(s);
   };
+  // two copy streams per direction (halves of the buffers), 4 streams at once for "both"
+  {
+    cudaStream_t q[4];
+    for (auto& x : q) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    const size_t h = bytes / 2;
+    for (int mode = 0; mode < 3; ++mode) {  // 0: H2D x2, 1: D2H x2, 2: both x2
+      float best = 1e30f;
+      for (int r = 0; r < 4; ++r) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(e0, q[0]));
+        for (int i = 1; i < 4; ++i) CK(cudaStreamWaitEvent(q[i], e0, 0));
+        if (mode != 1)
+          for (int i = 0; i < 2; ++i)
+            CK(cudaMemcpyAsync((char*)d_a + i * h, (char*)h_in + i * h, h, cudaMemcpyHostToDevice, q[i]));
+        if (mode != 0)
+          for (int i = 0; i < 2; ++i)
+            CK(cudaMemcpyAsync((char*)h_out + i * h, (char*)d_b + i * h, h, cudaMemcpyDeviceToHost, q[2 + i]));
+        for (int i = 1; i < 4; ++i) {
+          CK(cudaEventRecord(e2, q[i]));
+          CK(cudaStreamWaitEvent(q[0], e2, 0));
+        }
+        CK(cudaEventRecord(e1, q[0]));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (r && ms < best) best = ms;
+      }
+      const char* name = mode == 0 ? "ce_h2d_x2" : mode == 1 ? "ce_d2h_x2" : "ce_both_x2";
+      const double dirs = mode == 2 ? 2.0 : 1.0;
+      printf("{\"scenario\": \"%s\", \"ms\": %.3f, \"gbs_each\": %.1f, \"gbs_total\": %.1f}\n", name, best,
+             bytes / (best * 1e-3) / 1e9, dirs * bytes / (best * 1e-3) / 1e9);
+    }
+  }
   for (auto& c : sc) {
     float best = 1e30f;
     for (int r = 0; r < 4; ++r) {
