@@ -9,9 +9,10 @@
 //              range does not change; it stays where it is in the src arena).
 // Every refined fragment becomes one strided 2-D copy (rows x row_bytes, two pitches)
 // from its source cell into its final offset of the destination cell, i.e. split, move
-// and merge are fused into a single write; no staging, no merge pass.  Copies are split
-// into ~256 KiB tiles and executed by one persistent kernel per source GPU (push: a
-// cross-GPU tile stores straight into the peer's dst arena over NVLink).
+// and merge are fused into a single write; no staging, no merge pass.  The host lowers
+// each copy to a few pieces (DevPiece); prepare() uploads them and the GPU expands them into
+// shared-memory-stage-sized tiles, executed by one persistent kernel per source GPU (push:
+// a cross-GPU tile stores straight into the peer's dst arena over NVLink).
 #pragma once
 
 #include <cstdint>
