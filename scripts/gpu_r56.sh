@@ -1,0 +1,6 @@
+#!/bin/bash
+set -u
+OUT=gpurun_out/r56
+mkdir -p "$OUT"
+timeout 900 python -m pytest tests/test_gpu_executor.py -m gpu -x -q -k "larger_than_4gib" > "$OUT/pytest.log" 2>&1; echo "rc=$?" >> "$OUT/pytest.log"
+echo done > "$OUT/DONE"

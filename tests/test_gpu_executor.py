@@ -406,3 +406,16 @@ def test_broadcast_fan_out_push(rs, ctx, kernel, monkeypatch):
         ctx.free(0, src)
     with pytest.raises(rs.ReshardError, match="InvalidArgument"):
         rs.broadcast(ctx, 0, 0, [1 << 20], 16)
+
+
+def test_cell_larger_than_4gib(rs, ctx):
+    """A single contiguous run above 2^32 bytes (one 4.5 GiB cell replicated to a new DP
+    rank): the piece's run is 64-bit, its tiles are not; every destination byte verified."""
+    n = (4 << 30) // 4 + (128 << 20)  # F32 elements: 4.5 GiB
+    cat = rs.Catalog.from_entries([("param/huge", 0, (n,), -1, 0)])
+    a = cat.build_strategy(DEV(1), 1, 1, 1)
+    b = cat.build_strategy(DEV(2), 1, 1, 2)
+    plan = rs.generate_plan(a, b)
+    ex, t = _run(rs, ctx, plan, 1, 2)
+    assert t[0]["bytes"] == 4 * n
+    assert ex.verify() == 0
