@@ -102,3 +102,32 @@ def test_reference_tensor_value_api_on_gpu(tensor_values):
     assert lines[:5] == EXPECTED_ERRORS
     assert lines[8] == "slice [0:4,2:4]: 2 3 8 9 14 15 20 21"
     assert lines[9] == "quadrant round trip: equal"
+
+
+@pytest.fixture(scope="module")
+def reshard_cli(rs, tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("cpp") / "reshard_cli")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run([CXX, "-std=c++20", "-O1", "-I", os.path.join(PKG, "csrc"), "-I", os.path.join(cuda, "include"),
+                    os.path.join(ROOT, "examples", "reshard_cli.cpp"), "-L", PKG, "-lreshard_b200",
+                    "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{PKG}", "-o", out], check=True)
+    return out
+
+
+def test_reshard_cli_compiles_and_fails_loudly_without_gpu(reshard_cli, rs):
+    """The whole reconfiguration driven from C++ (examples/reshard_cli.cpp): without a GPU
+    it stops with DeviceUnavailable (no CPU path)."""
+    if rs.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    p = subprocess.run([reshard_cli], capture_output=True, text=True)
+    assert p.returncode == 1 + rs._capi.ERRC.index("DeviceUnavailable") and p.stderr.startswith("DeviceUnavailable")
+
+
+@pytest.mark.gpu
+def test_reshard_cli_on_gpu(reshard_cli):
+    """examples/reshard_cli.cpp on a B200: GPT-2 small (2,1,1) -> (1,2,1) and GPT-3 1.3B
+    (2,1,1) -> (2,1,2) from C++, every destination byte verified."""
+    for args in (["768", "12", "1024", "50304", "2", "1", "1", "1", "2", "1"], []):
+        p = subprocess.run([reshard_cli, *args], capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr
+        assert "mismatched bytes 0" in p.stdout
