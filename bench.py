@@ -595,6 +595,8 @@ def run_ours(args):
     tiles = sum(ex.tiles(rank)[0] for ex in exs)
     copy_bytes = sum(ex.tiles(rank)[1] for ex in exs)  # bytes written
     read_bytes = sum(ex.read_bytes(rank) for ex in exs)  # bytes read (fan-out tiles read once)
+    # this rank's egress row of the fragment all-to-all (entry `rank`: its local writes)
+    row = [sum(v) for v in zip(*(ex.bytes_to(rank) for ex in exs))] if world > 1 else None
 
     def barrier():
         ctx.sync(rank)
@@ -700,15 +702,40 @@ def run_ours(args):
                "d2h_bytes_per_step": int(totals[1].item()), "steps": args.e2e_steps,
                "note": "per rank: H2D | barrier | kernels | barrier | D2H, max over ranks"}
 
+    fabric = None
+    if world > 1:  # T_roof = max_g max(in_g / BW_nvl, out_g / BW_nvl, hbm_g / BW_hbm)
+        import torch
+
+        dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
+        m = torch.zeros(world, world, dtype=torch.float64, device=dev)
+        m[rank] = torch.tensor([float(x) for x in row], dtype=torch.float64, device=dev)
+        rb = torch.zeros(world, dtype=torch.float64, device=dev)
+        rb[rank] = float(read_bytes)
+        dist.all_reduce(m)
+        dist.all_reduce(rb)
+        m, rb = m.cpu().tolist(), rb.cpu().tolist()
+        bw_nvl, (bw_hbm, _) = 900.0, measured_peaks()  # GB/s per direction (NVLink 5 spec), measured HBM
+        t_roof, worst = 0.0, None
+        for g in range(world):
+            out_g = sum(m[g][w] for w in range(world) if w != g)
+            in_g = sum(m[r][g] for r in range(world) if r != g)
+            hbm_g = rb[g] + sum(m[r][g] for r in range(world))  # reads of its tiles + every write landing in it
+            for kind, t in (("nvlink_out", out_g / bw_nvl), ("nvlink_in", in_g / bw_nvl), ("hbm", hbm_g / bw_hbm)):
+                if t / 1e6 > t_roof:
+                    t_roof, worst = t / 1e6, {"gpu": g, "term": kind}
+        fabric = {"t_roof_ms": round(t_roof, 3), "frac": round(t_roof / ms, 4) if ms else None, "bottleneck": worst,
+                  "bw_nvlink_gbs": bw_nvl, "bw_nvlink_kind": "spec (900 GB/s per direction; no measured P2P peak)",
+                  "max_egress_gb": round(max(sum(m[g][w] for w in range(world) if w != g) for g in range(world)) / 1e9, 3),
+                  "max_ingress_gb": round(max(sum(m[r][g] for r in range(world) if r != g) for g in range(world)) / 1e9, 3)}
+    kname = copy_kernel_name()
+    # the committed ncu capture is of the one-GPU launch; a rank of a larger world launches a share of it
+    traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" and world == 1 else None
     if rank != 0:
         return
     peak, peak_kind = measured_peaks()
     # roofline of the dominant (only) kernel: HBM read + write of every copied byte
     alg_bytes = read_bytes + copy_bytes
     achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
-    kname = copy_kernel_name()
-    # the committed ncu capture is of the one-GPU launch; a rank of a larger world launches a share of it
-    traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" and world == 1 else None
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
@@ -717,6 +744,7 @@ def run_ours(args):
                    (" (1-GPU emulation of all logical devices)" if N == 1 else ", logical device d on GPU d%N"),
                    "l2": "inputs larger than L2 (no flush)", "tile_kib": args.tile_kib, "mode": args.mode},
         "effective_gbs": round((stats["moved_bytes"] + stats["relayout_bytes"]) / (ms * 1e-3) / 1e9, 1),
+        "fabric": fabric,
         "moved_bytes": stats["moved_bytes"], "relayout_bytes": stats["relayout_bytes"],
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

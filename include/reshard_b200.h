@@ -255,6 +255,9 @@ int rs_executor_dst_cells(const rs_executor* e, int cap, rs_cell_binding* out, i
                           int32_t* cell, int* n);
 int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes);
 int rs_executor_read_bytes(const rs_executor* e, int gpu, uint64_t* bytes);
+/* bytes GPU `gpu`'s tiles write into each world GPU (bytes[w], n >= world): the egress row
+ * of the fragment all-to-all; bytes[gpu] are its local HBM writes */
+int rs_executor_bytes_to(const rs_executor* e, int gpu, int n, uint64_t* bytes);
 
 /* ---- PTX1 container and checkpoints (ptx_io.hpp:10-20) ------------ */
 int rs_ptx_encoded_size(int dtype, int rank, const uint64_t* shape, uint64_t* bytes);

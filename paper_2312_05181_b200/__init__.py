@@ -611,6 +611,13 @@ class Executor:
         _chk(lib.rs_executor_read_bytes(self.h, gpu, C.byref(b)))
         return b.value
 
+    def bytes_to(self, gpu: int) -> list[int]:
+        """Bytes GPU `gpu`'s tiles write into each world GPU (its egress row; own entry = local)."""
+        n = self.ctx.world
+        arr = (C.c_uint64 * n)()
+        _chk(lib.rs_executor_bytes_to(self.h, gpu, n, arr))
+        return list(arr)
+
     def tiles(self, gpu: int) -> tuple[int, int]:
         t, b = C.c_uint64(), C.c_uint64()
         _chk(lib.rs_executor_tiles(self.h, gpu, C.byref(t), C.byref(b)))

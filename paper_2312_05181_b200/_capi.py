@@ -138,6 +138,7 @@ SIGNATURES = {
                                         C.POINTER(C.c_int)]),
     "rs_executor_tiles": (C.c_int, [P, C.c_int, U64P, U64P]),
     "rs_executor_read_bytes": (C.c_int, [P, C.c_int, U64P]),
+    "rs_executor_bytes_to": (C.c_int, [P, C.c_int, C.c_int, U64P]),
     "rs_ptx_encoded_size": (C.c_int, [C.c_int, C.c_int, U64P, U64P]),
     "rs_ptx_encode_header": (C.c_int, [C.c_int, C.c_int, U64P, P, C.c_uint64, U64P]),
     "rs_ptx_decode_header": (C.c_int, [P, C.c_uint64, I32P, I32P, U64P, U64P]),

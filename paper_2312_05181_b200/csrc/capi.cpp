@@ -647,6 +647,14 @@ int rs_executor_read_bytes(const rs_executor* e, int gpu, uint64_t* bytes) {
     *bytes = e->e->read_bytes_for(gpu);
   });
 }
+int rs_executor_bytes_to(const rs_executor* e, int gpu, int n, uint64_t* bytes) {
+  return guard([&] {
+    need(e, "executor"), need(bytes, "bytes");
+    const std::vector<uint64_t> v = e->e->bytes_to(gpu);
+    if (n < int(v.size())) raise(Errc::InvalidArgument, "bytes_to: array shorter than the world");
+    std::copy(v.begin(), v.end(), bytes);
+  });
+}
 int rs_executor_tiles(const rs_executor* e, int gpu, uint64_t* tiles, uint64_t* bytes) {
   return guard([&] {
     need(e, "executor");

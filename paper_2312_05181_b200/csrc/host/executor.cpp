@@ -935,6 +935,16 @@ uint64_t Executor::copy_bytes_for(int gpu) const {
     for (auto& x : logical_b_) n += uint64_t(x.rows) * x.row_bytes * x.n_dst;
   return n;
 }
+std::vector<uint64_t> Executor::bytes_to(int gpu) const {
+  std::vector<uint64_t> out(size_t(ctx_.world()), 0);
+  auto add = [&](const std::vector<Logical>& v) {
+    for (auto& x : v)
+      for (uint32_t d = 0; d < x.n_dst; ++d) out[size_t(x.dst_gpu[d])] += uint64_t(x.rows) * x.row_bytes;
+  };
+  add(logical_[size_t(gpu)]);
+  if (gpu == central_) add(logical_b_);
+  return out;
+}
 uint64_t Executor::read_bytes_for(int gpu) const {
   uint64_t n = 0;
   const bool bulk = is_bulk(cfg_.kernel);

@@ -189,6 +189,9 @@ class Executor {
   uint64_t tiles_for(int gpu) const;
   uint64_t copy_bytes_for(int gpu) const;  // bytes written by the tiles GPU `gpu` executes
   uint64_t read_bytes_for(int gpu) const;  // bytes they read (fan-out reads once)
+  // bytes GPU `gpu`'s tiles write into each world GPU's memory (index = destination GPU):
+  // the egress row of the all-to-all (entry `gpu` itself: local HBM writes)
+  std::vector<uint64_t> bytes_to(int gpu) const;
 
  private:
   struct Logical {  // a piece (DevPiece geometry) before arena bases are known; n_dst > 1: fan-out

@@ -241,3 +241,25 @@ def test_broadcast_argument_errors(rs):
         with pytest.raises(rs.ReshardError) as e:
             rs.broadcast(ctx, 0, src, dsts, 64)
         assert e.value.name == "InvalidArgument"
+
+
+def test_bytes_to_rows_of_the_all_to_all(rs):
+    """Executor.bytes_to(g): GPU g's egress row of the fragment all-to-all.  Rows sum to the
+    executed bytes, the DP scale-out 2 -> 4 over 4 GPUs moves the replicas across GPUs, and
+    planning-only contexts (no GPU) compute it (the multi-rank bench's NVLink roofline)."""
+    cat = rs.Catalog.gpt(64, 2, 16, 128, rs.MIXED_ADAM)
+    a = cat.build_strategy([(0, 0), (0, 1)], 2, 1, 1)
+    b = cat.build_strategy([(0, i) for i in range(4)], 2, 1, 2)
+    plan = rs.generate_plan(a, b)
+    ctx = rs.Context(4, [], [])
+    ex = rs.Executor(ctx, plan, [0, 1], [0, 1, 2, 3], 4096)
+    rows = [ex.bytes_to(g) for g in range(4)]
+    for g in range(4):
+        assert sum(rows[g]) == ex.tiles(g)[1]
+    st = plan.stats()
+    # every moved byte crosses to the new replica's GPUs (2, 3); choose_source balances the
+    # egress of the two source GPUs (SPEC.md:238)
+    assert sum(rows[0][2:]) + sum(rows[1][2:]) == st["moved_bytes"]
+    assert abs(sum(rows[0]) - sum(rows[1])) < 0.1 * st["moved_bytes"]
+    assert rows[0][:2] == [0, 0] and rows[1][:2] == [0, 0]  # the kept replica moves nothing
+    assert rows[2] == [0, 0, 0, 0] and rows[3] == [0, 0, 0, 0]
