@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <exception>
+#include <thread>
+#include <map>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
@@ -181,30 +185,71 @@ Tensor ptx_read_file(const std::string& path) {
   return ptx_decode(b);
 }
 
+// Cells move through W host threads (RESHARD_IO_THREADS, default min(8, cores)): each worker
+// takes the next cell, with its own pinned double buffer and stream per GPU, so file I/O of
+// one cell overlaps the D2H / H2D of others (r61: one thread reached 3.3 GB/s save and 6.2
+// GB/s load to tmpfs).
+struct CellJob {
+  int gpu;
+  fs::path path;
+  Dtype dtype;
+  Shape shape;
+  char* dev;
+  uint64_t bytes;
+};
+template <class Fn>
+void run_cell_jobs(Context& ctx, const std::vector<CellJob>& jobs, Fn&& fn) {
+  const char* v = std::getenv("RESHARD_IO_THREADS");
+  const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  uint64_t total = 0;
+  for (const CellJob& j : jobs) total += j.bytes;
+  // one worker per ~1 GiB (each pins 2 staging buffers): small checkpoints stay single-threaded
+  const size_t by_size = size_t(std::max<uint64_t>(1, total >> 30));
+  const size_t workers = std::max<size_t>(
+      1, std::min<size_t>({jobs.size(), by_size, v && *v ? size_t(std::atoi(v)) : std::min<size_t>(8, hw)}));
+  std::atomic<size_t> next{0};
+  std::vector<std::exception_ptr> err(workers);
+  auto work = [&](size_t w) {
+    try {
+      std::map<int, std::unique_ptr<Staging>> st;  // per GPU
+      for (size_t i; (i = next.fetch_add(1)) < jobs.size();) {
+        const CellJob& j = jobs[i];
+        auto& s = st[j.gpu];
+        if (!s) {
+          ck(cudaSetDevice(ctx.cuda_device(j.gpu)), "cudaSetDevice");
+          s = std::make_unique<Staging>();
+        }
+        ck(cudaSetDevice(ctx.cuda_device(j.gpu)), "cudaSetDevice");
+        fn(*s, j);
+      }
+    } catch (...) {
+      err[w] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> th;
+  for (size_t w = 1; w < workers; ++w) th.emplace_back(work, w);
+  work(0);
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
 IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
   TraceRange trace_("checkpoint_save");
   const auto t0 = std::chrono::steady_clock::now();
   const ReconfigPlan& plan = ex.plan();
   Context& ctx = ex.context();
   IoStats io;
-  std::unique_ptr<Staging> st;
-  int cur_gpu = -1;
-  auto stage_for = [&](int gpu) -> Staging& {
-    if (gpu != cur_gpu) {
-      st.reset();
-      ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
-      st = std::make_unique<Staging>();
-      cur_gpu = gpu;
-    }
-    return *st;
-  };
+  std::vector<CellJob> jobs;
+  std::set<fs::path> dirs;
   auto save = [&](const PTC& ptc, uint32_t dev, uint32_t t, uint32_t c, const CellBinding& b) {
     if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) return;
     const TensorSpec& e = ptc.catalog.tensors[t];
     const fs::path p = fs::path(dir) / std::to_string(dev) / (e.path + ".ptx");
-    const char* base = static_cast<const char*>(ex.arena_base(b.gpu, b.arena));
+    char* base = static_cast<char*>(ex.arena_base(b.gpu, b.arena));
     if (!base) raise(Errc::InvalidArgument, "checkpoint_save: arena not bound");
-    write_cell(stage_for(b.gpu), p, e.dtype, ptc.cells[t][c].extents(), base + b.offset, b.bytes);
+    dirs.insert(p.parent_path());
+    jobs.push_back(CellJob{b.gpu, p, e.dtype, ptc.cells[t][c].extents(), base + b.offset, b.bytes});
     io.files += 1, io.bytes += b.bytes;
   };
   if (side == 0) {
@@ -219,6 +264,8 @@ IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
       save(b, dc.dst_device, dc.tensor, dc.cell, ex.dst_bindings()[j]);
     }
   }
+  for (const fs::path& d : dirs) fs::create_directories(d);  // before the workers: no creation races
+  run_cell_jobs(ctx, jobs, [](Staging& st, const CellJob& j) { write_cell(st, j.path, j.dtype, j.shape, j.dev, j.bytes); });
   io.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return io;
 }
@@ -240,26 +287,20 @@ IoStats checkpoint_load(Executor& ex, const std::string& dir) {
     raise(Errc::LayoutMismatch, "checkpoint has " + std::to_string(ranks.size()) + " ranks, layout has " +
                                     std::to_string(want.size()));
   IoStats io;
-  std::unique_ptr<Staging> st;
-  int cur_gpu = -1;
+  std::vector<CellJob> jobs;
   size_t k = 0;
   for (uint32_t i = 0; i < a.devices.size(); ++i)
     for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
       const CellBinding& b = ex.src_bindings()[k++];
       if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) continue;
-      if (b.gpu != cur_gpu) {
-        st.reset();
-        ck(cudaSetDevice(ctx.cuda_device(b.gpu)), "cudaSetDevice");
-        st = std::make_unique<Staging>();
-        cur_gpu = b.gpu;
-      }
       char* base = static_cast<char*>(ex.arena_base(b.gpu, 0));
       if (!base) raise(Errc::InvalidArgument, "checkpoint_load: arena not bound");
       const TensorSpec& e = a.catalog.tensors[t];
-      read_cell(*st, fs::path(dir) / std::to_string(i) / (e.path + ".ptx"), e.dtype, a.cells[t][c].extents(),
-                base + b.offset, b.bytes);
+      jobs.push_back(CellJob{b.gpu, fs::path(dir) / std::to_string(i) / (e.path + ".ptx"), e.dtype, a.cells[t][c].extents(),
+                             base + b.offset, b.bytes});
       io.files += 1, io.bytes += b.bytes;
     }
+  run_cell_jobs(ctx, jobs, [](Staging& st, const CellJob& j) { read_cell(st, j.path, j.dtype, j.shape, j.dev, j.bytes); });
   io.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return io;
 }
