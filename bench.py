@@ -703,6 +703,26 @@ def run_ours(args):
                "note": "per rank: H2D | barrier | kernels | barrier | D2H, max over ranks"}
 
     fabric = None
+    if world == 1 and len(exs) >= 1:  # derived: the same plan over its own GPU count (no such box here)
+        n_native = max(len(WORKLOADS[args.workload][1][3]), len(WORKLOADS[args.workload][2][3]))
+        if n_native > 1:
+            pctx = rs.Context(n_native, [], [])  # planning-only: layouts and tiles, no device
+            _, _, _, nplan, nsrc, ndst = build_plan(rs, args.workload, n_native)
+            pex = rs.Executor(pctx, nplan, nsrc, ndst, args.tile_kib << 10)
+            rows = [pex.bytes_to(g) for g in range(n_native)]
+            rbs = [pex.read_bytes(g) for g in range(n_native)]
+            bw_hbm = measured_peaks()[0]
+            t_roof, worst = 0.0, None
+            for g in range(n_native):
+                out_g = sum(rows[g][w] for w in range(n_native) if w != g)
+                in_g = sum(rows[r][g] for r in range(n_native) if r != g)
+                hbm_g = rbs[g] + sum(rows[r][g] for r in range(n_native))
+                for kind, t in (("nvlink_out", out_g / 900.0), ("nvlink_in", in_g / 900.0), ("hbm", hbm_g / bw_hbm)):
+                    if t / 1e6 > t_roof:
+                        t_roof, worst = t / 1e6, {"gpu": g, "term": kind}
+            fabric = {"derived_for_gpus": n_native, "t_roof_ms": round(t_roof, 3), "bottleneck": worst,
+                      "note": "not measured: SURVEY 8d's T_roof of this plan on its own GPU count (NVLink 900 GB/s "
+                              "per direction, measured HBM peak), for comparison with the 1-GPU emulation above"}
     if world > 1:  # T_roof = max_g max(in_g / BW_nvl, out_g / BW_nvl, hbm_g / BW_hbm)
         import torch
 
