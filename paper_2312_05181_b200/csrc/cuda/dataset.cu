@@ -584,61 +584,92 @@ struct L2FetchScope {
 // ---- K8: bit-exact parallel Fisher-Yates (deterministic reservations) -----------------------
 // The sequential shuffle (host shuffle_epoch) performs swap(A[i], A[H[i]]) for i = N-1 .. 1
 // with H[i] = splitmix64 draw (N-1-i) mod (i+1).  The draws are counter-based, so every
-// H[i] is computed up front.  Iteration i may run once no earlier (higher-index) pending
-// iteration touches location i or H[i]: each round, every pending iteration reserves both
-// its locations with atomicMax of (round << 32 | i); an iteration holding both
-// reservations swaps, the others carry over to the next round.  The result is identical
-// to the sequential loop (Shun et al., SODA'15, "deterministic reservations"); rounds are
-// O(log N) (about 70 for N = 10^8).
+// H[i] is computed where it is needed.  Iteration i may run once no earlier (higher-index)
+// pending iteration touches location i or H[i]: each round, every active iteration reserves
+// both its locations with atomicMax of (round << 32 | i); an iteration holding both
+// reservations swaps, the others carry over to the next round.  The result is identical to
+// the sequential loop (Shun et al., SODA'15, "deterministic reservations").
 __device__ __forceinline__ unsigned long long mix64d(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
   return z ^ (z >> 31);
 }
 
-__global__ void shuffle_init_kernel(unsigned long long* perm, unsigned long long* resv, unsigned long long* list,
-                                    unsigned long long n, unsigned long long s0) {
-  for (unsigned long long x = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; x < n;
-       x += (unsigned long long)gridDim.x * blockDim.x) {
-    perm[x] = x;
-    resv[x] = 0;
-    if (x >= 1) {
-      const unsigned long long draw = mix64d(s0 + (n - x) * 0x9e3779b97f4a7c15ull);  // draw number n-1-x
-      list[x - 1] = (x << 32) | (draw % (x + 1));
-    }
+// Windowed rounds: a round's active set is the iterations carried over from the last round
+// plus the next fresh (highest unprocessed) iterations, up to `window` in all.  Every pending
+// iteration of higher priority than an active one is itself active, so the result is still
+// the sequential loop's; but the low iterations, which almost always lose their reservations
+// while the high ones are pending, no longer reserve and fail round after round (work ~1.1 N
+// at window N/160 instead of ~3.5 N with every pending iteration active).  Fresh iterations
+// compute their draw inline (no N-entry list), and the round state lives on the device.
+// N = 10^8: 33 ms (all pending active, r04-r30) -> 14 ms (window, r67) -> 12.5 (packed
+// reservations, r70) -> 8.5 ms (6-round graphs, state checked one batch behind, N/160; r71).
+struct ShufState {
+  unsigned carried;          // iterations carried into this round (in the carried list)
+  unsigned pad;
+  unsigned long long lo;     // highest unprocessed fresh iteration (fresh: lo, lo-1, .., 1)
+};
+
+__device__ __forceinline__ unsigned long long shuf_entry(const unsigned long long* __restrict__ carried, unsigned c,
+                                                         unsigned long long lo, unsigned long long n,
+                                                         unsigned long long s0, unsigned long long t) {
+  if (t < c) return carried[t];
+  const unsigned long long i = lo - (t - c);
+  const unsigned long long draw = mix64d(s0 + (n - i) * 0x9e3779b97f4a7c15ull);  // draw number n-1-i
+  return (i << 32) | (draw % (i + 1));
+}
+
+__device__ __forceinline__ unsigned long long shuf_active(const ShufState& st, unsigned long long window) {
+  const unsigned long long take = window > st.carried ? window - st.carried : 0;
+  return st.carried + (take < st.lo ? take : st.lo);
+}
+
+// Reservations live in the high word of the permutation entry itself, A[x] = reserver << 32
+// | value (values and iterations are < 2^32), so a reservation and the value it guards share
+// one DRAM sector; key = i (>= 1, 0 = free).  A winner stores its swapped values with the high
+// word cleared, which releases both its locations; a loser still holding a location is pending
+// and re-reserves it next round, so no stale key can block, and the finished array is the u64
+// permutation with no extra pass.  (A separate N-entry array of round << 32 | i keys, r67-r68,
+// moved two random sectors per location instead of one: 14.3 vs 12.5 ms, profiles/r70.)
+__global__ void shuffle_win_reserve_kernel(const unsigned long long* __restrict__ carried, ShufState* state,
+                                           unsigned long long* perm, unsigned round, unsigned long long window,
+                                           unsigned long long n, unsigned long long s0) {
+  const ShufState st = state[round % 3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) state[(round + 1) % 3].carried = 0;  // commit appends into it
+  const unsigned long long m = shuf_active(st, window);
+  auto* hi = reinterpret_cast<unsigned*>(perm) + 1;  // the high word of A[x] is hi[2x]
+  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < m;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long e = shuf_entry(carried, st.carried, st.lo, n, s0, t), i = e >> 32, h = e & 0xffffffffull;
+    atomicMax(hi + 2 * i, unsigned(i));
+    if (h != i) atomicMax(hi + 2 * h, unsigned(i));
   }
 }
 
-__global__ void shuffle_reserve_kernel(const unsigned long long* __restrict__ list, const unsigned* __restrict__ count,
-                                       unsigned long long* resv, unsigned long long round) {
-  const unsigned n = *count;
-  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const unsigned long long e = list[k], i = e >> 32, h = e & 0xffffffffull;
-    const unsigned long long key = (round << 32) | i;
-    atomicMax(resv + i, key);
-    if (h != i) atomicMax(resv + h, key);
+__global__ void shuffle_win_commit_kernel(const unsigned long long* __restrict__ carried, ShufState* state,
+                                          unsigned long long* perm, unsigned long long* next, unsigned round,
+                                          unsigned long long window, unsigned long long n, unsigned long long s0,
+                                          unsigned* rounds_done) {
+  const ShufState st = state[round % 3];
+  const unsigned long long m = shuf_active(st, window);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[(round + 1) % 3].lo = st.lo - (m - st.carried);
+    if (m) atomicAdd(rounds_done, 1u);
   }
-}
-
-__global__ void shuffle_commit_kernel(const unsigned long long* __restrict__ list, const unsigned* __restrict__ count,
-                                      const unsigned long long* __restrict__ resv, unsigned long long* perm,
-                                      unsigned long long* next, unsigned* next_count, unsigned long long round) {
-  const unsigned n = *count;
+  unsigned* next_count = &state[(round + 1) % 3].carried;
   const unsigned lane = threadIdx.x & 31;
-  // grid-stride with whole-warp trip counts so the ballot below is warp-uniform
-  for (unsigned base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < n; base += gridDim.x * blockDim.x) {
-    const unsigned k = base + lane;
+  for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) & ~31ull; base < m;
+       base += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long t = base + lane;
     bool pending = false;
     unsigned long long e = 0;
-    if (k < n) {
-      e = list[k];
-      const unsigned long long i = e >> 32, h = e & 0xffffffffull, key = (round << 32) | i;
-      if (__ldcg(resv + i) == key && __ldcg(resv + h) == key) {
-        if (h != i) {
-          const unsigned long long a = perm[i];
-          perm[i] = perm[h];
-          perm[h] = a;
-        }
+    if (t < m) {
+      e = shuf_entry(carried, st.carried, st.lo, n, s0, t);
+      const unsigned long long i = e >> 32, h = e & 0xffffffffull;
+      const unsigned long long a = __ldcg(perm + i), b = h != i ? __ldcg(perm + h) : a;
+      if ((a >> 32) == i && (b >> 32) == i) {
+        perm[i] = b & 0xffffffffull;
+        if (h != i) perm[h] = a & 0xffffffffull;
       } else {
         pending = true;
       }
@@ -652,9 +683,32 @@ __global__ void shuffle_commit_kernel(const unsigned long long* __restrict__ lis
   }
 }
 
+__global__ void shuffle_win_init_kernel(unsigned long long* perm, ShufState* state, unsigned* rounds_done,
+                                        unsigned long long n) {
+  for (unsigned long long x = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; x < n;
+       x += (unsigned long long)gridDim.x * blockDim.x)
+    perm[x] = x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[1].carried = 0, state[1].lo = n - 1;  // round 1 reads slot 1
+    *rounds_done = 0;
+  }
+}
+
+// active iterations per round: N/160 (at least 64 Ki; RESHARD_K8_WINDOW overrides), capped at
+// the carried-list capacity the scratch provides
+uint64_t shuffle_window_cap(uint64_t n) {
+  return std::min<uint64_t>(std::max<uint64_t>(n / 20, 1ull << 16), std::max<uint64_t>(n, 1));
+}
+uint64_t shuffle_window(uint64_t n) {
+  uint64_t w = std::max<uint64_t>(n / 160, 1ull << 16);
+  if (const char* v = std::getenv("RESHARD_K8_WINDOW"))
+    if (const uint64_t e = std::strtoull(v, nullptr, 10)) w = e;
+  return std::min(w, shuffle_window_cap(n));
+}
 }  // namespace
 
-uint64_t shuffle_scratch_bytes(uint64_t n) { return 256 + 3 * align256(n * 8); }
+// round state [3] + rounds counter, two carried lists (window cap each)
+uint64_t shuffle_scratch_bytes(uint64_t n) { return 256 + 2 * align256(shuffle_window_cap(n) * 8); }
 
 Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm, void* scratch) {
   TraceRange trace_("shuffle_epoch_device");
@@ -663,37 +717,71 @@ Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, ui
   L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
   char* sc = static_cast<char*>(scratch);
-  auto* counts = reinterpret_cast<unsigned*>(sc);  // [2] list sizes (ping-pong)
-  auto* resv = reinterpret_cast<unsigned long long*>(sc + 256);
-  unsigned long long* lists[2] = {reinterpret_cast<unsigned long long*>(sc + 256 + align256(n * 8)),
-                                  reinterpret_cast<unsigned long long*>(sc + 256 + 2 * align256(n * 8))};
+  const uint64_t cap = align256(shuffle_window_cap(n) * 8);
+  unsigned long long* lists[2] = {reinterpret_cast<unsigned long long*>(sc + 256),
+                                  reinterpret_cast<unsigned long long*>(sc + 256 + cap)};
   cudaEvent_t e0, e1;
   ck(cudaEventCreate(&e0), "event");
   ck(cudaEventCreate(&e1), "event");
-  ck(cudaEventRecord(e0, st), "event");
   Timing t;
-  unsigned* pinned = nullptr;
-  ck(cudaMallocHost(&pinned, sizeof(unsigned)), "pinned");
-  const unsigned init = n ? unsigned(n - 1) : 0u;
-  ck(cudaMemcpyAsync(counts, &init, sizeof(unsigned), cudaMemcpyHostToDevice, st), "count");
+  void* pinned = nullptr;
+  ck(cudaMallocHost(&pinned, 256), "pinned");
   const int grid_full = ctx.sm_count(gpu) * 8;  // 8 resident 256-thread CTAs per SM
-  shuffle_init_kernel<<<grid_full, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(perm), resv, lists[0], n,
-                                                 seed ^ epoch);
-  ck(cudaGetLastError(), "shuffle init");
-  t.launches = 1;
-  unsigned pending = init;
-  for (unsigned long long round = 1, cur = 0; pending > 0; ++round, cur ^= 1) {
-    const int grid = int(std::min<unsigned long long>(grid_full, (pending + 255) / 256));
-    ck(cudaMemsetAsync(counts + (cur ^ 1), 0, sizeof(unsigned), st), "reset count");
-    shuffle_reserve_kernel<<<grid, 256, 0, st>>>(lists[cur], counts + cur, resv, round);
-    shuffle_commit_kernel<<<grid, 256, 0, st>>>(lists[cur], counts + cur, resv, reinterpret_cast<unsigned long long*>(perm),
-                                                lists[cur ^ 1], counts + (cur ^ 1), round);
-    ck(cudaGetLastError(), "shuffle round");
-    t.launches += 2;
-    ck(cudaMemcpyAsync(pinned, counts + (cur ^ 1), sizeof(unsigned), cudaMemcpyDeviceToHost, st), "count d2h");
+  auto* p64 = reinterpret_cast<unsigned long long*>(perm);
+  auto* state = reinterpret_cast<ShufState*>(sc);  // slots [3]; rounds counter at sc + 64
+  auto* rounds_done = reinterpret_cast<unsigned*>(sc + 64);
+  const uint64_t window = shuffle_window(n);
+  const int grid = int(std::min<unsigned long long>(grid_full, (window + 255) / 256));
+  const unsigned long long s0 = seed ^ epoch;
+  // One batch = 6 rounds (the state slots cycle mod 3, the carried lists mod 2), captured
+  // once as a graph and replayed; the host checks a batch's final state while the next batch
+  // runs, so the GPU does not drain between batches (the last batch is empty rounds).
+  cudaGraphExec_t exec = nullptr;
+  if (n > 1) {
+    cudaStream_t cs;
+    ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
+    ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture");
+    for (unsigned round = 1; round <= 6; ++round) {
+      const unsigned cur = round & 1;
+      shuffle_win_reserve_kernel<<<grid, 256, 0, cs>>>(lists[cur], state, p64, round, window, n, s0);
+      shuffle_win_commit_kernel<<<grid, 256, 0, cs>>>(lists[cur], state, p64, lists[cur ^ 1], round, window, n, s0,
+                                                      rounds_done);
+    }
+    cudaGraph_t graph;
+    ck(cudaStreamEndCapture(cs, &graph), "capture end");
+    ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+  }
+  ck(cudaEventRecord(e0, st), "event");
+  if (n > 1) {
+    shuffle_win_init_kernel<<<grid_full, 256, 0, st>>>(p64, state, rounds_done, n);
+    ck(cudaGetLastError(), "shuffle init");
+    t.launches = 1;
+    auto* snap = static_cast<ShufState*>(pinned);  // [2] batch snapshots
+    cudaEvent_t done_ev[2];
+    ck(cudaEventCreateWithFlags(&done_ev[0], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&done_ev[1], cudaEventDisableTiming), "event");
+    for (unsigned b = 0;; ++b) {
+      ck(cudaGraphLaunch(exec, st), "graph launch");
+      t.launches += 12;
+      ck(cudaMemcpyAsync(snap + (b & 1), state + 1, sizeof(ShufState), cudaMemcpyDeviceToHost, st), "state d2h");
+      ck(cudaEventRecord(done_ev[b & 1], st), "event");
+      if (b == 0) continue;
+      ck(cudaEventSynchronize(done_ev[(b - 1) & 1]), "shuffle sync");
+      const ShufState s = snap[(b - 1) & 1];
+      if (s.carried == 0 && s.lo == 0) break;
+    }
+    ck(cudaMemcpyAsync(static_cast<char*>(pinned) + 64, rounds_done, sizeof(unsigned), cudaMemcpyDeviceToHost, st),
+       "rounds d2h");
     ck(cudaStreamSynchronize(st), "shuffle sync");
-    pending = *pinned;
-    t.tiles = round;  // rounds
+    t.tiles = *reinterpret_cast<unsigned*>(static_cast<char*>(pinned) + 64);
+    cudaEventDestroy(done_ev[0]);
+    cudaEventDestroy(done_ev[1]);
+    cudaGraphExecDestroy(exec);
+  } else if (n == 1) {
+    const unsigned long long zero = 0;
+    ck(cudaMemcpyAsync(perm, &zero, 8, cudaMemcpyHostToDevice, st), "perm");
   }
   ck(cudaEventRecord(e1, st), "event");
   ck(cudaEventSynchronize(e1), "sync");

@@ -218,7 +218,10 @@ def test_host_buffer_path_matches_oracle(rs, orc, ctx, eb):
 
 @pytest.mark.gpu
 def test_k8_gpu_shuffle_bit_identical(rs, ctx):
-    for n, seed, ep in [(1, 3, 0), (2, 3, 1), (1000, 0x5EED, 0), (123_457, 9, 4), (3_000_000, 0x5EED, 2)]:
+    # 65_536 / 65_537: the window (64 Ki minimum) covers all or all but one iteration; 3M runs
+    # many 6-round graph batches with the window 64 Ki
+    for n, seed, ep in [(1, 3, 0), (2, 3, 1), (3, 7, 0), (1000, 0x5EED, 0), (65_536, 1, 1), (65_537, 2, 2),
+                        (123_457, 9, 4), (3_000_000, 0x5EED, 2)]:
         p = ctx.malloc(0, 8 * n)
         t = rs.shuffle_epoch_device(ctx, 0, n, seed, ep, p)
         got = np.empty(n, np.uint64)
