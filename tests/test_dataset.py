@@ -216,6 +216,52 @@ def test_host_buffer_path_matches_oracle(rs, orc, ctx, eb):
     rs.host_free(h_samp)
 
 
+def _k8_rounds(n, seed, epoch, window):
+    """Round-level restatement of K8's schedule (csrc/cuda/dataset.cu, shuffle_win_*): windowed
+    active sets, reservations packed into the high word of the permutation entry (atomicMax of
+    i), winners storing their swapped values with the high word cleared, losers carried.  A
+    kernel round is this function's round: winners touch disjoint locations and losers do not
+    write, so the order of threads inside a launch cannot change the outcome."""
+    gamma, mask = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xFFFFFFFF)
+
+    def draws(i):  # H[i] = splitmix64 draw number n-1-i mod (i+1), i as uint64 array
+        with np.errstate(over="ignore"):
+            z = np.uint64(seed ^ epoch) + (np.uint64(n) - i) * gamma
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+        return z % (i + np.uint64(1))
+
+    a = np.arange(n, dtype=np.uint64)
+    carried, lo, rounds = np.empty(0, np.uint64), n - 1, 0
+    while carried.size or lo:
+        take = min(max(window - carried.size, 0), lo)
+        i = np.concatenate([carried, np.arange(lo, lo - take, -1, dtype=np.uint64)])
+        lo -= take
+        h = draws(i)
+        hi = a >> np.uint64(32)
+        np.maximum.at(hi, i.astype(np.int64), i)
+        np.maximum.at(hi, h.astype(np.int64), i)
+        a = (a & mask) | (hi << np.uint64(32))
+        win = ((a[i.astype(np.int64)] >> np.uint64(32)) == i) & ((a[h.astype(np.int64)] >> np.uint64(32)) == i)
+        wi, wh = i[win].astype(np.int64), h[win].astype(np.int64)
+        vi, vh = a[wi] & mask, a[wh] & mask
+        a[wi], a[wh] = vh, vi  # h == i: both writes store the same value
+        carried = i[~win]
+        rounds += 1
+    return a, rounds
+
+
+def test_k8_schedule_restatement_matches_host_shuffle(rs):
+    """The packed-reservation, windowed schedule K8 runs is the sequential Fisher-Yates: a
+    finished iteration leaves no key behind, so no stale reservation can block or reorder."""
+    for n, seed, ep, w in [(2, 3, 1, 1), (3, 7, 0, 1), (1000, 0x5EED, 0, 7), (1000, 0x5EED, 0, 1000),
+                           (20_000, 9, 4, 125), (65_537, 2, 2, 65_536), (200_000, 1, 3, 1250)]:
+        got, rounds = _k8_rounds(n, seed, ep, w)
+        assert np.array_equal(got, rs.shuffle_epoch(n, seed, ep)), (n, w)
+        assert rounds >= (n - 1 + w - 1) // w
+
+
 @pytest.mark.gpu
 def test_k8_gpu_shuffle_bit_identical(rs, ctx):
     # 65_536 / 65_537: the window (64 Ki minimum) covers all or all but one iteration; 3M runs
