@@ -307,7 +307,9 @@ typedef struct rs_partition_host {  /* host pointers (pinned for full PCIe rate)
 } rs_partition_host;
 
 /* K8: shuffle_epoch on the GPU, bit-identical to rs_shuffle_epoch (deterministic
- * reservations); perm_dev: n x u64 device buffer; scratch: rs_shuffle_scratch_bytes(n) */
+ * reservations, kept in the high words of perm_dev while it runs); n < 2^32; perm_dev: n x u64
+ * device buffer; scratch: rs_shuffle_scratch_bytes(n) (the carried-iteration lists, 16 B per
+ * window entry: max(n/20, 64 Ki) entries).  Synchronous; timing->tiles = rounds. */
 int rs_shuffle_scratch_bytes(uint64_t n, uint64_t* bytes);
 int rs_shuffle_epoch_device(rs_context* ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm_dev,
                             void* scratch, rs_timing* timing);

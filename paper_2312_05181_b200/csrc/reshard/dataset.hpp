@@ -59,8 +59,9 @@ struct PartitionHost {
 };
 
 // K8: the same permutation as shuffle_epoch, computed on the GPU (bit-identical; parallel
-// Fisher-Yates by deterministic reservations).  perm: device, n entries; scratch:
-// shuffle_scratch_bytes(n) of device memory.  Timing.tiles = rounds.
+// Fisher-Yates by deterministic reservations in windowed rounds, the reservations packed into
+// the high words of perm while it runs).  perm: device, n entries (n < 2^32); scratch:
+// shuffle_scratch_bytes(n) of device memory (the carried-iteration lists).  Timing.tiles = rounds.
 uint64_t shuffle_scratch_bytes(uint64_t n);
 Timing shuffle_epoch_device(Context& ctx, int gpu, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t* perm,
                             void* scratch);
