@@ -221,7 +221,8 @@ def _k8_rounds(n, seed, epoch, window):
     active sets, reservations packed into the high word of the permutation entry (atomicMax of
     i), winners storing their swapped values with the high word cleared, losers carried.  A
     kernel round is this function's round: winners touch disjoint locations and losers do not
-    write, so the order of threads inside a launch cannot change the outcome."""
+    write, so the order of threads inside a launch cannot change the outcome (checked below:
+    the losers stay losers when the winners' stores are visible)."""
     gamma, mask = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xFFFFFFFF)
 
     def draws(i):  # H[i] = splitmix64 draw number n-1-i mod (i+1), i as uint64 array
@@ -243,10 +244,16 @@ def _k8_rounds(n, seed, epoch, window):
         np.maximum.at(hi, i.astype(np.int64), i)
         np.maximum.at(hi, h.astype(np.int64), i)
         a = (a & mask) | (hi << np.uint64(32))
-        win = ((a[i.astype(np.int64)] >> np.uint64(32)) == i) & ((a[h.astype(np.int64)] >> np.uint64(32)) == i)
+        def wins(arr):
+            return ((arr[i.astype(np.int64)] >> np.uint64(32)) == i) & ((arr[h.astype(np.int64)] >> np.uint64(32)) == i)
+
+        win = wins(a)
         wi, wh = i[win].astype(np.int64), h[win].astype(np.int64)
         vi, vh = a[wi] & mask, a[wh] & mask
         a[wi], a[wh] = vh, vi  # h == i: both writes store the same value
+        # inside a launch a check may see winners' stores (values with the key cleared) or not:
+        # the winner set must be the same either way (a rule accepting a cleared key would not be)
+        assert np.array_equal(wins(a)[~win], np.zeros((~win).sum(), bool))
         carried = i[~win]
         rounds += 1
     return a, rounds
