@@ -1,5 +1,6 @@
 #!/bin/bash
-# r67: windowed K8 (bit-identity tests + window sweep vs the full-active-set variant)
+# r67: windowed K8 (bit-identity tests + window sweep vs the full-active-set variant;
+# RESHARD_K8=full was retired after this run, so today the second pytest line runs the default)
 set -u
 OUT=gpurun_out/r67
 mkdir -p "$OUT"

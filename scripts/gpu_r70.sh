@@ -1,6 +1,6 @@
 #!/bin/bash
 # r70: K8 with packed reservations (high word of the permutation entry) vs separate
-# reservations (RESHARD_K8=sep): tests, window sweeps, launch list of the packed variant
+# reservations (RESHARD_K8=sep, retired after this run): tests, window sweeps, launch list
 set -u
 OUT=gpurun_out/r70
 mkdir -p "$OUT"
