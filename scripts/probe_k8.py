@@ -30,8 +30,12 @@ def main() -> int:
     want = rs.shuffle_epoch(n, seed, ep)
     d = ctx.malloc(0, 8 * n)
     got = np.empty(n, np.uint64)
-    for w in (n // f for f in map(int, args.fracs.split(","))):
-        os.environ["RESHARD_K8_WINDOW"] = str(w)
+    for f in map(int, args.fracs.split(",")):  # 0: the default window
+        w = n // f if f else "default"
+        if f:
+            os.environ["RESHARD_K8_WINDOW"] = str(w)
+        else:
+            os.environ.pop("RESHARD_K8_WINDOW", None)
         ts = [rs.shuffle_epoch_device(ctx, 0, n, seed, ep, d) for _ in range(7)][2:]
         ctx.dtoh(0, got.ctypes.data, d, 8 * n)
         print(json.dumps({"window": w, "n": n, "ms_median": round(statistics.median(t["ms"] for t in ts), 3),
