@@ -259,7 +259,13 @@ int rs_executor_read_bytes(const rs_executor* e, int gpu, uint64_t* bytes);
  * of the fragment all-to-all; bytes[gpu] are its local HBM writes */
 int rs_executor_bytes_to(const rs_executor* e, int gpu, int n, uint64_t* bytes);
 
-/* ---- PTX1 container and checkpoints (ptx_io.hpp:10-20) ------------ */
+/* ---- PTX1 container and checkpoints (ptx_io.hpp:10-20) ------------
+ * PTX1 defines dtype codes 0..3 only: BF16 (4) payloads are WRITTEN WITH THE F16 CODE (1), same
+ * width, so reference readers accept the files; decoding such a file yields F16.  A checkpoint
+ * load takes the real dtype from the executor's layout, not from the file.
+ * Checkpoint files: <dir>/<rank>/<tensor path>.ptx, or <tensor path>.c<cell>.ptx when the rank
+ * hosts several cells of that tensor.  Tensor paths must be relative without '..'
+ * (InvalidArgument).  A failed write or close is IoError. */
 int rs_ptx_encoded_size(int dtype, int rank, const uint64_t* shape, uint64_t* bytes);
 int rs_ptx_encode_header(int dtype, int rank, const uint64_t* shape, uint8_t* out, uint64_t cap, uint64_t* written);
 /* validates a whole PTX1 buffer (header + payload) */

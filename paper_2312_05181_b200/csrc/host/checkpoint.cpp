@@ -15,6 +15,7 @@
 #include <cstring>
 #include <filesystem>
 #include <set>
+#include <tuple>
 
 namespace reshard {
 
@@ -29,6 +30,9 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) raise(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// PTX1 has codes 0..3 only.  BF16 payloads are written with the F16 code (same
+// width; payloads are opaque bytes) so reference readers accept the files; the
+// real dtype is the layout's, which checkpoint_load takes from the catalog, not the file.
 uint8_t wire_code(Dtype d) { return d == Dtype::BF16 ? uint8_t(Dtype::F16) : uint8_t(d); }
 
 struct File {
@@ -36,10 +40,35 @@ struct File {
   File(const fs::path& p, const char* mode) : f(std::fopen(p.c_str(), mode)) {
     if (!f) raise(Errc::IoError, "cannot open " + p.string());
   }
+  // explicit close for writers: a buffered write that fails at close (ENOSPC) is an error
+  void close(const fs::path& p) {
+    std::FILE* g = f;
+    f = nullptr;
+    if (std::fclose(g) != 0) raise(Errc::IoError, "close " + p.string());
+  }
   ~File() {
     if (f) std::fclose(f);
   }
 };
+
+// <dir>/<rank>/<tensor path>[.c<cell>].ptx.  The cell suffix appears only when
+// the rank hosts several cells of the tensor, so the common one-cell layout keeps the plain
+// name.  Tensor paths are relative and may not climb out of the rank directory.
+fs::path cell_file(const std::string& dir, uint32_t rank, const std::string& tensor, uint32_t cell, bool several) {
+  const fs::path rel(tensor);
+  if (tensor.empty() || rel.is_absolute() || rel.has_root_name())
+    raise(Errc::InvalidArgument, "checkpoint: tensor path '" + tensor + "' is not relative");
+  for (const auto& part : rel)
+    if (part == "..") raise(Errc::InvalidArgument, "checkpoint: tensor path '" + tensor + "' contains '..'");
+  return fs::path(dir) / std::to_string(rank) / (tensor + (several ? ".c" + std::to_string(cell) : std::string()) + ".ptx");
+}
+
+// per (device, tensor): how many cells the device hosts
+std::map<std::pair<uint32_t, uint32_t>, uint32_t> cells_per_device(const std::vector<std::tuple<uint32_t, uint32_t, uint32_t>>& v) {
+  std::map<std::pair<uint32_t, uint32_t>, uint32_t> n;
+  for (auto [d, t, c] : v) ++n[{d, t}];
+  return n;
+}
 
 // Two pinned staging buffers and a stream on the current device.
 struct Staging {
@@ -78,6 +107,7 @@ void write_cell(Staging& st, const fs::path& p, Dtype dt, const Shape& shape, co
     const uint64_t len = std::min<uint64_t>(kChunk, bytes - i * kChunk);
     if (std::fwrite(st.buf[i & 1], 1, len, f.f) != len) raise(Errc::IoError, "write " + p.string());
   }
+  f.close(p);
 }
 
 void read_cell(Staging& st, const fs::path& p, Dtype dt, const Shape& shape, char* dev, uint64_t bytes) {
@@ -242,27 +272,32 @@ IoStats checkpoint_save(Executor& ex, int side, const std::string& dir) {
   IoStats io;
   std::vector<CellJob> jobs;
   std::set<fs::path> dirs;
-  auto save = [&](const PTC& ptc, uint32_t dev, uint32_t t, uint32_t c, const CellBinding& b) {
-    if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) return;
+  // (device, tensor, cell) and binding of every cell on this side, in layout order
+  std::vector<std::tuple<uint32_t, uint32_t, uint32_t>> cells;
+  std::vector<const CellBinding*> binds;
+  const PTC& ptc = side == 0 ? *plan.from : *plan.to;
+  if (side == 0) {
+    size_t k = 0;
+    for (uint32_t i = 0; i < ptc.devices.size(); ++i)
+      for (auto [t, c] : hosted_subtensors(ptc, ptc.devices[i])) cells.emplace_back(i, t, c), binds.push_back(&ex.src_bindings()[k++]);
+  } else {
+    for (size_t j = 0; j < plan.dst_cells.size(); ++j) {
+      const PlanDstCell& dc = plan.dst_cells[j];
+      cells.emplace_back(dc.dst_device, dc.tensor, dc.cell), binds.push_back(&ex.dst_bindings()[j]);
+    }
+  }
+  const auto per = cells_per_device(cells);
+  for (size_t k = 0; k < cells.size(); ++k) {
+    const auto [dev, t, c] = cells[k];
+    const CellBinding& b = *binds[k];
     const TensorSpec& e = ptc.catalog.tensors[t];
-    const fs::path p = fs::path(dir) / std::to_string(dev) / (e.path + ".ptx");
+    const fs::path p = cell_file(dir, dev, e.path, c, per.at({dev, t}) > 1);  // validates every path
+    if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) continue;
     char* base = static_cast<char*>(ex.arena_base(b.gpu, b.arena));
     if (!base) raise(Errc::InvalidArgument, "checkpoint_save: arena not bound");
     dirs.insert(p.parent_path());
     jobs.push_back(CellJob{b.gpu, p, e.dtype, ptc.cells[t][c].extents(), base + b.offset, b.bytes});
     io.files += 1, io.bytes += b.bytes;
-  };
-  if (side == 0) {
-    const PTC& a = *plan.from;
-    size_t k = 0;
-    for (uint32_t i = 0; i < a.devices.size(); ++i)
-      for (auto [t, c] : hosted_subtensors(a, a.devices[i])) save(a, i, t, c, ex.src_bindings()[k++]);
-  } else {
-    const PTC& b = *plan.to;
-    for (size_t j = 0; j < plan.dst_cells.size(); ++j) {
-      const PlanDstCell& dc = plan.dst_cells[j];
-      save(b, dc.dst_device, dc.tensor, dc.cell, ex.dst_bindings()[j]);
-    }
   }
   for (const fs::path& d : dirs) fs::create_directories(d);  // before the workers: no creation races
   run_cell_jobs(ctx, jobs, [](Staging& st, const CellJob& j) { write_cell(st, j.path, j.dtype, j.shape, j.dev, j.bytes); });
@@ -288,18 +323,21 @@ IoStats checkpoint_load(Executor& ex, const std::string& dir) {
                                     std::to_string(want.size()));
   IoStats io;
   std::vector<CellJob> jobs;
-  size_t k = 0;
+  std::vector<std::tuple<uint32_t, uint32_t, uint32_t>> cells;
   for (uint32_t i = 0; i < a.devices.size(); ++i)
-    for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
-      const CellBinding& b = ex.src_bindings()[k++];
-      if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) continue;
-      char* base = static_cast<char*>(ex.arena_base(b.gpu, 0));
-      if (!base) raise(Errc::InvalidArgument, "checkpoint_load: arena not bound");
-      const TensorSpec& e = a.catalog.tensors[t];
-      jobs.push_back(CellJob{b.gpu, fs::path(dir) / std::to_string(i) / (e.path + ".ptx"), e.dtype, a.cells[t][c].extents(),
-                             base + b.offset, b.bytes});
-      io.files += 1, io.bytes += b.bytes;
-    }
+    for (auto [t, c] : hosted_subtensors(a, a.devices[i])) cells.emplace_back(i, t, c);
+  const auto per = cells_per_device(cells);
+  for (size_t k = 0; k < cells.size(); ++k) {
+    const auto [i, t, c] = cells[k];
+    const CellBinding& b = ex.src_bindings()[k];
+    const TensorSpec& e = a.catalog.tensors[t];
+    fs::path p = cell_file(dir, i, e.path, c, per.at({i, t}) > 1);
+    if (b.gpu < 0 || ctx.local_of(b.gpu) < 0) continue;
+    char* base = static_cast<char*>(ex.arena_base(b.gpu, 0));
+    if (!base) raise(Errc::InvalidArgument, "checkpoint_load: arena not bound");
+    jobs.push_back(CellJob{b.gpu, std::move(p), e.dtype, a.cells[t][c].extents(), base + b.offset, b.bytes});
+    io.files += 1, io.bytes += b.bytes;
+  }
   run_cell_jobs(ctx, jobs, [](Staging& st, const CellJob& j) { read_cell(st, j.path, j.dtype, j.shape, j.dev, j.bytes); });
   io.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return io;

@@ -153,6 +153,10 @@ std::shared_ptr<const ReconfigPlan> recover(std::shared_ptr<const PTC> from, con
                                             std::shared_ptr<const PTC> to) {
   for (auto& f : failed)
     if (from->ordinal(f) < 0) raise(Errc::UnknownDevice, "failed device " + f.to_string() + " not in the layout");
+  // the target layout must leave the failed devices out (a Move into a dead device is a bug)
+  for (auto& f : failed)
+    if (to->ordinal(f) >= 0)
+      raise(Errc::InvalidArgument, "failed device " + f.to_string() + " is part of the target layout");
   return plan_impl(std::move(from), std::move(to), failed);
 }
 

@@ -109,3 +109,53 @@ def test_checkpoint_round_trip_and_recovery(rs, ctx, tmp_path):
     ck.checkpoint_load(ex6, d3)
     ex6.apply()
     assert ex6.verify() == 0
+
+
+def test_checkpoint_rejects_escaping_tensor_paths(rs, tmp_path):
+    """A tensor path that is absolute or climbs with '..' is refused before anything is
+    written: checked on a planning-only context, no GPU needed."""
+    from paper_2312_05181_b200 import checkpoint as ck
+
+    for bad in ("/tmp/x", "a/../../x"):
+        cat = rs.Catalog.from_entries([(bad, 0, (8,), 0, 0)])
+        a = cat.build_strategy(DEV(2), 2, 1, 1)
+        ctx = rs.Context(1, [], [])
+        ex = rs.Executor(ctx, rs.generate_plan(a, a), [0, 0], [0, 0])
+        with pytest.raises(rs.ReshardError) as e:
+            ck.checkpoint_save(ex, str(tmp_path / "c"), side=0)
+        assert e.value.name == "InvalidArgument"
+        assert not os.path.exists(tmp_path / "c")
+
+
+@pytest.mark.gpu
+def test_checkpoint_rank_hosting_two_cells(rs, ctx, tmp_path):
+    """A rank may host several cells of one tensor (parse_parallel_config accepts it): each
+    cell gets its own file (<path>.c<cell>.ptx), and the round trip restores both."""
+    import json
+
+    from paper_2312_05181_b200 import checkpoint as ck
+    from paper_2312_05181_b200.config import parse_parallel_config
+
+    leaf = lambda r: {"base": "w", "shape": [12, 4], "range": r, "dtype": "f32"}  # noqa: E731
+    doc = json.dumps([{"w0": leaf([[0, 3], [0, 4]]), "w1": leaf([[3, 6], [0, 4]])},
+                      {"w2": leaf([[6, 12], [0, 4]])}])
+    a = parse_parallel_config(doc)
+    assert len(a.hosted_subtensors((0, 0))) == 2
+    b = rs.Catalog.from_entries([("w", 0, (12, 4), 0, 0)]).build_strategy(DEV(2), 1, 1, 2)
+    plan = rs.generate_plan(a, b)
+    ex = rs.Executor(ctx, plan, [0, 0], [0, 0])
+    ex.allocate_local()
+    ex.prepare()
+    ex.fill_sources()
+    d = str(tmp_path / "two")
+    st = ck.checkpoint_save(ex, d, side=0)
+    assert st["files"] == 3
+    assert sorted(os.listdir(os.path.join(d, "0"))) == ["w.c0.ptx", "w.c1.ptx"]
+    assert os.listdir(os.path.join(d, "1")) == ["w.ptx"]
+    ex2 = rs.Executor(ctx, plan, [0, 0], [0, 0])
+    ex2.allocate_local()
+    ex2.prepare()
+    ctx.memset(0, ex2.arenas[0][0], 0, ex2.arena_bytes(0)[0])
+    ck.checkpoint_load(ex2, d)
+    ex2.apply()
+    assert ex2.verify() == 0

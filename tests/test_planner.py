@@ -174,8 +174,11 @@ def test_recovery(rs):
     assert e.value.name == "CheckpointRequired"
     d1 = cat.build_strategy(DEV(8), 4, 2, 1)
     with pytest.raises(rs.ReshardError) as e:
-        rs.recover(d1, [(0, 3)], cat.build_strategy(DEV(4), 2, 2, 1))
+        rs.recover(d1, [(0, 3)], cat.build_strategy([(0, 0), (0, 1), (0, 2), (0, 4)], 2, 2, 1))
     assert e.value.name == "CheckpointRequired"      # D=1, any failure
+    with pytest.raises(rs.ReshardError) as e:      # the target may not contain a failed device
+        rs.recover(a, DEV(8, 8), cat.build_strategy(DEV(16), 4, 2, 2))
+    assert e.value.name == "InvalidArgument"
     # a failed device that hosts only replicas others still hold moves nothing extra
     assert survivors
 
