@@ -4,13 +4,18 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
 
 A step is one apply_plan of the workload's reconfiguration over state already resident
-in HBM (synthetic random-init payload of the named model shapes).  `value` is the reshard
-time in ms (max over ranks, CUDA events on the launch stream); `e2e` is the same metric
-through the C-ABI with host buffers (H2D of the source arena from pinned memory, the
-reshard kernel, D2H of the destination arena).  Inputs (>= 18 GB) exceed the 126 MB L2, so
-no flush is needed between steps.  N>1 runs under torchrun, one process per GPU: logical
-device d lives on GPU d % N, destination arenas are exchanged through CUDA IPC and
-cross-GPU fragments are pushed over NVLink by the source GPU's kernel.
+in HBM (synthetic random-init payload of the named model shapes), started from a barrier.
+`value` is the reshard time in ms: from one common start to the last GPU's completion (CUDA
+events; one process driving N GPUs) or, under torchrun (one process per GPU), each rank's
+event time from a per-step barrier, max over ranks.  `e2e` is the same metric through the
+C-ABI with host buffers (H2D of the source arenas from pinned memory, the reshard kernels,
+D2H of the destination arenas).  Inputs (>= 18 GB) exceed the 126 MB L2, so no flush is
+needed between steps.  Logical device d lives on GPU d % N; cross-GPU fragments are pushed
+over NVLink by the source GPU's kernels (peer stores into the destination's arena).
+
+    python bench.py --gpus N            one process, N GPUs (peer access), needs N devices —
+                                        or RESHARD_SAME_GPU=1: the N-GPU world emulated on cuda:0
+    torchrun ... bench.py --gpus N      one process per GPU, dst arenas exchanged by CUDA IPC
 """
 from __future__ import annotations
 
@@ -41,8 +46,7 @@ WORKLOADS = {
                            [1, 3, 4, 6]),
 }
 DEFAULT_WORKLOAD = "gpt3-1.3b-dp-scaleout"
-# (workload, n_gpus) -> waves needed to fit 180 GB per GPU
-WAVES = {("gpt3-6.7b-tp4pp2-to-tp2pp2dp2", 1): 3, ("gpt3-6.7b-recovery", 1): 2}
+WIDTH_OF = {0: 4, 1: 2, 2: 8, 3: 1, 4: 2}  # dtype code -> bytes (F32, F16, I64, U8, BF16)
 # configs[4]: dataset index repartition of a 100M-sample corpus under DP 2 -> 4 -> 8
 DATASET = {"dataset-100m-dp2to4to8": dict(n=100_000_000, B=1280, seed=0x5EED, epoch=0, files=1000,
                                           per_file=100_000, sample_bytes=8206, events=[(25_000, 4), (50_000, 8)])}
@@ -196,9 +200,8 @@ def run_dataset(args, rs, dist=None):
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (100M-sample index, 1000 files)",
-        "config": {"workload": args.workload, "events": spec["events"], "B": spec["B"], "n": n,
-                   "l2": "inputs larger than L2 (no flush)",
-                   "index_layout": "padded 32-byte records" if eb == 32 else "packed 24-byte records"},
+        "config": workload_config(args.workload, args.gpus),
+        "index_layout": "padded 32-byte records" if eb == 32 else "packed 24-byte records",
         "index_pad_ms_once": None if pad_ms is None else round(pad_ms, 3),
         "samples_per_step": done, "gsamples_per_s": round(done / (ms * 1e-3) / 1e9, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -446,13 +449,51 @@ def build_plan(rs, name, n_gpus):
     return cat, a, b, plan, src_gpu, dst_gpu
 
 
+def workload_config(name: str, n_gpus: int, mode: str = "distributed") -> dict:
+    """The `config` both arms print for a workload (identical dicts: same_config)."""
+    if name in DATASET:
+        spec = DATASET[name]
+        return {"workload": name, "events": spec["events"], "B": spec["B"], "n": spec["n"], "n_gpus": n_gpus,
+                "placement": "new DP rank d on GPU d % n_gpus", "l2": "inputs larger than L2 (no flush)"}
+    _, (T1, P1, D1, devs1), (T2, P2, D2, devs2), failed = WORKLOADS[name]
+    return {"workload": name, "transition": f"(TP{T1},PP{P1},DP{D1})->(TP{T2},PP{P2},DP{D2})",
+            "failed_devices": failed, "logical_devices": max(len(devs1), len(devs2)), "n_gpus": n_gpus,
+            "placement": "logical device d on GPU d % n_gpus", "mode": mode, "l2": "inputs larger than L2 (no flush)"}
+
+
+def host_info() -> dict:
+    """CPU model, core count and RAM of this host (SURVEY §8d / BASELINE.md §3)."""
+    model, ram = None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+        with open("/proc/meminfo") as f:
+            kb = next(int(ln.split()[1]) for ln in f if ln.startswith("MemTotal"))
+        ram = round(kb / 2**20, 1)
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram}
+
+
+def host_available_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            return next(int(ln.split()[1]) for ln in f if ln.startswith("MemAvailable")) * 1024
+    except Exception:
+        return 0
+
+
 # ---------------------------------------------------------------------------------------
-def cpu_reference_leg(name: str, sample_frac: float, steps: int, warmup: int):
-    """The reference's CPU path on this host: SPEC-restated planner/executor over the
-    reference's own compiled slice()/merge() (oracle/_ref/libptc_ref.so), destination cells
-    drained by every host core (SPEC.md:504's per-destination tasks, split per cell), on a
-    bounded sample of the catalog.  Falls back to the
-    restated oracle (kind "port") when the reference build is absent."""
+def cpu_reference_run(name: str, steps: int, warmup: int, variants=("queue",), dst_budget_gb: float = 48.0) -> dict:
+    """The reference's CPU path on this host over the WHOLE workload: the SPEC-restated
+    planner/executor over the reference's own compiled slice()/merge() (oracle/_ref/libptc_ref.so;
+    the restated oracle, kind "port", when that build is absent).  The source state is filled once
+    (off the clock); the catalog is applied in windows whose destination state fits next to it in
+    host RAM (GPT-3 6.7B: SURVEY §8d's "stream per base tensor"), and a step's time is the sum of
+    the windows' apply times (steady_clock inside orc_apply: barrier 1 to barrier 2).
+    Variants: "queue" — every host core drains a shared (destination, tensor, cell) queue (the
+    headline); "per_device" — one thread per destination device (SPEC.md:504), capped at nproc;
+    "1thread" — one thread (one step)."""
     from oracle.oracle import Oracle, lib_path
 
     ref = os.path.exists(lib_path(True))
@@ -463,26 +504,58 @@ def cpu_reference_leg(name: str, sample_frac: float, steps: int, warmup: int):
     b = cat.build_strategy([(0, d) for d in devs2], T2, P2, D2)
     plan = a.plan(b, failed=[(0, d) for d in failed])
     st = plan.stats()
-    n_t = len(cat)
-    t1 = max(1, int(round(n_t * sample_frac)))
-    src = a.fill(0, t1)
+    ent = cat.entries()
+    per_t = []
+    for _, dt, shape, _, _ in ent:
+        n = WIDTH_OF[dt]
+        for e in shape:
+            n *= e
+        per_t.append(n)
+    ratio = st["dst_bytes"] / max(sum(per_t), 1)  # destination bytes per base byte
+    windows, t0, acc = [], 0, 0
+    for t, nb in enumerate(per_t):
+        if acc and (acc + nb) * ratio > dst_budget_gb * 1e9:
+            windows.append((t0, t))
+            t0, acc = t, 0
+        acc += nb
+    windows.append((t0, len(per_t)))
+    tf = time.perf_counter()
+    src = a.fill()
+    fill_s = time.perf_counter() - tf
     threads = os.cpu_count() or 1
-    times, sample_bytes = [], 0
-    for i in range(warmup + steps):
-        out, rep = plan.apply(src, n_threads=threads, t0=0, t1=t1)
-        del out
-        if i >= warmup:
-            times.append(rep["seconds"])
-            sample_bytes = rep["moved"] + rep["local"]
-    full_bytes = st["moved_bytes"] + st["relayout_bytes"]
-    scale = full_bytes / max(sample_bytes, 1)
-    ms = [t * 1e3 * scale for t in times]
+    n_dst_dev = len(devs2)
+
+    def one_step(n_threads, per_device):
+        secs, moved = 0.0, 0
+        for w0, w1 in windows:
+            out, rep = plan.apply(src, n_threads=n_threads, t0=w0, t1=w1, per_device=per_device)
+            del out
+            secs += rep["seconds"]
+            moved += rep["moved"] + rep["local"]
+        return secs * 1e3, moved
+
+    res = {}
+    for v in variants:
+        nt, pd, k, wu = {"queue": (threads, False, steps, warmup),
+                         "per_device": (min(threads, n_dst_dev), True, max(1, min(steps, 3)), 0),
+                         "1thread": (1, False, 1, 0)}[v]
+        ms = []
+        for i in range(wu + k):
+            t, moved = one_step(nt, pd)
+            if i >= wu:
+                ms.append(t)
+        res[v] = {"ms": round(statistics.mean(ms), 3), "threads": nt, "steps": k, "ms_samples": [round(x, 3) for x in ms],
+                  "copied_bytes": moved}
+    del src
+    head = res[variants[0]]
     return {
-        "value": statistics.mean(ms), "ms_samples": ms, "unit": "ms", "cores": threads,
+        "value": head["ms"], "ms_samples": head["ms_samples"], "unit": "ms", "cores": head["threads"],
         "kind": "reference" if ref else "port",
-        "sample": (f"tensors [0,{t1}) of {n_t} ({sample_bytes / 1e9:.2f} of {full_bytes / 1e9:.2f} GB moved), "
-                   f"time scaled by bytes; {threads} threads over destination cells; "
-                   f"host nproc={os.cpu_count()}"),
+        "sample": (f"full workload: all {len(per_t)} tensors, {head['copied_bytes'] / 1e9:.2f} GB copied per step "
+                   f"in {len(windows)} catalog window(s) over one filled source state; "
+                   f"{head['threads']} threads draining destination cells"),
+        "variants": res, "host": host_info(), "fill_s_once": round(fill_s, 2),
+        "plan": {k: st[k] for k in ("n_move", "n_merge", "moved_bytes", "relayout_bytes")},
     }
 
 
@@ -507,9 +580,10 @@ def run_reference(args):
             if i >= args.warmup:
                 ms.append(secs * 1e3)
         leg = {"value": statistics.mean(ms), "cores": threads, "kind": "port",
-               "sample": f"full workload, restated gather (oracle.cpp orc_dataset_gather), {threads} threads"}
+               "sample": f"full workload, restated gather (oracle.cpp orc_dataset_gather), {threads} threads",
+               "host": host_info()}
     else:
-        leg = cpu_reference_leg(args.workload, args.sample_frac, args.steps, args.warmup)
+        leg = cpu_reference_run(args.workload, args.steps, args.warmup, variants=("queue",))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(leg["value"], 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(leg["value"], 3),
@@ -517,15 +591,97 @@ def run_reference(args):
         "dtype": "u64" if args.workload in DATASET else "u8",
         "data": "synthetic (100M-sample index, 1000 files)" if args.workload in DATASET
         else "synthetic (splitmix64 payload of the model shapes)",
-        "config": {"workload": args.workload, "parallelism": "cpu"},
+        "config": workload_config(args.workload, args.gpus, args.mode),
         "cpu_baseline": {"value": round(leg["value"], 3), "unit": "ms", "cores": leg["cores"], "kind": leg["kind"],
-                         "sample": leg["sample"]},
+                         "sample": leg["sample"], "host": leg["host"]},
         "e2e": {"value": round(leg["value"], 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------------------
+def gpu_map(rs, n_gpus: int):
+    """World GPU -> CUDA device for a single-process N-GPU world: one device per world GPU when
+    the box has N, else (RESHARD_SAME_GPU=1) every world GPU on cuda:0 — the correctness
+    emulation of an N-GPU world on one device (its peer stores are local stores)."""
+    n = rs.device_count()
+    if n >= n_gpus:
+        return list(range(n_gpus)), False
+    if os.environ.get("RESHARD_SAME_GPU"):
+        return [0] * n_gpus, True
+    raise SystemExit(f"--gpus {n_gpus}: {n} CUDA device(s) visible (RESHARD_SAME_GPU=1 emulates the world on cuda:0)")
+
+
+def windows_of(cat, waves: int):
+    """Catalog windows of ~equal bytes (waves: executed one after another over reused arenas)."""
+    ent = cat.entries()
+    per_t = []
+    for e in ent:
+        n = WIDTH_OF[e[1]]
+        for x in e[2]:
+            n *= x
+        per_t.append(n)
+    total_b, bounds, acc = sum(per_t), [0], 0
+    for t, nb in enumerate(per_t):
+        acc += nb
+        if len(bounds) < waves and acc >= total_b * len(bounds) / waves:
+            bounds.append(t + 1)
+    bounds.append(len(ent))
+    return [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
+
+
+def p2p_probe(rs, ctx, cuda_of, nbytes: int = 1 << 30, reps: int = 3) -> dict:
+    """Measured NVLink peer bandwidth on this box (off the clock; distinct GPUs only).
+    pair_sm: our K1 LDG/STG kernel on GPU 0 storing 1 GiB into GPU 1's memory (rs_broadcast,
+    SM stores over NVLink); pair_ce / ring_ce: copy-engine peer copies (torch), GPU 0 -> 1 alone
+    and every GPU -> the next one at once.  `peak` = the best per-GPU one-way rate seen."""
+    import torch
+
+    n = len(cuda_of)
+    out = {"probe_bytes": nbytes}
+    src = ctx.malloc(0, nbytes)
+    dst = ctx.malloc(1, nbytes)
+    old = os.environ.get("RESHARD_COPY_KERNEL")
+    os.environ["RESHARD_COPY_KERNEL"] = "ldg"
+    try:
+        ms = min(rs.broadcast(ctx, 0, src, [dst], nbytes)["ms"] for _ in range(reps))
+        out["pair_sm_gbs"] = round(nbytes / (ms * 1e-3) / 1e9, 1)
+    finally:
+        if old is None:
+            os.environ.pop("RESHARD_COPY_KERNEL", None)
+        else:
+            os.environ["RESHARD_COPY_KERNEL"] = old
+        ctx.free(0, src)
+        ctx.free(1, dst)
+    bufs = [(torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{c}"),
+             torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{c}")) for c in cuda_of]
+
+    def timed(pairs):
+        best = float("inf")
+        for _ in range(reps):
+            for c in cuda_of:
+                torch.cuda.synchronize(c)
+            ev = []
+            for s, d in pairs:
+                with torch.cuda.device(cuda_of[s]):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    bufs[d][1].copy_(bufs[s][0], non_blocking=True)
+                    e1.record()
+                ev.append((e0, e1))
+            for c in cuda_of:
+                torch.cuda.synchronize(c)
+            best = min(best, max(a.elapsed_time(b) for a, b in ev))
+        return best
+
+    out["pair_ce_gbs"] = round(nbytes / (timed([(0, 1)]) * 1e-3) / 1e9, 1)
+    out["ring_ce_gbs_per_gpu"] = round(nbytes / (timed([(g, (g + 1) % n) for g in range(n)]) * 1e-3) / 1e9, 1)
+    del bufs
+    torch.cuda.empty_cache()
+    out["peak"] = max(out["pair_sm_gbs"], out["pair_ce_gbs"], out["ring_ce_gbs_per_gpu"])
+    return out
+
+
 def run_ours(args):
     import paper_2312_05181_b200 as rs
 
@@ -546,140 +702,195 @@ def run_ours(args):
     if args.workload in DATASET:
         return run_dataset(args, rs, dist)
     cat, a, b, plan, src_gpu, dst_gpu = build_plan(rs, args.workload, N)
-    ctx = rs.Context(N, [rank], [local])
-    # waves: catalog windows of ~equal bytes executed one after another over reused arenas
-    # (a plan larger than the world's HBM, e.g. GPT-3 6.7B on one GPU)
-    waves = max(1, args.waves if args.waves else WAVES.get((args.workload, N), 1))
-    ent = cat.entries()
-    per_t = [rs.WIDTH[e[1]] * int(__import__("math").prod(e[2])) for e in ent]
-    total_b, bounds, acc = sum(per_t), [0], 0
-    for t, nb in enumerate(per_t):
-        acc += nb
-        if len(bounds) < waves and acc >= total_b * len(bounds) / waves:
-            bounds.append(t + 1)
-    bounds.append(len(ent))
-    windows = [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
-    t_lower = time.perf_counter()
-    if args.mode == "central":  # apply_plan(central): one process drives the world, staging on GPU 0
-        if world > 1 or len(windows) > 1:
-            raise SystemExit("--mode central: single-process, single-wave workloads only")
-        exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10, central=0)]
+    # the world GPUs this process drives: its own (one process per GPU, torchrun), or all N
+    if world > 1:
+        mine, cuda_of, emulated = [rank], [local], bool(os.environ.get("RESHARD_SAME_GPU"))
     else:
-        exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, args.tile_kib << 10, window=w if len(windows) > 1 else None)
-               for w in windows]
-    lower_ms = (time.perf_counter() - t_lower) * 1e3  # arena layout + fragments -> tiles (host)
-    s_bytes = max(e.arena_bytes(rank)[0] for e in exs)
-    d_bytes = max(e.arena_bytes(rank)[1] for e in exs)
-    src_ptr, dst_ptr = ctx.malloc(rank, max(s_bytes, 256)), ctx.malloc(rank, max(d_bytes, 256))
-    for ex in exs:
-        ex.bind(rank, src_ptr, dst_ptr)
-    opened = []
+        mine = list(range(N))
+        cuda_of, emulated = gpu_map(rs, N)
+    ctx = rs.Context(N, mine, cuda_of)
+    tile = args.tile_kib << 10
+
+    # waves: the fewest catalog windows whose arenas fit each CUDA device (180 GB HBM3e each)
+    import torch
+
+    budget = {}
+    for c in set(cuda_of):
+        free, _ = torch.cuda.mem_get_info(c)
+        budget[c] = int(free * 0.92) // (N if (world > 1 and emulated) else 1)
+    pctx = rs.Context(N, [], [])  # planning-only view: layouts, no device work
+    windows, s_need, d_need = None, None, None
+    for waves in ([args.waves] if args.waves else range(1, 9)):
+        wins = windows_of(cat, waves)
+        pexs = [rs.Executor(pctx, plan, src_gpu, dst_gpu, tile, window=w if len(wins) > 1 else None) for w in wins]
+        s_need = {g: max(p.arena_bytes(g)[0] for p in pexs) for g in mine}
+        d_need = {g: max(p.arena_bytes(g)[1] for p in pexs) for g in mine}
+        per_dev = {}
+        for g, c in zip(mine, cuda_of):
+            per_dev[c] = per_dev.get(c, 0) + s_need[g] + d_need[g]
+        del pexs
+        windows = wins
+        if all(per_dev[c] <= budget[c] for c in per_dev):
+            break
+    if args.mode == "central" and (world > 1 or len(windows) > 1):
+        raise SystemExit("--mode central: single-process, single-wave workloads only")
+    t_lower = time.perf_counter()
+    if args.mode == "central":
+        exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, tile, central=0)]
+    else:
+        exs = [rs.Executor(ctx, plan, src_gpu, dst_gpu, tile, window=w if len(windows) > 1 else None) for w in windows]
+    lower_ms = (time.perf_counter() - t_lower) * 1e3  # arena layout + fragments -> pieces (host)
+    src_ptr, dst_ptr = {}, {}
+    for g in mine:
+        s_b = max(e.arena_bytes(g)[0] for e in exs)
+        d_b = max(e.arena_bytes(g)[1] for e in exs)
+        s_need[g], d_need[g] = s_b, d_b
+        src_ptr[g], dst_ptr[g] = ctx.malloc(g, max(s_b, 256)), ctx.malloc(g, max(d_b, 256))
+        for ex in exs:
+            ex.bind(g, src_ptr[g], dst_ptr[g])
     if dist is not None:
         # destination arenas of every GPU, mapped into this process (CUDA IPC over NVLink)
-        mine = ctx.ipc_handle(rank, dst_ptr) if d_bytes else None
+        handle = ctx.ipc_handle(rank, dst_ptr[rank]) if d_need[rank] else None
         handles = [None] * world
-        dist.all_gather_object(handles, mine)
+        dist.all_gather_object(handles, handle)
         for g in range(world):
             if g != rank and handles[g] is not None:
                 p = ctx.ipc_open(rank, handles[g])
-                opened.append(p)
                 for ex in exs:
                     ex.bind(g, 0, p)
     t_prep = time.perf_counter()
     for ex in exs:
-        ex.prepare()  # lower fragments to tiles, upload the descriptors once
+        ex.prepare()  # bind bases into the pieces, upload them; the GPU expands them into tiles
     prepare_ms = (time.perf_counter() - t_prep) * 1e3
     if len(exs) == 1:
         exs[0].fill_sources()
     stats = plan.stats()
-    tiles = sum(ex.tiles(rank)[0] for ex in exs)
-    copy_bytes = sum(ex.tiles(rank)[1] for ex in exs)  # bytes written
-    read_bytes = sum(ex.read_bytes(rank) for ex in exs)  # bytes read (fan-out tiles read once)
-    # this rank's egress row of the fragment all-to-all (entry `rank`: its local writes)
-    row = [sum(v) for v in zip(*(ex.bytes_to(rank) for ex in exs))] if world > 1 else None
 
     def barrier():
-        ctx.sync(rank)
+        for g in mine:
+            ctx.sync(g)
         if dist is not None:
             dist.barrier()
 
     def step(verify=False):
-        ms, bad, launches = 0.0, 0, 0
+        """One reshard: every wave from a barrier (every GPU idle, every rank here), timed from
+        one common start to the last GPU's completion (single process: world events; one
+        process per GPU: this GPU's events, max over ranks afterwards)."""
+        ms, gpu_ms, bad, launches = 0.0, 0.0, 0, 0
         for ex in exs:
             if len(exs) > 1:
-                ex.fill_sources()  # the window's sources (off the clock: events bracket the kernel only)
-            t = ex.apply()[0]
-            ms, launches = ms + t["ms"], launches + t["launches"]
+                ex.fill_sources()  # the window's sources (off the clock)
+            barrier()
+            ex.run()
+            t = ex.wait()
+            ms += ex.world_ms()
+            gpu_ms += max(x["ms"] for x in t)
+            launches += sum(x["launches"] for x in t)
             if verify and len(exs) > 1:
+                barrier()  # every peer's pushes of this wave landed before anyone checks it
                 bad += ex.verify()
-        return ms, bad, launches
+        return ms, gpu_ms, bad, launches
 
     for _ in range(args.warmup):
         step()
     barrier()
-    step_ms, launches_total = [], 0
-    with ClockSampler(local) as clocks:
+    step_ms, gpu_step_ms, launches_total, bad_w = [], [], 0, 0
+    with ClockSampler(cuda_of[0]) as clocks:
         t0 = time.perf_counter()
         for i in range(args.steps):
-            ms_i, bad_w, l_i = step(verify=(i == args.steps - 1))
+            ms_i, g_i, b_i, l_i = step(verify=(i == args.steps - 1))
             step_ms.append(ms_i)
+            gpu_step_ms.append(g_i)
             launches_total += l_i
+            bad_w += b_i
         barrier()
         wall = time.perf_counter() - t0
-    total_ms = sum(step_ms)
-    if dist is not None:
-        import torch
-
-        t = torch.tensor([total_ms], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms = total_ms / args.steps
+    if dist is not None:  # per step: the slowest rank (each rank's steps start at a common barrier)
+        dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
+        tt = torch.tensor(step_ms + [float(launches_total)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt[:-1], op=dist.ReduceOp.MAX)
+        step_ms = [float(x) for x in tt[:-1].tolist()]
+        gpu_step_ms = list(step_ms)
+        lt = torch.tensor([float(launches_total)], dtype=torch.float64, device=dev)
+        dist.all_reduce(lt)
+        launches_total = int(lt.item())
+    ms = statistics.mean(step_ms)
     bad = exs[0].verify() if len(exs) == 1 else bad_w
-    ex = exs[0]
     if dist is not None:
-        import torch
+        tb = torch.tensor([bad], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu", dtype=torch.int64)
+        dist.all_reduce(tb)
+        bad = int(tb.item())
 
-        t = torch.tensor([bad], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu", dtype=torch.int64)
-        dist.all_reduce(t)
-        bad = int(t.item())
+    # the all-to-all: bytes each GPU's tiles write into every GPU, and the bytes they read
+    rows = [[0] * N for _ in range(N)]
+    rbs = [0] * N
+    for g in mine:
+        rows[g] = [sum(v) for v in zip(*(ex.bytes_to(g) for ex in exs))]
+        rbs[g] = sum(ex.read_bytes(g) for ex in exs)
+    if dist is not None:
+        dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
+        m = torch.tensor(rows, dtype=torch.float64, device=dev)
+        rb = torch.tensor(rbs, dtype=torch.float64, device=dev)
+        dist.all_reduce(m)
+        dist.all_reduce(rb)
+        rows = [[int(x) for x in r] for r in m.cpu().tolist()]
+        rbs = [int(x) for x in rb.cpu().tolist()]
 
-    # e2e through the C-ABI with host buffers (single-GPU world)
+    # e2e through the C-ABI with host buffers
+    ex = exs[0]
     e2e = None
     if len(exs) > 1:
-        e2e = {"value": None, "unit": "ms", "note": "waves: host-buffer path not run (state exceeds one GPU)"}
-    elif world == 1 and not args.no_e2e:
-        try:
-            hs, hd = rs.host_alloc(s_bytes), rs.host_alloc(max(d_bytes, 1))
-            ctx.dtoh(0, hs, src_ptr, s_bytes)
-            for _ in range(1):
-                ex.run_host(0, hs, hd)
-            e2e_ms = [ex.run_host(0, hs, hd)["ms"] for _ in range(args.e2e_steps)]
-            bad_e2e = ex.verify()
-            rs.host_free(hs)
-            rs.host_free(hd)
-            e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms", "h2d_bytes_per_step": s_bytes,
-                   "d2h_bytes_per_step": d_bytes - ex.staging_bytes(), "steps": args.e2e_steps,
-                   "mismatched_bytes": bad_e2e}
-            try:  # the PCIe bound of this path, measured on the same box
-                link = pcie_probe()
-                d_eff = d_bytes - ex.staging_bytes()
-                if args.mode == "central":  # H2D, both phases, D2H in sequence (no chunk pipeline)
-                    bound_ms = (s_bytes / (link["h2d_gbs"] * 1e9) + d_eff / (link["d2h_gbs"] * 1e9)) * 1e3
-                else:  # chunk pipeline: both directions at once
-                    bound_ms = max(s_bytes / (link["h2d_gbs"] * 1e9), d_eff / (link["d2h_gbs"] * 1e9),
-                                   max(s_bytes, d_eff) / (link["bidir_gbs_each"] * 1e9)) * 1e3
-                e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
-                                   "frac": round(bound_ms / e2e["value"], 4)}
-            except Exception as exc:
-                e2e["roofline"] = {"error": str(exc)[:200]}
-        except Exception as exc:  # e.g. not enough pinned host memory
-            e2e = {"value": None, "unit": "ms", "h2d_bytes_per_step": s_bytes, "d2h_bytes_per_step": d_bytes,
-                   "error": str(exc)[:200]}
-    elif world > 1 and not args.no_e2e:
-        # every rank: H2D of its src arena | barrier | push kernels | barrier | D2H of its dst
-        # arena; CUDA events mark to mark on each rank's stream, max over ranks
-        hs, hd = rs.host_alloc(max(s_bytes, 1)), rs.host_alloc(max(d_bytes, 1))
-        ctx.dtoh(rank, hs, src_ptr, s_bytes)
+        e2e = {"value": None, "unit": "ms", "note": "waves: host-buffer path not run (state exceeds the GPUs' HBM)"}
+    elif args.no_e2e:
+        e2e = None
+    elif world == 1:
+        total_host = sum(s_need.values()) + sum(d_need.values())
+        if total_host > 0.6 * host_available_bytes():
+            e2e = {"value": None, "unit": "ms", "note": f"host buffers of {total_host / 1e9:.1f} GB exceed 60% of host RAM"}
+        else:
+            hs = {g: rs.host_alloc(max(s_need[g], 1)) for g in mine}
+            hd = {g: rs.host_alloc(max(d_need[g], 1)) for g in mine}
+            try:
+                for g in mine:
+                    ctx.dtoh(g, hs[g], src_ptr[g], s_need[g])
+                if N == 1:  # one GPU: the chunk-pipelined host path (H2D | kernels | D2H overlapped)
+                    ex.run_host(0, hs[0], hd[0])
+                    e2e_ms = [ex.run_host(0, hs[0], hd[0])["ms"] for _ in range(args.e2e_steps)]
+                    path = "rs_executor_run_host: chunk-pipelined H2D | copy kernel | D2H, pinned host buffers"
+                else:  # all GPUs from one common start: H2D | world barrier | kernels | barrier | D2H
+                    hs_l, hd_l = [hs[g] for g in range(N)], [hd[g] for g in range(N)]
+                    ex.run_host_world(hs_l, hd_l)
+                    e2e_ms = [ex.run_host_world(hs_l, hd_l) for _ in range(args.e2e_steps)]
+                    path = "rs_executor_run_host_world: H2D of every src arena | kernels | D2H of every dst arena"
+                bad_e2e = ex.verify()
+                d_eff = sum(d_need.values()) - ex.staging_bytes()
+                e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms",
+                       "h2d_bytes_per_step": sum(s_need.values()), "d2h_bytes_per_step": d_eff,
+                       "steps": args.e2e_steps, "mismatched_bytes": bad_e2e, "path": path}
+                if N == 1:
+                    try:  # the PCIe bound of this path, measured on the same box
+                        link = pcie_probe()
+                        if args.mode == "central":  # H2D, both phases, D2H in sequence (no chunk pipeline)
+                            bound_ms = (s_need[0] / (link["h2d_gbs"] * 1e9) + d_eff / (link["d2h_gbs"] * 1e9)) * 1e3
+                        else:  # chunk pipeline: both directions at once
+                            bound_ms = max(s_need[0] / (link["h2d_gbs"] * 1e9), d_eff / (link["d2h_gbs"] * 1e9),
+                                           max(s_need[0], d_eff) / (link["bidir_gbs_each"] * 1e9)) * 1e3
+                        e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
+                                           "frac": round(bound_ms / e2e["value"], 4)}
+                    except Exception as exc:
+                        e2e["roofline"] = {"error": str(exc)[:200]}
+            except Exception as exc:  # e.g. not enough pinned host memory
+                e2e = {"value": None, "unit": "ms", "h2d_bytes_per_step": sum(s_need.values()),
+                       "d2h_bytes_per_step": sum(d_need.values()), "error": str(exc)[:200]}
+            finally:
+                for g in mine:
+                    rs.host_free(hs[g])
+                    rs.host_free(hd[g])
+    else:
+        # one process per GPU: H2D of its src arena | barrier | push kernels | barrier | D2H of
+        # its dst arena; CUDA events mark to mark on each rank's stream, max over ranks
+        hs, hd = rs.host_alloc(max(s_need[rank], 1)), rs.host_alloc(max(d_need[rank], 1))
+        ctx.dtoh(rank, hs, src_ptr[rank], s_need[rank])
         e2e_ms = []
         for i in range(1 + args.e2e_steps):
             ex.host_phase(rank, 0, hs)
@@ -689,104 +900,138 @@ def run_ours(args):
             ex.host_phase(rank, 2, hd)
             if i:
                 e2e_ms.append(ex.host_elapsed(rank))
-        import torch
-
-        t = torch.tensor([statistics.mean(e2e_ms)], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
+        dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
+        t = torch.tensor([statistics.mean(e2e_ms)], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        totals = torch.tensor([s_bytes, d_bytes], dtype=torch.int64,
-                              device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
+        totals = torch.tensor([s_need[rank], d_need[rank]], dtype=torch.int64, device=dev)
         dist.all_reduce(totals)
         rs.host_free(hs)
         rs.host_free(hd)
         e2e = {"value": round(float(t.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(totals[0].item()),
                "d2h_bytes_per_step": int(totals[1].item()), "steps": args.e2e_steps,
-               "note": "per rank: H2D | barrier | kernels | barrier | D2H, max over ranks"}
+               "path": "per rank: H2D | barrier | kernels | barrier | D2H (rs_executor_host_phase), max over ranks"}
+
+    # NVLink peak measured on this box (distinct GPUs only), else the NVLink 5 spec
+    p2p = None
+    if world == 1 and N > 1 and not emulated and not args.no_p2p_probe:
+        try:
+            p2p = p2p_probe(rs, ctx, cuda_of)
+        except Exception as exc:  # noqa: BLE001
+            p2p = {"error": str(exc)[:200]}
+    bw_nvl = p2p["peak"] if p2p and "peak" in p2p else 900.0
+    bw_nvl_kind = "measured (p2p_probe)" if p2p and "peak" in p2p else "spec (NVLink 5: 900 GB/s per direction)"
+    peak, peak_kind = measured_peaks()
+
+    def fabric_of(rows, rbs, n, bw_link):
+        """T_roof = max_g max(in_g / BW_nvl, out_g / BW_nvl, hbm_g / BW_hbm)."""
+        t_roof, worst, terms = 0.0, None, []
+        for g in range(n):
+            out_g = sum(rows[g][w] for w in range(n) if w != g)
+            in_g = sum(rows[r][g] for r in range(n) if r != g)
+            hbm_g = rbs[g] + sum(rows[r][g] for r in range(n))  # reads of its tiles + every write landing in it
+            terms.append((out_g, in_g, hbm_g))
+            for kind, t in (("nvlink_out", out_g / bw_link), ("nvlink_in", in_g / bw_link), ("hbm", hbm_g / peak)):
+                if t / 1e6 > t_roof:
+                    t_roof, worst = t / 1e6, {"gpu": g, "term": kind}
+        return t_roof, worst, terms
 
     fabric = None
-    if world == 1 and len(exs) >= 1:  # derived: the same plan over its own GPU count (no such box here)
+    if N == 1:  # derived: the same plan over its own GPU count (no such box here)
         n_native = max(len(WORKLOADS[args.workload][1][3]), len(WORKLOADS[args.workload][2][3]))
         if n_native > 1:
-            pctx = rs.Context(n_native, [], [])  # planning-only: layouts and tiles, no device
             _, _, _, nplan, nsrc, ndst = build_plan(rs, args.workload, n_native)
-            pex = rs.Executor(pctx, nplan, nsrc, ndst, args.tile_kib << 10)
-            rows = [pex.bytes_to(g) for g in range(n_native)]
-            rbs = [pex.read_bytes(g) for g in range(n_native)]
-            bw_hbm = measured_peaks()[0]
-            t_roof, worst = 0.0, None
-            for g in range(n_native):
-                out_g = sum(rows[g][w] for w in range(n_native) if w != g)
-                in_g = sum(rows[r][g] for r in range(n_native) if r != g)
-                hbm_g = rbs[g] + sum(rows[r][g] for r in range(n_native))
-                for kind, t in (("nvlink_out", out_g / 900.0), ("nvlink_in", in_g / 900.0), ("hbm", hbm_g / bw_hbm)):
-                    if t / 1e6 > t_roof:
-                        t_roof, worst = t / 1e6, {"gpu": g, "term": kind}
+            pex = rs.Executor(rs.Context(n_native, [], []), nplan, nsrc, ndst, tile)
+            t_roof, worst, _ = fabric_of([pex.bytes_to(g) for g in range(n_native)],
+                                         [pex.read_bytes(g) for g in range(n_native)], n_native, 900.0)
             fabric = {"derived_for_gpus": n_native, "t_roof_ms": round(t_roof, 3), "bottleneck": worst,
                       "note": "not measured: SURVEY 8d's T_roof of this plan on its own GPU count (NVLink 900 GB/s "
                               "per direction, measured HBM peak), for comparison with the 1-GPU emulation above"}
-    if world > 1:  # T_roof = max_g max(in_g / BW_nvl, out_g / BW_nvl, hbm_g / BW_hbm)
-        import torch
-
-        dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
-        m = torch.zeros(world, world, dtype=torch.float64, device=dev)
-        m[rank] = torch.tensor([float(x) for x in row], dtype=torch.float64, device=dev)
-        rb = torch.zeros(world, dtype=torch.float64, device=dev)
-        rb[rank] = float(read_bytes)
-        dist.all_reduce(m)
-        dist.all_reduce(rb)
-        m, rb = m.cpu().tolist(), rb.cpu().tolist()
-        bw_nvl, (bw_hbm, _) = 900.0, measured_peaks()  # GB/s per direction (NVLink 5 spec), measured HBM
-        t_roof, worst = 0.0, None
-        for g in range(world):
-            out_g = sum(m[g][w] for w in range(world) if w != g)
-            in_g = sum(m[r][g] for r in range(world) if r != g)
-            hbm_g = rb[g] + sum(m[r][g] for r in range(world))  # reads of its tiles + every write landing in it
-            for kind, t in (("nvlink_out", out_g / bw_nvl), ("nvlink_in", in_g / bw_nvl), ("hbm", hbm_g / bw_hbm)):
-                if t / 1e6 > t_roof:
-                    t_roof, worst = t / 1e6, {"gpu": g, "term": kind}
-        fabric = {"t_roof_ms": round(t_roof, 3), "frac": round(t_roof / ms, 4) if ms else None, "bottleneck": worst,
-                  "bw_nvlink_gbs": bw_nvl, "bw_nvlink_kind": "spec (900 GB/s per direction; no measured P2P peak)",
-                  "max_egress_gb": round(max(sum(m[g][w] for w in range(world) if w != g) for g in range(world)) / 1e9, 3),
-                  "max_ingress_gb": round(max(sum(m[r][g] for r in range(world) if r != g) for g in range(world)) / 1e9, 3)}
-    kname = copy_kernel_name()
-    # the committed ncu capture is of the one-GPU launch; a rank of a larger world launches a share of it
-    traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" and world == 1 else None
+    else:
+        t_roof, worst, terms = fabric_of(rows, rbs, N, bw_nvl)
+        fabric = {"t_roof_ms": round(t_roof, 3), "frac": round(t_roof / ms, 4) if ms and not emulated else None,
+                  "bottleneck": worst, "bw_nvlink_gbs": bw_nvl, "bw_nvlink_kind": bw_nvl_kind, "p2p_probe": p2p,
+                  "max_egress_gb": round(max(t[0] for t in terms) / 1e9, 3),
+                  "max_ingress_gb": round(max(t[1] for t in terms) / 1e9, 3),
+                  "max_hbm_gb": round(max(t[2] for t in terms) / 1e9, 3)}
+        if emulated:
+            fabric["note"] = ("RESHARD_SAME_GPU: every world GPU on cuda:0 (peer stores are local stores); "
+                              "T_roof is the plan's on N real GPUs, not comparable with this time")
     if rank != 0:
         return
-    peak, peak_kind = measured_peaks()
-    # roofline of the dominant (only) kernel: HBM read + write of every copied byte
-    alg_bytes = read_bytes + copy_bytes
-    achieved = alg_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9
+    writes = sum(sum(r) for r in rows)
+    reads = sum(rbs)
+    kname = copy_kernel_name()
+    if N == 1 or emulated:
+        # every byte on one device: HBM read + write of every copied byte over the step time
+        achieved = (reads + writes) / (ms * 1e-3) / 1e9
+        traffic = ncu_traffic(args.workload, kname) if args.mode == "distributed" and N == 1 else None
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind, "peak_how": peak_how(),
+                    "kernel": kname, "algorithmic_bytes_per_step": reads + writes,
+                    "launches_per_step": launches_total // max(args.steps, 1)}
+        if emulated:
+            roofline["note"] = f"{N} world GPUs emulated on cuda:0: the whole all-to-all is HBM traffic of one device"
+    else:
+        # the fabric: the busiest GPU's NVLink direction over the world time
+        _, _, terms = fabric_of(rows, rbs, N, bw_nvl)
+        link = max(max(t[0], t[1]) for t in terms)
+        hbm_max = max(t[2] for t in terms)
+        achieved = link / (ms * 1e-3) / 1e9
+        roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": bw_nvl, "unit": "GB/s",
+                    "frac": round(achieved / bw_nvl, 4), "traffic": None, "peak_kind": bw_nvl_kind,
+                    "kernel": kname + " + copy_fan_v16_kernel / copy_v16_kernel (peer stores)",
+                    "algorithmic_bytes_per_step": {"busiest_link": link, "all_writes": writes, "all_reads": reads},
+                    "hbm": {"achieved": round(hbm_max / (ms * 1e-3) / 1e9, 1), "peak": peak,
+                            "frac": round(hbm_max / (ms * 1e-3) / 1e9 / peak, 4)},
+                    "launches_per_step": launches_total // max(args.steps, 1)}
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 payload of the model shapes)",
-        "config": {"workload": args.workload, "parallelism": f"{N} GPU" + ("s" if N > 1 else "") +
-                   (" (1-GPU emulation of all logical devices)" if N == 1 else ", logical device d on GPU d%N"),
-                   "l2": "inputs larger than L2 (no flush)", "tile_kib": args.tile_kib, "mode": args.mode},
+        "config": workload_config(args.workload, N, args.mode),
+        "timing": ("one process: common start event on GPU 0, every GPU waits on it, GPU 0 joins every GPU's end"
+                   if world == 1 else "one process per GPU: per-step barrier, each rank's events, max over ranks"),
+        "ms_max_gpu_kernel": round(statistics.mean(gpu_step_ms), 4),
+        "emulated_on_one_gpu": emulated if N > 1 else None,
         "effective_gbs": round((stats["moved_bytes"] + stats["relayout_bytes"]) / (ms * 1e-3) / 1e9, 1),
         "fabric": fabric,
         "moved_bytes": stats["moved_bytes"], "relayout_bytes": stats["relayout_bytes"],
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind, "peak_how": peak_how(),
-                     "kernel": kname,
-                     "algorithmic_bytes_per_launch": alg_bytes // max(1, launches_total // max(args.steps, 1)),
-                     "launches_per_step": launches_total // max(args.steps, 1)},
+        "roofline": roofline,
         "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs),
         "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "wall_s": round(wall, 4),
-        "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4), "tiles": tiles,
+        "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4),
+        "tiles": sum(ex.tiles(g)[0] for ex in exs for g in mine),
         "host_ms": {"plan": round(build_plan.plan_ms, 2), "lower": round(lower_ms, 2), "prepare": round(prepare_ms, 2),
-                    "note": "off the clock, once per reconfiguration: Alg. 1 planning, arena layout + tile "
-                            "lowering, descriptor binding + upload"},
+                    "note": "off the clock, once per reconfiguration: Alg. 1 planning, arena layout + piece "
+                            "lowering, descriptor binding + upload + device expansion"},
     }
     if N == 1 and not args.no_cpu_baseline:
         try:
-            leg = cpu_reference_leg(args.workload, args.sample_frac, 3, 1)
-            line["cpu_baseline"] = {"value": round(leg["value"], 3), "unit": "ms", "cores": leg["cores"],
-                                    "kind": leg["kind"], "sample": leg["sample"]}
+            variants = ["queue", "per_device"] + (["1thread"] if stats["moved_bytes"] < 40e9 else [])
+            leg = cpu_reference_run(args.workload, 2, 1, variants=variants)
+            line["cpu_baseline"] = {"value": leg["value"], "unit": "ms", "cores": leg["cores"], "kind": leg["kind"],
+                                    "sample": leg["sample"], "variants": leg["variants"], "host": leg["host"]}
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args) -> None:
+    """`--gpus N` with no launcher on a per-rank path (the dataset workload): re-exec this
+    command under torch.distributed.run, one process per GPU (gloo when RESHARD_SAME_GPU puts
+    every rank on cuda:0)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    if env.get("RESHARD_SAME_GPU"):
+        env.setdefault("RESHARD_DIST_BACKEND", "gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execvpe(sys.executable, cmd, env)
 
 
 def main():
@@ -800,15 +1045,17 @@ def main():
     ap.add_argument("--mode", choices=["distributed", "central"], default="distributed",
                     help="apply_plan mode (SPEC.md:466): central stages every moved fragment on GPU 0")
     ap.add_argument("--waves", type=int, default=0, help="catalog windows run one after another (0: automatic)")
-    ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-p2p-probe", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.workload in DATASET:
+        relaunch_under_torchrun(args)
     else:
         run_ours(args)
 

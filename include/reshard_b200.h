@@ -247,6 +247,16 @@ int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src_arena, vo
  * its stream work completes.  rs_executor_host_elapsed: event time mark to mark. */
 int rs_executor_host_phase(rs_executor* e, int gpu, int phase, void* host_buf);
 int rs_executor_host_elapsed(rs_executor* e, int gpu, float* ms);
+/* World time of the last rs_executor_wait: from one common start mark (recorded on the first
+ * local GPU, waited on by every other local GPU before its kernels) to the end of the last local
+ * GPU's kernels, peer pushes included (single-process multi-GPU worlds; = the GPU's own time
+ * for one local GPU).  Replaces SPEC.md:501's "timestamps across all participating workers". */
+int rs_executor_world_ms(const rs_executor* e, float* ms);
+/* End to end through host buffers over every local GPU of a single-process world: H2D of every
+ * src arena (all GPUs at once), world barrier, every GPU's kernels, world barrier, D2H of every
+ * dst arena; *ms from the common start to the last D2H.  host_src / host_dst: n = world
+ * entries, indexed by world GPU (entries of non-local GPUs are ignored). */
+int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_src, void* const* host_dst, float* ms);
 int rs_executor_fill_sources(rs_executor* e);
 int rs_executor_verify(rs_executor* e, uint64_t* mismatched_bytes);
 /* bindings: src cells in (from-device, tensor, cell) order; dst cells in plan order */

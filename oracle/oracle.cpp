@@ -899,7 +899,11 @@ struct ApplyReport {
 };
 
 // apply_plan, distributed mode.
-static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1, int n_threads, ApplyReport* rep) {
+// per_device: SPEC.md:504 literally — one task per destination device, i.e. thread k runs the
+// cells of destination devices k, k + nt, ... in order (nt = min(n_threads, devices)); else any
+// thread takes the next (destination, tensor, cell) from a shared queue.
+static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1, int n_threads, ApplyReport* rep,
+                        bool per_device = false) {
   const Ptc& a = *plan.a;
   const Ptc& b = *plan.b;
   // (dst, tensor, fragment) -> source, from the plan's Moves
@@ -916,12 +920,13 @@ static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1
   // number of host threads drain it (the CPU arm uses every core it has).
   struct Task {
     const Dev* dst;
-    size_t t, i;
+    size_t t, i, dev;
   };
   std::vector<Task> tasks;
-  for (auto& r2 : b.devices)
-    for (auto [t, i] : hosted(b, r2))
-      if (in_range(t, t0, t1)) tasks.push_back({&r2, t, i});
+  for (size_t k = 0; k < b.devices.size(); ++k)
+    for (auto [t, i] : hosted(b, b.devices[k]))
+      if (in_range(t, t0, t1)) tasks.push_back({&b.devices[k], t, i, k});
+  const int nt = std::max(1, std::min<int>(n_threads, int(per_device ? b.devices.size() : tasks.size())));
   std::map<Dev, std::mutex> store_mu;
   for (auto& d : b.devices) store_mu[d];
   std::atomic<size_t> next{0};
@@ -930,10 +935,16 @@ static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1
   std::mutex em;
   // barrier 1: every source store is complete before any fetch.
   auto t_start = std::chrono::steady_clock::now();
-  auto worker = [&]() {
+  auto worker = [&](int me) {
     try {
-      for (;;) {
-        size_t k = next.fetch_add(1);
+      for (size_t pos = 0;;) {
+        size_t k;
+        if (per_device) {  // this thread's devices, in task order
+          while (pos < tasks.size() && int(tasks[pos].dev % size_t(nt)) != me) ++pos;
+          k = pos++;
+        } else {
+          k = next.fetch_add(1);
+        }
         if (k >= tasks.size()) return;
         const Dev& r2 = *tasks[k].dst;
         const size_t t = tasks[k].t, i = tasks[k].i;
@@ -973,9 +984,8 @@ static State apply_plan(const Plan& plan, const State& src, size_t t0, size_t t1
       errs.push_back(f);
     }
   };
-  int nt = std::max(1, std::min<int>(n_threads, int(tasks.size())));
   std::vector<std::thread> pool;
-  for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
+  for (int i = 0; i < nt; ++i) pool.emplace_back(worker, i);
   for (auto& th : pool) th.join();  // barrier 2: all fetches and merges done
   auto t_end = std::chrono::steady_clock::now();
   if (!errs.empty()) throw errs.front();
@@ -1390,12 +1400,12 @@ int orc_state_fill(const void* ptc, int64_t t0, int64_t t1, void** out) {
 }
 void orc_state_free(void* s) { delete static_cast<State*>(s); }
 
-int orc_apply(const void* plan, const void* src, int64_t t0, int64_t t1, int n_threads, double* seconds,
+int orc_apply(const void* plan, const void* src, int64_t t0, int64_t t1, int n_threads, int per_device, double* seconds,
               uint64_t* moved, uint64_t* local, void** out) {
   return guard([&] {
     ApplyReport rep;
     *out = new State(apply_plan(static_cast<const OrcPlan*>(plan)->p, *static_cast<const State*>(src), size_t(t0),
-                                size_t(t1), n_threads, &rep));
+                                size_t(t1), n_threads, &rep, per_device != 0));
     if (seconds) *seconds = rep.seconds;
     if (moved) *moved = rep.moved;
     if (local) *local = rep.local;

@@ -440,14 +440,16 @@ class Plan(_Handle):
                                              e.ctypes.data_as(C.c_void_p), C.byref(n)))
         return {(int(w[k]), int(l[k])): (int(i[k]), int(e[k])) for k in range(n.value)}
 
-    def apply(self, src: "State", n_threads=1, t0=0, t1=1 << 62):
+    def apply(self, src: "State", n_threads=1, t0=0, t1=1 << 62, per_device=False):
+        """apply_plan distributed; per_device: one task per destination device
+        (SPEC.md:504), else every thread drains a shared (destination, tensor, cell) queue."""
         out = C.c_void_p()
         secs = C.c_double()
         moved = C.c_uint64()
         local = C.c_uint64()
         self.o._chk(self.o.lib.orc_apply(C.c_void_p(self.h), C.c_void_p(src.h), C.c_int64(t0), C.c_int64(t1),
-                                         C.c_int(n_threads), C.byref(secs), C.byref(moved), C.byref(local),
-                                         C.byref(out)))
+                                         C.c_int(n_threads), C.c_int(1 if per_device else 0), C.byref(secs),
+                                         C.byref(moved), C.byref(local), C.byref(out)))
         st = State(self.o, out.value, self.b)
         return st, dict(seconds=secs.value, moved=moved.value, local=local.value)
 

@@ -580,6 +580,21 @@ class Executor:
         _chk(lib.rs_executor_host_elapsed(self.h, gpu, C.byref(ms)))
         return ms.value
 
+    def world_ms(self) -> float:
+        """The last wait()'s world time: common start -> last local GPU done (peer pushes included)."""
+        ms = C.c_float()
+        _chk(lib.rs_executor_world_ms(self.h, C.byref(ms)))
+        return ms.value
+
+    def run_host_world(self, host_src: Sequence[int], host_dst: Sequence[int]) -> float:
+        """End to end over every local GPU: H2D of all src arenas | kernels | D2H of all dst
+        arenas, from one common start (ms).  One pinned host buffer pair per world GPU."""
+        n = self.ctx.world
+        hs, hd = (C.c_void_p * n)(*[p or None for p in host_src]), (C.c_void_p * n)(*[p or None for p in host_dst])
+        ms = C.c_float()
+        _chk(lib.rs_executor_run_host_world(self.h, n, hs, hd, C.byref(ms)))
+        return ms.value
+
     def fill_sources(self) -> None:
         _chk(lib.rs_executor_fill_sources(self.h))
 

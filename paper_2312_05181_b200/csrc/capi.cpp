@@ -606,6 +606,19 @@ int rs_executor_host_elapsed(rs_executor* e, int gpu, float* ms) {
     *ms = e->e->host_elapsed(gpu);
   });
 }
+int rs_executor_world_ms(const rs_executor* e, float* ms) {
+  return guard([&] {
+    need(e, "executor"), need(ms, "ms");
+    *ms = e->e->world_ms();
+  });
+}
+int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_src, void* const* host_dst, float* ms) {
+  return guard([&] {
+    need(e, "executor"), need(host_src, "host_src"), need(host_dst, "host_dst"), need(ms, "ms");
+    if (n != e->e->context().world()) raise(reshard::Errc::InvalidArgument, "one host buffer pair per world GPU");
+    *ms = e->e->run_host_world(std::vector<const void*>(host_src, host_src + n), std::vector<void*>(host_dst, host_dst + n));
+  });
+}
 int rs_executor_fill_sources(rs_executor* e) {
   return guard([&] {
     need(e, "executor");

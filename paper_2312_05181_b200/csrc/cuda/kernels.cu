@@ -7,6 +7,8 @@
 //                      widest common alignment (16 B vectors for every GPT-catalog tile).
 //                      Loads are non-coherent streaming loads (L1 no-allocate, 256 B L2
 //                      prefetch); a tile whose dst is a peer mapping stores over NVLink (K2).
+//  K2 fan-out       — copy_fan_v16_kernel: a DP-replicated fragment read once, stored to every
+//                      destination (local and peer) — the multi-GPU fan-out default.
 //  K6 fill_cell      — counter-based splitmix64 payload (proj/include/reshard/util/hash.hpp:46-51)
 //                      for any sub-box of a base tensor, bit-identical to the CPU stream.
 //  K7 verify_cell    — regenerates K6's bytes and counts mismatches (off the clock).
@@ -111,6 +113,69 @@ __global__ void __launch_bounds__(256) copy_any_kernel(const DevTile* __restrict
     else if ((a & 3) == 0) copy_tile<unsigned, 4>(t);
     else if ((a & 1) == 0) copy_tile<unsigned short, 4>(t);
     else copy_tile<unsigned char, 4>(t);
+  }
+}
+
+// K2 fan-out: one source box read ONCE (16-byte LDG) and stored to each of its n_dst
+// destinations (STG; local HBM or peer memory over NVLink).  The multi-GPU default for DP
+// replicas whose destinations include a peer: every source byte crosses HBM once however many
+// replicas it feeds.  Same incremental 32-bit offset walk as copy_tile, one walk per
+// destination on the store side (each destination has its own pitch).
+struct DevFanTileL {
+  unsigned long long src, src_pitch;
+  unsigned rows, row_bytes, n_dst, pad;
+  unsigned long long dst[kMaxFan];
+  unsigned long long dst_pitch[kMaxFan];
+};
+static_assert(sizeof(DevFanTileL) == sizeof(FanTile), "fan tile layout");
+
+template <int U>
+__device__ __forceinline__ void copy_fan_tile(const DevFanTileL& t) {
+  constexpr unsigned W = 16;
+  const unsigned vpr = t.row_bytes / W;
+  const unsigned n = t.rows * vpr;
+  const unsigned B = blockDim.x;
+  const unsigned drow = B / vpr, dcol = B % vpr;
+  const unsigned sp = unsigned(t.src_pitch);
+  const unsigned s_step = drow * sp + dcol * W, s_wrap = sp - vpr * W;
+  const unsigned nd = t.n_dst;
+  unsigned col = threadIdx.x % vpr;
+  unsigned so = (threadIdx.x / vpr) * sp + col * W;
+  unsigned doff[kMaxFan];
+#pragma unroll
+  for (int d = 0; d < kMaxFan; ++d) doff[d] = (threadIdx.x / vpr) * unsigned(t.dst_pitch[d]) + col * W;
+  const char* s = reinterpret_cast<const char*>(t.src);
+  for (unsigned i = threadIdx.x; i < n; i += U * B) {
+    uint4 v[U];
+    const unsigned col0 = col;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i + u * B < n) v[u] = ld_nc(reinterpret_cast<const uint4*>(s + so));
+      col += dcol, so += s_step;
+      if (col >= vpr) col -= vpr, so += s_wrap;
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxFan; ++d) {
+      if (d >= int(nd)) break;
+      char* dd = reinterpret_cast<char*>(t.dst[d]);
+      const unsigned dp = unsigned(t.dst_pitch[d]);
+      const unsigned d_step = drow * dp + dcol * W, d_wrap = dp - vpr * W;
+      unsigned c = col0, o = doff[d];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i + u * B < n) st_na(reinterpret_cast<uint4*>(dd + o), v[u]);
+        c += dcol, o += d_step;
+        if (c >= vpr) c -= vpr, o += d_wrap;
+      }
+      doff[d] = o;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512, 2) copy_fan_v16_kernel(const DevFanTileL* __restrict__ tiles, unsigned long long n) {
+  for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
+    const DevFanTileL t = tiles[k];
+    copy_fan_tile<4>(t);
   }
 }
 
@@ -511,6 +576,14 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
     copy_v16_kernel<4, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
   }
   check(cudaGetLastError(), "copy launch");
+}
+
+void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
+  if (n_tiles == 0) return;
+  const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(std::min(cfg.ctas_per_sm < 2 ? 2 : cfg.ctas_per_sm, 2))));
+  copy_fan_v16_kernel<<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTileL*>(d_tiles),
+                                                                           n_tiles);
+  check(cudaGetLastError(), "fan copy launch");
 }
 
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {

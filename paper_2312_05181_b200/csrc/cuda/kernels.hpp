@@ -23,6 +23,9 @@ struct CellGeom {
 // tile list.  aligned16: every tile is 16-byte aligned (else the generic-width kernel runs).
 void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
                  void* stream);
+// K2 fan-out (LDG/STG): every tile 16-byte aligned, n_dst <= kMaxFan destinations, natural
+// order; the source is read once for all destinations (peer destinations store over NVLink).
+void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);
 // K3 with fan-out: every tile 16-byte aligned and <= cfg.stage_bytes.  The array must be in
 // interleave_for_grid order for bulk_grid(n_tiles, sms, cfg) CTAs.
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);

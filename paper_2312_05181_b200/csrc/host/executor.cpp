@@ -158,6 +158,22 @@ Context::Context(int world, std::vector<int> world_ids, std::vector<int> cuda_de
     int sm = 0;
     ck(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, cuda_devs_[i]), "sm count");
     sms_.push_back(sm);
+    // Pre-size the stream-ordered pool the copy schedules come from: the pool keeps what it
+    // maps (release threshold: never) and is primed once per device here, at context creation,
+    // so a reconfiguration's prepare() sub-allocates descriptors without mapping new memory.
+    if (std::find(cuda_devs_.begin(), cuda_devs_.begin() + long(i), cuda_devs_[i]) == cuda_devs_.begin() + long(i)) {
+      cudaMemPool_t pool;
+      ck(cudaDeviceGetDefaultMemPool(&pool, cuda_devs_[i]), "default mem pool");
+      uint64_t keep = UINT64_MAX;
+      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool release threshold");
+      const uint64_t prime = uint64_t(std::max(0, env_int("RESHARD_DESC_POOL_MIB", 256))) << 20;
+      if (prime) {
+        void* p = nullptr;
+        ck(cudaMallocAsync(&p, prime, s), "prime descriptor pool");
+        ck(cudaFreeAsync(p, s), "prime descriptor pool");
+        ck(cudaStreamSynchronize(s), "prime descriptor pool");
+      }
+    }
     // direct peer access between the local GPUs (single-process multi-GPU runs)
     for (size_t j = 0; j < cuda_devs_.size(); ++j) {
       if (j == i) continue;
@@ -249,22 +265,31 @@ struct Executor::Local {
   FanTile* d_fan = nullptr;     // bulk kernel tiles (sorted by first destination, interleaved for the grid)
   FanTile* d_fan_chunks = nullptr;  // the same tiles, interleaved per host chunk (pipelined host path)
   CopyTile* d_tiles = nullptr;  // [LDG aligned tiles, sorted by dst | misaligned tiles]
-  uint64_t n_fan = 0, n_aligned = 0, n_misc = 0, bytes = 0, read_bytes = 0;
+  FanTile* d_fanl = nullptr;    // K2 fan-out tiles (LDG once, STG to every destination; peers included)
+  uint64_t n_fan = 0, n_aligned = 0, n_misc = 0, n_fanl = 0, bytes = 0, read_bytes = 0;
+  cudaEvent_t e_h2d = nullptr, e_kern = nullptr, e_d2h = nullptr;  // run_host_world phase marks
   cudaEvent_t start = nullptr, stop = nullptr;
   unsigned long long* d_count = nullptr;
   std::vector<HostChunk> chunks;
+  std::vector<DevPiece> chunk_pieces;  // the one tile list the host pipeline cuts into chunks (lazy)
+  bool chunks_ready = true;           // chunks planned (or not applicable)
+  bool chunk_fan = false;             // chunk_pieces feed the bulk kernel (else the aligned LDG kernel)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaStream_t s_aux = nullptr;                       // LDG/STG tiles beside the bulk kernel
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> ev;
   std::unique_ptr<Local> phase_b;  // central mode, on the central GPU: staging -> destination tiles
-  uint64_t launches() const { return (n_fan ? 1 : 0) + (n_aligned ? 1 : 0) + (n_misc ? 1 : 0); }
+  uint64_t launches() const { return (n_fan ? 1 : 0) + (n_aligned ? 1 : 0) + (n_misc ? 1 : 0) + (n_fanl ? 1 : 0); }
+  uint64_t tiles() const { return n_fan + n_aligned + n_misc + n_fanl; }
   ~Local() {
     if (dev < 0) return;
     cudaSetDevice(dev);
     if (d_fan) cudaFree(d_fan);
     if (d_fan_chunks) cudaFree(d_fan_chunks);
     if (d_tiles) cudaFree(d_tiles);
+    if (d_fanl) cudaFree(d_fanl);
+    for (auto e : {e_h2d, e_kern, e_d2h})
+      if (e) cudaEventDestroy(e);
     if (d_count) cudaFree(d_count);
     if (start) cudaEventDestroy(start);
     if (stop) cudaEventDestroy(stop);
@@ -284,7 +309,7 @@ struct Executor::Local {
 void Executor::launch_local(Local& l, void* stream) {
   const int sms = ctx_.sm_count(l.world);
   auto s = static_cast<cudaStream_t>(stream);
-  const bool both = l.n_fan && (l.n_aligned || l.n_misc);
+  const bool both = l.n_fan && (l.n_aligned || l.n_misc || l.n_fanl);
   cudaStream_t side = s;
   if (both) {
     if (!l.s_aux) {
@@ -299,6 +324,7 @@ void Executor::launch_local(Local& l, void* stream) {
   cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, s);
   cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, side);
   cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, side);
+  cuda::launch_copy_fan(l.d_fanl, l.n_fanl, cfg_, sms, side);
   if (both) {
     ck(cudaEventRecord(l.join, side), "join");
     ck(cudaStreamWaitEvent(s, l.join, 0), "join wait");
@@ -332,11 +358,14 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
   src_base_.assign(size_t(G), nullptr);
   dst_base_.assign(size_t(G), nullptr);
 
-  // src arena layout
+  // src arena layout (a failed device of a recovery plan holds nothing: no storage, no fill)
+  std::vector<char> dead(a.devices.size(), 0);
+  for (const DeviceId& f : plan_->failed)
+    if (int o = a.ordinal(f); o >= 0) dead[size_t(o)] = 1;
   SrcLookup src_lookup(a.devices.size());
   for (uint32_t i = 0; i < a.devices.size(); ++i)
     for (auto [t, c] : hosted_subtensors(a, a.devices[i])) {
-      if (!in(t)) {  // outside this executor's tensor window: no storage, no work
+      if (!in(t) || dead[i]) {  // outside this executor's tensor window / failed: no storage, no work
         src_lookup[i][(uint64_t(t) << 32) | c] = src_bind_.size();
         src_bind_.push_back(CellBinding{-1, 0, 0, 0});
         continue;
@@ -378,11 +407,17 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     ck(cudaEventCreate(&l->start), "cudaEventCreate");
     ck(cudaEventCreate(&l->stop), "cudaEventCreate");
     ck(cudaMalloc(&l->d_count, sizeof(unsigned long long)), "cudaMalloc");
+    for (cudaEvent_t* e : {&l->e_h2d, &l->e_kern, &l->e_d2h}) ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     if (w == central_) {
       l->phase_b = std::make_unique<Local>();
       l->phase_b->world = w, l->phase_b->dev = l->dev;
     }
     local_.push_back(std::move(l));
+  }
+  if (!local_.empty()) {  // world marks on the first local GPU: one common start, the last GPU's end
+    DeviceGuard g(local_[0]->dev);
+    ck(cudaEventCreate(reinterpret_cast<cudaEvent_t*>(&w_start_)), "cudaEventCreate");
+    ck(cudaEventCreate(reinterpret_cast<cudaEvent_t*>(&w_stop_)), "cudaEventCreate");
   }
 }
 
@@ -453,7 +488,7 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
   const PTC& a = *plan_->from;
   const PTC& b = *plan_->to;
   const char* fan_env = std::getenv("RESHARD_FANOUT");
-  const bool fan = is_bulk(cfg_.kernel) && !(fan_env && std::string(fan_env) == "0");
+  const bool fan = !(fan_env && std::string(fan_env) == "0");  // K3 (TMA) or K2 (LDG) fan-out tiles
   struct Member {
     int32_t dst_gpu;
     uint64_t dst_base;
@@ -544,7 +579,13 @@ void Executor::build_distributed(const SrcLookup& src_lookup) {
   for (const Group& grp : groups) lower_group(grp, logical_);
 }
 
-Executor::~Executor() = default;
+Executor::~Executor() {
+  if (!local_.empty()) {
+    cudaSetDevice(local_[0]->dev);
+    if (w_start_) cudaEventDestroy(static_cast<cudaEvent_t>(w_start_));
+    if (w_stop_) cudaEventDestroy(static_cast<cudaEvent_t>(w_stop_));
+  }
+}
 
 void Executor::bind(int gpu, void* src, void* dst) {
   if (gpu < 0 || gpu >= ctx_.world()) raise(Errc::InvalidArgument, "bind: GPU out of range");
@@ -577,7 +618,7 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   const char* bp = std::getenv("RESHARD_BULK_PEER");
   const bool bulk_peer = bp && std::string(bp) == "1";
   Local* l = &local;
-  std::vector<DevPiece> fanp, alignedp, miscp;
+  std::vector<DevPiece> fanp, alignedp, miscp, fanlp;
   uint64_t bytes = 0, read_bytes = 0;
   for (const Logical& x : lt) {
     char* s = static_cast<char*>(x.src_arena ? dst_base_[size_t(x.src_gpu)] : src_base_[size_t(x.src_gpu)]);
@@ -609,6 +650,13 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
       read_bytes += pb;
       continue;
     }
+    // several destinations, one of them (at least) a peer: K2 fan-out reads the source once
+    // and stores every replica (local HBM and NVLink) from registers
+    if (x.n_dst > 1 && (bits & 15) == 0) {
+      fanlp.push_back(q);
+      read_bytes += pb;
+      continue;
+    }
     for (uint32_t d = 0; d < x.n_dst; ++d) {  // one single-destination piece per destination
       DevPiece one = q;
       one.n_dst = 1, one.dst[0] = q.dst[d], one.dst_pitch[0] = q.dst_pitch[d];
@@ -629,53 +677,24 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
     for (DevPiece& q : v) q.first = n, n += piece_tile_count(q.rows, q.row_bytes, q.per, q.tile);
     return n;
   };
-  const uint64_t nf = number(fanp), na = number(alignedp), nm = number(miscp);
+  by_dst(fanlp);
+  const uint64_t nf = number(fanp), na = number(alignedp), nm = number(miscp), nl = number(fanlp);
   if (trace) std::fprintf(stderr, "prepare-trace pieces %.1f ms (%zu pieces -> %llu tiles)\n", ms_since(t_mark), lt.size(),
-                          (unsigned long long)(nf + na + nm)), t_mark = clk::now();
+                          (unsigned long long)(nf + na + nm + nl)), t_mark = clk::now();
   l->chunks.clear();
-  const bool one_list = nm == 0 && ((nf == 0) != (na == 0));
-  if (host_chunks && ctx_.world() == 1 && one_list) {
-    // host-buffer pipeline: chunks of ~bytes / host_chunks in tile order, each with the
-    // source spans its tiles read and the lowest destination it writes (tile math on the host)
-    const std::vector<DevPiece>& pv = nf ? fanp : alignedp;
-    const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
-    const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
-    const uint64_t target = std::max<uint64_t>(bytes / uint64_t(cfg_.host_chunks), 1);
-    const uint64_t n = nf ? nf : na;
-    HostChunk c{0, 0, 0, UINT64_MAX, {}};
-    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);
-    uint64_t acc = 0, i = 0;
-    for (const DevPiece& q : pv) {
-      const uint64_t nt = piece_tile_count(q.rows, q.row_bytes, q.per, q.tile);
-      for (uint64_t t = 0; t < nt; ++t, ++i) {
-        uint64_t r0, cc;
-        uint32_t nr, nb;
-        piece_tile(q.rows, q.row_bytes, q.per, q.tile, t, r0, cc, nr, nb);
-        const uint64_t s0 = q.src + r0 * q.src_pitch + cc - sb, s1 = s0 + (nr ? (nr - 1) * q.src_pitch : 0) + nb;
-        auto& sv = spans.back();  // consecutive tiles usually continue the previous source run
-        if (!sv.empty() && s0 >= sv.back().first && s0 <= sv.back().second) sv.back().second = std::max(sv.back().second, s1);
-        else sv.emplace_back(s0, s1);
-        c.src_end = std::max(c.src_end, s1);
-        for (uint32_t d = 0; d < q.n_dst; ++d) c.dst_min = std::min(c.dst_min, q.dst[d] + r0 * q.dst_pitch[d] + cc - db);
-        acc += uint64_t(nr) * nb * q.n_dst;
-        if (acc >= target || i + 1 == n) {
-          c.t1 = i + 1;
-          l->chunks.push_back(c);
-          c = HostChunk{i + 1, 0, 0, UINT64_MAX, {}};
-          if (i + 1 < n) spans.emplace_back();
-          acc = 0;
-        }
-      }
-    }
-    plan_uploads(l->chunks, spans);
-  }
-  if (trace) std::fprintf(stderr, "prepare-trace chunks %.1f ms\n", ms_since(t_mark)), t_mark = clk::now();
+  l->chunk_pieces.clear();
+  const bool one_list = nm == 0 && nl == 0 && ((nf == 0) != (na == 0));
+  // the host-buffer pipeline's chunks are planned on first use (run_host), not here: they are
+  // a per-tile host walk that the device-resident path never needs
+  l->chunks_ready = !(host_chunks && ctx_.world() == 1 && one_list);
+  if (!l->chunks_ready) l->chunk_pieces = nf ? fanp : alignedp, l->chunk_fan = nf != 0;
   DeviceGuard g(l->dev);
   auto st = static_cast<cudaStream_t>(ctx_.stream(l->world));
   const int sms = ctx_.sm_count(l->world);
   if (l->d_fan) cudaFree(l->d_fan), l->d_fan = nullptr;
   if (l->d_fan_chunks) cudaFree(l->d_fan_chunks), l->d_fan_chunks = nullptr;
   if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
+  if (l->d_fanl) cudaFree(l->d_fanl), l->d_fanl = nullptr;
   // stream-ordered pool allocations (a plain cudaMalloc after the arenas took 62 ms, r47b)
   auto upload = [&](const std::vector<DevPiece>& v) -> DevPiece* {
     if (v.empty()) return nullptr;
@@ -687,29 +706,31 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   DevPiece* dfan = upload(fanp);
   DevPiece* dal = upload(alignedp);
   DevPiece* dmi = upload(miscp);
+  DevPiece* dfl = upload(fanlp);
+  if (trace) std::fprintf(stderr, "prepare-trace upload %.2f ms\n", ms_since(t_mark)), t_mark = clk::now();
   if (nf) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan), nf * sizeof(FanTile), st), "cudaMallocAsync tiles");
     cuda::launch_expand_fan(dfan, uint32_t(fanp.size()), 0, nf, l->d_fan,
                             interleave ? unsigned(cuda::bulk_grid(nf, sms, cfg_)) : 0u, sms, st);
-    if (!l->chunks.empty() && interleave) {  // each host chunk is its own launch, interleaved for its grid
-      ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan_chunks), nf * sizeof(FanTile), st), "cudaMallocAsync tiles");
-      for (const HostChunk& c : l->chunks)
-        cuda::launch_expand_fan(dfan, uint32_t(fanp.size()), c.t0, c.t1, l->d_fan_chunks + c.t0,
-                                unsigned(cuda::bulk_grid(c.t1 - c.t0, sms, cfg_)), sms, st);
-    }  // natural order: the chunks are slices of d_fan
   }
   if (na + nm) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_tiles), (na + nm) * sizeof(CopyTile), st), "cudaMallocAsync tiles");
     cuda::launch_expand_copy(dal, uint32_t(alignedp.size()), na, l->d_tiles, sms, st);
     cuda::launch_expand_copy(dmi, uint32_t(miscp.size()), nm, l->d_tiles + na, sms, st);
   }
-  for (DevPiece* d : {dfan, dal, dmi})
+  if (nl) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fanl), nl * sizeof(FanTile), st), "cudaMallocAsync tiles");
+    cuda::launch_expand_fan(dfl, uint32_t(fanlp.size()), 0, nl, l->d_fanl, 0u, sms, st);
+  }
+  for (DevPiece* d : {dfan, dal, dmi, dfl})
     if (d) ck(cudaFreeAsync(d, st), "cudaFreeAsync pieces");
+  if (trace) std::fprintf(stderr, "prepare-trace alloc+expand launch %.2f ms\n", ms_since(t_mark)), t_mark = clk::now();
   ck(cudaStreamSynchronize(st), "expand schedule");
-  if (trace) std::fprintf(stderr, "prepare-trace expand %.1f ms\n", ms_since(t_mark));
+  if (trace) std::fprintf(stderr, "prepare-trace expand sync %.2f ms\n", ms_since(t_mark));
   l->n_fan = nf;
   l->n_aligned = na;
   l->n_misc = nm;
+  l->n_fanl = nl;
   l->bytes = bytes;
   l->read_bytes = read_bytes;
 }
@@ -717,9 +738,17 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
 void Executor::run() {
   TraceRange trace_("Executor::run");
   Local* central = nullptr;
+  if (local_.empty()) return;
+  auto ws = static_cast<cudaEvent_t>(w_start_), we = static_cast<cudaEvent_t>(w_stop_);
+  auto origin = static_cast<cudaStream_t>(ctx_.stream(local_[0]->world));
+  {
+    DeviceGuard g(local_[0]->dev);
+    ck(cudaEventRecord(ws, origin), "cudaEventRecord");
+  }
   for (auto& l : local_) {
     DeviceGuard g(l->dev);
     auto s = static_cast<cudaStream_t>(ctx_.stream(l->world));
+    if (l != local_[0]) ck(cudaStreamWaitEvent(s, ws, 0), "common start");  // every GPU starts at the same mark
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     launch_local(*l, s);
     ck(cudaEventRecord(l->stop, s), "cudaEventRecord");
@@ -733,6 +762,10 @@ void Executor::run() {
     launch_local(*central->phase_b, s);
     ck(cudaEventRecord(central->stop, s), "cudaEventRecord");
   }
+  DeviceGuard g(local_[0]->dev);  // the world is done when the last GPU's kernels (and pushes) are
+  for (auto& l : local_)
+    if (l != local_[0]) ck(cudaStreamWaitEvent(origin, l->stop, 0), "join");
+  ck(cudaEventRecord(we, origin), "cudaEventRecord");
 }
 
 std::vector<Timing> Executor::wait() {
@@ -743,17 +776,87 @@ std::vector<Timing> Executor::wait() {
     ck(cudaEventSynchronize(l->stop), "cudaEventSynchronize");
     Timing t;
     ck(cudaEventElapsedTime(&t.ms, l->start, l->stop), "cudaEventElapsedTime");
-    t.tiles = l->n_fan + l->n_aligned + l->n_misc;
+    t.tiles = l->tiles();
     t.bytes = l->bytes;
     t.read_bytes = l->read_bytes;
     t.launches = l->launches();
     if (const Local* p = l->phase_b.get()) {
-      t.tiles += p->n_fan + p->n_aligned + p->n_misc;
+      t.tiles += p->tiles();
       t.bytes += p->bytes, t.read_bytes += p->read_bytes, t.launches += p->launches();
     }
     out.push_back(t);
   }
+  if (!local_.empty()) {
+    DeviceGuard g(local_[0]->dev);
+    ck(cudaEventSynchronize(static_cast<cudaEvent_t>(w_stop_)), "cudaEventSynchronize");
+    ck(cudaEventElapsedTime(&world_ms_, static_cast<cudaEvent_t>(w_start_), static_cast<cudaEvent_t>(w_stop_)),
+       "cudaEventElapsedTime");
+  }
   return out;
+}
+
+// End to end over every local GPU from one common start: H2D of each GPU's src arena (all GPUs
+// at once), a world barrier, every GPU's kernels, a world barrier, D2H of each dst arena; the
+// origin stream joins the last D2H.  Host buffers are indexed by world GPU (null: not local).
+float Executor::run_host_world(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst) {
+  TraceRange trace_("Executor::run_host_world");
+  if (local_.empty()) raise(Errc::DeviceUnavailable, "run_host_world: no local GPU");
+  if (central_ >= 0) raise(Errc::InvalidArgument, "run_host_world: distributed mode only");
+  if (host_src.size() != size_t(ctx_.world()) || host_dst.size() != size_t(ctx_.world()))
+    raise(Errc::InvalidArgument, "run_host_world: one host buffer pair per world GPU");
+  auto ws = static_cast<cudaEvent_t>(w_start_), we = static_cast<cudaEvent_t>(w_stop_);
+  auto origin = static_cast<cudaStream_t>(ctx_.stream(local_[0]->world));
+  auto stream_of = [&](const Local& l) { return static_cast<cudaStream_t>(ctx_.stream(l.world)); };
+  {
+    DeviceGuard g(local_[0]->dev);
+    ck(cudaEventRecord(ws, origin), "cudaEventRecord");
+  }
+  auto barrier = [&](cudaEvent_t Local::*mark) {  // every local stream waits for every other's mark
+    for (auto& l : local_) {
+      DeviceGuard g(l->dev);
+      for (auto& o : local_)
+        if (o != l) ck(cudaStreamWaitEvent(stream_of(*l), (*o).*mark, 0), "world barrier");
+    }
+  };
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    auto s = stream_of(*l);
+    const size_t w = size_t(l->world);
+    if (l != local_[0]) ck(cudaStreamWaitEvent(s, ws, 0), "common start");
+    if (src_size_[w]) {
+      if (!host_src[w]) raise(Errc::InvalidArgument, "run_host_world: null host source for a local GPU");
+      ck(cudaMemcpyAsync(src_base_[w], host_src[w], src_size_[w], cudaMemcpyHostToDevice, s), "h2d src arena");
+    }
+    ck(cudaEventRecord(l->e_h2d, s), "cudaEventRecord");
+  }
+  barrier(&Local::e_h2d);
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    launch_local(*l, stream_of(*l));
+    ck(cudaEventRecord(l->e_kern, stream_of(*l)), "cudaEventRecord");
+  }
+  barrier(&Local::e_kern);  // peers' pushes into this GPU's dst arena have landed
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    const size_t w = size_t(l->world);
+    if (dst_size_[w]) {
+      if (!host_dst[w]) raise(Errc::InvalidArgument, "run_host_world: null host destination for a local GPU");
+      ck(cudaMemcpyAsync(host_dst[w], dst_base_[w], dst_size_[w], cudaMemcpyDeviceToHost, stream_of(*l)), "d2h dst arena");
+    }
+    ck(cudaEventRecord(l->e_d2h, stream_of(*l)), "cudaEventRecord");
+  }
+  DeviceGuard g(local_[0]->dev);
+  for (auto& l : local_)
+    if (l != local_[0]) ck(cudaStreamWaitEvent(origin, l->e_d2h, 0), "join");
+  ck(cudaEventRecord(we, origin), "cudaEventRecord");
+  ck(cudaEventSynchronize(we), "cudaEventSynchronize");
+  for (auto& l : local_) {
+    DeviceGuard gl(l->dev);
+    ck(cudaEventSynchronize(l->e_d2h), "cudaEventSynchronize");
+  }
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, ws, we), "cudaEventElapsedTime");
+  return ms;
 }
 
 void Executor::host_phase(int gpu, int phase, void* host_buf) {
@@ -795,6 +898,59 @@ float Executor::host_elapsed(int gpu) {
   raise(Errc::DeviceUnavailable, "host_elapsed: GPU " + std::to_string(gpu) + " is not local");
 }
 
+// Host-buffer pipeline (run_host): chunks of ~bytes / host_chunks in tile order, each with the
+// source spans its tiles read and the lowest destination it writes (tile math on the host).
+void Executor::plan_host_chunks(Local& local) {
+  Local* l = &local;
+  l->chunks_ready = true;
+  const std::vector<DevPiece>& pv = l->chunk_pieces;
+  if (pv.empty()) return;
+  const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
+  const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
+  const uint64_t target = std::max<uint64_t>(l->bytes / uint64_t(cfg_.host_chunks), 1);
+  const uint64_t n = l->chunk_fan ? l->n_fan : l->n_aligned;
+  HostChunk c{0, 0, 0, UINT64_MAX, {}};
+  std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);
+  uint64_t acc = 0, i = 0;
+  for (const DevPiece& q : pv) {
+    const uint64_t nt = piece_tile_count(q.rows, q.row_bytes, q.per, q.tile);
+    for (uint64_t t = 0; t < nt; ++t, ++i) {
+      uint64_t r0, cc;
+      uint32_t nr, nb;
+      piece_tile(q.rows, q.row_bytes, q.per, q.tile, t, r0, cc, nr, nb);
+      const uint64_t s0 = q.src + r0 * q.src_pitch + cc - sb, s1 = s0 + (nr ? (nr - 1) * q.src_pitch : 0) + nb;
+      auto& sv = spans.back();  // consecutive tiles usually continue the previous source run
+      if (!sv.empty() && s0 >= sv.back().first && s0 <= sv.back().second) sv.back().second = std::max(sv.back().second, s1);
+      else sv.emplace_back(s0, s1);
+      c.src_end = std::max(c.src_end, s1);
+      for (uint32_t d = 0; d < q.n_dst; ++d) c.dst_min = std::min(c.dst_min, q.dst[d] + r0 * q.dst_pitch[d] + cc - db);
+      acc += uint64_t(nr) * nb * q.n_dst;
+      if (acc >= target || i + 1 == n) {
+        c.t1 = i + 1;
+        l->chunks.push_back(c);
+        c = HostChunk{i + 1, 0, 0, UINT64_MAX, {}};
+        if (i + 1 < n) spans.emplace_back();
+        acc = 0;
+      }
+    }
+  }
+  plan_uploads(l->chunks, spans);
+  if (l->chunk_fan && cfg_.kernel == CopyKernel::Bulk) {  // each chunk its own launch, interleaved for its grid
+    DeviceGuard g(l->dev);
+    auto st = static_cast<cudaStream_t>(ctx_.stream(l->world));
+    const int sms = ctx_.sm_count(l->world);
+    DevPiece* d = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&d), pv.size() * sizeof(DevPiece), st), "cudaMallocAsync pieces");
+    ck(cudaMemcpyAsync(d, pv.data(), pv.size() * sizeof(DevPiece), cudaMemcpyHostToDevice, st), "upload pieces");
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan_chunks), l->n_fan * sizeof(FanTile), st), "cudaMallocAsync tiles");
+    for (const HostChunk& k : l->chunks)
+      cuda::launch_expand_fan(d, uint32_t(pv.size()), k.t0, k.t1, l->d_fan_chunks + k.t0,
+                              unsigned(cuda::bulk_grid(k.t1 - k.t0, sms, cfg_)), sms, st);
+    ck(cudaFreeAsync(d, st), "cudaFreeAsync pieces");
+    ck(cudaStreamSynchronize(st), "expand chunks");
+  }  // other kernels walk the natural order: the chunks are slices of the tile array
+}
+
 Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   TraceRange trace_("Executor::run_host");
   Local* l = nullptr;
@@ -802,6 +958,7 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     if (x->world == gpu) l = x.get();
   if (!l) raise(Errc::DeviceUnavailable, "run_host: GPU " + std::to_string(gpu) + " is not local");
   if (ctx_.world() != 1) raise(Errc::InvalidArgument, "run_host: single-GPU worlds only");
+  if (!l->chunks_ready) plan_host_chunks(*l);
   DeviceGuard g(l->dev);
   auto s = static_cast<cudaStream_t>(ctx_.stream(gpu));
   char* dsrc = static_cast<char*>(src_base_[size_t(gpu)]);
@@ -810,7 +967,7 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
   char* hdst = static_cast<char*>(host_dst);
   const uint64_t ssize = src_size_[size_t(gpu)], dsize = dst_size_[size_t(gpu)];
   Timing t;
-  t.tiles = l->n_fan + l->n_aligned + l->n_misc, t.bytes = l->bytes, t.read_bytes = l->read_bytes;
+  t.tiles = l->tiles(), t.bytes = l->bytes, t.read_bytes = l->read_bytes;
   if (l->chunks.empty()) {  // sequential: H2D, kernels, D2H
     ck(cudaEventRecord(l->start, s), "cudaEventRecord");
     ck(cudaMemcpyAsync(dsrc, hsrc, ssize, cudaMemcpyHostToDevice, s), "h2d src arena");
@@ -945,12 +1102,19 @@ std::vector<uint64_t> Executor::bytes_to(int gpu) const {
   if (gpu == central_) add(logical_b_);
   return out;
 }
+// A fan-out piece is read once when it is 16-byte aligned (K3 TMA or K2 LDG fan-out tiles, as
+// lower_tiles routes it; arenas are 256-byte aligned, so the offsets decide), else once per
+// destination (the generic-width kernel).
 uint64_t Executor::read_bytes_for(int gpu) const {
   uint64_t n = 0;
-  const bool bulk = is_bulk(cfg_.kernel);
-  for (auto& x : logical_[size_t(gpu)]) n += uint64_t(x.rows) * x.row_bytes * (bulk ? 1 : x.n_dst);
+  auto add = [&](const Logical& x) {
+    uint64_t bits = x.src_off | x.row_bytes | (x.per ? 0 : x.tile) | (x.rows > 1 ? x.src_pitch : 0);
+    for (uint32_t d = 0; d < x.n_dst; ++d) bits |= x.dst_off[d] | (x.rows > 1 ? x.dst_pitch[d] : 0);
+    n += uint64_t(x.rows) * x.row_bytes * ((bits & 15) == 0 ? 1 : x.n_dst);
+  };
+  for (auto& x : logical_[size_t(gpu)]) add(x);
   if (gpu == central_)
-    for (auto& x : logical_b_) n += uint64_t(x.rows) * x.row_bytes * (bulk ? 1 : x.n_dst);
+    for (auto& x : logical_b_) add(x);
   return n;
 }
 

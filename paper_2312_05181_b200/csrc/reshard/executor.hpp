@@ -163,8 +163,15 @@ class Executor {
   void bind(int gpu, void* src_base, void* dst_base);
   void prepare();  // lower fragments to tiles for the local GPUs and upload them
 
-  void run();                       // launch on every local GPU (async)
+  void run();                       // launch on every local GPU (async), all from one common start mark
   std::vector<Timing> wait();       // per local GPU, after completion
+  // The last wait()'s world time: from the common start (recorded on the first local GPU,
+  // waited on by every other) to the end of the last local GPU's kernels, peer pushes included.
+  float world_ms() const { return world_ms_; }
+  // End to end through host buffers over every local GPU (multi-GPU single-process worlds,
+  // and one GPU): H2D of each src arena, world barrier, kernels, world barrier, D2H of each
+  // dst arena, all GPUs concurrently; returns the ms from the common start to the last D2H.
+  float run_host_world(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst);
   // End-to-end on host buffers (single-GPU world): H2D of the whole src arena from
   // `host_src`, the copy kernel, D2H of the whole dst arena into `host_dst`; CUDA events
   // bracket all three.  Pinned host memory gives full PCIe bandwidth.
@@ -211,6 +218,7 @@ class Executor {
   void build_distributed(const SrcLookup& src_lookup);
   void build_central(const SrcLookup& src_lookup);
   void lower_tiles(Local& l, const std::vector<Logical>& lt, bool host_chunks);
+  void plan_host_chunks(Local& l);
   uint64_t payload_pass(const std::vector<std::vector<cuda::PayloadTask>>& per_local, bool verify);
 
   Context& ctx_;
@@ -227,6 +235,9 @@ class Executor {
   uint64_t staging_bytes_ = 0;
   std::vector<void*> src_base_, dst_base_;
   std::vector<std::unique_ptr<Local>> local_;   // per local GPU: device tiles, events
+  void* w_start_ = nullptr;  // cudaEvent_t on local_[0]'s device: world marks
+  void* w_stop_ = nullptr;
+  float world_ms_ = 0;
 };
 
 // DP replication as a single push (SURVEY §8(b) rs_broadcast): `bytes` at `src` on world GPU

@@ -39,12 +39,13 @@ def test_two_ranks_one_gpu_ipc_push(kernel):
 
 
 def test_two_ranks_dataset_repartition():
-    """configs[4] through torchrun with 2 ranks sharing cuda:0: new DP rank d of each event
-    runs on GPU d % 2, the line aggregates every rank's samples (10^8 x 1.04) and each
-    rank's spot check of positions / entries against the host restatement passes."""
-    env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
-           "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+    """configs[4] with --gpus 2 and NO launcher: bench.py re-executes itself under torchrun
+    (2 ranks sharing cuda:0, gloo): new DP rank d of each event runs on GPU d % 2, the line
+    aggregates every rank's samples (10^8 x 1.04) and each rank's spot check of positions /
+    entries against the host restatement passes."""
+    env = dict(os.environ, RESHARD_SAME_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
            "--workload", "dataset-100m-dp2to4to8", "--no-cpu-baseline", "--no-e2e"]
     p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stderr[-3000:]
@@ -52,3 +53,39 @@ def test_two_ranks_dataset_repartition():
     assert line["n_gpus"] == 2 and line["samples_per_step"] == 104_000_000
     assert line["spot_check"] == {"pos": True, "ent": True}
     assert line["shuffle_epoch_gpu"]["bit_identical_to_host"]
+
+
+def _bench_no_launcher(n, workload, *extra, timeout=1200):
+    env = dict(os.environ, RESHARD_SAME_GPU="1")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    cmd = [sys.executable, "bench.py", "--gpus", str(n), "--steps", "3", "--warmup", "3", "--workload", workload,
+           "--no-cpu-baseline", "--e2e-steps", "1", *extra]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+    assert p.returncode == 0, p.stderr[-3000:]
+    return json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+
+
+@pytest.mark.parametrize("n", [2, 8])
+def test_single_process_world_no_launcher(n):
+    """`python bench.py --gpus N` with no launcher drives an N-GPU world from one
+    process (here every world GPU emulated on cuda:0): one common start event, every GPU's
+    kernels, the last GPU's end; the host-buffer path through rs_executor_run_host_world; every
+    destination byte verifies (GPUs 2..7 of the 8-GPU world host nothing: empty arenas)."""
+    line = _bench_no_launcher(n, "gpt2-small-tp2-to-pp2")
+    assert line["n_gpus"] == n and line["verify_mismatched_bytes"] == 0 and line["emulated_on_one_gpu"]
+    assert line["config"]["n_gpus"] == n and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["mismatched_bytes"] == 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and "run_host_world" in line["e2e"]["path"]
+    assert line["value"] >= line["ms_max_gpu_kernel"] * 0.999  # the world time contains every GPU's kernels
+    assert line["fabric"]["t_roof_ms"] > 0 and line["roofline"]["bound"] == "hbm"
+
+
+def test_single_process_world_scaleout_full_size():
+    """BASELINE configs[1] at full size as the driver's N=4 scaling run launches it (no
+    launcher), emulated on one GPU: GPT-3 1.3B (TP2,PP1,DP1)->(TP2,PP1,DP2), 18.5 GB moved,
+    every destination byte verified (K7), the host-buffer path included."""
+    line = _bench_no_launcher(4, "gpt3-1.3b-dp-scaleout")
+    assert line["verify_mismatched_bytes"] == 0 and line["moved_bytes"] == 18_484_379_648
+    assert line["e2e"]["mismatched_bytes"] == 0
+    assert line["fabric"]["max_egress_gb"] > 9
