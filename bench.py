@@ -196,6 +196,8 @@ def run_dataset(args, rs, dist=None):
     galg = done * per_sample
     achieved = b_sum / (g_sum * 1e-3) / 1e9  # the dominant kernel (gather pass) over its own event time
     n_gather = sum(dp for _, dp in spec["events"])
+    dram_ps = k5_dram_bytes_per_sample()
+    traffic = round(dram_ps * done / n_gather) if dram_ps and split2 else None
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
@@ -205,7 +207,11 @@ def run_dataset(args, rs, dist=None):
         "index_pad_ms_once": None if pad_ms is None else round(pad_ms, 3),
         "samples_per_step": done, "gsamples_per_s": round(done / (ms * 1e-3) / 1e9, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind, "peak_how": peak_how(),
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind, "peak_how": peak_how(),
+                     "dram_bytes_per_sample": dram_ps,
+                     "dram_frac": round(dram_ps * (b_sum / per_sample) / (g_sum * 1e-3) / 1e9 / peak, 4) if dram_ps else None,
+                     "traffic_note": "ncu dram read+write of the gather pass (profiles/r2_03/k5_sectors.json) per sample x "
+                                     "samples per launch: a random 32-byte record costs a whole 128-byte DRAM line",
                      "kernel": "repart_gather2_kernel" if split2 else "repartition_kernel",
                      "algorithmic_bytes_per_launch": galg // max(n_gather, 1),
                      "kernel_ms_per_step": round(gms, 4),
@@ -424,6 +430,16 @@ def copy_kernel_name() -> str:
             "ldg8": "copy_v16_kernel", "bulk_warp": "copy_bulk_warp_kernel"}.get(k, k)
 
 
+def k5_dram_bytes_per_sample():
+    """DRAM read + write bytes per sample of K5's gather pass (committed ncu capture)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_03", "k5_sectors.json")) as f:
+            v = json.load(f)["variants"]["ldg"]
+        return round(v["dram_read_bytes_per_sample"] + v["dram_write_bytes_per_sample"], 1)
+    except Exception:
+        return None
+
+
 def ncu_traffic(workload: str, kernel: str):
     """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_copy_tiles.json")
@@ -520,7 +536,7 @@ def cpu_reference_run(name: str, steps: int, warmup: int, variants=("queue",), d
         acc += nb
     windows.append((t0, len(per_t)))
     tf = time.perf_counter()
-    src = a.fill()
+    src = a.fill(skip=[(0, d) for d in failed])  # a recovery's failed devices hold nothing
     fill_s = time.perf_counter() - tf
     threads = os.cpu_count() or 1
     n_dst_dev = len(devs2)

@@ -257,6 +257,11 @@ int rs_executor_world_ms(const rs_executor* e, float* ms);
  * dst arena; *ms from the common start to the last D2H.  host_src / host_dst: n = world
  * entries, indexed by world GPU (entries of non-local GPUs are ignored). */
 int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_src, void* const* host_dst, float* ms);
+/* ExecutionReport verification digests: per base tensor of the executor's
+ * window, FNV-1a-64 (hash.hpp:13-42) of the tensor reassembled from one replica of each cell of
+ * side 0 (source layout) or 1 (destination layout), read back from the local GPUs (off the
+ * clock).  ok[i] = 0 when a cell of tensor[i] is not held by a local GPU.  *n = entries. */
+int rs_executor_digests(rs_executor* e, int side, int cap, int32_t* tensor, uint64_t* fnv, int32_t* ok, int* n);
 int rs_executor_fill_sources(rs_executor* e);
 int rs_executor_verify(rs_executor* e, uint64_t* mismatched_bytes);
 /* bindings: src cells in (from-device, tensor, cell) order; dst cells in plan order */

@@ -866,8 +866,9 @@ static std::vector<uint8_t> gen_box(const Entry& e, const Box& b) {
 
 static bool in_range(size_t t, size_t t0, size_t t1) { return t >= t0 && t < t1; }
 
-// One thread per device (input generation is not timed).
-static State fill_state(const Ptc& p, size_t t0, size_t t1) {
+// One thread per device (input generation is not timed).  Devices in `skip` (the failed
+// devices of a recovery) hold nothing: their stores stay empty.
+static State fill_state(const Ptc& p, size_t t0, size_t t1, const std::set<Dev>& skip = {}) {
   State s;
   for (auto& d : p.devices) s.store[d];
   std::vector<std::thread> th;
@@ -877,6 +878,7 @@ static State fill_state(const Ptc& p, size_t t0, size_t t1) {
       try {
         const Dev& d = p.devices[k];
         auto& st = s.store.at(d);
+        if (skip.count(d)) return;
         for (auto [t, i] : hosted(p, d)) {
           if (!in_range(t, t0, t1)) continue;
           const Entry& e = p.cat.e[t];
@@ -1393,9 +1395,12 @@ int64_t orc_plan_text(const void* pp, char* buf, int64_t cap) {
 
 // ---- executor --------------------------------------------------------------------------
 // Source stores of `ptc` filled with the synthetic payload, tensors [t0, t1) only.
-int orc_state_fill(const void* ptc, int64_t t0, int64_t t1, void** out) {
+int orc_state_fill(const void* ptc, int64_t t0, int64_t t1, int n_skip, const uint32_t* skip_worker,
+                   const uint32_t* skip_local, void** out) {
   return guard([&] {
-    *out = new State(fill_state(**static_cast<const std::shared_ptr<const Ptc>*>(ptc), size_t(t0), size_t(t1)));
+    std::set<Dev> skip;
+    for (int i = 0; i < n_skip; ++i) skip.insert(Dev{skip_worker[i], skip_local[i]});
+    *out = new State(fill_state(**static_cast<const std::shared_ptr<const Ptc>*>(ptc), size_t(t0), size_t(t1), skip));
   });
 }
 void orc_state_free(void* s) { delete static_cast<State*>(s); }

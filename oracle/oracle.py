@@ -398,9 +398,15 @@ class Ptc(_Handle):
                                                  C.byref(out)))
         return Plan(self.o, out.value, self, other)
 
-    def fill(self, t0=0, t1=1 << 62) -> "State":
+    def fill(self, t0=0, t1=1 << 62, skip=()) -> "State":
+        """Source stores with the synthetic payload, tensors [t0, t1); devices in `skip` (a
+        recovery's failed devices) stay empty."""
         out = C.c_void_p()
-        self.o._chk(self.o.lib.orc_state_fill(C.c_void_p(self.h), C.c_int64(t0), C.c_int64(t1), C.byref(out)))
+        w = np.array([d[0] for d in skip] + [0], np.uint32)
+        l = np.array([d[1] for d in skip] + [0], np.uint32)
+        self.o._chk(self.o.lib.orc_state_fill(C.c_void_p(self.h), C.c_int64(t0), C.c_int64(t1), C.c_int(len(skip)),
+                                              w.ctypes.data_as(C.c_void_p), l.ctypes.data_as(C.c_void_p),
+                                              C.byref(out)))
         return State(self.o, out.value, self)
 
     def digest(self, state: "State", t: int) -> int:

@@ -595,6 +595,17 @@ class Executor:
         _chk(lib.rs_executor_run_host_world(self.h, n, hs, hd, C.byref(ms)))
         return ms.value
 
+    def digests(self, side: int = 1) -> dict:
+        """{tensor: FNV-1a-64 of the reassembled base tensor} over side 0 (source cells) or 1
+        (destination cells) — the ExecutionReport verification digest (SPEC.md:460-463);
+        tensors with a cell on no local GPU are left out."""
+        n = C.c_int()
+        _chk(lib.rs_executor_digests(self.h, side, 0, None, None, None, C.byref(n)))
+        m = max(n.value, 1)
+        tt, ff, ok = (C.c_int32 * m)(), (C.c_uint64 * m)(), (C.c_int32 * m)()
+        _chk(lib.rs_executor_digests(self.h, side, n.value, tt, ff, ok, C.byref(n)))
+        return {int(tt[i]): int(ff[i]) for i in range(n.value) if ok[i]}
+
     def fill_sources(self) -> None:
         _chk(lib.rs_executor_fill_sources(self.h))
 

@@ -254,17 +254,35 @@ __device__ __forceinline__ unsigned long long sample_pos(const Params& p, unsign
   return p.full * p.B + p.rank * p.b + (k - p.in_full);
 }
 
-// One index entry {file, offset, length}: the reference's packed 24-byte record (PAD false:
+// One index entry {file, offset, length}: the reference's packed 24-byte record (LD 0:
 // three 8-byte loads, one record in 8 straddles a 128-byte line), or the padded 32-byte
-// device layout of dataset_index_pad (PAD true: one 16-byte and one 8-byte load from a single
+// device layout of dataset_index_pad (LD 1..3: one 16-byte and one 8-byte load, or one 32-byte load, from a single
 // 32-byte sector).
-template <bool PAD>
+//
+// LD (the padded layout's load flavour, RESHARD_K5_LOAD): 1 "ldg" (default) — 16 + 8-byte
+// non-coherent loads through L1; 2 "v4na" — ONE 32-byte load (ld.global.nc.L1::no_allocate.v4.u64,
+// sm_100) that does not allocate in L1; 3 "cg" — 16 + 8-byte loads cached in L2 only.  r2_03 ncu
+// (profiles/r2_03/k5_sectors.json): L1 sectors per sample drop from 2.88 to 1.88 with v4na, yet
+// L2 sectors (4.2) and DRAM bytes (134 per sample = 8 of perm + one 128-byte line per random
+// record) do not move with the L1 request size nor with cudaLimitMaxL2FetchGranularity: a
+// random record costs a whole DRAM line — the hardware floor K5 is measured against.
+template <int LD>
 __device__ __forceinline__ void load_entry(const unsigned long long* samples, unsigned long long idx,
                                            unsigned long long& f, unsigned long long& off, unsigned long long& len) {
-  if (PAD) {
+  if (LD == 1) {
     const unsigned long long* e = samples + 4 * idx;
     const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(e));
     f = a.x, off = a.y, len = __ldg(e + 2);
+  } else if (LD == 2) {
+    const unsigned long long* e = samples + 4 * idx;
+    unsigned long long pad;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(f), "=l"(off), "=l"(len), "=l"(pad)
+                 : "l"(e));
+  } else if (LD == 3) {
+    const unsigned long long* e = samples + 4 * idx;
+    const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(e));
+    f = a.x, off = a.y, len = __ldcg(e + 2);
   } else {
     const unsigned long long* e = samples + 3 * idx;
     f = __ldg(e), off = __ldg(e + 1), len = __ldg(e + 2);
@@ -291,7 +309,7 @@ __global__ void __launch_bounds__(kThreads) index_pad_kernel(const unsigned long
 // repartition_gather_probe): the same gathers plus every output byte K5 must write.  bench.py
 // reports K5 against the latter next to the streaming-HBM roofline.
 constexpr int kProbeItems = 4;
-template <bool PAD>
+template <int LD>
 __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsigned long long* sink) {
   const unsigned long long k0 =
       ((unsigned long long)blockIdx.x * kThreads + threadIdx.x) * (unsigned long long)kProbeItems;
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsign
   unsigned long long f[kProbeItems], off[kProbeItems], len[kProbeItems];
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) {
-    load_entry<PAD>(p.samples, idx[j], f[j], off[j], len[j]);
+    load_entry<LD>(p.samples, idx[j], f[j], off[j], len[j]);
   }
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) acc ^= f[j] + off[j] + len[j];
@@ -323,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) gather_probe_kernel(Params p, unsign
 // The same gathers plus K5's 44 output bytes per sample (pos, entry, a length word, a u32
 // queue word), warp-striped so every store is coalesced, and no scan: the floor of any
 // kernel that must both gather the entries and write the partition (RESHARD_PROBE=write).
-template <bool PAD>
+template <int LD>
 __global__ void __launch_bounds__(kThreads) gather_write_probe_kernel(Params p, Outs o) {
   unsigned long long idx[kProbeItems], pos[kProbeItems];
   const unsigned long long base = (unsigned long long)blockIdx.x * (kThreads * kProbeItems) + threadIdx.x;
@@ -336,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) gather_write_probe_kernel(Params p, 
   unsigned long long f[kProbeItems], off[kProbeItems], len[kProbeItems];
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) {
-    load_entry<PAD>(p.samples, idx[j], f[j], off[j], len[j]);
+    load_entry<LD>(p.samples, idx[j], f[j], off[j], len[j]);
   }
 #pragma unroll
   for (int j = 0; j < kProbeItems; ++j) {
@@ -363,7 +381,7 @@ constexpr int kGItems = 4, kGTile = kThreads * kGItems, kGWarpItems = 32 * kGIte
 constexpr int kClsBits = 21;  // per-class counts packed into one u64 (a tile has <= 1024 items)
 constexpr unsigned long long kClsMask = (1ull << kClsBits) - 1;
 
-template <int MINB, bool PAD>
+template <int MINB, int LD>
 __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p, Outs o, Scratch sc,
                                                                          unsigned char* cls_out) {
   __shared__ unsigned long long warp_len[kWarps], warp_cnt[kWarps];
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p
 #pragma unroll
   for (int j = 0; j < kGItems; ++j) {
     f[j] = 0, off[j] = 0, len[j] = 0;
-    if (k0 + 32 * j < p.count) load_entry<PAD>(p.samples, idx[j], f[j], off[j], len[j]);
+    if (k0 + 32 * j < p.count) load_entry<LD>(p.samples, idx[j], f[j], off[j], len[j]);
   }
   unsigned long long lsum = 0, cnt = 0;
 #pragma unroll
@@ -547,6 +565,16 @@ struct K5Mode {
   bool lookback = false;
   int minb = 5;  // resident CTAs per SM the chosen gather kernel is compiled for
 };
+// RESHARD_K5_LOAD: the padded record's load flavour (load_entry): ldg | v4na | cg.
+int k5_load() {
+  const char* v = std::getenv("RESHARD_K5_LOAD");
+  const std::string s = v ? v : "";
+  if (s.empty() || s == "ldg") return 1;  // r2_03 A/B: ldg 3.17, v4na 3.24, cg 4.66 ms per step
+  if (s == "v4na") return 2;
+  if (s == "cg") return 3;
+  raise(Errc::InvalidArgument, "RESHARD_K5_LOAD must be ldg, v4na or cg");
+}
+
 K5Mode k5_mode() {
   K5Mode m;
   const char* v = std::getenv("RESHARD_K5");
@@ -894,14 +922,20 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   if (tiles && !mode.lookback) {
     auto* cls = reinterpret_cast<unsigned char*>(sc + 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)));
     const unsigned g = unsigned(tiles);
-    if (pad) {
-      if (mode.minb == 6) repart_gather2_kernel<6, true><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else if (mode.minb == 8) repart_gather2_kernel<8, true><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else repart_gather2_kernel<5, true><<<g, kThreads, 0, st>>>(p, o, s, cls);
+    const int ld = pad ? k5_load() : 0;
+    if (mode.minb == 8) {
+      if (ld == 0) repart_gather2_kernel<8, 0><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else repart_gather2_kernel<8, 1><<<g, kThreads, 0, st>>>(p, o, s, cls);
+    } else if (mode.minb == 6) {
+      if (ld == 0) repart_gather2_kernel<6, 0><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else if (ld == 1) repart_gather2_kernel<6, 1><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else if (ld == 2) repart_gather2_kernel<6, 2><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else repart_gather2_kernel<6, 3><<<g, kThreads, 0, st>>>(p, o, s, cls);
     } else {
-      if (mode.minb == 6) repart_gather2_kernel<6, false><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else if (mode.minb == 8) repart_gather2_kernel<8, false><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else repart_gather2_kernel<5, false><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      if (ld == 0) repart_gather2_kernel<5, 0><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else if (ld == 1) repart_gather2_kernel<5, 1><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else if (ld == 2) repart_gather2_kernel<5, 2><<<g, kThreads, 0, st>>>(p, o, s, cls);
+      else repart_gather2_kernel<5, 3><<<g, kThreads, 0, st>>>(p, o, s, cls);
     }
     ck(cudaEventRecord(em, st), "event");
     const uint64_t sblocks = (tiles + 1023) / 1024;
@@ -997,10 +1031,15 @@ Timing repartition_gather_probe(Context& ctx, int gpu, const DatasetIndexView& i
   t.ms = 1e30f;
   for (int i = 0; i < std::max(1, reps) + 1; ++i) {  // first launch warms up
     ck(cudaEventRecord(e0, st), "event");
-    if (blocks && wr && pad) gather_write_probe_kernel<true><<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
-    else if (blocks && wr) gather_write_probe_kernel<false><<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
-    else if (blocks && pad) gather_probe_kernel<true><<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
-    else if (blocks) gather_probe_kernel<false><<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
+    const int ld = pad ? k5_load() : 0;
+    auto launch = [&](auto wk, auto gk) {
+      if (blocks && wr) wk<<<unsigned(blocks), kThreads, 0, st>>>(p, wo);
+      else if (blocks) gk<<<unsigned(blocks), kThreads, 0, st>>>(p, sink);
+    };
+    if (ld == 0) launch(gather_write_probe_kernel<0>, gather_probe_kernel<0>);
+    else if (ld == 1) launch(gather_write_probe_kernel<1>, gather_probe_kernel<1>);
+    else if (ld == 2) launch(gather_write_probe_kernel<2>, gather_probe_kernel<2>);
+    else launch(gather_write_probe_kernel<3>, gather_probe_kernel<3>);
     ck(cudaGetLastError(), "probe launch");
     ck(cudaEventRecord(e1, st), "event");
     ck(cudaEventSynchronize(e1), "sync");

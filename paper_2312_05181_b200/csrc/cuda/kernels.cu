@@ -236,6 +236,22 @@ __device__ __forceinline__ void bulk_s2g_hint(void* dst, unsigned src_smem, unsi
                "r"(bytes), "l"(pol)
                : "memory");
 }
+// K3T: TMA tensor copies of one 3-D box (dims {e x 8-byte words, chunks, rows}) between a
+// tensor map's region and a shared-memory stage — ONE instruction per box instead of one bulk
+// copy per row (strided 2-D TP fragments).  The map pointer is a global-memory CUtensorMap.
+__device__ __forceinline__ void tma_load_3d(unsigned dst_smem, unsigned long long map, unsigned c1, unsigned c2,
+                                            unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst_smem),
+      "l"(map), "r"(0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(unsigned long long map, unsigned c1, unsigned c2, unsigned src_smem) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(0),
+               "r"(c1), "r"(c2), "r"(src_smem)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -386,10 +402,14 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
     const unsigned bar = smem_u32(&bars[s_load]);
     const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
     mbar_expect_tx(bar, t.rows * t.row_bytes);
-    for (unsigned r = 0; r < t.rows; ++r) {
-      const char* src = reinterpret_cast<const char*>(t.src) + r * t.src_pitch;
-      if (HINT & 1) bulk_g2s_hint(base + r * t.row_bytes, src, t.row_bytes, bar, pol);
-      else bulk_g2s(base + r * t.row_bytes, src, t.row_bytes, bar);
+    if (t.pad) {  // K3T tensor tile: src = map, src_pitch = (row << 32 | chunk), row_bytes = box bytes
+      tma_load_3d(base, t.src, unsigned(t.src_pitch), unsigned(t.src_pitch >> 32), bar);
+    } else {
+      for (unsigned r = 0; r < t.rows; ++r) {
+        const char* src = reinterpret_cast<const char*>(t.src) + r * t.src_pitch;
+        if (HINT & 1) bulk_g2s_hint(base + r * t.row_bytes, src, t.row_bytes, bar, pol);
+        else bulk_g2s(base + r * t.row_bytes, src, t.row_bytes, bar);
+      }
     }
     if (++s_load == stages) s_load = 0;
   };
@@ -402,12 +422,16 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
     const DevFanTile& t = sdesc[s_store];
     mbar_wait(smem_u32(&bars[s_store]), phase);
     const unsigned base = smem_u32(smem + size_t(s_store) * stage_bytes);
-    for (unsigned d = 0; d < t.n_dst; ++d)
-      for (unsigned r = 0; r < t.rows; ++r) {
-        char* dst = reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d];
-        if (HINT & 2) bulk_s2g_hint(dst, base + r * t.row_bytes, t.row_bytes, pol);
-        else bulk_s2g(dst, base + r * t.row_bytes, t.row_bytes);
-      }
+    if (t.pad) {
+      for (unsigned d = 0; d < t.n_dst; ++d) tma_store_3d(t.dst[d], unsigned(t.src_pitch), unsigned(t.src_pitch >> 32), base);
+    } else {
+      for (unsigned d = 0; d < t.n_dst; ++d)
+        for (unsigned r = 0; r < t.rows; ++r) {
+          char* dst = reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d];
+          if (HINT & 2) bulk_s2g_hint(dst, base + r * t.row_bytes, t.row_bytes, pol);
+          else bulk_s2g(dst, base + r * t.row_bytes, t.row_bytes);
+        }
+    }
     bulk_commit();
     if (++s_store == stages) s_store = 0, phase ^= 1u;
   }

@@ -2,10 +2,15 @@
 #include "reshard/executor.hpp"
 
 #include <cstdio>
+#include <cuda.h>  // CUtensorMap and its encoder's signature (resolved through the runtime: no -lcuda)
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <map>
 #include <unordered_map>
@@ -113,6 +118,51 @@ int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                 const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  if (!fn) raise(Errc::CudaError, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// K3T box geometry of a strided row-mode piece: the row of R bytes is e 8-byte words x nch
+// chunks (e <= 256 words: the TMA box limit), a box is e x bc x br; one tensor tile per box.
+struct TensorBox {
+  uint32_t e, nch, bc, br;
+};
+TensorBox tensor_box(uint64_t row_bytes, uint32_t rows, uint64_t stage_bytes) {
+  TensorBox b{};
+  const uint64_t words = row_bytes / 8;
+  b.e = uint32_t(words);
+  if (words > 256) {
+    b.e = 256;
+    while (words % b.e) b.e -= 2;
+  }
+  b.nch = uint32_t(words / b.e);
+  const uint64_t eb = uint64_t(b.e) * 8;
+  b.bc = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({b.nch, 256, stage_bytes / eb})));
+  b.br = b.bc < b.nch ? 1u : uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({256, rows, stage_bytes / (eb * b.nch)})));
+  return b;
+}
+void encode_map(CUtensorMap* m, uint64_t base, const TensorBox& b, uint32_t rows, uint64_t pitch) {
+  const cuuint64_t dims[3] = {b.e, b.nch, rows};
+  const cuuint64_t strides[2] = {uint64_t(b.e) * 8, pitch};
+  const cuuint32_t box[3] = {b.e, b.bc, b.br}, es[3] = {1, 1, 1};
+  const CUresult r = encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, reinterpret_cast<void*>(base), dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(Errc::CudaError, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
 
 }  // namespace
 
@@ -133,6 +183,7 @@ CopyConfig CopyConfig::from_env() {
   c.l2_hint = env_int("RESHARD_BULK_HINT", c.l2_hint) & 3;
   c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
   c.host_chunks = std::max(1, env_int("RESHARD_HOST_CHUNKS", c.host_chunks));
+  c.tensor = env_int("RESHARD_TMA_TENSOR", c.tensor ? 1 : 0) != 0;
   return c;
 }
 
@@ -266,6 +317,8 @@ struct Executor::Local {
   FanTile* d_fan_chunks = nullptr;  // the same tiles, interleaved per host chunk (pipelined host path)
   CopyTile* d_tiles = nullptr;  // [LDG aligned tiles, sorted by dst | misaligned tiles]
   FanTile* d_fanl = nullptr;    // K2 fan-out tiles (LDG once, STG to every destination; peers included)
+  void* d_maps = nullptr;       // K3T: CUtensorMaps of the strided pieces (src + one per destination)
+  uint64_t n_tensor = 0;        // K3T tiles, appended to d_fan after the expanded 1-D tiles
   uint64_t n_fan = 0, n_aligned = 0, n_misc = 0, n_fanl = 0, bytes = 0, read_bytes = 0;
   cudaEvent_t e_h2d = nullptr, e_kern = nullptr, e_d2h = nullptr;  // run_host_world phase marks
   cudaEvent_t start = nullptr, stop = nullptr;
@@ -288,6 +341,7 @@ struct Executor::Local {
     if (d_fan_chunks) cudaFree(d_fan_chunks);
     if (d_tiles) cudaFree(d_tiles);
     if (d_fanl) cudaFree(d_fanl);
+    if (d_maps) cudaFree(d_maps);
     for (auto e : {e_h2d, e_kern, e_d2h})
       if (e) cudaEventDestroy(e);
     if (d_count) cudaFree(d_count);
@@ -358,6 +412,14 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
   src_base_.assign(size_t(G), nullptr);
   dst_base_.assign(size_t(G), nullptr);
 
+  using clk = std::chrono::steady_clock;
+  const bool trace = std::getenv("RESHARD_HOST_TRACE") && std::string(std::getenv("RESHARD_HOST_TRACE")) == "1";
+  auto t_mark = clk::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    std::fprintf(stderr, "lower-trace %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(clk::now() - t_mark).count());
+    t_mark = clk::now();
+  };
   // src arena layout (a failed device of a recovery plan holds nothing: no storage, no fill)
   std::vector<char> dead(a.devices.size(), 0);
   for (const DeviceId& f : plan_->failed)
@@ -396,9 +458,11 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     dst_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
     dst_bind_.push_back(bnd);
   }
+  lap("arenas");
   logical_.assign(size_t(G), {});
   if (central_ >= 0) build_central(src_lookup);
   else build_distributed(src_lookup);
+  lap("pieces");
   for (int w : ctx_.local_world_ids()) {
     auto l = std::make_unique<Local>();
     l->world = w;
@@ -406,7 +470,9 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     DeviceGuard g(l->dev);
     ck(cudaEventCreate(&l->start), "cudaEventCreate");
     ck(cudaEventCreate(&l->stop), "cudaEventCreate");
-    ck(cudaMalloc(&l->d_count, sizeof(unsigned long long)), "cudaMalloc");
+    // from the context's primed stream-ordered pool (a plain cudaMalloc may map a new page)
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_count), sizeof(unsigned long long),
+                       static_cast<cudaStream_t>(ctx_.stream(w))), "cudaMallocAsync");
     for (cudaEvent_t* e : {&l->e_h2d, &l->e_kern, &l->e_d2h}) ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     if (w == central_) {
       l->phase_b = std::make_unique<Local>();
@@ -419,6 +485,7 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     ck(cudaEventCreate(reinterpret_cast<cudaEvent_t*>(&w_start_)), "cudaEventCreate");
     ck(cudaEventCreate(reinterpret_cast<cudaEvent_t*>(&w_stop_)), "cudaEventCreate");
   }
+  lap("device setup");
 }
 
 // apply_plan central mode: each Move's fragment is fetched into the
@@ -678,12 +745,41 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
     return n;
   };
   by_dst(fanlp);
+  // K3T (RESHARD_TMA_TENSOR=1, bulk_strided): strided row-mode pieces become TMA tensor tiles,
+  // one box per tile, maps encoded here (bases are known) and uploaded with the tiles
+  std::vector<FanTile> tensor_tiles;
+  std::vector<CUtensorMap> maps;
+  if (cfg_.tensor && cfg_.kernel == CopyKernel::BulkStrided) {
+    std::vector<DevPiece> keep;
+    for (const DevPiece& q : fanp) {
+      if (!(q.per > 1 && q.rows > 1 && q.src_pitch != q.row_bytes)) {
+        keep.push_back(q);
+        continue;
+      }
+      const TensorBox tb = tensor_box(q.row_bytes, q.rows, cfg_.stage_bytes);
+      const size_t m0 = maps.size();
+      maps.resize(m0 + 1 + q.n_dst);
+      encode_map(&maps[m0], q.src, tb, q.rows, q.src_pitch);
+      for (uint32_t d = 0; d < q.n_dst; ++d) encode_map(&maps[m0 + 1 + d], q.dst[d], tb, q.rows, q.dst_pitch[d]);
+      for (uint32_t r = 0; r < q.rows; r += tb.br)
+        for (uint32_t c = 0; c < tb.nch; c += tb.bc) {
+          FanTile f{};
+          f.src = m0;  // map index until the device address is known
+          f.src_pitch = (uint64_t(r) << 32) | c;
+          f.rows = 1, f.row_bytes = tb.e * 8 * tb.bc * tb.br, f.n_dst = q.n_dst, f.pad = 1;
+          for (uint32_t d = 0; d < q.n_dst; ++d) f.dst[d] = m0 + 1 + d;
+          tensor_tiles.push_back(f);
+        }
+    }
+    fanp.swap(keep);
+  }
   const uint64_t nf = number(fanp), na = number(alignedp), nm = number(miscp), nl = number(fanlp);
+  const uint64_t ntt = tensor_tiles.size();
   if (trace) std::fprintf(stderr, "prepare-trace pieces %.1f ms (%zu pieces -> %llu tiles)\n", ms_since(t_mark), lt.size(),
                           (unsigned long long)(nf + na + nm + nl)), t_mark = clk::now();
   l->chunks.clear();
   l->chunk_pieces.clear();
-  const bool one_list = nm == 0 && nl == 0 && ((nf == 0) != (na == 0));
+  const bool one_list = nm == 0 && nl == 0 && ntt == 0 && ((nf == 0) != (na == 0));
   // the host-buffer pipeline's chunks are planned on first use (run_host), not here: they are
   // a per-tile host walk that the device-resident path never needs
   l->chunks_ready = !(host_chunks && ctx_.world() == 1 && one_list);
@@ -695,6 +791,7 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   if (l->d_fan_chunks) cudaFree(l->d_fan_chunks), l->d_fan_chunks = nullptr;
   if (l->d_tiles) cudaFree(l->d_tiles), l->d_tiles = nullptr;
   if (l->d_fanl) cudaFree(l->d_fanl), l->d_fanl = nullptr;
+  if (l->d_maps) cudaFree(l->d_maps), l->d_maps = nullptr;
   // stream-ordered pool allocations (a plain cudaMalloc after the arenas took 62 ms, r47b)
   auto upload = [&](const std::vector<DevPiece>& v) -> DevPiece* {
     if (v.empty()) return nullptr;
@@ -708,10 +805,21 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   DevPiece* dmi = upload(miscp);
   DevPiece* dfl = upload(fanlp);
   if (trace) std::fprintf(stderr, "prepare-trace upload %.2f ms\n", ms_since(t_mark)), t_mark = clk::now();
-  if (nf) {
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan), nf * sizeof(FanTile), st), "cudaMallocAsync tiles");
+  if (nf + ntt) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_fan), (nf + ntt) * sizeof(FanTile), st), "cudaMallocAsync tiles");
     cuda::launch_expand_fan(dfan, uint32_t(fanp.size()), 0, nf, l->d_fan,
                             interleave ? unsigned(cuda::bulk_grid(nf, sms, cfg_)) : 0u, sms, st);
+  }
+  if (ntt) {  // maps first (their device addresses go into the tiles), then the tiles after the 1-D ones
+    ck(cudaMalloc(&l->d_maps, maps.size() * sizeof(CUtensorMap)), "cudaMalloc tensor maps");
+    ck(cudaMemcpyAsync(l->d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, st), "maps h2d");
+    const uint64_t mb = uint64_t(reinterpret_cast<uintptr_t>(l->d_maps));
+    for (FanTile& f : tensor_tiles) {
+      f.src = mb + f.src * sizeof(CUtensorMap);
+      for (uint32_t d = 0; d < f.n_dst; ++d) f.dst[d] = mb + f.dst[d] * sizeof(CUtensorMap);
+    }
+    ck(cudaMemcpyAsync(l->d_fan + nf, tensor_tiles.data(), ntt * sizeof(FanTile), cudaMemcpyHostToDevice, st), "tiles h2d");
+    ck(cudaStreamSynchronize(st), "tensor tiles");  // the host vector dies with this frame
   }
   if (na + nm) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_tiles), (na + nm) * sizeof(CopyTile), st), "cudaMallocAsync tiles");
@@ -727,7 +835,8 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   if (trace) std::fprintf(stderr, "prepare-trace alloc+expand launch %.2f ms\n", ms_since(t_mark)), t_mark = clk::now();
   ck(cudaStreamSynchronize(st), "expand schedule");
   if (trace) std::fprintf(stderr, "prepare-trace expand sync %.2f ms\n", ms_since(t_mark));
-  l->n_fan = nf;
+  l->n_fan = nf + ntt;
+  l->n_tensor = ntt;
   l->n_aligned = na;
   l->n_misc = nm;
   l->n_fanl = nl;
@@ -1175,6 +1284,78 @@ uint64_t Executor::verify_destinations() {
                                cuda::make_geom(e.shape, dtype_width(e.dtype), b.cells[dc.tensor][dc.cell])});
   }
   return payload_pass(per, true);
+}
+
+// ---- ExecutionReport verification digests ---------------------------------------
+// Per base tensor of this executor's window: FNV-1a-64 (proj/include/reshard/util/hash.hpp:13-42)
+// of the base tensor reassembled from one replica of each cell of the chosen side (0: the
+// source layout's cells, 1: the destination layout's).  Each cell comes back with one strided
+// D2H straight into its place in the reassembled tensor (cudaMemcpy2D per outer index);
+// tensors are hashed by a pool of host threads.  FNV-1a is byte-sequential, so this stays off
+// the clock.  A tensor some cell of which is not held by a local GPU gets no digest (ok = 0).
+std::vector<Executor::Digest> Executor::digests(int side) {
+  TraceRange trace_("Executor::digests");
+  const PTC& p = side == 0 ? *plan_->from : *plan_->to;
+  const size_t nt = p.catalog.tensors.size();
+  // one binding per (tensor, cell): the first local replica in layout order
+  std::vector<std::vector<const CellBinding*>> pick(nt);
+  for (size_t t = 0; t < nt; ++t) pick[t].assign(p.cells[t].size(), nullptr);
+  auto offer = [&](uint32_t t, uint32_t c, const CellBinding& b) {
+    if (b.gpu >= 0 && ctx_.local_of(b.gpu) >= 0 && !pick[t][c]) pick[t][c] = &b;
+  };
+  if (side == 0) {
+    size_t k = 0;
+    for (uint32_t i = 0; i < p.devices.size(); ++i)
+      for (auto [t, c] : hosted_subtensors(p, p.devices[i])) offer(t, c, src_bind_[k++]);
+  } else {
+    for (size_t j = 0; j < plan_->dst_cells.size(); ++j) offer(plan_->dst_cells[j].tensor, plan_->dst_cells[j].cell, dst_bind_[j]);
+  }
+  std::vector<Digest> out;
+  for (uint32_t t = t_begin_; t < std::min<uint32_t>(t_end_, uint32_t(nt)); ++t) out.push_back(Digest{t, 0, 0});
+  std::atomic<size_t> next{0};
+  std::vector<std::exception_ptr> err;
+  std::mutex em;
+  auto work = [&] {
+    try {
+      std::vector<uint8_t> buf;
+      for (size_t i; (i = next.fetch_add(1)) < out.size();) {
+        const uint32_t t = out[i].tensor;
+        const TensorSpec& e = p.catalog.tensors[t];
+        const uint64_t w = dtype_width(e.dtype);
+        const Shape& shape = e.shape;
+        bool all = true;
+        for (auto* b : pick[t]) all &= b != nullptr;
+        if (!all) continue;
+        buf.assign(shape_elements(shape) * w, 0);
+        for (size_t c = 0; c < p.cells[t].size(); ++c) {
+          const CellBinding& b = *pick[t][c];
+          DeviceGuard g(ctx_.cuda_device(b.gpu));
+          const char* dev = static_cast<const char*>(b.arena == 0 ? src_base_[size_t(b.gpu)] : dst_base_[size_t(b.gpu)]) + b.offset;
+          const Range& box = p.cells[t][c];
+          Shape lo, ext = box.extents();
+          for (int d = 0; d < box.rank(); ++d) lo.push_back(box.dim(d).lo);
+          lower_box(ext, Shape(ext.size(), 0), ext, lo, shape, w, uint64_t(1) << 30,
+                    [&](uint64_t so, uint64_t dof, uint64_t sp, uint64_t dp, uint64_t rows, uint64_t run) {
+                      ck(cudaMemcpy2D(buf.data() + dof, rows > 1 ? dp : run, dev + so, rows > 1 ? sp : run, run, rows,
+                                      cudaMemcpyDeviceToHost),
+                         "digest d2h");
+                    });
+        }
+        out[i].fnv = fnv1a64(buf.data(), buf.size());
+        out[i].ok = 1;
+      }
+    } catch (...) {
+      std::lock_guard<std::mutex> g(em);
+      err.push_back(std::current_exception());
+    }
+  };
+  const size_t workers = std::max<size_t>(1, std::min<size_t>({out.size(), 16, std::max(1u, std::thread::hardware_concurrency())}));
+  std::vector<std::thread> th;
+  for (size_t k = 1; k < workers; ++k) th.emplace_back(work);
+  work();
+  for (auto& x : th) x.join();
+  if (!err.empty()) std::rethrow_exception(err.front());
+  return out;
 }
 
 // ---- broadcast (fan-out push) ----------------------------------------------------------------

@@ -97,6 +97,7 @@ struct CopyConfig {
   int stages = 7;               // bulk: shared-memory ring depth
   unsigned stage_bytes = 29696; // bulk: bytes per stage (tiles are cut to fit one stage); r09 A/B
   int host_chunks = 64;         // pipeline depth of the host-buffer path (run_host); r13 sweep
+  bool tensor = false;          // bulk_strided: strided 2-D pieces as TMA tensor boxes (K3T, RESHARD_TMA_TENSOR=1)
   int l2_hint = 0;              // bulk_strided: L2 evict_first on loads (1), stores (2), both (3); r25 A/B: 0 is best (loads evict_first -2.3 %)
   static CopyConfig from_env();
 };
@@ -187,6 +188,16 @@ class Executor {
   // destination cell on local GPUs (kept cells included).  Returns mismatching bytes.
   void fill_sources();
   uint64_t verify_destinations();
+  // ExecutionReport verification digests: per base tensor of the window,
+  // FNV-1a-64 of the tensor reassembled from one replica of each cell of side 0 (source
+  // layout) or 1 (destination layout), read back from the local GPUs (off the clock).
+  // End-to-end preservation <=> digests(0) == digests(1).
+  struct Digest {
+    uint32_t tensor;
+    uint32_t ok;   // 0: some cell is not held by a local GPU (no digest)
+    uint64_t fnv;
+  };
+  std::vector<Digest> digests(int side);
 
   void* arena_base(int gpu, int arena) const { return arena == 0 ? src_base_[size_t(gpu)] : dst_base_[size_t(gpu)]; }
   Context& context() const { return ctx_; }

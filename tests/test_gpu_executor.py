@@ -419,3 +419,54 @@ def test_cell_larger_than_4gib(rs, ctx):
     ex, t = _run(rs, ctx, plan, 1, 2)
     assert t[0]["bytes"] == 4 * n
     assert ex.verify() == 0
+
+
+def test_tma_tensor_path_bytes_exact(rs, orc, ctx, monkeypatch):
+    """K3T (RESHARD_TMA_TENSOR=1): strided row-mode pieces move as 3-D TMA tensor boxes
+    (cp.async.bulk.tensor, one instruction per box; UTMALDG/UTMASTG in SASS) — random
+    transitions with strided TP fragments, tile sizes that force partial boxes at the edges,
+    and BASELINE configs[0] (dim-1 TP merges of 1536-byte rows), every destination byte
+    equal to the oracle's."""
+    monkeypatch.setenv("RESHARD_TMA_TENSOR", "1")
+    rng = random.Random(99)
+    ents = [("param/w", 0, (48, 40), 1, 0), ("param/v", 1, (64, 96), 1, 0), ("exp_avg/w", 2, (24, 16), 0, 1),
+            ("param/big", 0, (40, 1152), 1, 1), ("param/ln", 0, (64,), -1, -1)]
+    for (T1, P1, D1), (T2, P2, D2) in [((2, 1, 1), (1, 2, 1)), ((4, 2, 1), (2, 2, 2)), ((1, 1, 1), (4, 1, 2)),
+                                       ((2, 2, 2), (4, 1, 1)), ((4, 1, 1), (2, 1, 1))]:
+        n1, n2 = T1 * P1 * D1, T2 * P2 * D2
+        a, b, plan, oa, ob, oplan = _pair(rs, orc, ents, (T1, P1, D1, DEV(n1)), (T2, P2, D2, DEV(n2)))
+        for tile in (4096, 65536, 256 << 10):
+            ex, _ = _run(rs, ctx, plan, n1, n2, tile)
+            ost, _ = oplan.apply(oa.fill(), n_threads=4)
+            _compare_with_oracle(rs, ctx, ex, b, ost, DEV(n2))
+            assert ex.verify() == 0
+            del ex
+    cat = rs.Catalog.gpt(768, 12, 1024, 50304, rs.FP32_ADAM)
+    a, b = cat.build_strategy(DEV(2), 2, 1, 1), cat.build_strategy(DEV(2), 1, 2, 1)
+    ex, t = _run(rs, ctx, rs.generate_plan(a, b), 2, 2)
+    assert ex.verify() == 0
+    assert rng is not None
+
+
+def test_execution_report_digests(rs, orc, ctx):
+    """ExecutionReport verification digests: per base tensor, FNV-1a-64 of
+    the tensor reassembled from the destination cells (one replica each) equals the digest
+    reassembled from the source cells and the oracle's digest of the generated base tensor
+    (End-to-end preservation) — for a reshard with splits, merges and DP
+    replicas, and for the Fig. 6 transition."""
+    cat = rs.Catalog.gpt(64, 4, 16, 128, rs.MIXED_ADAM)
+    ocat = orc.catalog_gpt(64, 4, 16, 128, 1)
+    for (T1, P1, D1), (T2, P2, D2) in [((4, 2, 1), (2, 2, 2)), ((2, 2, 2), (1, 4, 1)), ((1, 1, 1), (2, 1, 2))]:
+        n1, n2 = T1 * P1 * D1, T2 * P2 * D2
+        a, b = cat.build_strategy(DEV(n1), T1, P1, D1), cat.build_strategy(DEV(n2), T2, P2, D2)
+        ex, _ = _run(rs, ctx, rs.generate_plan(a, b), n1, n2)
+        src, dst = ex.digests(0), ex.digests(1)
+        assert len(dst) == len(cat) and src == dst
+        for t in range(0, len(cat), 7):
+            assert dst[t] == ocat.base_digest(t), f"tensor {t}"
+        del ex
+    entries = [("t1", 0, (6,), 0, 0), ("t2", 0, (6,), 0, 1)]
+    a, b, plan, oa, ob, oplan = _pair(rs, orc, entries, (2, 1, 1, DEV(2)), (3, 2, 1, DEV(6)))
+    ex, _ = _run(rs, ctx, plan, 2, 6)
+    ocat2 = orc.catalog(entries)
+    assert ex.digests(1) == {0: ocat2.base_digest(0), 1: ocat2.base_digest(1)} == ex.digests(0)
