@@ -253,8 +253,9 @@ int rs_executor_host_elapsed(rs_executor* e, int gpu, float* ms);
  * for one local GPU).  Replaces SPEC.md:501's "timestamps across all participating workers". */
 int rs_executor_world_ms(const rs_executor* e, float* ms);
 /* End to end through host buffers over every local GPU of a single-process world: H2D of every
- * src arena (all GPUs at once), world barrier, every GPU's kernels, world barrier, D2H of every
- * dst arena; *ms from the common start to the last D2H.  host_src / host_dst: n = world
+ * src arena (all GPUs at once), each GPU's kernels once its own src arena landed (a GPU's tiles
+ * read only its own src arena), world barrier, D2H of every dst arena; *ms from the common
+ * start to the last D2H.  host_src / host_dst: n = world
  * entries, indexed by world GPU (entries of non-local GPUs are ignored). */
 int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_src, void* const* host_dst, float* ms);
 /* ExecutionReport verification digests: per base tensor of the executor's

@@ -905,8 +905,10 @@ std::vector<Timing> Executor::wait() {
 }
 
 // End to end over every local GPU from one common start: H2D of each GPU's src arena (all GPUs
-// at once), a world barrier, every GPU's kernels, a world barrier, D2H of each dst arena; the
-// origin stream joins the last D2H.  Host buffers are indexed by world GPU (null: not local).
+// at once), each GPU's kernels as soon as ITS source landed (push: a GPU's tiles read only its
+// own src arena), a world barrier (every peer's pushes into a GPU's dst arena are done), D2H
+// of each dst arena; the origin stream joins the last D2H.  Host buffers are indexed by world
+// GPU (null: not local).
 float Executor::run_host_world(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst) {
   TraceRange trace_("Executor::run_host_world");
   if (local_.empty()) raise(Errc::DeviceUnavailable, "run_host_world: no local GPU");
@@ -938,7 +940,6 @@ float Executor::run_host_world(const std::vector<const void*>& host_src, const s
     }
     ck(cudaEventRecord(l->e_h2d, s), "cudaEventRecord");
   }
-  barrier(&Local::e_h2d);
   for (auto& l : local_) {
     DeviceGuard g(l->dev);
     launch_local(*l, stream_of(*l));

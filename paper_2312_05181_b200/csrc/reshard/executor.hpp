@@ -170,8 +170,9 @@ class Executor {
   // waited on by every other) to the end of the last local GPU's kernels, peer pushes included.
   float world_ms() const { return world_ms_; }
   // End to end through host buffers over every local GPU (multi-GPU single-process worlds,
-  // and one GPU): H2D of each src arena, world barrier, kernels, world barrier, D2H of each
-  // dst arena, all GPUs concurrently; returns the ms from the common start to the last D2H.
+  // and one GPU): H2D of each src arena, each GPU's kernels once its own src landed, world
+  // barrier, D2H of each dst arena, all GPUs concurrently; returns the ms from the common start
+  // to the last D2H.
   float run_host_world(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst);
   // End-to-end on host buffers (single-GPU world): H2D of the whole src arena from
   // `host_src`, the copy kernel, D2H of the whole dst arena into `host_dst`; CUDA events

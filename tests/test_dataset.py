@@ -270,7 +270,7 @@ def test_k8_schedule_restatement_matches_host_shuffle(rs):
 
 
 @pytest.mark.gpu
-def test_k8_gpu_shuffle_bit_identical(rs, ctx):
+def test_k8_gpu_shuffle_bit_identical(rs, orc, ctx):
     # 65_536 / 65_537: the window (64 Ki minimum) covers all or all but one iteration; 3M runs
     # many 6-round graph batches with the window 64 Ki
     for n, seed, ep in [(1, 3, 0), (2, 3, 1), (3, 7, 0), (1000, 0x5EED, 0), (65_536, 1, 1), (65_537, 2, 2),
@@ -280,6 +280,8 @@ def test_k8_gpu_shuffle_bit_identical(rs, ctx):
         got = np.empty(n, np.uint64)
         ctx.dtoh(0, got.ctypes.data, p, 8 * n)
         assert np.array_equal(got, rs.shuffle_epoch(n, seed, ep)), n
+        if n <= 200_000:  # and directly against the oracle's restated Fisher-Yates
+            assert np.array_equal(got, orc.shuffle_epoch(n, seed, ep)), n
         assert n < 3 or t["rounds"] >= 1
         ctx.free(0, p)
 
@@ -298,6 +300,7 @@ def test_config5_full_size_matches_oracle(rs, orc, ctx):
     samples[:, 2] = sb
     del k
     perm = rs.shuffle_epoch(n, 0x5EED, 0)
+    assert np.array_equal(perm, orc.shuffle_epoch(n, 0x5EED, 0))  # the host loop is the oracle's
     d_perm, d_samp = ctx.malloc(0, 8 * n), ctx.malloc(0, 24 * n)
     ctx.htod(0, d_samp, samples.ctypes.data, 24 * n)
     rs.shuffle_epoch_device(ctx, 0, n, 0x5EED, 0, d_perm)
