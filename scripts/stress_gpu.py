@@ -2,8 +2,10 @@
 """GPU stress run of the apply_plan data plane (beyond the suite's 200 transitions): random
 catalogs (rank 1-3, all dtypes, TP dims or replicated, up to 8 layers), random (T,P,D) pairs
 including fresh destination devices and failure recovery, random tile sizes, every copy
-kernel, and single-process worlds of 1, 2, 4 or 8 GPUs mapped onto cuda:0 (peer tiles, fan-out
-with mixed local / remote replicas, TMA peer stores on or off).  Every destination cell is
+kernel (K3T tensor-map tiles on or off), DP up to 8 (fan-out groups beyond kMaxFan), and
+single-process worlds of 1, 2, 4 or 8 GPUs mapped onto cuda:0 (peer tiles, K2 fan-out with
+mixed local / remote replicas, TMA peer stores on or off); every 10th case also checks the
+ExecutionReport digests (destination == source == the oracle's base-tensor FNV).  Every destination cell is
 compared with the oracle's apply_plan (bytes moved by the reference's slice / merge).
 
     python scripts/stress_gpu.py [--cases N] [--seed S] > stress.jsonl
@@ -45,9 +47,10 @@ def main() -> int:
     args = ap.parse_args()
     rng = random.Random(args.seed)
     orc = Oracle()
-    cfgs = [(T, P, D) for T in (1, 2, 3, 4) for P in (1, 2, 3) for D in (1, 2, 4) if T * P * D <= 8]
+    cfgs = [(T, P, D) for T in (1, 2, 3, 4) for P in (1, 2, 3) for D in (1, 2, 4, 8) if T * P * D <= 8]
     ctxs = {w: rs.Context(w, list(range(w)), [0] * w) for w in (1, 2, 4, 8)}
-    done, cells, t0, stats = 0, 0, time.time(), {"recovery": 0, "fresh": 0, "bulk_peer": 0}
+    done, cells, t0 = 0, 0, time.time()
+    stats = {"recovery": 0, "fresh": 0, "bulk_peer": 0, "tma_tensor": 0, "fanout_gt4": 0, "digest_checks": 0}
     while done < args.cases:
         ents = entries(rng)
         (T1, P1, D1), (T2, P2, D2) = rng.choice(cfgs), rng.choice(cfgs)
@@ -86,6 +89,8 @@ def main() -> int:
         os.environ["RESHARD_COPY_KERNEL"] = rng.choice(KERNELS)
         peer = rng.random() < 0.3
         os.environ["RESHARD_BULK_PEER"] = "1" if peer else "0"
+        tensor = rng.random() < 0.3  # K3T: strided pieces as TMA tensor boxes (bulk_strided only)
+        os.environ["RESHARD_TMA_TENSOR"] = "1" if tensor else "0"
         ctx = ctxs[world]
         # logical device -> world GPU: the device ordinal's index in the layout, mod world
         all_devs = sorted(set(d1) | set(d2))
@@ -98,6 +103,12 @@ def main() -> int:
         if ex.verify() != 0:
             print(json.dumps({"error": "verify mismatch", "case": done}), flush=True)
             return 1
+        if done % 10 == 0:  # ExecutionReport digests: destination == source == oracle
+            dd, sd = ex.digests(1), ex.digests(0)
+            if dd != sd or any(dd[t] != ocat.base_digest(t) for t in dd):
+                print(json.dumps({"error": "digest mismatch", "case": done}), flush=True)
+                return 1
+            stats["digest_checks"] += 1
         ost, _ = oplan.apply(oa.fill(), n_threads=4)
         for dev, t, c, bnd in ex.dst_cells():
             got = np.zeros(bnd.nbytes, np.uint8)
@@ -110,6 +121,8 @@ def main() -> int:
         stats["recovery"] += recovery
         stats["fresh"] += (not recovery) and d2[0][1] >= n1
         stats["bulk_peer"] += peer and world > 1
+        stats["tma_tensor"] += tensor and os.environ["RESHARD_COPY_KERNEL"] == "bulk_strided"
+        stats["fanout_gt4"] += D2 > 4
         done += 1
         if done % 100 == 0:
             print(json.dumps({"cases": done, "cells": cells, "s": round(time.time() - t0, 1)}), flush=True)
