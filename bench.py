@@ -929,11 +929,21 @@ def run_ours(args):
 
     # NVLink peak measured on this box (distinct GPUs only), else the NVLink 5 spec
     p2p = None
-    if world == 1 and N > 1 and not emulated and not args.no_p2p_probe:
-        try:
-            p2p = p2p_probe(rs, ctx, cuda_of)
-        except Exception as exc:  # noqa: BLE001
-            p2p = {"error": str(exc)[:200]}
+    if N > 1 and not emulated and not args.no_p2p_probe:
+        if world == 1:
+            try:
+                p2p = p2p_probe(rs, ctx, cuda_of)
+            except Exception as exc:  # noqa: BLE001
+                p2p = {"error": str(exc)[:200]}
+        else:  # one process per GPU: rank 0 probes every GPU of the node while the others wait
+            dist.barrier()
+            if rank == 0:
+                try:
+                    devs = list(range(min(N, torch.cuda.device_count())))
+                    p2p = p2p_probe(rs, rs.Context(len(devs), devs, devs), devs)
+                except Exception as exc:  # noqa: BLE001
+                    p2p = {"error": str(exc)[:200]}
+            dist.barrier()
     bw_nvl = p2p["peak"] if p2p and "peak" in p2p else 900.0
     bw_nvl_kind = "measured (p2p_probe)" if p2p and "peak" in p2p else "spec (NVLink 5: 900 GB/s per direction)"
     peak, peak_kind = measured_peaks()

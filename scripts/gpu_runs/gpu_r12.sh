@@ -1,6 +1,6 @@
 #!/bin/bash
 # r12: full GPU suite after the API-completeness work, default bench + reference arm, and the
-# random-gather probe that bounds K5.  Usage: gpurun -- 'bash scripts/gpu_r12.sh'
+# random-gather probe that bounds K5.  Usage: gpurun -- 'bash scripts/gpu_runs/gpu_r12.sh'
 set -u
 TAG=${1:-r12}
 OUT=gpurun_out/$TAG

@@ -1,6 +1,6 @@
 #!/bin/bash
 # r13: GPU suite (incl. full-size config 5 parity), bench with the PCIe probe, host-chunk
-# sweep of the e2e pipeline, K5 register/occupancy A/B.  Usage: gpurun -- 'bash scripts/gpu_r13.sh'
+# sweep of the e2e pipeline, K5 register/occupancy A/B.  Usage: gpurun -- 'bash scripts/gpu_runs/gpu_r13.sh'
 set -u
 TAG=${1:-r13}
 OUT=gpurun_out/$TAG

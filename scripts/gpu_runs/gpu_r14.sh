@@ -1,6 +1,6 @@
 #!/bin/bash
 # r14: GPU suite (central mode, reference fixtures on device), default bench, central-mode
-# bench, dataset bench with the random-gather floor.  Usage: gpurun -- 'bash scripts/gpu_r14.sh'
+# bench, dataset bench with the random-gather floor.  Usage: gpurun -- 'bash scripts/gpu_runs/gpu_r14.sh'
 set -u
 TAG=${1:-r14}
 OUT=gpurun_out/$TAG

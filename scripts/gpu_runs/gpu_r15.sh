@@ -1,6 +1,6 @@
 #!/bin/bash
 # r15: full GPU suite, default bench, K5 persistent (software-pipelined) variants:
-# same-box A/B + ncu.  Usage: gpurun -- 'bash scripts/gpu_r15.sh'
+# same-box A/B + ncu.  Usage: gpurun -- 'bash scripts/gpu_runs/gpu_r15.sh'
 set -u
 TAG=${1:-r15}
 OUT=gpurun_out/$TAG
