@@ -698,6 +698,36 @@ def p2p_probe(rs, ctx, cuda_of, nbytes: int = 1 << 30, reps: int = 3) -> dict:
     return out
 
 
+def world_e2e(rs, plan, src_gpu, dst_gpu, n_gpus, cuda_devs, tile, steps) -> dict:
+    """The step end to end from pinned host buffers through rs_executor_run_host_world, one
+    process driving every GPU (own context, arenas and executor; sources filled with K6 and
+    copied to the host buffers first, off the clock)."""
+    ctx = rs.Context(n_gpus, list(range(n_gpus)), list(cuda_devs))
+    ex = rs.Executor(ctx, plan, src_gpu, dst_gpu, tile)
+    ex.allocate_local()
+    ex.prepare()
+    ex.fill_sources()
+    hs, hd, s_tot, d_tot = [], [], 0, 0
+    try:
+        for g in range(n_gpus):
+            s_b, d_b = ex.arena_bytes(g)
+            s_tot, d_tot = s_tot + s_b, d_tot + d_b
+            hs.append(rs.host_alloc(max(s_b, 1)))
+            hd.append(rs.host_alloc(max(d_b, 1)))
+            ctx.dtoh(g, hs[g], ex.arenas[g][0], s_b)
+        ex.run_host_world(hs, hd)
+        ms = [ex.run_host_world(hs, hd) for _ in range(steps)]
+        bad = ex.verify()
+    finally:
+        for p in hs + hd:
+            rs.host_free(p)
+        del ex
+    return {"value": round(statistics.mean(ms), 3), "unit": "ms", "h2d_bytes_per_step": s_tot, "d2h_bytes_per_step": d_tot,
+            "steps": steps, "mismatched_bytes": bad,
+            "path": "rs_executor_run_host_world from one process driving every GPU: pipelined rounds of H2D | "
+                    "pushes | D2H (RESHARD_WORLD_PIPELINE=0: three phases)"}
+
+
 def run_ours(args):
     import paper_2312_05181_b200 as rs
 
@@ -877,7 +907,8 @@ def run_ours(args):
                     hs_l, hd_l = [hs[g] for g in range(N)], [hd[g] for g in range(N)]
                     ex.run_host_world(hs_l, hd_l)
                     e2e_ms = [ex.run_host_world(hs_l, hd_l) for _ in range(args.e2e_steps)]
-                    path = "rs_executor_run_host_world: H2D of every src arena | kernels | D2H of every dst arena"
+                    path = ("rs_executor_run_host_world: pipelined rounds of H2D | pushes | D2H over every GPU "
+                            "(RESHARD_WORLD_PIPELINE=0: three phases)")
                 bad_e2e = ex.verify()
                 d_eff = sum(d_need.values()) - ex.staging_bytes()
                 e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms",
@@ -926,6 +957,20 @@ def run_ours(args):
         e2e = {"value": round(float(t.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(totals[0].item()),
                "d2h_bytes_per_step": int(totals[1].item()), "steps": args.e2e_steps,
                "path": "per rank: H2D | barrier | kernels | barrier | D2H (rs_executor_host_phase), max over ranks"}
+        # the same step through the single-process world API (rank 0 drives every GPU of the node,
+        # pipelined rounds) while the other ranks wait; the line reports the faster of the two
+        dist.barrier()
+        world_line = None
+        if rank == 0:
+            try:
+                devs = list(cuda_of) * N if emulated else list(range(N))
+                world_line = world_e2e(rs, plan, src_gpu, dst_gpu, N, devs[:N], tile, args.e2e_steps)
+            except Exception as exc:  # noqa: BLE001
+                world_line = {"error": str(exc)[:200]}
+        dist.barrier()
+        if rank == 0 and world_line and world_line.get("value") and world_line["mismatched_bytes"] == 0:
+            e2e = dict(world_line, per_rank_phases=e2e) if world_line["value"] < e2e["value"] else \
+                dict(e2e, world_api=world_line)
 
     # NVLink peak measured on this box (distinct GPUs only), else the NVLink 5 spec
     p2p = None
@@ -944,8 +989,11 @@ def run_ours(args):
                 except Exception as exc:  # noqa: BLE001
                     p2p = {"error": str(exc)[:200]}
             dist.barrier()
-    bw_nvl = p2p["peak"] if p2p and "peak" in p2p else 900.0
-    bw_nvl_kind = "measured (p2p_probe)" if p2p and "peak" in p2p else "spec (NVLink 5: 900 GB/s per direction)"
+    # the NVLink denominator: the P2P peak measured on this box, else the pool's measured peer copy
+    # (B200_PROFILING.md: 770 GB/s per direction; 900 nominal)
+    bw_nvl = p2p["peak"] if p2p and "peak" in p2p else 770.0
+    bw_nvl_kind = ("measured on this box (p2p_probe)" if p2p and "peak" in p2p
+                   else "fallback: B200_PROFILING.md measured peer copy, 770 GB/s per direction (900 nominal)")
     peak, peak_kind = measured_peaks()
 
     def fabric_of(rows, rbs, n, bw_link):
@@ -967,11 +1015,15 @@ def run_ours(args):
         if n_native > 1:
             _, _, _, nplan, nsrc, ndst = build_plan(rs, args.workload, n_native)
             pex = rs.Executor(rs.Context(n_native, [], []), nplan, nsrc, ndst, tile)
-            t_roof, worst, _ = fabric_of([pex.bytes_to(g) for g in range(n_native)],
-                                         [pex.read_bytes(g) for g in range(n_native)], n_native, 900.0)
+            rows_n = [pex.bytes_to(g) for g in range(n_native)]
+            rbs_n = [pex.read_bytes(g) for g in range(n_native)]
+            t_roof, worst, _ = fabric_of(rows_n, rbs_n, n_native, 900.0)
+            t_roof_770, _, _ = fabric_of(rows_n, rbs_n, n_native, 770.0)
             fabric = {"derived_for_gpus": n_native, "t_roof_ms": round(t_roof, 3), "bottleneck": worst,
+                      "t_roof_ms_at_measured_peer_copy": round(t_roof_770, 3),
                       "note": "not measured: SURVEY 8d's T_roof of this plan on its own GPU count (NVLink 900 GB/s "
-                              "per direction, measured HBM peak), for comparison with the 1-GPU emulation above"}
+                              "per direction nominal; 770 GB/s = the pool's measured peer copy; measured HBM peak), "
+                              "for comparison with the 1-GPU emulation above"}
     else:
         t_roof, worst, terms = fabric_of(rows, rbs, N, bw_nvl)
         fabric = {"t_roof_ms": round(t_roof, 3), "frac": round(t_roof / ms, 4) if ms and not emulated else None,

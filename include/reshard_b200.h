@@ -252,10 +252,13 @@ int rs_executor_host_elapsed(rs_executor* e, int gpu, float* ms);
  * GPU's kernels, peer pushes included (single-process multi-GPU worlds; = the GPU's own time
  * for one local GPU).  Replaces SPEC.md:501's "timestamps across all participating workers". */
 int rs_executor_world_ms(const rs_executor* e, float* ms);
-/* End to end through host buffers over every local GPU of a single-process world: H2D of every
- * src arena (all GPUs at once), each GPU's kernels once its own src arena landed (a GPU's tiles
- * read only its own src arena), world barrier, D2H of every dst arena; *ms from the common
- * start to the last D2H.  host_src / host_dst: n = world
+/* End to end through host buffers over every local GPU of a single-process world, from one
+ * common start to the last D2H (*ms).  Default: pipelined rounds — every GPU's tile lists cut
+ * into chunks; round k uploads the source ranges chunk k first reads, runs chunk k on every GPU,
+ * and once chunk k is done everywhere moves down each dst-arena prefix no later chunk writes,
+ * so H2D, pushes and D2H overlap on every link.  RESHARD_WORLD_PIPELINE=0 (or a world with
+ * non-local GPUs): H2D of every src arena, each GPU's kernels once its own src arena landed,
+ * world barrier, D2H of every dst arena.  host_src / host_dst: n = world
  * entries, indexed by world GPU (entries of non-local GPUs are ignored). */
 int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_src, void* const* host_dst, float* ms);
 /* ExecutionReport verification digests: per base tensor of the executor's

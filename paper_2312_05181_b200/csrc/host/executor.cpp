@@ -327,6 +327,17 @@ struct Executor::Local {
   std::vector<DevPiece> chunk_pieces;  // the one tile list the host pipeline cuts into chunks (lazy)
   bool chunks_ready = true;           // chunks planned (or not applicable)
   bool chunk_fan = false;             // chunk_pieces feed the bulk kernel (else the aligned LDG kernel)
+  // world host pipeline (run_host_world): the piece lists per kernel (0 K3 bulk, 1 aligned LDG,
+  // 2 misaligned, 3 K2 fan-out), their chunks, and per round the end of this GPU's dst-arena
+  // prefix that no later chunk of any GPU writes
+  std::vector<DevPiece> lists[4];
+  struct WorldChunk {
+    uint64_t t0[4] = {0, 0, 0, 0}, t1[4] = {0, 0, 0, 0};
+    std::vector<std::pair<uint64_t, uint64_t>> uploads;  // src arena ranges first read by this chunk
+  };
+  std::vector<WorldChunk> wchunks;
+  std::vector<uint64_t> wsafe;
+  std::vector<cudaEvent_t> wev;  // per chunk: H2D landed, kernels done (2K events)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaStream_t s_aux = nullptr;                       // LDG/STG tiles beside the bulk kernel
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -842,6 +853,8 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   l->n_fanl = nl;
   l->bytes = bytes;
   l->read_bytes = read_bytes;
+  l->lists[0] = std::move(fanp), l->lists[1] = std::move(alignedp), l->lists[2] = std::move(miscp), l->lists[3] = std::move(fanlp);
+  world_chunks_ready_ = false;
 }
 
 void Executor::run() {
@@ -909,8 +922,97 @@ std::vector<Timing> Executor::wait() {
 // own src arena), a world barrier (every peer's pushes into a GPU's dst arena are done), D2H
 // of each dst arena; the origin stream joins the last D2H.  Host buffers are indexed by world
 // GPU (null: not local).
+// The world host pipeline's chunks (lazy, first run_host_world): every local GPU's tile lists
+// cut into K chunks of equal tile counts (lists are in destination order); per chunk the source
+// ranges it first reads (uploaded in chunk order) and, per destination GPU, the lowest offset it
+// writes.  After round k (chunk k done on every GPU) a GPU's dst arena is final below the lowest
+// offset any later chunk of any GPU writes: that prefix goes down while later rounds run.
+bool Executor::plan_world_chunks() {
+  world_chunks_ready_ = true;
+  world_pipelined_ = false;
+  if (central_ >= 0 || cfg_.kernel == CopyKernel::Bulk) return false;  // interleaved tiles: no sub-ranges
+  for (auto& l : local_)
+    if (l->n_tensor) return false;
+  const size_t K = size_t(std::max(1, cfg_.host_chunks / 4));  // rounds
+  const int G = ctx_.world();
+  // absolute dst address -> (world GPU, arena offset)
+  std::vector<std::pair<uint64_t, int>> bases;
+  for (int j = 0; j < G; ++j)
+    if (dst_base_[size_t(j)] && dst_size_[size_t(j)]) bases.emplace_back(uint64_t(reinterpret_cast<uintptr_t>(dst_base_[size_t(j)])), j);
+  std::sort(bases.begin(), bases.end());
+  auto locate = [&](uint64_t a, int& j, uint64_t& off) {
+    auto it = std::upper_bound(bases.begin(), bases.end(), std::make_pair(a, INT32_MAX));
+    if (it == bases.begin()) return false;
+    --it;
+    j = it->second, off = a - it->first;
+    return off < dst_size_[size_t(j)];
+  };
+  // min_dst[g][j][k]: lowest offset of GPU j's dst arena written by chunk k of local GPU g
+  std::vector<std::vector<std::vector<uint64_t>>> min_dst(local_.size(), std::vector<std::vector<uint64_t>>(size_t(G), std::vector<uint64_t>(K, UINT64_MAX)));
+  for (size_t li = 0; li < local_.size(); ++li) {
+    Local& l = *local_[li];
+    l.wchunks.assign(K, {});
+    const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[size_t(l.world)]));
+    const uint64_t n[4] = {l.n_fan, l.n_aligned, l.n_misc, l.n_fanl};
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(K);
+    for (int i = 0; i < 4; ++i) {
+      for (size_t k = 0; k < K; ++k) l.wchunks[k].t0[i] = n[i] * k / K, l.wchunks[k].t1[i] = n[i] * (k + 1) / K;
+      uint64_t t = 0;
+      size_t k = 0;
+      for (const DevPiece& q : l.lists[i]) {
+        const uint64_t nt = piece_tile_count(q.rows, q.row_bytes, q.per, q.tile);
+        for (uint64_t u = 0; u < nt; ++u, ++t) {
+          while (k + 1 < K && t >= l.wchunks[k].t1[i]) ++k;
+          uint64_t r0, cc;
+          uint32_t nr, nb;
+          piece_tile(q.rows, q.row_bytes, q.per, q.tile, u, r0, cc, nr, nb);
+          const uint64_t s0 = q.src + r0 * q.src_pitch + cc - sb, s1 = s0 + (nr ? (nr - 1) * q.src_pitch : 0) + nb;
+          auto& sv = spans[k];
+          if (!sv.empty() && s0 >= sv.back().first && s0 <= sv.back().second) sv.back().second = std::max(sv.back().second, s1);
+          else sv.emplace_back(s0, s1);
+          for (uint32_t d = 0; d < q.n_dst; ++d) {
+            int j;
+            uint64_t off;
+            if (!locate(q.dst[d] + r0 * q.dst_pitch[d] + cc, j, off)) return false;  // not a dst arena: no pipeline
+            uint64_t& m = min_dst[li][size_t(j)][k];
+            m = std::min(m, off);
+          }
+        }
+      }
+    }
+    std::vector<HostChunk> hc(K);
+    plan_uploads(hc, spans);
+    for (size_t k = 0; k < K; ++k) l.wchunks[k].uploads = std::move(hc[k].uploads);
+    while (l.wev.size() < 2 * K) {
+      DeviceGuard g(l.dev);
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      l.wev.push_back(e);
+    }
+  }
+  // every destination GPU must be local (the D2H side): single-process worlds only
+  for (auto& l : local_) {
+    const size_t j = size_t(l->world);
+    l->wsafe.assign(K, dst_size_[j]);
+    uint64_t m = dst_size_[j];
+    for (size_t k = K; k-- > 0;) {
+      l->wsafe[k] = m;  // final below m once rounds 0..k are done
+      for (size_t li = 0; li < local_.size(); ++li) m = std::min(m, min_dst[li][j][k]);
+    }
+  }
+  world_pipelined_ = true;
+  return true;
+}
+
 float Executor::run_host_world(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst) {
   TraceRange trace_("Executor::run_host_world");
+  // RESHARD_WORLD_PIPELINE=0: the three-phase form below (A/B); default: pipelined rounds
+  // whenever every GPU of the world is local and the tile lists can be cut into sub-ranges
+  const char* pv = std::getenv("RESHARD_WORLD_PIPELINE");
+  if (!(pv && std::string(pv) == "0") && local_.size() == size_t(ctx_.world())) {
+    if (!world_chunks_ready_) plan_world_chunks();
+    if (world_pipelined_) return run_host_world_pipelined(host_src, host_dst);
+  }
   if (local_.empty()) raise(Errc::DeviceUnavailable, "run_host_world: no local GPU");
   if (central_ >= 0) raise(Errc::InvalidArgument, "run_host_world: distributed mode only");
   if (host_src.size() != size_t(ctx_.world()) || host_dst.size() != size_t(ctx_.world()))
@@ -964,6 +1066,110 @@ float Executor::run_host_world(const std::vector<const void*>& host_src, const s
     DeviceGuard gl(l->dev);
     ck(cudaEventSynchronize(l->e_d2h), "cudaEventSynchronize");
   }
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, ws, we), "cudaEventElapsedTime");
+  return ms;
+}
+
+// Rounds k = 0..K-1 over every local GPU g: the H2D of the source ranges chunk k of g first
+// reads (g's upload stream), chunk k of g's tile lists once they landed (g's stream), then on
+// every GPU j's download stream — after chunk k is done on EVERY GPU (cross-device event waits)
+// — the D2H of j's dst-arena bytes that no later chunk writes.  H2D, kernels and D2H of
+// different rounds overlap on every link; peers' pushes are ordered by the events.
+float Executor::run_host_world_pipelined(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst) {
+  if (host_src.size() != size_t(ctx_.world()) || host_dst.size() != size_t(ctx_.world()))
+    raise(Errc::InvalidArgument, "run_host_world: one host buffer pair per world GPU");
+  const size_t K = local_[0]->wchunks.size();
+  auto ws = static_cast<cudaEvent_t>(w_start_), we = static_cast<cudaEvent_t>(w_stop_);
+  auto origin = static_cast<cudaStream_t>(ctx_.stream(local_[0]->world));
+  auto stream_of = [&](const Local& l) { return static_cast<cudaStream_t>(ctx_.stream(l.world)); };
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    if (!l->s_h2d) {
+      ck(cudaStreamCreateWithFlags(&l->s_h2d, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&l->s_d2h, cudaStreamNonBlocking), "stream");
+    }
+    const size_t w = size_t(l->world);
+    if (src_size_[w] && !host_src[w]) raise(Errc::InvalidArgument, "run_host_world: null host source for a local GPU");
+    if (dst_size_[w] && !host_dst[w]) raise(Errc::InvalidArgument, "run_host_world: null host destination for a local GPU");
+  }
+  {
+    DeviceGuard g(local_[0]->dev);
+    ck(cudaEventRecord(ws, origin), "cudaEventRecord");
+  }
+  for (auto& l : local_) {
+    DeviceGuard g(l->dev);
+    for (cudaStream_t s : {stream_of(*l), l->s_h2d, l->s_d2h})
+      if (s != origin) ck(cudaStreamWaitEvent(s, ws, 0), "common start");
+  }
+  std::vector<uint64_t> down(local_.size(), 0);
+  for (size_t k = 0; k < K; ++k) {
+    for (auto& l : local_) {
+      DeviceGuard g(l->dev);
+      const size_t w = size_t(l->world);
+      char* dsrc = static_cast<char*>(src_base_[w]);
+      const char* hsrc = static_cast<const char*>(host_src[w]);
+      for (auto [off, len] : l->wchunks[k].uploads)
+        ck(cudaMemcpyAsync(dsrc + off, hsrc + off, len, cudaMemcpyHostToDevice, l->s_h2d), "h2d piece");
+      ck(cudaEventRecord(l->wev[k], l->s_h2d), "event");
+      cudaStream_t s = stream_of(*l);
+      ck(cudaStreamWaitEvent(s, l->wev[k], 0), "wait h2d");
+      const int sms = ctx_.sm_count(l->world);
+      const auto& c = l->wchunks[k];
+      cuda::launch_bulk(l->d_fan + c.t0[0], c.t1[0] - c.t0[0], cfg_, sms, s);
+      cuda::launch_copy(l->d_tiles + c.t0[1], c.t1[1] - c.t0[1], cfg_, sms, true, s);
+      cuda::launch_copy(l->d_tiles + l->n_aligned + c.t0[2], c.t1[2] - c.t0[2], cfg_, sms, false, s);
+      cuda::launch_copy_fan(l->d_fanl + c.t0[3], c.t1[3] - c.t0[3], cfg_, sms, s);
+      ck(cudaEventRecord(l->wev[K + k], s), "event");
+    }
+    for (size_t lj = 0; lj < local_.size(); ++lj) {
+      Local& j = *local_[lj];
+      DeviceGuard g(j.dev);
+      const size_t w = size_t(j.world);
+      const uint64_t safe = j.wsafe[k];
+      if (safe <= down[lj]) continue;
+      for (auto& l : local_) ck(cudaStreamWaitEvent(j.s_d2h, l->wev[K + k], 0), "wait round");
+      ck(cudaMemcpyAsync(static_cast<char*>(host_dst[w]) + down[lj], static_cast<char*>(dst_base_[w]) + down[lj], safe - down[lj],
+                         cudaMemcpyDeviceToHost, j.s_d2h),
+         "d2h piece");
+      down[lj] = safe;
+    }
+  }
+  for (size_t lj = 0; lj < local_.size(); ++lj) {  // the tail, and the source bytes no tile reads
+    Local& j = *local_[lj];
+    DeviceGuard g(j.dev);
+    const size_t w = size_t(j.world);
+    if (dst_size_[w] > down[lj]) {
+      for (auto& l : local_) ck(cudaStreamWaitEvent(j.s_d2h, l->wev[2 * K - 1], 0), "wait last round");
+      ck(cudaMemcpyAsync(static_cast<char*>(host_dst[w]) + down[lj], static_cast<char*>(dst_base_[w]) + down[lj],
+                         dst_size_[w] - down[lj], cudaMemcpyDeviceToHost, j.s_d2h),
+         "d2h tail");
+    }
+    std::vector<std::pair<uint64_t, uint64_t>> all;
+    for (auto& c : j.wchunks)
+      for (auto [off, len] : c.uploads) all.emplace_back(off, off + len);
+    std::sort(all.begin(), all.end());
+    uint64_t cur = 0;
+    char* dsrc = static_cast<char*>(src_base_[w]);
+    const char* hsrc = static_cast<const char*>(host_src[w]);
+    for (auto [a, b] : all) {
+      if (a > cur) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, a - cur, cudaMemcpyHostToDevice, j.s_h2d), "h2d rest");
+      cur = std::max(cur, b);
+    }
+    if (cur < src_size_[w]) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, src_size_[w] - cur, cudaMemcpyHostToDevice, j.s_h2d), "h2d rest");
+  }
+  DeviceGuard g(local_[0]->dev);
+  for (auto& l : local_) {
+    for (cudaStream_t s : {l->s_h2d, l->s_d2h, stream_of(*l)}) {
+      if (s == origin) continue;
+      DeviceGuard gl(l->dev);
+      ck(cudaEventRecord(l->e_d2h, s), "event");
+      DeviceGuard g0(local_[0]->dev);
+      ck(cudaStreamWaitEvent(origin, l->e_d2h, 0), "join");
+    }
+  }
+  ck(cudaEventRecord(we, origin), "cudaEventRecord");
+  ck(cudaEventSynchronize(we), "cudaEventSynchronize");
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, ws, we), "cudaEventElapsedTime");
   return ms;

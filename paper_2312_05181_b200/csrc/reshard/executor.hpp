@@ -231,6 +231,8 @@ class Executor {
   void build_central(const SrcLookup& src_lookup);
   void lower_tiles(Local& l, const std::vector<Logical>& lt, bool host_chunks);
   void plan_host_chunks(Local& l);
+  bool plan_world_chunks();
+  float run_host_world_pipelined(const std::vector<const void*>& host_src, const std::vector<void*>& host_dst);
   uint64_t payload_pass(const std::vector<std::vector<cuda::PayloadTask>>& per_local, bool verify);
 
   Context& ctx_;
@@ -250,6 +252,7 @@ class Executor {
   void* w_start_ = nullptr;  // cudaEvent_t on local_[0]'s device: world marks
   void* w_stop_ = nullptr;
   float world_ms_ = 0;
+  bool world_chunks_ready_ = false, world_pipelined_ = false;
 };
 
 // DP replication as a single push (SURVEY §8(b) rs_broadcast): `bytes` at `src` on world GPU

@@ -470,3 +470,48 @@ def test_execution_report_digests(rs, orc, ctx):
     ex, _ = _run(rs, ctx, plan, 2, 6)
     ocat2 = orc.catalog(entries)
     assert ex.digests(1) == {0: ocat2.base_digest(0), 1: ocat2.base_digest(1)} == ex.digests(0)
+
+
+@pytest.mark.parametrize("pipeline", ["1", "0"])
+def test_run_host_world_matches_device_result(rs, pipeline, monkeypatch):
+    """e2e through rs_executor_run_host_world over a 4- and an 8-GPU world in one process (all
+    world GPUs on cuda:0): pipelined rounds (default) and the three-phase form.  Every source
+    byte comes from the host buffers (device src arenas zeroed first), every destination cell
+    verifies, and every GPU's host dst buffer equals its device dst arena (prefixes moved down
+    while later rounds still push into the same arena included)."""
+    monkeypatch.setenv("RESHARD_WORLD_PIPELINE", pipeline)
+    cat = rs.Catalog.gpt(256, 6, 64, 1024, rs.MIXED_ADAM)
+    for world, (a_cfg, b_cfg) in [(4, ((2, 1, 1, 2), (2, 1, 2, 4))), (8, ((4, 2, 1, 8), (2, 2, 2, 8))),
+                                  (4, ((2, 2, 2, 8), (4, 1, 1, 4)))]:
+        ctx = rs.Context(world, list(range(world)), [0] * world)
+        a = cat.build_strategy(DEV(a_cfg[3]), *a_cfg[:3])
+        b = cat.build_strategy(DEV(b_cfg[3]), *b_cfg[:3])
+        ex = rs.Executor(ctx, rs.generate_plan(a, b), [d % world for d in range(a_cfg[3])],
+                         [d % world for d in range(b_cfg[3])], 16 << 10)
+        ex.allocate_local()
+        ex.prepare()
+        ex.fill_sources()
+        hs, hd, sz = [0] * world, [0] * world, {}
+        for g in range(world):
+            s_b, d_b = ex.arena_bytes(g)
+            sz[g] = (s_b, d_b)
+            hs[g], hd[g] = rs.host_alloc(max(s_b, 1)), rs.host_alloc(max(d_b, 1))
+            sp, dp = ex.arenas[g]
+            ctx.dtoh(g, hs[g], sp, s_b)
+            ctx.memset(g, sp, 0, s_b)
+            ctx.memset(g, dp, 0, d_b)
+        ms = ex.run_host_world(hs, hd)
+        assert ms > 0
+        assert ex.verify() == 0
+        for g in range(world):
+            d_b = sz[g][1]
+            if not d_b:
+                continue
+            dev = np.zeros(d_b, np.uint8)
+            ctx.dtoh(g, dev.ctypes.data, ex.arenas[g][1], d_b)
+            host = np.ctypeslib.as_array((ctypes.c_uint8 * d_b).from_address(hd[g]))
+            assert np.array_equal(dev, host), f"world {world} GPU {g}"
+        for g in range(world):
+            rs.host_free(hs[g])
+            rs.host_free(hd[g])
+        del ex

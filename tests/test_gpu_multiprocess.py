@@ -35,6 +35,10 @@ def test_two_ranks_one_gpu_ipc_push(kernel):
     line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["verify_mismatched_bytes"] == 0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0  # multi-rank host-buffer path ran
+    # both host-buffer forms ran: per-rank phases and rank 0's single-process world API
+    assert "world_api" in line["e2e"] or "per_rank_phases" in line["e2e"]
+    world = line["e2e"].get("world_api", line["e2e"])
+    assert world["mismatched_bytes"] == 0 and "run_host_world" in world["path"]
     assert line["fabric"]["t_roof_ms"] > 0 and line["fabric"]["bottleneck"]["term"] in ("hbm", "nvlink_in", "nvlink_out")
 
 
