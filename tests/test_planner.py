@@ -266,3 +266,29 @@ def test_catalog_mismatch(rs):
     with pytest.raises(rs.ReshardError) as e:
         rs.generate_plan(c1.build_strategy(DEV(1), 1, 1, 1), c2.build_strategy(DEV(1), 1, 1, 1))
     assert e.value.name == "CatalogMismatch"
+
+
+def test_fanout_sources_read_once_config3(rs):
+    """on a planning-only 8-GPU context for BASELINE configs[2] (GPT-3
+    6.7B (4,2,1)->(2,2,2)), the bytes the executing GPUs read (rs_executor_read_bytes summed
+    over GPUs) equal the source boxes read ONCE: the union of the Moves' (source device,
+    tensor, box) — every DP-replicated fragment feeds both replicas from one read (K3 fan-out
+    tiles locally, K2 copy_fan_v16_kernel when a replica is on a peer), and every resident
+    relayout fragment is also the source of a Move to the other replica.  Writes are every
+    Move and relayout byte once (proj/src/tensor/tensor.cpp:61-78: one slice per source box)."""
+    import re
+
+    import bench
+
+    cat, a, b, plan, src_gpu, dst_gpu = bench.build_plan(rs, "gpt3-6.7b-tp4pp2-to-tp2pp2dp2", 8)
+    ex = rs.Executor(rs.Context(8, [], []), plan, src_gpu, dst_gpu)
+    st = plan.stats()
+    boxes = {}
+    for ln in plan.text().splitlines():
+        if ln.startswith("MOVE"):
+            m = re.match(r"MOVE t=(\S+) r=(\S+) (\S+) -> (\S+) bytes=(\d+)", ln)
+            boxes[(m.group(3), m.group(1), m.group(2))] = int(m.group(5))
+    reads = sum(ex.read_bytes(g) for g in range(8))
+    writes = sum(sum(ex.bytes_to(g)) for g in range(8))
+    assert reads == sum(boxes.values()) == 93_220_651_008
+    assert writes == st["moved_bytes"] + st["relayout_bytes"]  # ~2x: both DP replicas from one read
