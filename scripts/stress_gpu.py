@@ -47,7 +47,7 @@ def main() -> int:
     args = ap.parse_args()
     rng = random.Random(args.seed)
     orc = Oracle()
-    cfgs = [(T, P, D) for T in (1, 2, 3, 4) for P in (1, 2, 3) for D in (1, 2, 4, 8) if T * P * D <= 8]
+    cfgs = [(T, P, D) for T in (1, 2, 3, 4, 8) for P in (1, 2, 3) for D in (1, 2, 4, 8) if T * P * D <= 8]
     ctxs = {w: rs.Context(w, list(range(w)), [0] * w) for w in (1, 2, 4, 8)}
     done, cells, t0 = 0, 0, time.time()
     stats = {"recovery": 0, "fresh": 0, "bulk_peer": 0, "tma_tensor": 0, "fanout_gt4": 0, "digest_checks": 0}
