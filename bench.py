@@ -698,6 +698,15 @@ def p2p_probe(rs, ctx, cuda_of, nbytes: int = 1 << 30, reps: int = 3) -> dict:
     return out
 
 
+def pinned_total(dist, local, nbytes: int) -> int:
+    """Pinned host bytes every rank of the world would allocate (all ranks call this)."""
+    import torch
+
+    t = torch.tensor([float(nbytes)], dtype=torch.float64, device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t)
+    return int(t.item())
+
+
 def world_e2e(rs, plan, src_gpu, dst_gpu, n_gpus, cuda_devs, tile, steps) -> dict:
     """The step end to end from pinned host buffers through rs_executor_run_host_world, one
     process driving every GPU (own context, arenas and executor; sources filled with K6 and
@@ -933,6 +942,8 @@ def run_ours(args):
                 for g in mine:
                     rs.host_free(hs[g])
                     rs.host_free(hd[g])
+    elif pinned_total(dist, local, s_need[rank] + d_need[rank]) > 0.6 * host_available_bytes():
+        e2e = {"value": None, "unit": "ms", "note": "pinned host buffers of all ranks exceed 60% of host RAM"}
     else:
         # one process per GPU: H2D of its src arena | barrier | push kernels | barrier | D2H of
         # its dst arena; CUDA events mark to mark on each rank's stream, max over ranks
@@ -1081,6 +1092,7 @@ def run_ours(args):
         "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4),
         "tiles": sum(ex.tiles(g)[0] for ex in exs for g in mine),
         "host_ms": {"plan": round(build_plan.plan_ms, 2), "lower": round(lower_ms, 2), "prepare": round(prepare_ms, 2),
+                    "reconfiguration_total_ms": round(build_plan.plan_ms + lower_ms + prepare_ms + ms, 2),
                     "note": "off the clock, once per reconfiguration: Alg. 1 planning, arena layout + piece "
                             "lowering, descriptor binding + upload + device expansion"},
     }
