@@ -827,18 +827,51 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
+    # one process per GPU: a common start and the last rank's end on the device, through
+    # interprocess events — rank 0 records start + "go", every other rank's stream waits on "go"
+    # before its kernels and records its "done", rank 0's stream waits on every "done" and records
+    # the end (SPEC.md:501's two barriers; host barriers only order the enqueues)
+    if dist is not None:
+        go = rs.Event(ctx, rank, "ipc") if rank == 0 else None
+        done = rs.Event(ctx, rank, "ipc")
+        handles = [None] * world
+        dist.all_gather_object(handles, (go.handle if go else None, done.handle))
+        if rank == 0:
+            peers_done = [rs.Event(ctx, 0, "ipc", handles[r][1]) for r in range(1, world)]
+            t_start, t_end = rs.Event(ctx, 0), rs.Event(ctx, 0)
+        else:
+            go_peer = rs.Event(ctx, rank, "ipc", handles[0][0])
+
     def step(verify=False):
         """One reshard: every wave from a barrier (every GPU idle, every rank here), timed from
         one common start to the last GPU's completion (single process: world events; one
-        process per GPU: this GPU's events, max over ranks afterwards)."""
+        process per GPU: interprocess events into rank 0's timeline; the max over ranks of each
+        rank's own kernel time beside it)."""
         ms, gpu_ms, bad, launches = 0.0, 0.0, 0, 0
         for ex in exs:
             if len(exs) > 1:
                 ex.fill_sources()  # the window's sources (off the clock)
             barrier()
-            ex.run()
-            t = ex.wait()
-            ms += ex.world_ms()
+            if dist is not None:
+                if rank == 0:
+                    t_start.record()
+                    go.record()
+                dist.barrier()  # "go" is enqueued before anyone waits on it
+                if rank != 0:
+                    go_peer.wait()
+                ex.run()
+                done.record()
+                dist.barrier()  # every "done" is enqueued before rank 0 waits on them
+                if rank == 0:
+                    for e in peers_done:
+                        e.wait()
+                    t_end.record()
+                t = ex.wait()
+                ms += t_end.elapsed_since(t_start) if rank == 0 else 0.0
+            else:
+                ex.run()
+                t = ex.wait()
+                ms += ex.world_ms()
             gpu_ms += max(x["ms"] for x in t)
             launches += sum(x["launches"] for x in t)
             if verify and len(exs) > 1:
@@ -860,12 +893,12 @@ def run_ours(args):
             bad_w += b_i
         barrier()
         wall = time.perf_counter() - t0
-    if dist is not None:  # per step: the slowest rank (each rank's steps start at a common barrier)
+    if dist is not None:  # per step: rank 0's world time; the slowest rank's own kernel time beside it
         dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
-        tt = torch.tensor(step_ms + [float(launches_total)], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt[:-1], op=dist.ReduceOp.MAX)
-        step_ms = [float(x) for x in tt[:-1].tolist()]
-        gpu_step_ms = list(step_ms)
+        tt = torch.tensor(step_ms + gpu_step_ms, dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = [float(x) for x in tt[:args.steps].tolist()]
+        gpu_step_ms = [float(x) for x in tt[args.steps:].tolist()]
         lt = torch.tensor([float(launches_total)], dtype=torch.float64, device=dev)
         dist.all_reduce(lt)
         launches_total = int(lt.item())
@@ -1079,7 +1112,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 payload of the model shapes)",
         "config": workload_config(args.workload, N, args.mode),
         "timing": ("one process: common start event on GPU 0, every GPU waits on it, GPU 0 joins every GPU's end"
-                   if world == 1 else "one process per GPU: per-step barrier, each rank's events, max over ranks"),
+                   if world == 1 else "one process per GPU: rank 0's start + interprocess 'go' event every rank waits "
+                                      "on, every rank's interprocess 'done' event rank 0 waits on before its end event"),
         "ms_max_gpu_kernel": round(statistics.mean(gpu_step_ms), 4),
         "emulated_on_one_gpu": emulated if N > 1 else None,
         "effective_gbs": round((stats["moved_bytes"] + stats["relayout_bytes"]) / (ms * 1e-3) / 1e9, 1),

@@ -157,6 +157,23 @@ int rs_ipc_open_handle(rs_context* ctx, int gpu, const void* handle64, void** ou
 int rs_ipc_close_handle(rs_context* ctx, int gpu, void* ptr);
 
 /* ---- tensor core on device (reference slice / merge semantics and error precedence) --- */
+/* Stream events across processes (one process per GPU, SPEC.md:501's barriers on the device):
+ * rs_ipc_event_create makes an interprocess event on `gpu` and writes its 64-byte handle;
+ * another rank opens it with rs_ipc_event_open.  rs_event_record / rs_event_wait enqueue a
+ * record / a wait on the GPU's context stream (a wait binds to the LAST record enqueued before
+ * it — order them with a host barrier).  rs_timing_event_create + rs_event_elapsed time a span
+ * on one GPU's stream (elapsed synchronizes on the second event).  `bench.py` under torchrun:
+ * rank 0 records start + "go", every rank waits on "go" before its kernels and records "done",
+ * rank 0 waits on every "done" and records the end: one common start, the last rank's end. */
+typedef struct rs_event rs_event;
+int rs_ipc_event_create(rs_context* ctx, int gpu, void* handle64, rs_event** out);
+int rs_ipc_event_open(rs_context* ctx, int gpu, const void* handle64, rs_event** out);
+int rs_timing_event_create(rs_context* ctx, int gpu, rs_event** out);
+int rs_event_record(rs_context* ctx, int gpu, rs_event* ev);
+int rs_event_wait(rs_context* ctx, int gpu, rs_event* ev);
+int rs_event_elapsed(rs_event* start, rs_event* stop, float* ms);
+void rs_event_destroy(rs_event* ev);
+
 int rs_slice(rs_context* ctx, int gpu, const rs_tensor* t, const rs_range* r, void* out);
 int rs_merge(rs_context* ctx, int gpu, int n_parts, const rs_range* ranges, const rs_tensor* parts, int rank,
              const uint64_t* target_shape, void* out);

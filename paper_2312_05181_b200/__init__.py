@@ -237,6 +237,41 @@ class Context:
         return p.value
 
 
+class Event:
+    """A stream event on one GPU of a context: an interprocess event (create: new + its 64-byte
+    handle in .handle; open: a peer rank's handle) or a timing event; record / wait enqueue on
+    the GPU's context stream (rs_event_*)."""
+
+    def __init__(self, ctx: Context, gpu: int, kind: str = "timing", handle: bytes | None = None):
+        h = C.c_void_p()
+        self.ctx, self.gpu, self.handle = ctx, gpu, None
+        if kind == "ipc" and handle is None:
+            buf = C.create_string_buffer(64)
+            _chk(lib.rs_ipc_event_create(ctx.h, gpu, buf, C.byref(h)))
+            self.handle = buf.raw
+        elif kind == "ipc":
+            _chk(lib.rs_ipc_event_open(ctx.h, gpu, C.create_string_buffer(handle, 64), C.byref(h)))
+        else:
+            _chk(lib.rs_timing_event_create(ctx.h, gpu, C.byref(h)))
+        self.h = h.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.rs_event_destroy(self.h)
+            self.h = None
+
+    def record(self) -> None:
+        _chk(lib.rs_event_record(self.ctx.h, self.gpu, self.h))
+
+    def wait(self) -> None:
+        _chk(lib.rs_event_wait(self.ctx.h, self.gpu, self.h))
+
+    def elapsed_since(self, start: "Event") -> float:
+        ms = C.c_float()
+        _chk(lib.rs_event_elapsed(start.h, self.h, C.byref(ms)))
+        return ms.value
+
+
 def host_alloc(nbytes: int) -> int:
     p = C.c_void_p()
     _chk(lib.rs_host_alloc(nbytes, C.byref(p)))

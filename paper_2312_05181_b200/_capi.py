@@ -134,6 +134,13 @@ SIGNATURES = {
     "rs_executor_world_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
     "rs_executor_run_host_world": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_float)]),
     "rs_executor_digests": (C.c_int, [P, C.c_int, C.c_int, I32P, U64P, I32P, C.POINTER(C.c_int)]),
+    "rs_ipc_event_create": (C.c_int, [P, C.c_int, P, C.POINTER(P)]),
+    "rs_ipc_event_open": (C.c_int, [P, C.c_int, P, C.POINTER(P)]),
+    "rs_timing_event_create": (C.c_int, [P, C.c_int, C.POINTER(P)]),
+    "rs_event_record": (C.c_int, [P, C.c_int, P]),
+    "rs_event_wait": (C.c_int, [P, C.c_int, P]),
+    "rs_event_elapsed": (C.c_int, [P, P, C.POINTER(C.c_float)]),
+    "rs_event_destroy": (None, [P]),
     "rs_executor_fill_sources": (C.c_int, [P]),
     "rs_executor_verify": (C.c_int, [P, U64P]),
     "rs_executor_src_cells": (C.c_int, [P, C.c_int, C.POINTER(rs_cell_binding), C.POINTER(C.c_int)]),

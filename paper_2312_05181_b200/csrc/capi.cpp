@@ -283,6 +283,81 @@ int rs_ipc_close_handle(rs_context* c, int gpu, void* ptr) {
   });
 }
 
+// ---- cross-process stream events and stream timers (one process per GPU) -----------------------
+struct rs_event {
+  cudaEvent_t e = nullptr;
+  int dev = -1;
+  bool timing = false;
+  ~rs_event() {
+    if (e) {
+      cudaSetDevice(dev);
+      cudaEventDestroy(e);
+    }
+  }
+};
+int rs_ipc_event_create(rs_context* c, int gpu, void* h64, rs_event** out) {
+  return guard([&] {
+    need(h64, "handle"), need(out, "out");
+    static_assert(sizeof(cudaIpcEventHandle_t) == 64, "ipc event handle size");
+    auto ev = std::make_unique<rs_event>();
+    ev->dev = ctx_of(c).cuda_device(gpu);
+    cuda_ok(cudaSetDevice(ev->dev), "cudaSetDevice");
+    cuda_ok(cudaEventCreateWithFlags(&ev->e, cudaEventInterprocess | cudaEventDisableTiming), "cudaEventCreate");
+    cudaIpcEventHandle_t h;
+    cuda_ok(cudaIpcGetEventHandle(&h, ev->e), "cudaIpcGetEventHandle");
+    std::memcpy(h64, &h, 64);
+    *out = ev.release();
+  });
+}
+int rs_ipc_event_open(rs_context* c, int gpu, const void* h64, rs_event** out) {
+  return guard([&] {
+    need(h64, "handle"), need(out, "out");
+    auto ev = std::make_unique<rs_event>();
+    ev->dev = ctx_of(c).cuda_device(gpu);
+    cuda_ok(cudaSetDevice(ev->dev), "cudaSetDevice");
+    cudaIpcEventHandle_t h;
+    std::memcpy(&h, h64, 64);
+    cuda_ok(cudaIpcOpenEventHandle(&ev->e, h), "cudaIpcOpenEventHandle");
+    *out = ev.release();
+  });
+}
+int rs_timing_event_create(rs_context* c, int gpu, rs_event** out) {
+  return guard([&] {
+    need(out, "out");
+    auto ev = std::make_unique<rs_event>();
+    ev->dev = ctx_of(c).cuda_device(gpu), ev->timing = true;
+    cuda_ok(cudaSetDevice(ev->dev), "cudaSetDevice");
+    cuda_ok(cudaEventCreate(&ev->e), "cudaEventCreate");
+    *out = ev.release();
+  });
+}
+int rs_event_record(rs_context* c, int gpu, rs_event* ev) {
+  return guard([&] {
+    need(ev, "event");
+    Context& x = ctx_of(c);
+    cuda_ok(cudaSetDevice(x.cuda_device(gpu)), "cudaSetDevice");
+    cuda_ok(cudaEventRecord(ev->e, static_cast<cudaStream_t>(x.stream(gpu))), "cudaEventRecord");
+  });
+}
+int rs_event_wait(rs_context* c, int gpu, rs_event* ev) {
+  return guard([&] {
+    need(ev, "event");
+    Context& x = ctx_of(c);
+    cuda_ok(cudaSetDevice(x.cuda_device(gpu)), "cudaSetDevice");
+    cuda_ok(cudaStreamWaitEvent(static_cast<cudaStream_t>(x.stream(gpu)), ev->e, 0), "cudaStreamWaitEvent");
+  });
+}
+int rs_event_elapsed(rs_event* a, rs_event* b, float* ms) {
+  return guard([&] {
+    need(a, "event"), need(b, "event"), need(ms, "ms");
+    if (!a->timing || !b->timing) raise(reshard::Errc::InvalidArgument, "elapsed time needs two timing events");
+    cuda_ok(cudaSetDevice(b->dev), "cudaSetDevice");
+    cuda_ok(cudaEventSynchronize(b->e), "cudaEventSynchronize");
+    cuda_ok(cudaEventElapsedTime(ms, a->e, b->e), "cudaEventElapsedTime");
+  });
+}
+void rs_event_destroy(rs_event* ev) { delete ev; }
+
 // ---- tensor core on device ----------------------------------------------------------------
 int rs_slice(rs_context* c, int gpu, const rs_tensor* t, const rs_range* r, void* out) {
   return guard([&] {

@@ -34,6 +34,8 @@ def test_two_ranks_one_gpu_ipc_push(kernel):
     assert p.returncode == 0, p.stderr[-3000:]
     line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["verify_mismatched_bytes"] == 0
+    # world time from rank 0's start to the last rank's interprocess "done" event
+    assert "interprocess" in line["timing"] and line["value"] >= 0.99 * line["ms_max_gpu_kernel"] > 0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0  # multi-rank host-buffer path ran
     # both host-buffer forms ran: per-rank phases and rank 0's single-process world API
     assert "world_api" in line["e2e"] or "per_rank_phases" in line["e2e"]
