@@ -904,6 +904,16 @@ def run_ours(args):
         launches_total = int(lt.item())
     ms = statistics.mean(step_ms)
     bad = exs[0].verify() if len(exs) == 1 else bad_w
+    # ExecutionReport verification digests, off the clock: per base tensor the
+    # FNV-1a-64 of the tensor reassembled from the destination cells (the LAST DP copy of each, so
+    # the copies the reshard wrote are the ones hashed) against the source layout's
+    report = None
+    if len(exs) == 1 and world == 1 and args.mode == "distributed" and not args.no_digests and \
+            sum(s_need.values()) <= 40e9:
+        t_d = time.perf_counter()
+        d_src, d_dst = exs[0].digests(0), exs[0].digests(1, replica=-1)
+        report = {"digest": "fnv1a64 per base tensor", "tensors": len(d_dst), "match": d_src == d_dst and len(d_dst) == len(cat),
+                  "seconds": round(time.perf_counter() - t_d, 2)}
     if dist is not None:
         tb = torch.tensor([bad], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu", dtype=torch.int64)
         dist.all_reduce(tb)
@@ -1122,7 +1132,7 @@ def run_ours(args):
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
         "roofline": roofline,
         "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs),
-        "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "wall_s": round(wall, 4),
+        "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "execution_report": report, "wall_s": round(wall, 4),
         "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4),
         "tiles": sum(ex.tiles(g)[0] for ex in exs for g in mine),
         "host_ms": {"plan": round(build_plan.plan_ms, 2), "lower": round(lower_ms, 2), "prepare": round(prepare_ms, 2),
@@ -1173,6 +1183,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-p2p-probe", action="store_true")
+    ap.add_argument("--no-digests", action="store_true", help="skip the ExecutionReport FNV digests (off the clock)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -281,8 +281,11 @@ int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_sr
 /* ExecutionReport verification digests: per base tensor of the executor's
  * window, FNV-1a-64 (hash.hpp:13-42) of the tensor reassembled from one replica of each cell of
  * side 0 (source layout) or 1 (destination layout), read back from the local GPUs (off the
- * clock).  ok[i] = 0 when a cell of tensor[i] is not held by a local GPU.  *n = entries. */
-int rs_executor_digests(rs_executor* e, int side, int cap, int32_t* tensor, uint64_t* fnv, int32_t* ok, int* n);
+ * clock).  replica: which DP copy of a cell (0 = the first in layout order, -1 = the last; the
+ * nearest existing one when a cell has fewer).  ok[i] = 0 when a cell of tensor[i] is not held
+ * by a local GPU.  *n = entries. */
+int rs_executor_digests(rs_executor* e, int side, int replica, int cap, int32_t* tensor, uint64_t* fnv, int32_t* ok,
+                        int* n);
 int rs_executor_fill_sources(rs_executor* e);
 int rs_executor_verify(rs_executor* e, uint64_t* mismatched_bytes);
 /* bindings: src cells in (from-device, tensor, cell) order; dst cells in plan order */

@@ -630,15 +630,16 @@ class Executor:
         _chk(lib.rs_executor_run_host_world(self.h, n, hs, hd, C.byref(ms)))
         return ms.value
 
-    def digests(self, side: int = 1) -> dict:
+    def digests(self, side: int = 1, replica: int = 0) -> dict:
         """{tensor: FNV-1a-64 of the reassembled base tensor} over side 0 (source cells) or 1
-        (destination cells) — the ExecutionReport verification digest (SPEC.md:460-463);
-        tensors with a cell on no local GPU are left out."""
+        (destination cells), from DP copy `replica` of each cell (0 first, -1 last) — the
+        ExecutionReport verification digest; tensors with a cell on no local
+        GPU are left out."""
         n = C.c_int()
-        _chk(lib.rs_executor_digests(self.h, side, 0, None, None, None, C.byref(n)))
+        _chk(lib.rs_executor_digests(self.h, side, replica, 0, None, None, None, C.byref(n)))
         m = max(n.value, 1)
         tt, ff, ok = (C.c_int32 * m)(), (C.c_uint64 * m)(), (C.c_int32 * m)()
-        _chk(lib.rs_executor_digests(self.h, side, n.value, tt, ff, ok, C.byref(n)))
+        _chk(lib.rs_executor_digests(self.h, side, replica, n.value, tt, ff, ok, C.byref(n)))
         return {int(tt[i]): int(ff[i]) for i in range(n.value) if ok[i]}
 
     def fill_sources(self) -> None:

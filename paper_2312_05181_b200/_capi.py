@@ -133,7 +133,7 @@ SIGNATURES = {
     "rs_executor_host_elapsed": (C.c_int, [P, C.c_int, C.POINTER(C.c_float)]),
     "rs_executor_world_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
     "rs_executor_run_host_world": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_float)]),
-    "rs_executor_digests": (C.c_int, [P, C.c_int, C.c_int, I32P, U64P, I32P, C.POINTER(C.c_int)]),
+    "rs_executor_digests": (C.c_int, [P, C.c_int, C.c_int, C.c_int, I32P, U64P, I32P, C.POINTER(C.c_int)]),
     "rs_ipc_event_create": (C.c_int, [P, C.c_int, P, C.POINTER(P)]),
     "rs_ipc_event_open": (C.c_int, [P, C.c_int, P, C.POINTER(P)]),
     "rs_timing_event_create": (C.c_int, [P, C.c_int, C.POINTER(P)]),

@@ -694,11 +694,12 @@ int rs_executor_run_host_world(rs_executor* e, int n, const void* const* host_sr
     *ms = e->e->run_host_world(std::vector<const void*>(host_src, host_src + n), std::vector<void*>(host_dst, host_dst + n));
   });
 }
-int rs_executor_digests(rs_executor* e, int side, int cap, int32_t* tensor, uint64_t* fnv, int32_t* ok, int* n) {
+int rs_executor_digests(rs_executor* e, int side, int replica, int cap, int32_t* tensor, uint64_t* fnv, int32_t* ok,
+                        int* n) {
   return guard([&] {
     need(e, "executor"), need(n, "n");
     if (side != 0 && side != 1) raise(reshard::Errc::InvalidArgument, "side must be 0 (source) or 1 (destination)");
-    const auto d = e->e->digests(side);
+    const auto d = e->e->digests(side, replica);
     *n = int(d.size());
     for (int i = 0; i < *n && i < cap; ++i) {
       if (tensor) tensor[i] = int32_t(d[size_t(i)].tensor);

@@ -1500,15 +1500,16 @@ uint64_t Executor::verify_destinations() {
 // D2H straight into its place in the reassembled tensor (cudaMemcpy2D per outer index);
 // tensors are hashed by a pool of host threads.  FNV-1a is byte-sequential, so this stays off
 // the clock.  A tensor some cell of which is not held by a local GPU gets no digest (ok = 0).
-std::vector<Executor::Digest> Executor::digests(int side) {
+std::vector<Executor::Digest> Executor::digests(int side, int replica) {
   TraceRange trace_("Executor::digests");
   const PTC& p = side == 0 ? *plan_->from : *plan_->to;
   const size_t nt = p.catalog.tensors.size();
-  // one binding per (tensor, cell): the first local replica in layout order
-  std::vector<std::vector<const CellBinding*>> pick(nt);
-  for (size_t t = 0; t < nt; ++t) pick[t].assign(p.cells[t].size(), nullptr);
+  // one binding per (tensor, cell): the `replica`-th local replica in layout order (the last
+  // one when the cell has fewer; replica < 0 counts from the end)
+  std::vector<std::vector<std::vector<const CellBinding*>>> reps(nt);
+  for (size_t t = 0; t < nt; ++t) reps[t].resize(p.cells[t].size());
   auto offer = [&](uint32_t t, uint32_t c, const CellBinding& b) {
-    if (b.gpu >= 0 && ctx_.local_of(b.gpu) >= 0 && !pick[t][c]) pick[t][c] = &b;
+    if (b.gpu >= 0 && ctx_.local_of(b.gpu) >= 0) reps[t][c].push_back(&b);
   };
   if (side == 0) {
     size_t k = 0;
@@ -1517,6 +1518,13 @@ std::vector<Executor::Digest> Executor::digests(int side) {
   } else {
     for (size_t j = 0; j < plan_->dst_cells.size(); ++j) offer(plan_->dst_cells[j].tensor, plan_->dst_cells[j].cell, dst_bind_[j]);
   }
+  std::vector<std::vector<const CellBinding*>> pick(nt);
+  for (size_t t = 0; t < nt; ++t)
+    for (auto& v : reps[t]) {
+      const long n = long(v.size());
+      const long r = replica >= 0 ? std::min<long>(replica, n - 1) : std::max<long>(0, n + replica);
+      pick[t].push_back(n ? v[size_t(r)] : nullptr);
+    }
   std::vector<Digest> out;
   for (uint32_t t = t_begin_; t < std::min<uint32_t>(t_end_, uint32_t(nt)); ++t) out.push_back(Digest{t, 0, 0});
   std::atomic<size_t> next{0};

@@ -198,7 +198,7 @@ class Executor {
     uint32_t ok;   // 0: some cell is not held by a local GPU (no digest)
     uint64_t fnv;
   };
-  std::vector<Digest> digests(int side);
+  std::vector<Digest> digests(int side, int replica = 0);  // replica: which DP copy of each cell (< 0: from the end)
 
   void* arena_base(int gpu, int arena) const { return arena == 0 ? src_base_[size_t(gpu)] : dst_base_[size_t(gpu)]; }
   Context& context() const { return ctx_; }

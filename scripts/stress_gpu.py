@@ -104,7 +104,7 @@ def main() -> int:
             print(json.dumps({"error": "verify mismatch", "case": done}), flush=True)
             return 1
         if done % 10 == 0:  # ExecutionReport digests: destination == source == oracle
-            dd, sd = ex.digests(1), ex.digests(0)
+            dd, sd = ex.digests(1, replica=-1), ex.digests(0)
             if dd != sd or any(dd[t] != ocat.base_digest(t) for t in dd):
                 print(json.dumps({"error": "digest mismatch", "case": done}), flush=True)
                 return 1

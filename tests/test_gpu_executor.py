@@ -462,6 +462,7 @@ def test_execution_report_digests(rs, orc, ctx):
         ex, _ = _run(rs, ctx, rs.generate_plan(a, b), n1, n2)
         src, dst = ex.digests(0), ex.digests(1)
         assert len(dst) == len(cat) and src == dst
+        assert ex.digests(1, replica=-1) == dst  # the other DP copy of every replicated cell
         for t in range(0, len(cat), 7):
             assert dst[t] == ocat.base_digest(t), f"tensor {t}"
         del ex
