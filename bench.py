@@ -904,16 +904,6 @@ def run_ours(args):
         launches_total = int(lt.item())
     ms = statistics.mean(step_ms)
     bad = exs[0].verify() if len(exs) == 1 else bad_w
-    # ExecutionReport verification digests, off the clock: per base tensor the
-    # FNV-1a-64 of the tensor reassembled from the destination cells (the LAST DP copy of each, so
-    # the copies the reshard wrote are the ones hashed) against the source layout's
-    report = None
-    if len(exs) == 1 and world == 1 and args.mode == "distributed" and not args.no_digests and \
-            sum(s_need.values()) <= 40e9:
-        t_d = time.perf_counter()
-        d_src, d_dst = exs[0].digests(0), exs[0].digests(1, replica=-1)
-        report = {"digest": "fnv1a64 per base tensor", "tensors": len(d_dst), "match": d_src == d_dst and len(d_dst) == len(cat),
-                  "seconds": round(time.perf_counter() - t_d, 2)}
     if dist is not None:
         tb = torch.tensor([bad], device=f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu", dtype=torch.int64)
         dist.all_reduce(tb)
@@ -1026,6 +1016,17 @@ def run_ours(args):
             e2e = dict(world_line, per_rank_phases=e2e) if world_line["value"] < e2e["value"] else \
                 dict(e2e, world_api=world_line)
 
+    # ExecutionReport verification digests, off the clock (after the e2e runs,
+    # which rewrite the same destination bytes): per base tensor the
+    # FNV-1a-64 of the tensor reassembled from the destination cells (the LAST DP copy of each, so
+    # the copies the reshard wrote are the ones hashed) against the source layout's
+    report = None
+    if len(exs) == 1 and world == 1 and args.mode == "distributed" and not args.no_digests and \
+            sum(s_need.values()) <= 40e9:
+        t_d = time.perf_counter()
+        d_src, d_dst = exs[0].digests(0), exs[0].digests(1, replica=-1)
+        report = {"digest": "fnv1a64 per base tensor", "tensors": len(d_dst), "match": d_src == d_dst and len(d_dst) == len(cat),
+                  "seconds": round(time.perf_counter() - t_d, 2)}
     # NVLink peak measured on this box (distinct GPUs only), else the NVLink 5 spec
     p2p = None
     if N > 1 and not emulated and not args.no_p2p_probe:
