@@ -110,8 +110,8 @@ int rs_errc_count(void) { return kErrcCount; }
 uint64_t rs_fnv1a64(const void* data, uint64_t n) { return fnv1a64(data, n); }
 uint64_t rs_payload_seed(const char* path) { return payload_seed(path ? path : ""); }
 const char* rs_build_info(void) {
-  return "reshard_b200 sm_100a (K3 TMA bulk copy with fan-out, K1/K2 LDG/STG copy, K5 repartition, "
-         "K8 shuffle, K6/K7 payload); CUDA " RESHARD_CUDA_VERSION;
+  return "reshard_b200 sm_100a (K3 TMA bulk copy with fan-out, K3T TMA tensor-map boxes, K1/K2 LDG/STG copy with "
+         "read-once fan-out to peers, K5 repartition, K8 shuffle, K6/K7 payload); CUDA " RESHARD_CUDA_VERSION;
 }
 
 // ---- box algebra ------------------------------------------------------------------------
