@@ -744,10 +744,39 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
       read_bytes += pb;
     }
   }
-  // destination order (sequential writes; monotone destinations per host chunk when the
-  // pieces do not interleave), then each piece's first tile
-  auto by_dst = [](std::vector<DevPiece>& v) {
-    std::stable_sort(v.begin(), v.end(), [](const DevPiece& p, const DevPiece& q) { return p.dst[0] < q.dst[0]; });
+  // Order: by destination GPU in the all-to-all's shift order — this GPU's own arena first, then
+  // GPU world+1, world+2, ... (mod G) — and by destination address within a GPU (sequential
+  // writes; monotone destinations per host chunk).  The persistent kernels sweep their list
+  // front to back with every CTA, so at any moment a GPU pushes into one peer; with the shift
+  // every peer is the target of a different source at the same time and no GPU's NVLink ingress
+  // is oversubscribed while others idle (a plain address order would send every source to the
+  // lowest-address peer first).  A fan-out piece is keyed by its nearest remote member.
+  const int G = ctx_.world();
+  std::vector<std::pair<uint64_t, int>> dbases;
+  for (int j = 0; j < G; ++j)
+    if (dst_base_[size_t(j)]) dbases.emplace_back(uint64_t(reinterpret_cast<uintptr_t>(dst_base_[size_t(j)])), j);
+  std::sort(dbases.begin(), dbases.end());
+  auto gpu_of = [&](uint64_t a) {
+    auto it = std::upper_bound(dbases.begin(), dbases.end(), std::make_pair(a, INT32_MAX));
+    return it == dbases.begin() ? -1 : std::prev(it)->second;
+  };
+  auto by_dst = [&](std::vector<DevPiece>& v) {
+    std::vector<std::pair<uint64_t, size_t>> key(v.size());
+    for (size_t i = 0; i < v.size(); ++i) {
+      int best = G;
+      for (uint32_t d = 0; d < v[i].n_dst; ++d) {
+        const int j = gpu_of(v[i].dst[d]);
+        if (j >= 0 && j != l->world) best = std::min(best, (j - l->world + G) % G);
+      }
+      key[i] = {uint64_t(best == G ? 0 : best), i};
+    }
+    std::stable_sort(key.begin(), key.end(), [&](const auto& x, const auto& y) {
+      return x.first != y.first ? x.first < y.first : v[x.second].dst[0] < v[y.second].dst[0];
+    });
+    std::vector<DevPiece> out;
+    out.reserve(v.size());
+    for (auto& k : key) out.push_back(v[k.second]);
+    v.swap(out);
   };
   by_dst(fanp), by_dst(alignedp);
   auto number = [](std::vector<DevPiece>& v) {
