@@ -131,3 +131,21 @@ def test_reshard_cli_on_gpu(reshard_cli):
         p = subprocess.run([reshard_cli, *args], capture_output=True, text=True, timeout=600)
         assert p.returncode == 0, p.stderr
         assert "mismatched bytes 0" in p.stdout
+
+
+def test_c_abi_header_is_plain_c(rs, tmp_path):
+    """include/reshard_b200.h is the drop-in boundary for cgo / JNI / N-API / ctypes: it must
+    compile as ISO C11 (-pedantic, no C++), and a C program links libreshard_b200.so and
+    calls through it (no GPU needed for the error table)."""
+    src = tmp_path / "abi.c"
+    src.write_text('#include "reshard_b200.h"\n#include <string.h>\n'
+                   'int main(void) {\n'
+                   '  rs_range r;\n'
+                   '  if (rs_range_parse("[0:3,2:4]", &r) != 0 || r.rank != 2 || r.hi[1] != 4) return 2;\n'
+                   '  if (rs_range_parse("[x:1]", &r) == 0) return 3;\n'
+                   '  if (strchr(rs_last_error(), \':\') == NULL) return 4;  /* "<ErrcName>: <detail>" */\n'
+                   '  return rs_errc_count() > 0 ? 0 : 5;\n}\n')
+    out = str(tmp_path / "abi")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-pedantic", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-L", PKG, "-lreshard_b200", f"-Wl,-rpath,{PKG}", "-o", out], check=True)
+    assert subprocess.run([out]).returncode == 0
