@@ -427,7 +427,7 @@ def pcie_probe(nbytes: int = 2 << 30, reps: int = 3) -> dict:
 def copy_kernel_name() -> str:
     k = os.environ.get("RESHARD_COPY_KERNEL", "bulk_strided") or "bulk_strided"  # the library default
     return {"bulk": "copy_bulk_kernel", "bulk_strided": "copy_bulk_strided_kernel", "ldg": "copy_v16_kernel",
-            "ldg8": "copy_v16_kernel", "bulk_warp": "copy_bulk_warp_kernel"}.get(k, k)
+            "ldg8": "copy_v16_kernel", "bulk_warp": "copy_bulk_warp_kernel", "bulk_dyn": "copy_bulk_dyn_kernel"}.get(k, k)
 
 
 def k5_dram_bytes_per_sample():

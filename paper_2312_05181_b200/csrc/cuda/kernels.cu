@@ -438,6 +438,86 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
   bulk_wait_all();
 }
 
+// Variant RESHARD_COPY_KERNEL=bulk_dyn: the bulk_strided pipeline with DYNAMIC tile
+// assignment.  A static c, c+grid, ... split leaves the CTAs finishing up to 6 % of the kernel
+// apart on short launches (r2_09 ncu: sm__cycles_active min/max 0.94 on GPT-2 small); here each
+// CTA claims the next kClaim tiles of the natural order from a global counter (one atomic per
+// claim, issued one claim ahead so its latency hides behind the previous claim's tiles), so the
+// CTAs still sweep memory together as one window and finish together.  The last CTA out resets
+// the counter for the next launch on the stream.
+constexpr unsigned long long kClaim = 2;
+__global__ void __launch_bounds__(32, 1) copy_bulk_dyn_kernel(const DevFanTile* __restrict__ tiles, unsigned long long n,
+                                                              int stages, unsigned stage_bytes, unsigned long long* claim) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
+  __shared__ DevFanTile sdesc[kBulkMaxStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  unsigned long long cur = atomicAdd(claim, kClaim);
+  unsigned long long nxt_claim = atomicAdd(claim, kClaim);
+  unsigned long long end = cur < n ? min(cur + kClaim, n) : cur;
+  auto next_index = [&](unsigned long long& idx) -> bool {
+    if (cur >= end) {
+      if (nxt_claim >= n) return false;
+      cur = nxt_claim, end = min(cur + kClaim, n);
+      nxt_claim = atomicAdd(claim, kClaim);  // consumed a whole claim later: its latency is hidden
+    }
+    idx = cur++;
+    return true;
+  };
+  const int ahead = stages > 2 ? stages - 2 : 1;
+  int s_load = 0, s_store = 0;
+  unsigned phase = 0;
+  DevFanTile nxt;
+  unsigned long long ni = 0, issued = 0, stored = 0;
+  bool have = next_index(ni);
+  if (have) load_desc(tiles + ni, nxt);
+  auto issue_load = [&]() {
+    const DevFanTile t = nxt;
+    sdesc[s_load] = t;
+    have = next_index(ni);
+    if (have) load_desc(tiles + ni, nxt);
+    const unsigned bar = smem_u32(&bars[s_load]);
+    const unsigned base = smem_u32(smem + size_t(s_load) * stage_bytes);
+    mbar_expect_tx(bar, t.rows * t.row_bytes);
+    if (t.pad) {
+      tma_load_3d(base, t.src, unsigned(t.src_pitch), unsigned(t.src_pitch >> 32), bar);
+    } else {
+      for (unsigned r = 0; r < t.rows; ++r)
+        bulk_g2s(base + r * t.row_bytes, reinterpret_cast<const char*>(t.src) + r * t.src_pitch, t.row_bytes, bar);
+    }
+    if (++s_load == stages) s_load = 0;
+    ++issued;
+  };
+  while (have && issued < (unsigned long long)ahead) issue_load();
+  while (stored < issued) {
+    if (have) {
+      bulk_wait_read<1>();  // the stage about to be refilled was last read by the store two back
+      issue_load();
+    }
+    const DevFanTile& t = sdesc[s_store];
+    mbar_wait(smem_u32(&bars[s_store]), phase);
+    const unsigned base = smem_u32(smem + size_t(s_store) * stage_bytes);
+    if (t.pad) {
+      for (unsigned d = 0; d < t.n_dst; ++d) tma_store_3d(t.dst[d], unsigned(t.src_pitch), unsigned(t.src_pitch >> 32), base);
+    } else {
+      for (unsigned d = 0; d < t.n_dst; ++d)
+        for (unsigned r = 0; r < t.rows; ++r)
+          bulk_s2g(reinterpret_cast<char*>(t.dst[d]) + r * t.dst_pitch[d], base + r * t.row_bytes, t.row_bytes);
+    }
+    bulk_commit();
+    if (++s_store == stages) s_store = 0, phase ^= 1u;
+    ++stored;
+  }
+  bulk_wait_all();
+  __threadfence();  // this CTA's claims precede its exit count
+  if (atomicAdd(claim + 1, 1ull) == gridDim.x - 1) {
+    claim[0] = 0, claim[1] = 0;
+    __threadfence();
+  }
+}
+
 // Variant RESHARD_COPY_KERNEL=bulk_warp: the same schedule, but the 32 lanes share the
 // issue work — lane l issues the bulk copies of rows l, l+32, ... of a tile (strided 2-D
 // fragments such as row-parallel TP slices have tens of rows per stage).  Lane 0 owns the
@@ -610,8 +690,21 @@ void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig&
   check(cudaGetLastError(), "fan copy launch");
 }
 
-void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
+void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream,
+                 unsigned long long* claim) {
   if (n_tiles == 0) return;
+  if (cfg.kernel == CopyKernel::BulkDyn) {
+    if (!claim) raise(Errc::InvalidArgument, "bulk_dyn needs a zeroed claim counter");
+    const size_t smem = size_t(cfg.stages) * cfg.stage_bytes;
+    if (cfg.stages < 3 || cfg.stages > kBulkMaxStages || smem > 227 * 1024)
+      raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
+    check(cudaFuncSetAttribute(copy_bulk_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+          "bulk smem attribute");
+    copy_bulk_dyn_kernel<<<bulk_grid(n_tiles, sms, cfg), 32, smem, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles, cfg.stages, cfg.stage_bytes, claim);
+    check(cudaGetLastError(), "bulk copy launch");
+    return;
+  }
   if (cfg.stages < 3 || cfg.stages > kBulkMaxStages) raise(Errc::InvalidArgument, "bulk copy needs 3..16 stages");
   const bool strided = cfg.kernel == CopyKernel::BulkStrided || cfg.kernel == CopyKernel::BulkWarp;
   const size_t smem = size_t(cfg.stages) * cfg.stage_bytes + (strided ? 0 : kDescRingBytes);

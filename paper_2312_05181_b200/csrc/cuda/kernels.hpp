@@ -28,7 +28,10 @@ void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cf
 void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);
 // K3 with fan-out: every tile 16-byte aligned and <= cfg.stage_bytes.  The array must be in
 // interleave_for_grid order for bulk_grid(n_tiles, sms, cfg) CTAs.
-void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);
+// bulk_dyn (cfg.kernel == BulkDyn) claims tiles from `claim` (2 x u64, zero before the first
+// launch; the kernel leaves it zero again), required for that kernel only.
+void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream,
+                 unsigned long long* claim = nullptr);
 inline int bulk_grid(uint64_t n_tiles, int sms, const CopyConfig& cfg) {
   const uint64_t g = uint64_t(sms) * uint64_t(cfg.ctas_per_sm > 0 ? cfg.ctas_per_sm : 1);
   return int(n_tiles < g ? n_tiles : g);

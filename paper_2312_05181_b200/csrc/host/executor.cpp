@@ -175,8 +175,9 @@ CopyConfig CopyConfig::from_env() {
     else if (s == "bulk") c.kernel = CopyKernel::Bulk;
     else if (s == "bulk_strided") c.kernel = CopyKernel::BulkStrided;
     else if (s == "bulk_warp") c.kernel = CopyKernel::BulkWarp;
+    else if (s == "bulk_dyn") c.kernel = CopyKernel::BulkDyn;
     else if (!s.empty())
-      raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8, bulk, bulk_strided or bulk_warp");
+      raise(Errc::InvalidArgument, "RESHARD_COPY_KERNEL must be ldg, ldg8, bulk, bulk_strided, bulk_warp or bulk_dyn");
   }
   c.ctas_per_sm = std::max(1, env_int("RESHARD_CTAS_PER_SM", is_bulk(c.kernel) ? 1 : 3));
   c.stages = env_int("RESHARD_BULK_STAGES", c.stages);
@@ -323,6 +324,7 @@ struct Executor::Local {
   cudaEvent_t e_h2d = nullptr, e_kern = nullptr, e_d2h = nullptr;  // run_host_world phase marks
   cudaEvent_t start = nullptr, stop = nullptr;
   unsigned long long* d_count = nullptr;
+  unsigned long long* d_claim = nullptr;  // bulk_dyn's tile-claim counter (2 x u64, kept zero between launches)
   std::vector<HostChunk> chunks;
   std::vector<DevPiece> chunk_pieces;  // the one tile list the host pipeline cuts into chunks (lazy)
   bool chunks_ready = true;           // chunks planned (or not applicable)
@@ -356,6 +358,7 @@ struct Executor::Local {
     for (auto e : {e_h2d, e_kern, e_d2h})
       if (e) cudaEventDestroy(e);
     if (d_count) cudaFree(d_count);
+    if (d_claim) cudaFree(d_claim);
     if (start) cudaEventDestroy(start);
     if (stop) cudaEventDestroy(stop);
     for (auto e : ev) cudaEventDestroy(e);
@@ -386,7 +389,7 @@ void Executor::launch_local(Local& l, void* stream) {
     ck(cudaStreamWaitEvent(l.s_aux, l.fork, 0), "fork wait");
     side = l.s_aux;
   }
-  cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, s);
+  cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, s, l.d_claim);
   cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, side);
   cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, side);
   cuda::launch_copy_fan(l.d_fanl, l.n_fanl, cfg_, sms, side);
@@ -485,9 +488,16 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     ck(cudaMallocAsync(reinterpret_cast<void**>(&l->d_count), sizeof(unsigned long long),
                        static_cast<cudaStream_t>(ctx_.stream(w))), "cudaMallocAsync");
     for (cudaEvent_t* e : {&l->e_h2d, &l->e_kern, &l->e_d2h}) ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    auto claim_counter = [&](Local& x) {
+      auto st = static_cast<cudaStream_t>(ctx_.stream(w));
+      ck(cudaMallocAsync(reinterpret_cast<void**>(&x.d_claim), 2 * sizeof(unsigned long long), st), "cudaMallocAsync");
+      ck(cudaMemsetAsync(x.d_claim, 0, 2 * sizeof(unsigned long long), st), "memset claim");
+    };
+    claim_counter(*l);
     if (w == central_) {
       l->phase_b = std::make_unique<Local>();
       l->phase_b->world = w, l->phase_b->dev = l->dev;
+      claim_counter(*l->phase_b);
     }
     local_.push_back(std::move(l));
   }
@@ -789,7 +799,7 @@ void Executor::lower_tiles(Local& local, const std::vector<Logical>& lt, bool ho
   // one box per tile, maps encoded here (bases are known) and uploaded with the tiles
   std::vector<FanTile> tensor_tiles;
   std::vector<CUtensorMap> maps;
-  if (cfg_.tensor && cfg_.kernel == CopyKernel::BulkStrided) {
+  if (cfg_.tensor && (cfg_.kernel == CopyKernel::BulkStrided || cfg_.kernel == CopyKernel::BulkDyn)) {
     std::vector<DevPiece> keep;
     for (const DevPiece& q : fanp) {
       if (!(q.per > 1 && q.rows > 1 && q.src_pitch != q.row_bytes)) {
@@ -1145,7 +1155,7 @@ float Executor::run_host_world_pipelined(const std::vector<const void*>& host_sr
       ck(cudaStreamWaitEvent(s, l->wev[k], 0), "wait h2d");
       const int sms = ctx_.sm_count(l->world);
       const auto& c = l->wchunks[k];
-      cuda::launch_bulk(l->d_fan + c.t0[0], c.t1[0] - c.t0[0], cfg_, sms, s);
+      cuda::launch_bulk(l->d_fan + c.t0[0], c.t1[0] - c.t0[0], cfg_, sms, s, l->d_claim);
       cuda::launch_copy(l->d_tiles + c.t0[1], c.t1[1] - c.t0[1], cfg_, sms, true, s);
       cuda::launch_copy(l->d_tiles + l->n_aligned + c.t0[2], c.t1[2] - c.t0[2], cfg_, sms, false, s);
       cuda::launch_copy_fan(l->d_fanl + c.t0[3], c.t1[3] - c.t0[3], cfg_, sms, s);
@@ -1382,7 +1392,8 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
     for (size_t k = 0; k < K; ++k) {
       ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");
       const uint64_t n = l->chunks[k].t1 - l->chunks[k].t0;
-      if (l->n_fan) cuda::launch_bulk((l->d_fan_chunks ? l->d_fan_chunks : l->d_fan) + l->chunks[k].t0, n, cfg_, sms, s);
+      if (l->n_fan)
+        cuda::launch_bulk((l->d_fan_chunks ? l->d_fan_chunks : l->d_fan) + l->chunks[k].t0, n, cfg_, sms, s, l->d_claim);
       else cuda::launch_copy(l->d_tiles + l->chunks[k].t0, n, cfg_, sms, true, s);
       ck(cudaEventRecord(ec[k], s), "event");
     }
@@ -1641,9 +1652,13 @@ Timing broadcast(Context& ctx, int gpu, const void* src, const std::vector<void*
     const bool interleave = cfg.kernel == CopyKernel::Bulk;
     cuda::launch_expand_fan(dp, uint32_t(pieces.size()), 0, n, dt, interleave ? unsigned(cuda::bulk_grid(n, sms, cfg)) : 0u,
                             sms, s);
+    unsigned long long* claim = nullptr;  // bulk_dyn's counter
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&claim), 2 * sizeof(unsigned long long), s), "cudaMallocAsync");
+    ck(cudaMemsetAsync(claim, 0, 2 * sizeof(unsigned long long), s), "memset claim");
     ck(cudaEventRecord(e0, s), "event");
-    cuda::launch_bulk(dt, n, cfg, sms, s);
+    cuda::launch_bulk(dt, n, cfg, sms, s, claim);
     ck(cudaEventRecord(e1, s), "event");
+    ck(cudaFreeAsync(claim, s), "cudaFreeAsync");
     ck(cudaFreeAsync(dp, s), "cudaFreeAsync");
     ck(cudaFreeAsync(dt, s), "cudaFreeAsync");
     t.tiles = n, t.launches = 1, t.read_bytes = bytes * pieces.size();

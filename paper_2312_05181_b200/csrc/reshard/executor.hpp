@@ -87,9 +87,9 @@ RS_HD void piece_tile(uint32_t rows, uint64_t row_bytes, uint32_t per, uint32_t 
 // (ldg | ldg8 | bulk), RESHARD_CTAS_PER_SM, RESHARD_BULK_STAGES, RESHARD_BULK_STAGE_KIB.
 // Defaults from the round-1 B200 sweep (profiles/r02_sweep.json): TMA bulk, 1 CTA/SM,
 // 8 stages x 24 KiB reached 6.59 TB/s on GPT-3 1.3B vs 6.17 TB/s for LDG/STG at 3 CTAs/SM.
-enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2, BulkStrided = 3, BulkWarp = 4 };
+enum class CopyKernel : int { Ldg = 0, Ldg8 = 1, Bulk = 2, BulkStrided = 3, BulkWarp = 4, BulkDyn = 5 };
 inline bool is_bulk(CopyKernel k) {
-  return k == CopyKernel::Bulk || k == CopyKernel::BulkStrided || k == CopyKernel::BulkWarp;
+  return k == CopyKernel::Bulk || k == CopyKernel::BulkStrided || k == CopyKernel::BulkWarp || k == CopyKernel::BulkDyn;
 }
 struct CopyConfig {
   CopyKernel kernel = CopyKernel::BulkStrided;  // r08 same-box A/B: 3-4% faster than Bulk

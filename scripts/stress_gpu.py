@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 import paper_2312_05181_b200 as rs  # noqa: E402
 from oracle.oracle import Oracle  # noqa: E402  (the checker)
 
-KERNELS = ["bulk_strided", "bulk", "ldg"]
+KERNELS = ["bulk_strided", "bulk", "ldg", "bulk_dyn"]
 
 
 def entries(rng):
@@ -121,7 +121,7 @@ def main() -> int:
         stats["recovery"] += recovery
         stats["fresh"] += (not recovery) and d2[0][1] >= n1
         stats["bulk_peer"] += peer and world > 1
-        stats["tma_tensor"] += tensor and os.environ["RESHARD_COPY_KERNEL"] == "bulk_strided"
+        stats["tma_tensor"] += tensor and os.environ["RESHARD_COPY_KERNEL"] in ("bulk_strided", "bulk_dyn")
         stats["fanout_gt4"] += D2 > 4
         done += 1
         if done % 100 == 0:

@@ -385,7 +385,7 @@ def test_reference_fixtures_through_host_value_api(rs, ctx):
         assert got == {k: c[k] for k in ("ok", "error") if k in c}, c["target"]
 
 
-@pytest.mark.parametrize("kernel", ["bulk_strided", "bulk", "ldg"])
+@pytest.mark.parametrize("kernel", ["bulk_strided", "bulk", "ldg", "bulk_dyn"])
 def test_broadcast_fan_out_push(rs, ctx, kernel, monkeypatch):
     """rs_broadcast: one source to 1, 4, 6 destinations (fan-out groups of 4), aligned (TMA
     fan-out tiles) and misaligned (LDG/STG), every destination byte equal to the source."""
@@ -515,4 +515,20 @@ def test_run_host_world_matches_device_result(rs, pipeline, monkeypatch):
         for g in range(world):
             rs.host_free(hs[g])
             rs.host_free(hd[g])
+        del ex
+
+
+def test_bulk_dyn_kernel_bytes_exact(rs, orc, ctx, monkeypatch):
+    """RESHARD_COPY_KERNEL=bulk_dyn (dynamic tile claims from a global counter that the last
+    CTA resets): random transitions and repeated launches on one executor (the counter must be
+    back at zero for every launch), every destination byte equal to the oracle's."""
+    monkeypatch.setenv("RESHARD_COPY_KERNEL", "bulk_dyn")
+    cat = rs.Catalog.gpt(256, 6, 64, 1024, rs.MIXED_ADAM)
+    for (a_cfg, b_cfg) in [((2, 1, 1, 2), (2, 1, 2, 4)), ((4, 2, 1, 8), (2, 2, 2, 8)), ((2, 1, 1, 2), (1, 2, 1, 2))]:
+        a = cat.build_strategy(DEV(a_cfg[3]), *a_cfg[:3])
+        b = cat.build_strategy(DEV(b_cfg[3]), *b_cfg[:3])
+        ex, _ = _run(rs, ctx, rs.generate_plan(a, b), a_cfg[3], b_cfg[3], 16 << 10)
+        for _ in range(3):
+            ex.apply()
+        assert ex.verify() == 0
         del ex

@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("kernel", ["bulk_strided", "bulk", "ldg", "bulk_strided-peer"])
+@pytest.mark.parametrize("kernel", ["bulk_strided", "bulk", "ldg", "bulk_strided-peer", "bulk_dyn"])
 def test_two_ranks_one_gpu_ipc_push(kernel):
     env = dict(os.environ, RESHARD_DIST_BACKEND="gloo", RESHARD_SAME_GPU="1", RESHARD_COPY_KERNEL=kernel.split("-")[0])
     if kernel.endswith("-peer"):  # TMA bulk stores through the IPC mapping as well
