@@ -447,21 +447,30 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
 // the counter for the next launch on the stream.
 constexpr unsigned long long kClaim = 2;
 __global__ void __launch_bounds__(32, 1) copy_bulk_dyn_kernel(const DevFanTile* __restrict__ tiles, unsigned long long n,
-                                                              int stages, unsigned stage_bytes, unsigned long long* claim) {
+                                                              int stages, unsigned stage_bytes, unsigned long long* claim,
+                                                              unsigned long long n_static) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
   __shared__ DevFanTile sdesc[kBulkMaxStages];
   if (threadIdx.x != 0) return;
   for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  unsigned long long cur = atomicAdd(claim, kClaim);
-  unsigned long long nxt_claim = atomicAdd(claim, kClaim);
-  unsigned long long end = cur < n ? min(cur + kClaim, n) : cur;
+  // tiles [0, n_static) in the static c, c + grid, ... order; the rest claimed dynamically
+  unsigned long long s_next = blockIdx.x;
+  unsigned long long cur = n_static + atomicAdd(claim, kClaim);  // consumed after the static share
+  unsigned long long nxt_claim = n, end = cur < n ? min(cur + kClaim, n) : cur;
+  bool second = false;  // nxt_claim issued
   auto next_index = [&](unsigned long long& idx) -> bool {
+    if (s_next < n_static) {
+      idx = s_next;
+      s_next += gridDim.x;
+      return true;
+    }
+    if (!second) nxt_claim = n_static + atomicAdd(claim, kClaim), second = true;
     if (cur >= end) {
       if (nxt_claim >= n) return false;
       cur = nxt_claim, end = min(cur + kClaim, n);
-      nxt_claim = atomicAdd(claim, kClaim);  // consumed a whole claim later: its latency is hidden
+      nxt_claim = n_static + atomicAdd(claim, kClaim);  // consumed a whole claim later: its latency is hidden
     }
     idx = cur++;
     return true;
@@ -700,8 +709,12 @@ void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg
       raise(Errc::InvalidArgument, "bulk stages x stage bytes exceed shared memory");
     check(cudaFuncSetAttribute(copy_bulk_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
           "bulk smem attribute");
-    copy_bulk_dyn_kernel<<<bulk_grid(n_tiles, sms, cfg), 32, smem, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles, cfg.stages, cfg.stage_bytes, claim);
+    // the static prefix: all but `dyn_tail` tiles per CTA (RESHARD_DYN_TAIL; < 0: everything dynamic)
+    const uint64_t grid = uint64_t(bulk_grid(n_tiles, sms, cfg));
+    const uint64_t tail = cfg.dyn_tail < 0 ? n_tiles : uint64_t(cfg.dyn_tail) * grid;
+    const uint64_t n_static = n_tiles > tail ? (n_tiles - tail) / grid * grid : 0;
+    copy_bulk_dyn_kernel<<<unsigned(grid), 32, smem, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles, cfg.stages, cfg.stage_bytes, claim, n_static);
     check(cudaGetLastError(), "bulk copy launch");
     return;
   }

@@ -185,6 +185,7 @@ CopyConfig CopyConfig::from_env() {
   c.stage_bytes = unsigned(std::max(1, env_int("RESHARD_BULK_STAGE_KIB", int(c.stage_bytes >> 10)))) << 10;
   c.host_chunks = std::max(1, env_int("RESHARD_HOST_CHUNKS", c.host_chunks));
   c.tensor = env_int("RESHARD_TMA_TENSOR", c.tensor ? 1 : 0) != 0;
+  c.dyn_tail = env_int("RESHARD_DYN_TAIL", c.dyn_tail);
   return c;
 }
 

@@ -518,11 +518,13 @@ def test_run_host_world_matches_device_result(rs, pipeline, monkeypatch):
         del ex
 
 
-def test_bulk_dyn_kernel_bytes_exact(rs, orc, ctx, monkeypatch):
+@pytest.mark.parametrize("tail", ["-1", "1", "4"])
+def test_bulk_dyn_kernel_bytes_exact(rs, orc, ctx, monkeypatch, tail):
     """RESHARD_COPY_KERNEL=bulk_dyn (dynamic tile claims from a global counter that the last
     CTA resets): random transitions and repeated launches on one executor (the counter must be
     back at zero for every launch), every destination byte equal to the oracle's."""
     monkeypatch.setenv("RESHARD_COPY_KERNEL", "bulk_dyn")
+    monkeypatch.setenv("RESHARD_DYN_TAIL", tail)  # dynamic claims for everything / the last 1 or 4 tiles per CTA
     cat = rs.Catalog.gpt(256, 6, 64, 1024, rs.MIXED_ADAM)
     for (a_cfg, b_cfg) in [((2, 1, 1, 2), (2, 1, 2, 4)), ((4, 2, 1, 8), (2, 2, 2, 8)), ((2, 1, 1, 2), (1, 2, 1, 2))]:
         a = cat.build_strategy(DEV(a_cfg[3]), *a_cfg[:3])
