@@ -445,10 +445,9 @@ __global__ void __launch_bounds__(32, 1) copy_bulk_strided_kernel(const DevFanTi
 // claim, issued one claim ahead so its latency hides behind the previous claim's tiles), so the
 // CTAs still sweep memory together as one window and finish together.  The last CTA out resets
 // the counter for the next launch on the stream.
-constexpr unsigned long long kClaim = 2;
 __global__ void __launch_bounds__(32, 1) copy_bulk_dyn_kernel(const DevFanTile* __restrict__ tiles, unsigned long long n,
                                                               int stages, unsigned stage_bytes, unsigned long long* claim,
-                                                              unsigned long long n_static) {
+                                                              unsigned long long n_static, unsigned long long kClaim) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long bars[kBulkMaxStages];
   __shared__ DevFanTile sdesc[kBulkMaxStages];
@@ -714,7 +713,8 @@ void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg
     const uint64_t tail = cfg.dyn_tail < 0 ? n_tiles : uint64_t(cfg.dyn_tail) * grid;
     const uint64_t n_static = n_tiles > tail ? (n_tiles - tail) / grid * grid : 0;
     copy_bulk_dyn_kernel<<<unsigned(grid), 32, smem, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles, cfg.stages, cfg.stage_bytes, claim, n_static);
+        reinterpret_cast<const DevFanTile*>(d_tiles), n_tiles, cfg.stages, cfg.stage_bytes, claim, n_static,
+        (unsigned long long)std::max(1, cfg.dyn_claim));
     check(cudaGetLastError(), "bulk copy launch");
     return;
   }

@@ -186,6 +186,7 @@ CopyConfig CopyConfig::from_env() {
   c.host_chunks = std::max(1, env_int("RESHARD_HOST_CHUNKS", c.host_chunks));
   c.tensor = env_int("RESHARD_TMA_TENSOR", c.tensor ? 1 : 0) != 0;
   c.dyn_tail = env_int("RESHARD_DYN_TAIL", c.dyn_tail);
+  c.dyn_claim = env_int("RESHARD_DYN_CLAIM", c.dyn_claim);
   return c;
 }
 
