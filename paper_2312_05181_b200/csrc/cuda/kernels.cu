@@ -701,7 +701,12 @@ void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig&
 void launch_bulk(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream,
                  unsigned long long* claim) {
   if (n_tiles == 0) return;
-  if (cfg.kernel == CopyKernel::BulkDyn) {
+  // bulk_strided on a long launch switches to dynamic claims (r2_16-r2_18 same-box A/Bs: 2-3 %
+  // faster from ~6e5 tiles up, 2.5 % slower on GPT-2 small's 5e4), when a claim counter is given
+  const bool dyn = cfg.kernel == CopyKernel::BulkDyn ||
+                   (cfg.kernel == CopyKernel::BulkStrided && cfg.l2_hint == 0 && claim && cfg.dyn_min_tiles > 0 &&
+                    n_tiles >= uint64_t(cfg.dyn_min_tiles));
+  if (dyn) {
     if (!claim) raise(Errc::InvalidArgument, "bulk_dyn needs a zeroed claim counter");
     const size_t smem = size_t(cfg.stages) * cfg.stage_bytes;
     if (cfg.stages < 3 || cfg.stages > kBulkMaxStages || smem > 227 * 1024)

@@ -187,6 +187,7 @@ CopyConfig CopyConfig::from_env() {
   c.tensor = env_int("RESHARD_TMA_TENSOR", c.tensor ? 1 : 0) != 0;
   c.dyn_tail = env_int("RESHARD_DYN_TAIL", c.dyn_tail);
   c.dyn_claim = env_int("RESHARD_DYN_CLAIM", c.dyn_claim);
+  c.dyn_min_tiles = env_int("RESHARD_DYN_MIN_TILES", c.dyn_min_tiles);
   return c;
 }
 
