@@ -424,8 +424,14 @@ def pcie_probe(nbytes: int = 2 << 30, reps: int = 3) -> dict:
             "bidir_gbs_each": round(gb / (t_both * 1e-3), 1), "probe_bytes": nbytes}
 
 
-def copy_kernel_name() -> str:
+def copy_kernel_name(tiles_per_launch: int = 0) -> str:
+    """The dominant copy kernel: the library default is bulk_strided, which a launch of at least
+    RESHARD_DYN_MIN_TILES (2e5) tiles runs as bulk_dyn (dynamic claims)."""
     k = os.environ.get("RESHARD_COPY_KERNEL", "bulk_strided") or "bulk_strided"  # the library default
+    dyn_min = int(os.environ.get("RESHARD_DYN_MIN_TILES", "200000") or 0)
+    if k == "bulk_strided" and dyn_min > 0 and tiles_per_launch >= dyn_min and \
+            os.environ.get("RESHARD_BULK_HINT", "0") in ("", "0"):
+        k = "bulk_dyn"
     return {"bulk": "copy_bulk_kernel", "bulk_strided": "copy_bulk_strided_kernel", "ldg": "copy_v16_kernel",
             "ldg8": "copy_v16_kernel", "bulk_warp": "copy_bulk_warp_kernel", "bulk_dyn": "copy_bulk_dyn_kernel"}.get(k, k)
 
@@ -1093,7 +1099,8 @@ def run_ours(args):
         return
     writes = sum(sum(r) for r in rows)
     reads = sum(rbs)
-    kname = copy_kernel_name()
+    tiles_all = sum(ex.tiles(g)[0] for ex in exs for g in mine)
+    kname = copy_kernel_name(tiles_all // max(1, len(exs) * len(mine)))
     if N == 1 or emulated:
         # every byte on one device: HBM read + write of every copied byte over the step time
         achieved = (reads + writes) / (ms * 1e-3) / 1e9
@@ -1135,7 +1142,7 @@ def run_ours(args):
         "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs),
         "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "execution_report": report, "wall_s": round(wall, 4),
         "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4),
-        "tiles": sum(ex.tiles(g)[0] for ex in exs for g in mine),
+        "tiles": tiles_all,
         "host_ms": {"plan": round(build_plan.plan_ms, 2), "lower": round(lower_ms, 2), "prepare": round(prepare_ms, 2),
                     "reconfiguration_total_ms": round(build_plan.plan_ms + lower_ms + prepare_ms + ms, 2),
                     "note": "off the clock, once per reconfiguration: Alg. 1 planning, arena layout + piece "
