@@ -92,14 +92,50 @@ __device__ __forceinline__ void copy_tile(const DevTile& t) {
   }
 }
 
+// Tile schedule of the persistent LDG/STG kernels: the static grid-stride order (claim null),
+// or dynamic claims of 2 tiles from a global counter — thread 0 issues the next claim while
+// the CTA copies the current tiles, so the atomic's latency hides behind them; the last CTA
+// out resets the counter for the next launch on the stream (the drift argument of
+// copy_bulk_dyn_kernel, for the peer-push kernels).
+template <bool DYN, class F>
+__device__ __forceinline__ void for_each_tile(unsigned long long n, unsigned long long* claim, F&& f) {
+  if (!DYN) {
+    for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) f(k);
+    return;
+  }
+  constexpr unsigned long long B = 2;
+  __shared__ unsigned long long s_base[2];
+  if (threadIdx.x == 0) s_base[0] = atomicAdd(claim, B);
+  __syncthreads();
+  int buf = 0;
+  for (;;) {
+    const unsigned long long base = s_base[buf];
+    if (base >= n) break;
+    unsigned long long nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(claim, B);
+    for (unsigned long long k = base; k < base + B && k < n; ++k) f(k);
+    if (threadIdx.x == 0) s_base[buf ^ 1] = nxt;
+    __syncthreads();
+    buf ^= 1;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(claim + 1, 1ull) == gridDim.x - 1) {
+      claim[0] = 0, claim[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // K1 fast path: every tile 16-byte aligned (the host routes the others to copy_any_kernel).
 // Only the uint4 path is instantiated, so register use stays low enough for MINB CTAs/SM.
-template <int U, int MINB>
-__global__ void __launch_bounds__(512, MINB) copy_v16_kernel(const DevTile* __restrict__ tiles, unsigned long long n) {
-  for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
+template <int U, int MINB, bool DYN>
+__global__ void __launch_bounds__(512, MINB) copy_v16_kernel(const DevTile* __restrict__ tiles, unsigned long long n,
+                                                            unsigned long long* claim) {
+  for_each_tile<DYN>(n, claim, [&](unsigned long long k) {
     const DevTile t = tiles[k];
     copy_tile<uint4, U>(t);
-  }
+  });
 }
 
 // K1 general path: widest common alignment per tile.
@@ -172,11 +208,13 @@ __device__ __forceinline__ void copy_fan_tile(const DevFanTileL& t) {
   }
 }
 
-__global__ void __launch_bounds__(512, 2) copy_fan_v16_kernel(const DevFanTileL* __restrict__ tiles, unsigned long long n) {
-  for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
+template <bool DYN>
+__global__ void __launch_bounds__(512, 2) copy_fan_v16_kernel(const DevFanTileL* __restrict__ tiles, unsigned long long n,
+                                                             unsigned long long* claim) {
+  for_each_tile<DYN>(n, claim, [&](unsigned long long k) {
     const DevFanTileL t = tiles[k];
     copy_fan_tile<4>(t);
-  }
+  });
 }
 
 // ---- K3: TMA bulk-copy pipeline ------------------------------------------------------------
@@ -673,28 +711,37 @@ void check(cudaError_t e, const char* what) {
 }  // namespace
 
 void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
-                 void* stream) {
+                 void* stream, unsigned long long* claim) {
   if (n_tiles == 0) return;
+  if (!cfg.ldg_dyn) claim = nullptr;
   auto s = static_cast<cudaStream_t>(stream);
   auto tiles = reinterpret_cast<const DevTile*>(d_tiles);
   auto grid = [&](int per_sm) { return int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(per_sm))); };
   if (!aligned16) {
     copy_any_kernel<<<grid(8), 256, 0, s>>>(tiles, n_tiles);
   } else if (cfg.kernel == CopyKernel::Ldg8) {
-    copy_v16_kernel<8, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
+    copy_v16_kernel<8, 2, false><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles, nullptr);
+  } else if (claim) {
+    copy_v16_kernel<4, 2, true><<<grid(std::min(cfg.ctas_per_sm, 2)), 512, 0, s>>>(tiles, n_tiles, claim);
   } else if (cfg.ctas_per_sm >= 3) {
-    copy_v16_kernel<4, 3><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
+    copy_v16_kernel<4, 3, false><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles, nullptr);
   } else {
-    copy_v16_kernel<4, 2><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles);
+    copy_v16_kernel<4, 2, false><<<grid(cfg.ctas_per_sm), 512, 0, s>>>(tiles, n_tiles, nullptr);
   }
   check(cudaGetLastError(), "copy launch");
 }
 
-void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream) {
+void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream,
+                     unsigned long long* claim) {
   if (n_tiles == 0) return;
+  if (!cfg.ldg_dyn) claim = nullptr;
   const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(sms) * uint64_t(std::min(cfg.ctas_per_sm < 2 ? 2 : cfg.ctas_per_sm, 2))));
-  copy_fan_v16_kernel<<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const DevFanTileL*>(d_tiles),
-                                                                           n_tiles);
+  if (claim)
+    copy_fan_v16_kernel<true><<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const DevFanTileL*>(d_tiles), n_tiles, claim);
+  else
+    copy_fan_v16_kernel<false><<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const DevFanTileL*>(d_tiles), n_tiles, nullptr);
   check(cudaGetLastError(), "fan copy launch");
 }
 

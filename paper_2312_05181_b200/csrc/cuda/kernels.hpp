@@ -21,11 +21,14 @@ struct CellGeom {
 
 // K1/K2 (LDG/STG, 16-byte vectors) or K3 (TMA bulk pipeline): persistent tile copy over a
 // tile list.  aligned16: every tile is 16-byte aligned (else the generic-width kernel runs).
+// claim: a zeroed 2 x u64 counter for dynamic tile claims (used when cfg.ldg_dyn; the aligned
+// kernel only), else the static grid-stride order.
 void launch_copy(const CopyTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, bool aligned16,
-                 void* stream);
+                 void* stream, unsigned long long* claim = nullptr);
 // K2 fan-out (LDG/STG): every tile 16-byte aligned, n_dst <= kMaxFan destinations, natural
 // order; the source is read once for all destinations (peer destinations store over NVLink).
-void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream);
+void launch_copy_fan(const FanTile* d_tiles, uint64_t n_tiles, const CopyConfig& cfg, int sms, void* stream,
+                     unsigned long long* claim = nullptr);
 // K3 with fan-out: every tile 16-byte aligned and <= cfg.stage_bytes.  The array must be in
 // interleave_for_grid order for bulk_grid(n_tiles, sms, cfg) CTAs.
 // bulk_dyn (cfg.kernel == BulkDyn) claims tiles from `claim` (2 x u64, zero before the first

@@ -188,6 +188,7 @@ CopyConfig CopyConfig::from_env() {
   c.dyn_tail = env_int("RESHARD_DYN_TAIL", c.dyn_tail);
   c.dyn_claim = env_int("RESHARD_DYN_CLAIM", c.dyn_claim);
   c.dyn_min_tiles = env_int("RESHARD_DYN_MIN_TILES", c.dyn_min_tiles);
+  c.ldg_dyn = env_int("RESHARD_LDG_DYN", c.ldg_dyn ? 1 : 0) != 0;
   return c;
 }
 
@@ -328,6 +329,7 @@ struct Executor::Local {
   cudaEvent_t start = nullptr, stop = nullptr;
   unsigned long long* d_count = nullptr;
   unsigned long long* d_claim = nullptr;  // bulk_dyn's tile-claim counter (2 x u64, kept zero between launches)
+  unsigned long long* d_claim2 = nullptr; // the LDG/STG kernels' (they may run beside K3 on the side stream)
   std::vector<HostChunk> chunks;
   std::vector<DevPiece> chunk_pieces;  // the one tile list the host pipeline cuts into chunks (lazy)
   bool chunks_ready = true;           // chunks planned (or not applicable)
@@ -362,6 +364,7 @@ struct Executor::Local {
       if (e) cudaEventDestroy(e);
     if (d_count) cudaFree(d_count);
     if (d_claim) cudaFree(d_claim);
+    if (d_claim2) cudaFree(d_claim2);
     if (start) cudaEventDestroy(start);
     if (stop) cudaEventDestroy(stop);
     for (auto e : ev) cudaEventDestroy(e);
@@ -393,9 +396,9 @@ void Executor::launch_local(Local& l, void* stream) {
     side = l.s_aux;
   }
   cuda::launch_bulk(l.d_fan, l.n_fan, cfg_, sms, s, l.d_claim);
-  cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, side);
+  cuda::launch_copy(l.d_tiles, l.n_aligned, cfg_, sms, true, side, l.d_claim2);
   cuda::launch_copy(l.d_tiles + l.n_aligned, l.n_misc, cfg_, sms, false, side);
-  cuda::launch_copy_fan(l.d_fanl, l.n_fanl, cfg_, sms, side);
+  cuda::launch_copy_fan(l.d_fanl, l.n_fanl, cfg_, sms, side, l.d_claim2);
   if (both) {
     ck(cudaEventRecord(l.join, side), "join");
     ck(cudaStreamWaitEvent(s, l.join, 0), "join wait");
@@ -493,8 +496,10 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
     for (cudaEvent_t* e : {&l->e_h2d, &l->e_kern, &l->e_d2h}) ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     auto claim_counter = [&](Local& x) {
       auto st = static_cast<cudaStream_t>(ctx_.stream(w));
-      ck(cudaMallocAsync(reinterpret_cast<void**>(&x.d_claim), 2 * sizeof(unsigned long long), st), "cudaMallocAsync");
-      ck(cudaMemsetAsync(x.d_claim, 0, 2 * sizeof(unsigned long long), st), "memset claim");
+      for (unsigned long long** p : {&x.d_claim, &x.d_claim2}) {
+        ck(cudaMallocAsync(reinterpret_cast<void**>(p), 2 * sizeof(unsigned long long), st), "cudaMallocAsync");
+        ck(cudaMemsetAsync(*p, 0, 2 * sizeof(unsigned long long), st), "memset claim");
+      }
     };
     claim_counter(*l);
     if (w == central_) {
@@ -1159,9 +1164,9 @@ float Executor::run_host_world_pipelined(const std::vector<const void*>& host_sr
       const int sms = ctx_.sm_count(l->world);
       const auto& c = l->wchunks[k];
       cuda::launch_bulk(l->d_fan + c.t0[0], c.t1[0] - c.t0[0], cfg_, sms, s, l->d_claim);
-      cuda::launch_copy(l->d_tiles + c.t0[1], c.t1[1] - c.t0[1], cfg_, sms, true, s);
+      cuda::launch_copy(l->d_tiles + c.t0[1], c.t1[1] - c.t0[1], cfg_, sms, true, s, l->d_claim2);
       cuda::launch_copy(l->d_tiles + l->n_aligned + c.t0[2], c.t1[2] - c.t0[2], cfg_, sms, false, s);
-      cuda::launch_copy_fan(l->d_fanl + c.t0[3], c.t1[3] - c.t0[3], cfg_, sms, s);
+      cuda::launch_copy_fan(l->d_fanl + c.t0[3], c.t1[3] - c.t0[3], cfg_, sms, s, l->d_claim2);
       ck(cudaEventRecord(l->wev[K + k], s), "event");
     }
     for (size_t lj = 0; lj < local_.size(); ++lj) {
@@ -1397,7 +1402,7 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
       const uint64_t n = l->chunks[k].t1 - l->chunks[k].t0;
       if (l->n_fan)
         cuda::launch_bulk((l->d_fan_chunks ? l->d_fan_chunks : l->d_fan) + l->chunks[k].t0, n, cfg_, sms, s, l->d_claim);
-      else cuda::launch_copy(l->d_tiles + l->chunks[k].t0, n, cfg_, sms, true, s);
+      else cuda::launch_copy(l->d_tiles + l->chunks[k].t0, n, cfg_, sms, true, s, l->d_claim2);
       ck(cudaEventRecord(ec[k], s), "event");
     }
     for (size_t k = 0; k < K; ++k) {

@@ -99,6 +99,7 @@ struct CopyConfig {
   int host_chunks = 64;         // pipeline depth of the host-buffer path (run_host); r13 sweep
   int dyn_claim = 8;            // bulk_dyn: tiles per claim (RESHARD_DYN_CLAIM); r2_18: 1 loses 15 %, 2-4 1.5 %, 8 best
   int dyn_min_tiles = 200000;   // bulk_strided launches of at least this many tiles run as bulk_dyn (0: never; RESHARD_DYN_MIN_TILES)
+  bool ldg_dyn = false;         // K1/K2 aligned + fan-out kernels: dynamic tile claims (RESHARD_LDG_DYN)
   int dyn_tail = -1;            // bulk_dyn: tiles per CTA claimed dynamically at the end (-1: all; RESHARD_DYN_TAIL)
   bool tensor = false;          // bulk_strided: strided 2-D pieces as TMA tensor boxes (K3T, RESHARD_TMA_TENSOR=1)
   int l2_hint = 0;              // bulk_strided: L2 evict_first on loads (1), stores (2), both (3); r25 A/B: 0 is best (loads evict_first -2.3 %)

@@ -534,3 +534,29 @@ def test_bulk_dyn_kernel_bytes_exact(rs, orc, ctx, monkeypatch, tail):
             ex.apply()
         assert ex.verify() == 0
         del ex
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_ldg_dynamic_claims_bytes_exact(rs, orc, world, monkeypatch):
+    """RESHARD_LDG_DYN=1: the LDG/STG kernels (K1 aligned, K2 fan-out incl. peer stores in a
+    4-GPU world on cuda:0) claim tiles dynamically; repeated launches reuse the counter the last
+    CTA resets; every destination cell equals the oracle's."""
+    monkeypatch.setenv("RESHARD_LDG_DYN", "1")
+    monkeypatch.setenv("RESHARD_COPY_KERNEL", "ldg" if world == 1 else "bulk_strided")
+    ctx = rs.Context(world, list(range(world)), [0] * world)
+    entries = [("param/w", 1, (64, 32), 0, 0), ("param/d", 1, (32, 64), 1, 0), ("exp_avg/w", 2, (64, 32), 0, 1),
+               ("param/b", 3, (96,), 0, 1), ("param/ln", 2, (32,), -1, -1)]
+    for a_cfg, b_cfg in [((2, 1, 1, DEV(2)), (2, 1, 2, DEV(4))), ((4, 2, 1, DEV(8)), (2, 2, 2, DEV(8))),
+                         ((1, 2, 1, DEV(2)), (2, 1, 4, DEV(8)))]:
+        a, b, plan, oa, ob, oplan = _pair(rs, orc, entries, a_cfg, b_cfg)
+        n_src, n_dst = len(a_cfg[3]), len(b_cfg[3])
+        ex = rs.Executor(ctx, plan, [d % world for d in range(n_src)], [d % world for d in range(n_dst)], 4096)
+        ex.allocate_local()
+        ex.prepare()
+        ex.fill_sources()
+        for _ in range(3):
+            ex.apply()
+        assert ex.verify() == 0
+        ostate = oplan.apply(oa.fill())[0]
+        assert _compare_with_oracle(rs, ctx, ex, b, ostate, list(b_cfg[3])) > 0
+        del ex
