@@ -260,10 +260,14 @@ class Oracle:
 
     def dataset_gather(self, n, B, at_step, dp, d, perm, samples, file_class, n_threads=1):
         cnt = self.repartition_counts(n, B, at_step, dp)[d]
-        pos = np.zeros(max(cnt, 1), np.uint64)
-        ent = np.zeros((max(cnt, 1), 3), np.uint64)
-        boff = np.zeros(max(cnt, 1), np.uint64)
-        qidx = np.zeros(max(cnt, 1), np.uint32)
+        # outputs written once here, before the timed call: np.zeros maps pages lazily and the
+        # first-touch page faults (257-674 ms across boxes for config 5) would be timed as gather work
+        pos = np.empty(max(cnt, 1), np.uint64)
+        ent = np.empty((max(cnt, 1), 3), np.uint64)
+        boff = np.empty(max(cnt, 1), np.uint64)
+        qidx = np.empty(max(cnt, 1), np.uint32)
+        for a in (pos, ent, boff, qidx):
+            a.fill(0)
         qcount = np.zeros(3, np.uint64)
         secs = C.c_double(0)
         self._chk(self.lib.orc_dataset_gather(

@@ -1,18 +1,21 @@
 #!/bin/bash
-# round 2, call 21: dynamic claims in the LDG/STG kernels (K1 aligned / K2 fan-out) — parity and A/B
+# round 2, call 21: consolidated evidence after the dynamic tile claims — GPU suite, smoke, every workload's
+# line (both arms), emulated 2/4/8-GPU worlds, the default workload's launch list
 O=gpurun_out/r2_21; mkdir -p $O
-python -m pytest tests/test_gpu_executor.py -m gpu -q -x -k "ldg_dynamic or bulk_dyn or single_process" > $O/pytest.txt 2>&1; tail -2 $O/pytest.txt; grep -E "FAILED|rror" $O/pytest.txt | head -5
-ab() { n=$1; shift; env "$@" timeout 900 python bench.py --no-cpu-baseline --no-e2e --no-digests $W > $O/$n.json 2> $O/ab.err; python -c "import json;d=json.load(open('$O/$n.json'));print('$n',d['value'],d['ms_min'],d['roofline']['frac'],d['verify_mismatched_bytes'])"; tail -1 $O/ab.err; }
-for r in 1 2; do
-  for w in gpt3-1.3b-dp-scaleout gpt3-6.7b-recovery gpt2-small-tp2-to-pp2; do
-    W="--workload $w"
-    ab ${w}_ldg_static_$r RESHARD_COPY_KERNEL=ldg RESHARD_LDG_DYN=0
-    ab ${w}_ldg_dyn_$r RESHARD_COPY_KERNEL=ldg RESHARD_LDG_DYN=1
-  done
-  W="--gpus 4"
-  ab emu4_static_$r RESHARD_SAME_GPU=1 RESHARD_LDG_DYN=0
-  ab emu4_dyn_$r RESHARD_SAME_GPU=1 RESHARD_LDG_DYN=1
-  W="--gpus 8 --workload gpt3-6.7b-tp4pp2-to-tp2pp2dp2"
-  ab emu8_67b_static_$r RESHARD_SAME_GPU=1 RESHARD_LDG_DYN=0
-  ab emu8_67b_dyn_$r RESHARD_SAME_GPU=1 RESHARD_LDG_DYN=1
-done
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
+python -m pytest tests -m gpu -q > $O/pytest.txt 2>&1; tail -2 $O/pytest.txt; grep -E "FAILED" $O/pytest.txt | head
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -2 $O/smoke.txt
+run() { n=$1; shift; timeout 2400 python bench.py "$@" > $O/$n.json 2> $O/$n.err || echo "$n rc=$?"; python -c "import json;d=json.loads(open('$O/$n.json').read().strip().splitlines()[-1]);print('$n',d.get('value'),(d.get('roofline') or {}).get('frac'),(d.get('e2e') or {}).get('value'),(d.get('cpu_baseline') or {}).get('value'))" 2>&1 | tail -1; }
+run ref_default --impl reference
+run default
+run gpt2 --workload gpt2-small-tp2-to-pp2
+run ref_gpt2 --impl reference --workload gpt2-small-tp2-to-pp2
+run cfg3 --workload gpt3-6.7b-tp4pp2-to-tp2pp2dp2 --no-cpu-baseline
+run ref_cfg3 --impl reference --workload gpt3-6.7b-tp4pp2-to-tp2pp2dp2 --steps 3 --warmup 3
+run cfg4 --workload gpt3-6.7b-recovery --no-cpu-baseline
+run ref_cfg4 --impl reference --workload gpt3-6.7b-recovery --steps 3 --warmup 3
+run dataset --workload dataset-100m-dp2to4to8
+run ref_dataset --impl reference --workload dataset-100m-dp2to4to8 --steps 3 --warmup 3
+run central --mode central --no-cpu-baseline
+for n in 2 4 8; do RESHARD_SAME_GPU=1 run emu_n$n --gpus $n --no-cpu-baseline; done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-digests > $O/launches.out 2>&1; echo launches rc=$?
