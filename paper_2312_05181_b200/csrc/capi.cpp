@@ -79,12 +79,20 @@ Shape to_shape(int rank, const uint64_t* s) {
 SplitGrid to_grid(int rank, const int32_t* npts, const uint64_t* pts) {
   if (rank < 0 || rank > RS_MAX_RANK) raise(Errc::RankMismatch, "rank out of [0, 8]");
   std::vector<std::vector<uint64_t>> g(static_cast<size_t>(rank));
+  if (rank) need(npts, "split point counts");
   size_t k = 0;
-  for (int d = 0; d < rank; ++d)
+  for (int d = 0; d < rank; ++d) {
+    if (npts[d] < 0) raise(Errc::InvalidArgument, "negative split point count");
+    if (npts[d]) need(pts, "split points");
     for (int i = 0; i < npts[d]; ++i) g[size_t(d)].push_back(pts[k++]);
+  }
   return SplitGrid(std::move(g));
 }
 void from_grid(const SplitGrid& g, int32_t* npts, uint64_t* pts) {
+  if (g.rank()) need(npts, "split point count output");
+  size_t total = 0;
+  for (size_t d = 0; d < g.rank(); ++d) total += g.points()[d].size();
+  if (total) need(pts, "split point output");
   size_t k = 0;
   for (size_t d = 0; d < g.rank(); ++d) {
     npts[d] = int32_t(g.points()[d].size());
@@ -132,6 +140,8 @@ int rs_range_format(const rs_range* r, char* buf, uint64_t cap) {
 int rs_grid_cells(int rank, const uint64_t* shape, const int32_t* npts, const uint64_t* pts, int cap, rs_range* cells,
                   int* n) {
   return guard([&] {
+    need(n, "n");
+    if (cap > 0) need(cells, "cells");
     auto v = to_grid(rank, npts, pts).cells(to_shape(rank, shape));
     *n = int(v.size());
     for (int i = 0; i < int(v.size()) && i < cap; ++i) cells[i] = from_range(v[size_t(i)]);
