@@ -713,6 +713,52 @@ def pinned_total(dist, local, nbytes: int) -> int:
     return int(t.item())
 
 
+def windowed_e2e(rs, ctx, cat, plan, src_gpu, dst_gpu, tile, src_b, dst_b, src_ptr, dst_ptr,
+                 host_frac: float = 0.45) -> dict:
+    """The step end to end from pinned host buffers when the whole state does not fit the host
+    (GPT-3 6.7B: 94 GB of sources + 188 GB of destinations vs ~200 GB of host RAM) or the GPU
+    (waves): the catalog in the fewest host windows whose pinned src + dst buffers fit
+    `host_frac` of the available host RAM and whose arenas fit the device arenas already bound;
+    per window the sources are filled on the device and copied to the host buffer (off the
+    clock), one warm-up rs_executor_run_host (pins the pages, plans the host chunks), then one
+    timed run_host: H2D | copy kernel | D2H of that window.  value = sum over windows."""
+    avail = host_available_bytes()
+    pctx = rs.Context(1, [], [])
+    wins = None
+    for k in range(1, 65):
+        cand = windows_of(cat, k)
+        sizes = [rs.Executor(pctx, plan, src_gpu, dst_gpu, tile, window=w if len(cand) > 1 else None).arena_bytes(0)
+                 for w in cand]
+        if all(s <= src_b and d <= dst_b for s, d in sizes) and max(s + d for s, d in sizes) <= host_frac * avail:
+            wins = cand
+            break
+    if wins is None:
+        raise RuntimeError("no host window split fits the host RAM and the device arenas")
+    hs_b, hd_b = max(s for s, _ in sizes), max(d for _, d in sizes)
+    hs, hd = rs.host_alloc(max(hs_b, 1)), rs.host_alloc(max(hd_b, 1))
+    ms, bad, h2d, d2h, per = 0.0, 0, 0, 0, []
+    try:
+        for w, (s, d) in zip(wins, sizes):
+            ex = rs.Executor(ctx, plan, src_gpu, dst_gpu, tile, window=w if len(wins) > 1 else None)
+            ex.bind(0, src_ptr, dst_ptr)
+            ex.prepare()
+            ex.fill_sources()
+            ctx.dtoh(0, hs, src_ptr, s)
+            ex.run_host(0, hs, hd)
+            t = ex.run_host(0, hs, hd)["ms"]
+            bad += ex.verify()
+            ms, h2d, d2h = ms + t, h2d + s, d2h + d
+            per.append({"window": list(w), "ms": round(t, 2), "h2d": s, "d2h": d})
+            del ex
+    finally:
+        rs.host_free(hs)
+        rs.host_free(hd)
+    return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": 1,
+            "mismatched_bytes": bad, "windows": per, "host_buffers_gb": round((hs_b + hd_b) / 1e9, 1),
+            "path": f"rs_executor_run_host per host window ({len(wins)} catalog windows, sum of the windows' "
+                    "H2D | copy kernel | D2H times; the whole state exceeds host RAM)"}
+
+
 def world_e2e(rs, plan, src_gpu, dst_gpu, n_gpus, cuda_devs, tile, steps) -> dict:
     """The step end to end from pinned host buffers through rs_executor_run_host_world, one
     process driving every GPU (own context, arenas and executor; sources filled with K6 and
@@ -933,12 +979,26 @@ def run_ours(args):
     # e2e through the C-ABI with host buffers
     ex = exs[0]
     e2e = None
-    if len(exs) > 1:
-        e2e = {"value": None, "unit": "ms", "note": "waves: host-buffer path not run (state exceeds the GPUs' HBM)"}
-    elif args.no_e2e:
+    total_host = sum(s_need.values()) + sum(d_need.values())
+    if args.no_e2e:
         e2e = None
+    elif (len(exs) > 1 or total_host > 0.6 * host_available_bytes()) and world == 1 and N == 1 \
+            and args.mode == "distributed":
+        try:
+            e2e = windowed_e2e(rs, ctx, cat, plan, src_gpu, dst_gpu, tile, s_need[0], d_need[0], src_ptr[0], dst_ptr[0])
+            try:  # the PCIe bound of the same windows, both directions at once within each window
+                link = pcie_probe()
+                bound_ms = sum(max(w["h2d"] / (link["h2d_gbs"] * 1e9), w["d2h"] / (link["d2h_gbs"] * 1e9),
+                                   max(w["h2d"], w["d2h"]) / (link["bidir_gbs_each"] * 1e9)) for w in e2e["windows"]) * 1e3
+                e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
+                                   "frac": round(bound_ms / e2e["value"], 4)}
+            except Exception as exc:  # noqa: BLE001
+                e2e["roofline"] = {"error": str(exc)[:200]}
+        except Exception as exc:  # noqa: BLE001  (e.g. not enough pinned host memory)
+            e2e = {"value": None, "unit": "ms", "error": str(exc)[:200]}
+    elif len(exs) > 1:
+        e2e = {"value": None, "unit": "ms", "note": "waves at N > 1: host-buffer path not run (state exceeds the GPUs' HBM)"}
     elif world == 1:
-        total_host = sum(s_need.values()) + sum(d_need.values())
         if total_host > 0.6 * host_available_bytes():
             e2e = {"value": None, "unit": "ms", "note": f"host buffers of {total_host / 1e9:.1f} GB exceed 60% of host RAM"}
         else:
