@@ -424,6 +424,15 @@ def pcie_probe(nbytes: int = 2 << 30, reps: int = 3) -> dict:
             "bidir_gbs_each": round(gb / (t_both * 1e-3), 1), "probe_bytes": nbytes}
 
 
+def pcie_overlap_bound_ms(h2d: int, d2h: int, link: dict) -> float:
+    """Lower bound of a pipeline that moves h2d bytes up and d2h bytes down at once: both
+    directions at the measured bidirectional rate until the smaller side is done, then the rest
+    of the larger side at its one-way rate."""
+    lo, hi = min(h2d, d2h), max(h2d, d2h)
+    alone = link["h2d_gbs"] if h2d >= d2h else link["d2h_gbs"]
+    return (lo / (link["bidir_gbs_each"] * 1e9) + (hi - lo) / (alone * 1e9)) * 1e3
+
+
 def copy_kernel_name(tiles_per_launch: int = 0) -> str:
     """The dominant copy kernel: the library default is bulk_strided, which a launch of at least
     RESHARD_DYN_MIN_TILES (2e5) tiles runs as bulk_dyn (dynamic claims)."""
@@ -988,8 +997,7 @@ def run_ours(args):
             e2e = windowed_e2e(rs, ctx, cat, plan, src_gpu, dst_gpu, tile, s_need[0], d_need[0], src_ptr[0], dst_ptr[0])
             try:  # the PCIe bound of the same windows, both directions at once within each window
                 link = pcie_probe()
-                bound_ms = sum(max(w["h2d"] / (link["h2d_gbs"] * 1e9), w["d2h"] / (link["d2h_gbs"] * 1e9),
-                                   max(w["h2d"], w["d2h"]) / (link["bidir_gbs_each"] * 1e9)) for w in e2e["windows"]) * 1e3
+                bound_ms = sum(pcie_overlap_bound_ms(w["h2d"], w["d2h"], link) for w in e2e["windows"])
                 e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
                                    "frac": round(bound_ms / e2e["value"], 4)}
             except Exception as exc:  # noqa: BLE001
@@ -1028,8 +1036,7 @@ def run_ours(args):
                         if args.mode == "central":  # H2D, both phases, D2H in sequence (no chunk pipeline)
                             bound_ms = (s_need[0] / (link["h2d_gbs"] * 1e9) + d_eff / (link["d2h_gbs"] * 1e9)) * 1e3
                         else:  # chunk pipeline: both directions at once
-                            bound_ms = max(s_need[0] / (link["h2d_gbs"] * 1e9), d_eff / (link["d2h_gbs"] * 1e9),
-                                           max(s_need[0], d_eff) / (link["bidir_gbs_each"] * 1e9)) * 1e3
+                            bound_ms = pcie_overlap_bound_ms(s_need[0], d_eff, link)
                         e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
                                            "frac": round(bound_ms / e2e["value"], 4)}
                     except Exception as exc:

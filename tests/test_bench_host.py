@@ -43,3 +43,35 @@ def test_cpu_reference_whole_workload_gpt2():
 
 def test_k5_traffic_from_the_committed_capture():
     assert bench.k5_dram_bytes_per_sample() == pytest.approx(173.6, abs=0.5)
+
+
+def test_pcie_overlap_bound():
+    """Equal directions: the bidirectional rate alone; a larger side finishes at its one-way rate."""
+    link = {"h2d_gbs": 50.0, "d2h_gbs": 40.0, "bidir_gbs_each": 25.0}
+    assert bench.pcie_overlap_bound_ms(10**9, 10**9, link) == pytest.approx(40.0)
+    assert bench.pcie_overlap_bound_ms(10**9, 3 * 10**9, link) == pytest.approx(40.0 + 50.0)
+    assert bench.pcie_overlap_bound_ms(3 * 10**9, 10**9, link) == pytest.approx(40.0 + 40.0)
+    assert bench.pcie_overlap_bound_ms(0, 2 * 10**9, link) == pytest.approx(50.0)
+
+
+def test_windowed_e2e_splits_for_host_ram(rs, monkeypatch):
+    """The 6.7B state (94 GB of sources, 188 GB of destinations at N = 1) does not fit the host:
+    windowed_e2e picks the fewest catalog windows whose pinned buffers fit the given share of
+    host RAM and whose arenas fit the device arenas (planning only here: no GPU calls before
+    the split is chosen)."""
+    name = "gpt3-6.7b-tp4pp2-to-tp2pp2dp2"
+    cat, a, b, plan, src_gpu, dst_gpu = bench.build_plan(rs, name, 1)
+    pctx = rs.Context(1, [], [])
+    full = rs.Executor(pctx, plan, src_gpu, dst_gpu, 256 << 10).arena_bytes(0)
+    monkeypatch.setattr(bench, "host_available_bytes", lambda: 200 * 10**9)
+
+    class Stop(Exception):
+        pass
+
+    def no_pinned(n):
+        raise Stop(n)
+
+    monkeypatch.setattr(rs, "host_alloc", no_pinned)
+    with pytest.raises(Stop) as e:
+        bench.windowed_e2e(rs, None, cat, plan, src_gpu, dst_gpu, 256 << 10, full[0], full[1], 0, 0)
+    assert e.value.args[0] <= 0.45 * 200 * 10**9 and e.value.args[0] >= full[0] / 8
