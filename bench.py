@@ -745,7 +745,7 @@ def windowed_e2e(rs, ctx, cat, plan, src_gpu, dst_gpu, tile, src_b, dst_b, src_p
         raise RuntimeError("no host window split fits the host RAM and the device arenas")
     hs_b, hd_b = max(s for s, _ in sizes), max(d for _, d in sizes)
     hs, hd = rs.host_alloc(max(hs_b, 1)), rs.host_alloc(max(hd_b, 1))
-    ms, bad, h2d, d2h, per = 0.0, 0, 0, 0, []
+    ms, ms_full, bad, h2d, d2h, per = 0.0, 0.0, 0, 0, 0, []
     try:
         for w, (s, d) in zip(wins, sizes):
             ex = rs.Executor(ctx, plan, src_gpu, dst_gpu, tile, window=w if len(wins) > 1 else None)
@@ -753,19 +753,24 @@ def windowed_e2e(rs, ctx, cat, plan, src_gpu, dst_gpu, tile, src_b, dst_b, src_p
             ex.prepare()
             ex.fill_sources()
             ctx.dtoh(0, hs, src_ptr, s)
-            ex.run_host(0, hs, hd)
-            t = ex.run_host(0, hs, hd)["ms"]
+            ex.run_host(0, hs, hd, skip_unread=True)
+            t = ex.run_host(0, hs, hd, skip_unread=True)["ms"]
             bad += ex.verify()
-            ms, h2d, d2h = ms + t, h2d + s, d2h + d
-            per.append({"window": list(w), "ms": round(t, 2), "h2d": s, "d2h": d})
+            up = ex.host_upload_bytes(0, skip_unread=True)
+            t_full = ex.run_host(0, hs, hd)["ms"]  # the same with the whole src arena uploaded
+            ms, h2d, d2h, ms_full = ms + t, h2d + up, d2h + d, ms_full + t_full
+            per.append({"window": list(w), "ms": round(t, 2), "h2d": up, "d2h": d, "src_arena": s,
+                        "ms_full_src_upload": round(t_full, 2)})
             del ex
     finally:
         rs.host_free(hs)
         rs.host_free(hd)
     return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": 1,
             "mismatched_bytes": bad, "windows": per, "host_buffers_gb": round((hs_b + hd_b) / 1e9, 1),
-            "path": f"rs_executor_run_host per host window ({len(wins)} catalog windows, sum of the windows' "
-                    "H2D | copy kernel | D2H times; the whole state exceeds host RAM)"}
+            "ms_full_src_upload": round(ms_full, 3),
+            "path": f"rs_executor_run_host_flags(RS_HOST_SKIP_UNREAD) per host window ({len(wins)} catalog windows, "
+                    "sum of the windows' H2D of the source ranges the tiles read | copy kernel | D2H times; the "
+                    "whole state exceeds host RAM; cells kept in place stay in the host buffer)"}
 
 
 def world_e2e(rs, plan, src_gpu, dst_gpu, n_gpus, cuda_devs, tile, steps) -> dict:
@@ -1015,10 +1020,15 @@ def run_ours(args):
             try:
                 for g in mine:
                     ctx.dtoh(g, hs[g], src_ptr[g], s_need[g])
+                h2d_bytes = sum(s_need.values())
                 if N == 1:  # one GPU: the chunk-pipelined host path (H2D | kernels | D2H overlapped)
-                    ex.run_host(0, hs[0], hd[0])
-                    e2e_ms = [ex.run_host(0, hs[0], hd[0])["ms"] for _ in range(args.e2e_steps)]
-                    path = "rs_executor_run_host: chunk-pipelined H2D | copy kernel | D2H, pinned host buffers"
+                    skip = args.mode == "distributed"
+                    ex.run_host(0, hs[0], hd[0], skip_unread=skip)
+                    e2e_ms = [ex.run_host(0, hs[0], hd[0], skip_unread=skip)["ms"] for _ in range(args.e2e_steps)]
+                    h2d_bytes = ex.host_upload_bytes(0, skip_unread=skip)
+                    path = ("rs_executor_run_host_flags(RS_HOST_SKIP_UNREAD): chunk-pipelined H2D of the source "
+                            "ranges the tiles read | copy kernel | D2H, pinned host buffers") if skip else \
+                        "rs_executor_run_host: H2D | kernels | D2H, pinned host buffers"
                 else:  # all GPUs from one common start: H2D | world barrier | kernels | barrier | D2H
                     hs_l, hd_l = [hs[g] for g in range(N)], [hd[g] for g in range(N)]
                     ex.run_host_world(hs_l, hd_l)
@@ -1028,15 +1038,15 @@ def run_ours(args):
                 bad_e2e = ex.verify()
                 d_eff = sum(d_need.values()) - ex.staging_bytes()
                 e2e = {"value": round(statistics.mean(e2e_ms), 3), "unit": "ms",
-                       "h2d_bytes_per_step": sum(s_need.values()), "d2h_bytes_per_step": d_eff,
+                       "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d_eff,
                        "steps": args.e2e_steps, "mismatched_bytes": bad_e2e, "path": path}
                 if N == 1:
                     try:  # the PCIe bound of this path, measured on the same box
                         link = pcie_probe()
                         if args.mode == "central":  # H2D, both phases, D2H in sequence (no chunk pipeline)
-                            bound_ms = (s_need[0] / (link["h2d_gbs"] * 1e9) + d_eff / (link["d2h_gbs"] * 1e9)) * 1e3
+                            bound_ms = (h2d_bytes / (link["h2d_gbs"] * 1e9) + d_eff / (link["d2h_gbs"] * 1e9)) * 1e3
                         else:  # chunk pipeline: both directions at once
-                            bound_ms = pcie_overlap_bound_ms(s_need[0], d_eff, link)
+                            bound_ms = pcie_overlap_bound_ms(h2d_bytes, d_eff, link)
                         e2e["roofline"] = {"bound": "pcie", **link, "bound_ms": round(bound_ms, 2),
                                            "frac": round(bound_ms / e2e["value"], 4)}
                     except Exception as exc:

@@ -258,6 +258,15 @@ int rs_executor_wait(rs_executor* e, int cap, rs_timing* out, int* n); /* per lo
 /* end to end on host buffers (single-GPU world): H2D src arena, copy kernel, D2H dst arena,
  * all on the GPU's stream and bracketed by CUDA events; arenas must be bound */
 int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src_arena, void* host_dst_arena, rs_timing* out);
+/* The same with flags.  RS_HOST_SKIP_UNREAD: host -> device copies of only the source ranges
+ * the copy tiles read (pipelined path); source state no tile reads (cells a reshard keeps in
+ * place, e.g. the survivors' own cells in a recovery) stays in the host buffer and the device
+ * src arena is not refreshed there.  rs_executor_host_upload_bytes: the bytes such a call copies
+ * host -> device.  Unknown flag bits: InvalidArgument. */
+#define RS_HOST_SKIP_UNREAD 1u
+int rs_executor_run_host_flags(rs_executor* e, int gpu, const void* host_src_arena, void* host_dst_arena,
+                               unsigned flags, rs_timing* out);
+int rs_executor_host_upload_bytes(rs_executor* e, int gpu, unsigned flags, uint64_t* bytes);
 /* multi-process end-to-end step in phases separated by the caller's cross-rank barriers:
  * 0 = start mark + H2D of the GPU's src arena (host_buf = src), 1 = kernels (host_buf
  * unused), 2 = D2H of its dst arena (host_buf = dst) + stop mark; each phase returns after

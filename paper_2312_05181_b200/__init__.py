@@ -38,6 +38,7 @@ F32, F16, I64, U8, BF16 = 0, 1, 2, 3, 4
 WIDTH = {F32: 4, F16: 2, I64: 8, U8: 1, BF16: 2}
 FP32_ADAM, MIXED_ADAM, FP32_PARAM = 0, 1, 2
 LAYER_PRE, LAYER_POST = -1, -2
+HOST_SKIP_UNREAD = 1  # RS_HOST_SKIP_UNREAD (run_host flags)
 
 
 class ReshardError(Exception):
@@ -602,10 +603,19 @@ class Executor:
         self.run()
         return self.wait()
 
-    def run_host(self, gpu: int, host_src: int, host_dst: int) -> dict:
+    def run_host(self, gpu: int, host_src: int, host_dst: int, skip_unread: bool = False) -> dict:
+        """skip_unread: upload only the source ranges the tiles read (RS_HOST_SKIP_UNREAD)."""
         t = _capi.rs_timing()
-        _chk(lib.rs_executor_run_host(self.h, gpu, host_src, host_dst, C.byref(t)))
+        if skip_unread:
+            _chk(lib.rs_executor_run_host_flags(self.h, gpu, host_src, host_dst, HOST_SKIP_UNREAD, C.byref(t)))
+        else:
+            _chk(lib.rs_executor_run_host(self.h, gpu, host_src, host_dst, C.byref(t)))
         return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, read_bytes=t.read_bytes)
+
+    def host_upload_bytes(self, gpu: int, skip_unread: bool = False) -> int:
+        b = C.c_uint64()
+        _chk(lib.rs_executor_host_upload_bytes(self.h, gpu, HOST_SKIP_UNREAD if skip_unread else 0, C.byref(b)))
+        return b.value
 
     def host_phase(self, gpu: int, phase: int, host_buf: int = 0) -> None:
         _chk(lib.rs_executor_host_phase(self.h, gpu, phase, host_buf))

@@ -129,6 +129,8 @@ SIGNATURES = {
     "rs_executor_run": (C.c_int, [P]),
     "rs_executor_wait": (C.c_int, [P, C.c_int, C.POINTER(rs_timing), C.POINTER(C.c_int)]),
     "rs_executor_run_host": (C.c_int, [P, C.c_int, P, P, C.POINTER(rs_timing)]),
+    "rs_executor_run_host_flags": (C.c_int, [P, C.c_int, P, P, C.c_uint, C.POINTER(rs_timing)]),
+    "rs_executor_host_upload_bytes": (C.c_int, [P, C.c_int, C.c_uint, C.POINTER(C.c_uint64)]),
     "rs_executor_host_phase": (C.c_int, [P, C.c_int, C.c_int, P]),
     "rs_executor_host_elapsed": (C.c_int, [P, C.c_int, C.POINTER(C.c_float)]),
     "rs_executor_world_ms": (C.c_int, [P, C.POINTER(C.c_float)]),

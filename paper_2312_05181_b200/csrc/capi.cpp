@@ -679,6 +679,20 @@ int rs_executor_run_host(rs_executor* e, int gpu, const void* host_src, void* ho
     *out = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
+int rs_executor_run_host_flags(rs_executor* e, int gpu, const void* host_src, void* host_dst, unsigned flags,
+                               rs_timing* out) {
+  return guard([&] {
+    need(e, "executor"), need(out, "out");
+    Timing t = e->e->run_host(gpu, host_src, host_dst, flags);
+    *out = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
+  });
+}
+int rs_executor_host_upload_bytes(rs_executor* e, int gpu, unsigned flags, uint64_t* bytes) {
+  return guard([&] {
+    need(e, "executor"), need(bytes, "bytes");
+    *bytes = e->e->host_upload_bytes(gpu, flags);
+  });
+}
 int rs_executor_host_phase(rs_executor* e, int gpu, int phase, void* host_buf) {
   return guard([&] {
     need(e, "executor");

@@ -1314,13 +1314,28 @@ void Executor::plan_host_chunks(Local& local) {
   }  // other kernels walk the natural order: the chunks are slices of the tile array
 }
 
-Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
+uint64_t Executor::host_upload_bytes(int gpu, unsigned flags) {
+  Local* l = nullptr;
+  for (auto& x : local_)
+    if (x->world == gpu) l = x.get();
+  if (!l) raise(Errc::DeviceUnavailable, "host_upload_bytes: GPU " + std::to_string(gpu) + " is not local");
+  if (ctx_.world() != 1) raise(Errc::InvalidArgument, "host_upload_bytes: single-GPU worlds only");
+  if (!l->chunks_ready) plan_host_chunks(*l);
+  if (l->chunks.empty() || !(flags & kHostSkipUnread)) return src_size_[size_t(gpu)];
+  uint64_t n = 0;
+  for (const HostChunk& c : l->chunks)
+    for (auto [off, len] : c.uploads) n += len;
+  return n;
+}
+
+Timing Executor::run_host(int gpu, const void* host_src, void* host_dst, unsigned flags) {
   TraceRange trace_("Executor::run_host");
   Local* l = nullptr;
   for (auto& x : local_)
     if (x->world == gpu) l = x.get();
   if (!l) raise(Errc::DeviceUnavailable, "run_host: GPU " + std::to_string(gpu) + " is not local");
   if (ctx_.world() != 1) raise(Errc::InvalidArgument, "run_host: single-GPU worlds only");
+  if (flags & ~kHostSkipUnread) raise(Errc::InvalidArgument, "run_host: unknown flags");
   if (!l->chunks_ready) plan_host_chunks(*l);
   DeviceGuard g(l->dev);
   auto s = static_cast<cudaStream_t>(ctx_.stream(gpu));
@@ -1388,14 +1403,17 @@ Timing Executor::run_host(int gpu, const void* host_src, void* host_dst) {
       }
       ck(cudaEventRecord(eh[k], l->s_h2d), "event");
     }
-    // state no tile reads (kept cells nobody copies) still goes to the device, last
-    std::sort(all.begin(), all.end());
-    uint64_t cur = 0;
-    for (auto [a, b] : all) {
-      if (a > cur) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, a - cur, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
-      cur = std::max(cur, b);
+    // state no tile reads (kept cells nobody copies) still goes to the device, last — unless
+    // the caller keeps it on the host (kHostSkipUnread)
+    if (!(flags & kHostSkipUnread)) {
+      std::sort(all.begin(), all.end());
+      uint64_t cur = 0;
+      for (auto [a, b] : all) {
+        if (a > cur) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, a - cur, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
+        cur = std::max(cur, b);
+      }
+      if (cur < ssize) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, ssize - cur, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
     }
-    if (cur < ssize) ck(cudaMemcpyAsync(dsrc + cur, hsrc + cur, ssize - cur, cudaMemcpyHostToDevice, l->s_h2d), "h2d rest");
     const int sms = ctx_.sm_count(gpu);
     for (size_t k = 0; k < K; ++k) {
       ck(cudaStreamWaitEvent(s, eh[k], 0), "wait");

@@ -113,6 +113,9 @@ struct CellBinding {
   uint64_t bytes = 0;
 };
 
+// run_host flags (the C ABI's RS_HOST_* bits)
+enum : unsigned { kHostSkipUnread = 1u };
+
 struct Timing {
   float ms = 0;        // device time of the copy kernel(s), CUDA events on the launch stream
   uint64_t tiles = 0;
@@ -181,7 +184,11 @@ class Executor {
   // End-to-end on host buffers (single-GPU world): H2D of the whole src arena from
   // `host_src`, the copy kernel, D2H of the whole dst arena into `host_dst`; CUDA events
   // bracket all three.  Pinned host memory gives full PCIe bandwidth.
-  Timing run_host(int gpu, const void* host_src, void* host_dst);
+  // flags & kHostSkipUnread: upload only the source ranges the tiles read (the pipelined path);
+  // state no tile reads (kept cells) stays in the host buffer and is not copied to the device.
+  Timing run_host(int gpu, const void* host_src, void* host_dst, unsigned flags = 0);
+  // Bytes run_host(gpu, ..., flags) copies host -> device.
+  uint64_t host_upload_bytes(int gpu, unsigned flags);
   // The same end-to-end step for multi-process worlds, in phases the caller separates with
   // cross-rank barriers: 0 = start mark + H2D of this GPU's src arena, 1 = the kernels,
   // 2 = D2H of this GPU's dst arena + stop mark.  Each phase is async on the GPU's stream

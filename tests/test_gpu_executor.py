@@ -245,6 +245,41 @@ def test_run_host_pipelined_matches_device_result(rs, ctx):
         rs.host_free(hd)
 
 
+def test_run_host_skip_unread_recovery(rs, ctx):
+    """RS_HOST_SKIP_UNREAD on a recovery (survivors keep half of their cells in place): only the
+    source ranges the tiles read cross PCIe, and every destination byte still verifies and comes
+    back to the host buffer; unknown flag bits are rejected."""
+    cat = rs.Catalog.gpt(64, 4, 16, 128, rs.MIXED_ADAM)
+    a = cat.build_strategy(DEV(8), 2, 2, 2)
+    b = cat.build_strategy([(0, 0), (0, 2), (0, 5), (0, 7)], 2, 2, 1)
+    plan = rs.recover(a, [(0, 1), (0, 3), (0, 4), (0, 6)], b)
+    st = plan.stats()
+    ex, _ = _run(rs, ctx, plan, 8, 4, 16 << 10)
+    s_bytes, d_bytes = ex.arena_bytes(0)
+    up_all, up_read = ex.host_upload_bytes(0), ex.host_upload_bytes(0, skip_unread=True)
+    assert up_all == s_bytes
+    assert up_read == st["moved_bytes"] < s_bytes  # each moved byte read once, kept cells stay home
+    hs, hd = rs.host_alloc(s_bytes), rs.host_alloc(max(d_bytes, 1))
+    src_ptr, dst_ptr = ex.arenas[0]
+    ctx.dtoh(0, hs, src_ptr, s_bytes)
+    ctx.memset(0, src_ptr, 0, s_bytes)
+    ctx.memset(0, dst_ptr, 0, d_bytes)
+    ex.run_host(0, hs, hd, skip_unread=True)
+    # the kept cells (bound in the src arena) were not uploaded: bring them back, then every
+    # destination cell — the moved ones written by the run from the uploaded ranges alone — verifies
+    ctx.htod(0, src_ptr, hs, s_bytes)
+    assert ex.verify() == 0
+    dev = np.zeros(d_bytes, np.uint8)
+    ctx.dtoh(0, dev.ctypes.data, dst_ptr, d_bytes)
+    host = np.ctypeslib.as_array((ctypes.c_uint8 * d_bytes).from_address(hd))
+    assert np.array_equal(dev, host)
+    t = rs._capi.rs_timing()
+    rc = rs.lib.rs_executor_run_host_flags(ex.h, 0, hs, hd, 6, ctypes.byref(t))
+    assert rc != 0 and "flags" in rs.lib.rs_last_error().decode()
+    rs.host_free(hs)
+    rs.host_free(hd)
+
+
 def _kat():
     import json
     import os
