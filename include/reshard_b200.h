@@ -387,6 +387,21 @@ int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
  * locate_sample loops. */
 int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,
                    uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
+/* Several ranks' K5 on one GPU (a GPU hosting several new DP ranks): the gather passes one
+ * after another on the GPU's stream, each rank's tile scan + finalize on a second stream once
+ * its gather pass is done, so they overlap the next rank's gather pass.  idx->file_class is
+ * ignored: each job names its own (locator classes differ per rank).  total->ms: first launch
+ * to the last finalize (events); total->main_ms: the sum of the gather passes; per_job
+ * (nullable, n entries): each rank's gather-pass time in ms and main_ms, tiles, launches,
+ * algorithmic bytes.  Same outputs as n rs_repartition calls. */
+typedef struct rs_repartition_job {
+  uint64_t at_step, new_dp, rank;
+  const uint8_t* file_class;     /* device, per file: 0 local, 1 peer, 2 remote for this rank */
+  rs_partition_out out;
+  void* scratch;                 /* rs_repartition_scratch_bytes(count), device */
+} rs_repartition_job;
+int rs_repartition_batch(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch,
+                         const rs_repartition_job* jobs, int n, rs_timing* per_job, rs_timing* total);
 /* rs_repartition, then the rank's outputs back to host buffers on the same stream (count
  * entries of pos / ent / boff, qcount[c] entries of queue c).  timing->ms: kernels + D2H,
  * timing->main_ms: the gather pass, timing->bytes: D2H bytes. */

@@ -795,6 +795,24 @@ class Partition:
         return out
 
 
+def repartition_batch(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, n: int, global_batch: int,
+                      jobs: Sequence[tuple[int, int, int, int, "Partition"]], entry_bytes: int = 24) -> dict:
+    """K5 for several ranks on one GPU: jobs = [(at_step, new_dp, rank, class_ptr, partition)].
+    The gather passes run back to back, each rank's scan + finalize beside the next gather pass
+    (rs_repartition_batch).  ms: whole batch; gather_ms: sum of the gather passes; per_job:
+    each rank's gather-pass ms."""
+    idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, None, n, entry_bytes)
+    arr = (_capi.rs_repartition_job * max(len(jobs), 1))()
+    for i, (at, dp, d, cls, part) in enumerate(jobs):
+        arr[i].at_step, arr[i].new_dp, arr[i].rank, arr[i].file_class = at, dp, d, cls
+        arr[i].out, arr[i].scratch = part.c(), part.scratch
+    per = (_capi.rs_timing * max(len(jobs), 1))()
+    t = _capi.rs_timing()
+    _chk(lib.rs_repartition_batch(ctx.h, gpu, C.byref(idx), global_batch, arr, len(jobs), per, C.byref(t)))
+    return dict(ms=t.ms, tiles=t.tiles, bytes=t.bytes, launches=t.launches, gather_ms=t.main_ms,
+                per_job=[per[i].main_ms for i in range(len(jobs))])
+
+
 def repartition(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, class_ptr: int, n: int, global_batch: int,
                 at_step: int, new_dp: int, rank: int, part: "Partition", entry_bytes: int = 24) -> dict:
     """K5 for one rank.  entry_bytes 24: samples_ptr holds the packed reference records;

@@ -172,6 +172,8 @@ SIGNATURES = {
                                  P, C.POINTER(rs_timing)]),
     "rs_repartition_gather_probe": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                               C.c_int, C.POINTER(rs_timing)]),
+    "rs_repartition_batch": (C.c_int, [P, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p,
+                                       C.POINTER(rs_timing)]),
 }
 
 
@@ -188,6 +190,11 @@ class rs_partition_host(C.Structure):
 class rs_partition_out(C.Structure):
     _fields_ = [("pos", C.c_void_p), ("ent", C.c_void_p), ("boff", C.c_void_p), ("queue", C.c_void_p * 3),
                 ("qcount", C.c_void_p)]
+
+
+class rs_repartition_job(C.Structure):
+    _fields_ = [("at_step", C.c_uint64), ("new_dp", C.c_uint64), ("rank", C.c_uint64), ("file_class", C.c_void_p),
+                ("out", rs_partition_out), ("scratch", C.c_void_p)]
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:

@@ -922,6 +922,33 @@ int rs_repartition(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t
     if (timing) *timing = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
   });
 }
+int rs_repartition_batch(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t B, const rs_repartition_job* jobs,
+                         int n, rs_timing* per_job, rs_timing* total) {
+  return guard([&] {
+    need(idx, "index"), need(total, "total");
+    if (n < 0) raise(Errc::InvalidArgument, "negative job count");
+    if (n > 0) need(jobs, "jobs");
+    DatasetIndexView v{idx->perm, idx->samples, idx->file_class, idx->n, idx->entry_bytes};
+    std::vector<RepartJob> js;
+    js.reserve(size_t(n));
+    for (int i = 0; i < n; ++i) {
+      const rs_repartition_job& j = jobs[i];
+      need(j.scratch, "scratch"), need(j.file_class, "file_class");
+      js.push_back(RepartJob{j.at_step, j.new_dp, j.rank, j.file_class,
+                             PartitionOut{j.out.pos, j.out.ent, j.out.boff, {j.out.queue[0], j.out.queue[1], j.out.queue[2]},
+                                          j.out.qcount},
+                             j.scratch});
+    }
+    std::vector<Timing> pj;
+    Timing t = repartition_batch_device(ctx_of(c), gpu, v, B, js.data(), js.size(), per_job ? &pj : nullptr);
+    *total = rs_timing{t.ms, t.tiles, t.bytes, t.launches, t.read_bytes, t.main_ms};
+    if (per_job)
+      for (int i = 0; i < n; ++i) {
+        const Timing& r = pj[size_t(i)];
+        per_job[i] = rs_timing{r.ms, r.tiles, r.bytes, r.launches, r.read_bytes, r.main_ms};
+      }
+  });
+}
 int rs_repartition_gather_probe(rs_context* c, int gpu, const rs_dataset_index* idx, uint64_t B, uint64_t at_step,
                                 uint64_t dp, uint64_t rank, int reps, rs_timing* timing) {
   return guard([&] {

@@ -890,15 +890,74 @@ uint64_t repartition_scratch_bytes(uint64_t count) {
          2 * align256((tiles + 1023) / 1024 * sizeof(Agg));
 }
 
+// One rank's split2 launch state: kernel parameters and its scratch carved into the tile
+// counters / aggregates / class bytes / scan blocks (repartition_scratch_bytes).
+struct K5Job {
+  Params p;
+  Outs o;
+  Scratch s;
+  unsigned char* cls = nullptr;
+  Agg* blk = nullptr;
+  uint64_t count = 0, tiles = 0, sblocks = 0;
+};
+
+K5Job k5_job(const DatasetIndexView& idx, uint64_t B, uint64_t at_step, uint64_t new_dp, uint64_t rank,
+             const PartitionOut& out, void* scratch, uint64_t tile) {
+  K5Job j;
+  j.count = repartition_count(idx.n, B, at_step, new_dp, rank);
+  if (j.count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
+  j.tiles = (j.count + tile - 1) / tile;
+  j.sblocks = (j.tiles + 1023) / 1024;
+  char* sc = static_cast<char*>(scratch);
+  const uint64_t tl = j.tiles;
+  j.s = Scratch{reinterpret_cast<unsigned*>(sc), reinterpret_cast<unsigned*>(sc + 256),
+                reinterpret_cast<Agg*>(sc + 256 + align256(tl * 4)),
+                reinterpret_cast<Agg*>(sc + 256 + align256(tl * 4) + align256(tl * sizeof(Agg))), unsigned(tl)};
+  const uint64_t b = B / new_dp, full = idx.n / B;
+  using ull = unsigned long long;
+  j.p = Params{reinterpret_cast<const ull*>(idx.perm), reinterpret_cast<const ull*>(idx.samples), idx.file_class, idx.n, B,
+               at_step, b, rank, j.count, full > at_step ? (full - at_step) * b : 0, full};
+  j.o = Outs{reinterpret_cast<ull*>(out.pos), reinterpret_cast<ull*>(out.ent), reinterpret_cast<ull*>(out.boff),
+             out.queue[0], out.queue[1], out.queue[2], reinterpret_cast<ull*>(out.qcount)};
+  j.cls = reinterpret_cast<unsigned char*>(sc + 256 + align256(tl * 4) + 2 * align256(tl * sizeof(Agg)));
+  j.blk = reinterpret_cast<Agg*>(j.cls + align256(j.count));
+  return j;
+}
+
+// split2's gather pass (the dominant kernel) for one rank
+void k5_gather(const K5Job& j, const K5Mode& mode, bool pad, cudaStream_t st) {
+  K5Job k = j;  // the kernels take their arguments by value
+  const unsigned g = unsigned(k.tiles);
+  const int ld = pad ? k5_load() : 0;
+  if (mode.minb == 8) {
+    if (ld == 0) repart_gather2_kernel<8, 0><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else repart_gather2_kernel<8, 1><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+  } else if (mode.minb == 6) {
+    if (ld == 0) repart_gather2_kernel<6, 0><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else if (ld == 1) repart_gather2_kernel<6, 1><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else if (ld == 2) repart_gather2_kernel<6, 2><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else repart_gather2_kernel<6, 3><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+  } else {
+    if (ld == 0) repart_gather2_kernel<5, 0><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else if (ld == 1) repart_gather2_kernel<5, 1><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else if (ld == 2) repart_gather2_kernel<5, 2><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+    else repart_gather2_kernel<5, 3><<<g, kThreads, 0, st>>>(k.p, k.o, k.s, k.cls);
+  }
+}
+
+// split2's tile scan + finalize for one rank (after its gather pass on the same or another stream)
+void k5_finish(const K5Job& j, cudaStream_t st) {
+  K5Job k = j;
+  repart_tile_scan_kernel<<<unsigned(k.sblocks), 1024, 0, st>>>(k.s, k.blk, k.blk + k.sblocks, k.o);
+  repart_finalize2_kernel<<<unsigned(k.tiles), kThreads, 0, st>>>(k.p, k.o, k.s.inc, k.cls);
+}
+
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch) {
   TraceRange trace_("repartition_device");
-  const uint64_t count = repartition_count(idx.n, B, at_step, new_dp, rank);
-  if (count >= (1ull << 32)) raise(Errc::InvalidArgument, "partition above 2^32 samples (u32 queues)");
   const bool pad = entry_padded(idx);
   const K5Mode mode = k5_mode();
-  const uint64_t tile = mode.lookback ? kTile : kGTile;
-  const uint64_t tiles = (count + tile - 1) / tile;
+  const K5Job j = k5_job(idx, B, at_step, new_dp, rank, out, scratch, mode.lookback ? kTile : kGTile);
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
@@ -906,46 +965,18 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   ck(cudaEventCreate(&e0), "event");
   ck(cudaEventCreate(&e1), "event");
   ck(cudaEventCreate(&em), "event");
-  char* sc = static_cast<char*>(scratch);
-  Scratch s{reinterpret_cast<unsigned*>(sc), reinterpret_cast<unsigned*>(sc + 256),
-            reinterpret_cast<Agg*>(sc + 256 + align256(tiles * 4)),
-            reinterpret_cast<Agg*>(sc + 256 + align256(tiles * 4) + align256(tiles * sizeof(Agg))), unsigned(tiles)};
-  const uint64_t b = B / new_dp, full = idx.n / B;
-  using ull = unsigned long long;
-  Params p{reinterpret_cast<const ull*>(idx.perm), reinterpret_cast<const ull*>(idx.samples), idx.file_class, idx.n, B,
-           at_step, b, rank, count, full > at_step ? (full - at_step) * b : 0, full};
-  Outs o{reinterpret_cast<ull*>(out.pos), reinterpret_cast<ull*>(out.ent), reinterpret_cast<ull*>(out.boff),
-         out.queue[0], out.queue[1], out.queue[2], reinterpret_cast<ull*>(out.qcount)};
   if (mode.lookback && pad) raise(Errc::InvalidArgument, "RESHARD_K5=lookback reads the packed index only");
-  if (mode.lookback) ck(cudaMemsetAsync(scratch, 0, 256 + align256(tiles * 4), st), "clear scratch");
+  if (mode.lookback) ck(cudaMemsetAsync(scratch, 0, 256 + align256(j.tiles * 4), st), "clear scratch");
   ck(cudaEventRecord(e0, st), "event");
-  if (tiles && !mode.lookback) {
-    auto* cls = reinterpret_cast<unsigned char*>(sc + 256 + align256(tiles * 4) + 2 * align256(tiles * sizeof(Agg)));
-    const unsigned g = unsigned(tiles);
-    const int ld = pad ? k5_load() : 0;
-    if (mode.minb == 8) {
-      if (ld == 0) repart_gather2_kernel<8, 0><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else repart_gather2_kernel<8, 1><<<g, kThreads, 0, st>>>(p, o, s, cls);
-    } else if (mode.minb == 6) {
-      if (ld == 0) repart_gather2_kernel<6, 0><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else if (ld == 1) repart_gather2_kernel<6, 1><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else if (ld == 2) repart_gather2_kernel<6, 2><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else repart_gather2_kernel<6, 3><<<g, kThreads, 0, st>>>(p, o, s, cls);
-    } else {
-      if (ld == 0) repart_gather2_kernel<5, 0><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else if (ld == 1) repart_gather2_kernel<5, 1><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else if (ld == 2) repart_gather2_kernel<5, 2><<<g, kThreads, 0, st>>>(p, o, s, cls);
-      else repart_gather2_kernel<5, 3><<<g, kThreads, 0, st>>>(p, o, s, cls);
-    }
+  if (j.tiles && !mode.lookback) {
+    k5_gather(j, mode, pad, st);
     ck(cudaEventRecord(em, st), "event");
-    const uint64_t sblocks = (tiles + 1023) / 1024;
-    Agg* blk = reinterpret_cast<Agg*>(cls + align256(count));
-    repart_tile_scan_kernel<<<unsigned(sblocks), 1024, 0, st>>>(s, blk, blk + sblocks, o);
-    repart_finalize2_kernel<<<g, kThreads, 0, st>>>(p, o, s.inc, cls);
+    k5_finish(j, st);
     ck(cudaGetLastError(), "repartition launch");
-  } else if (tiles) {
-    if (mode.minb == 4) repartition_kernel<4><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
-    else repartition_kernel<3><<<unsigned(tiles), kThreads, 0, st>>>(p, o, s);
+  } else if (j.tiles) {
+    K5Job k = j;
+    if (mode.minb == 4) repartition_kernel<4><<<unsigned(k.tiles), kThreads, 0, st>>>(k.p, k.o, k.s);
+    else repartition_kernel<3><<<unsigned(k.tiles), kThreads, 0, st>>>(k.p, k.o, k.s);
     ck(cudaGetLastError(), "repartition launch");
   } else {
     ck(cudaMemsetAsync(out.qcount, 0, 3 * sizeof(uint64_t), st), "qcount");
@@ -954,14 +985,92 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   ck(cudaEventSynchronize(e1), "sync");
   Timing t;
   ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
-  if (tiles && !mode.lookback) ck(cudaEventElapsedTime(&t.main_ms, e0, em), "elapsed");
+  if (j.tiles && !mode.lookback) ck(cudaEventElapsedTime(&t.main_ms, e0, em), "elapsed");
   else t.main_ms = t.ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(em);
-  t.tiles = tiles;
-  t.bytes = count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
-  t.launches = tiles ? (mode.lookback ? 1 : 3) : 0;
+  t.tiles = j.tiles;
+  t.bytes = j.count * (8 + 24 + 8 + 24 + 8 + 4);  // algorithmic: perm+entry in, pos+entry+boff+queue out
+  t.launches = j.tiles ? (mode.lookback ? 1 : 3) : 0;
+  return t;
+}
+
+Timing repartition_batch_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, const RepartJob* jobs,
+                                size_t n, std::vector<Timing>* per_job) {
+  TraceRange trace_("repartition_batch_device");
+  const K5Mode mode = k5_mode();
+  if (per_job) per_job->assign(n, Timing{});
+  if (mode.lookback) {  // the single-pass variant: one rank after another
+    Timing t;
+    for (size_t i = 0; i < n; ++i) {
+      DatasetIndexView v = idx;
+      v.file_class = jobs[i].file_class;
+      Timing r = repartition_device(ctx, gpu, v, B, jobs[i].at_step, jobs[i].new_dp, jobs[i].rank, jobs[i].out, jobs[i].scratch);
+      if (per_job) (*per_job)[i] = r;
+      t.ms += r.ms, t.main_ms += r.main_ms, t.tiles += r.tiles, t.bytes += r.bytes, t.launches += r.launches;
+    }
+    return t;
+  }
+  const bool pad = entry_padded(idx);
+  std::vector<K5Job> kj;
+  kj.reserve(n);
+  for (size_t i = 0; i < n; ++i) {
+    DatasetIndexView v = idx;
+    v.file_class = jobs[i].file_class;
+    kj.push_back(k5_job(v, B, jobs[i].at_step, jobs[i].new_dp, jobs[i].rank, jobs[i].out, jobs[i].scratch, kGTile));
+  }
+  ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
+  L2FetchScope l2fetch;
+  auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  // sg: the gather passes, back to back, at the highest stream priority; sf: the ranks' tile
+  // scans + finalizes at the lowest, so their blocks fill the gather passes' tails instead of
+  // taking SMs from them (RESHARD_K5_PRIO=0: both at the default priority, A/B)
+  int least = 0, greatest = 0;
+  const char* pv = std::getenv("RESHARD_K5_PRIO");
+  if (!(pv && std::string(pv) == "0")) ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  cudaStream_t sg, sf;
+  ck(cudaStreamCreateWithPriority(&sg, cudaStreamNonBlocking, greatest), "stream");
+  ck(cudaStreamCreateWithPriority(&sf, cudaStreamNonBlocking, least), "stream");
+  std::vector<cudaEvent_t> ev(2 * n + 4);
+  for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+  cudaEvent_t e0 = ev[2 * n], e1 = ev[2 * n + 1], ef = ev[2 * n + 2], eg = ev[2 * n + 3];
+  ck(cudaEventRecord(e0, st), "event");
+  ck(cudaStreamWaitEvent(sg, e0, 0), "wait");
+  ck(cudaStreamWaitEvent(sf, e0, 0), "wait");
+  for (size_t i = 0; i < n; ++i) {
+    ck(cudaEventRecord(ev[2 * i], sg), "event");
+    if (kj[i].tiles) {
+      k5_gather(kj[i], mode, pad, sg);
+      ck(cudaEventRecord(ev[2 * i + 1], sg), "event");
+      ck(cudaStreamWaitEvent(sf, ev[2 * i + 1], 0), "wait gather");
+      k5_finish(kj[i], sf);
+    } else {
+      ck(cudaMemsetAsync(jobs[i].out.qcount, 0, 3 * sizeof(uint64_t), sg), "qcount");
+      ck(cudaEventRecord(ev[2 * i + 1], sg), "event");
+    }
+    ck(cudaGetLastError(), "repartition launch");
+  }
+  ck(cudaEventRecord(ef, sf), "event");
+  ck(cudaEventRecord(eg, sg), "event");
+  ck(cudaStreamWaitEvent(st, ef, 0), "join");
+  ck(cudaStreamWaitEvent(st, eg, 0), "join");
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  Timing t;
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  for (size_t i = 0; i < n; ++i) {
+    Timing r;
+    ck(cudaEventElapsedTime(&r.main_ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
+    r.ms = r.main_ms;  // the scan + finalize overlap the next gather pass: not attributable
+    r.tiles = kj[i].tiles, r.launches = kj[i].tiles ? 3 : 0;
+    r.bytes = kj[i].count * (8 + 24 + 8 + 24 + 8 + 4);
+    t.main_ms += r.main_ms, t.tiles += r.tiles, t.bytes += r.bytes, t.launches += r.launches;
+    if (per_job) (*per_job)[i] = r;
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(sg);
+  cudaStreamDestroy(sf);
   return t;
 }
 

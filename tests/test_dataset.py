@@ -147,6 +147,53 @@ def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, eb, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("eb", [24, 32])
+def test_k5_batch_matches_oracle(rs, orc, ctx, eb):
+    """rs_repartition_batch (a GPU hosting several new DP ranks: gather passes back to back,
+    each rank's scan + finalize on a second stream beside the next gather) against the oracle:
+    every rank of two DP events over one index, incl. empty ranks (at_step past the last full
+    batch) and ragged partitions, each with its own locator classes."""
+    rng = random.Random(77)
+    for n, nf, B, events in [(50_000, 13, 64, [(100, 4), (300, 8)]), (12_345, 5, 40, [(7, 8), (0, 2), (308, 4)]),
+                             (300_017, 29, 128, [(500, 4), (1000, 8), (2000, 2)])]:
+        samples = corpus(n, nf, rng)
+        perm = rs.shuffle_epoch(n, n, 3)
+        d_perm, d_samp = ctx.malloc(0, 8 * n), ctx.malloc(0, 24 * n)
+        ctx.htod(0, d_perm, perm.ctypes.data, 8 * n)
+        ctx.htod(0, d_samp, samples.ctypes.data, 24 * n)
+        d_idx = d_samp
+        if eb == 32:
+            d_idx = ctx.malloc(0, 32 * n)
+            rs.dataset_index_pad(ctx, 0, d_samp, d_idx, n)
+        jobs, fcs, held = [], [], []
+        for at, dp in events:
+            for d in range(dp):
+                fc = classes(nf, dp, d)
+                d_fc = ctx.malloc(0, nf)
+                ctx.htod(0, d_fc, fc.ctypes.data, nf)
+                part = rs.Partition(ctx, 0, rs.repartition_count(n, B, at, dp, d))
+                jobs.append((at, dp, d, d_fc, part))
+                fcs.append(fc)
+        t = rs.repartition_batch(ctx, 0, d_perm, d_idx, n, B, jobs, entry_bytes=eb)
+        assert t["launches"] == 3 * sum(1 for j in jobs if j[4].count)
+        assert len(t["per_job"]) == len(jobs) and t["ms"] > 0
+        for (at, dp, d, d_fc, part), fc in zip(jobs, fcs):
+            got = part.fetch()
+            want = orc.dataset_gather(n, B, at, dp, d, perm, samples, fc, n_threads=3)
+            assert np.array_equal(got["pos"], want["pos"])
+            assert np.array_equal(got["ent"], want["ent"])
+            assert np.array_equal(got["boff"], want["boff"])
+            assert got["qcount"] == want["qcount"]
+            assert np.array_equal(got["qidx"], want["qidx"])
+            part.free()
+            ctx.free(0, d_fc)
+        ctx.free(0, d_perm)
+        ctx.free(0, d_samp)
+        if eb == 32:
+            ctx.free(0, d_idx)
+
+
+@pytest.mark.gpu
 def test_index_pad_layout_and_errors(rs, ctx, monkeypatch):
     """rs_dataset_index_pad writes {file, offset, length, 0} per record; bad entry_bytes and
     the look-back variant on a padded index fail with InvalidArgument."""
