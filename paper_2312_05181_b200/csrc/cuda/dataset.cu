@@ -996,6 +996,18 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   return t;
 }
 
+// Streams and events of one batch, released on every exit path (a failed launch raises).
+struct BatchResources {
+  cudaStream_t sg = nullptr, sf = nullptr;
+  std::vector<cudaEvent_t> ev;
+  ~BatchResources() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (sg) cudaStreamDestroy(sg);
+    if (sf) cudaStreamDestroy(sf);
+  }
+};
+
 Timing repartition_batch_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, const RepartJob* jobs,
                                 size_t n, std::vector<Timing>* per_job) {
   TraceRange trace_("repartition_batch_device");
@@ -1029,10 +1041,12 @@ Timing repartition_batch_device(Context& ctx, int gpu, const DatasetIndexView& i
   int least = 0, greatest = 0;
   const char* pv = std::getenv("RESHARD_K5_PRIO");
   if (!(pv && std::string(pv) == "0")) ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
-  cudaStream_t sg, sf;
-  ck(cudaStreamCreateWithPriority(&sg, cudaStreamNonBlocking, greatest), "stream");
-  ck(cudaStreamCreateWithPriority(&sf, cudaStreamNonBlocking, least), "stream");
-  std::vector<cudaEvent_t> ev(2 * n + 4);
+  BatchResources res;
+  ck(cudaStreamCreateWithPriority(&res.sg, cudaStreamNonBlocking, greatest), "stream");
+  ck(cudaStreamCreateWithPriority(&res.sf, cudaStreamNonBlocking, least), "stream");
+  cudaStream_t sg = res.sg, sf = res.sf;
+  res.ev.assign(2 * n + 4, nullptr);
+  std::vector<cudaEvent_t>& ev = res.ev;
   for (auto& e : ev) ck(cudaEventCreate(&e), "event");
   cudaEvent_t e0 = ev[2 * n], e1 = ev[2 * n + 1], ef = ev[2 * n + 2], eg = ev[2 * n + 3];
   ck(cudaEventRecord(e0, st), "event");
@@ -1068,9 +1082,6 @@ Timing repartition_batch_device(Context& ctx, int gpu, const DatasetIndexView& i
     t.main_ms += r.main_ms, t.tiles += r.tiles, t.bytes += r.bytes, t.launches += r.launches;
     if (per_job) (*per_job)[i] = r;
   }
-  for (auto e : ev) cudaEventDestroy(e);
-  cudaStreamDestroy(sg);
-  cudaStreamDestroy(sf);
   return t;
 }
 
