@@ -125,9 +125,15 @@ def run_dataset(args, rs, dist=None):
             ctx.htod(rank, p_fc, fc.ctypes.data, spec["files"])
             jobs.append((at, dp, d, p_fc, rs.Partition(ctx, rank, rs.repartition_count(n, spec["B"], at, dp, d))))
 
-    # this GPU's ranks in one batch (gather passes back to back, each rank's scan + finalize
-    # beside the next gather pass); RESHARD_K5_BATCH=0: one rs_repartition call per rank
+    # this GPU's ranks in one batch: one launch per pass for all of them (default), or with
+    # RESHARD_K5_FUSE=0 the gather passes back to back and each rank's scan + finalize on a
+    # second stream; RESHARD_K5_BATCH=0: one rs_repartition call per rank
     batched = os.environ.get("RESHARD_K5_BATCH", "1") != "0"
+    fused = batched and os.environ.get("RESHARD_K5_FUSE", "1") != "0"
+    k5_schedule = ("rs_repartition_batch, fused: every rank of this GPU in one launch per pass (gather, tile scan, "
+                   "finalize)" if fused else
+                   "rs_repartition_batch: the ranks' gather passes back to back, each rank's scan + finalize on a "
+                   "low-priority second stream" if batched else "rs_repartition per rank, one after another")
 
     def step():
         if batched:
@@ -205,7 +211,7 @@ def run_dataset(args, rs, dist=None):
     gms = g_sum / world  # mean over GPUs of the gather-pass time per step
     galg = done * per_sample
     achieved = b_sum / (g_sum * 1e-3) / 1e9  # the dominant kernel (gather pass) over its own event time
-    n_gather = sum(dp for _, dp in spec["events"])
+    n_gather = max(1, launches // 3)  # gather launches per step: one per rank, or one per batch (fused)
     dram_ps = k5_dram_bytes_per_sample()
     traffic = round(dram_ps * done / n_gather) if dram_ps and split2 else None
     line = {
@@ -214,9 +220,7 @@ def run_dataset(args, rs, dist=None):
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (100M-sample index, 1000 files)",
         "config": workload_config(args.workload, args.gpus),
         "index_layout": "padded 32-byte records" if eb == 32 else "packed 24-byte records",
-        "k5_schedule": ("rs_repartition_batch: the GPU's ranks' gather passes back to back, each rank's scan + "
-                        "finalize on a second stream beside the next gather pass") if batched else
-                       "rs_repartition per rank, one after another",
+        "k5_schedule": k5_schedule,
         "index_pad_ms_once": None if pad_ms is None else round(pad_ms, 3),
         "samples_per_step": done, "gsamples_per_s": round(done / (ms * 1e-3) / 1e9, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -225,15 +229,17 @@ def run_dataset(args, rs, dist=None):
                      "dram_frac": round(dram_ps * (b_sum / per_sample) / (g_sum * 1e-3) / 1e9 / peak, 4) if dram_ps else None,
                      "traffic_note": "ncu dram read+write of the gather pass (profiles/r2_03/k5_sectors.json) per sample x "
                                      "samples per launch: a random 32-byte record costs a whole 128-byte DRAM line",
-                     "kernel": "repart_gather2_kernel" if split2 else "repartition_kernel",
+                     "kernel": ("repart_gather2_multi_kernel" if fused else "repart_gather2_kernel") if split2
+                     else "repartition_kernel",
                      "algorithmic_bytes_per_launch": galg // max(n_gather, 1),
                      "kernel_ms_per_step": round(gms, 4),
                      "step_achieved_gbs": round(alg / (ms * 1e-3) / 1e9, 1),
                      "gather_write_floor_ms": round(floor_ms, 4),
                      "kernel_frac_of_floor": round(floor_ms / gms, 4) if world == 1 else None,
                      "step_frac_of_floor": round(floor_ms / ms, 4),
-                     "floor_note": "gather_write_probe_kernel: the same perm + entry gathers and the 44 output "
-                                   "bytes per sample, coalesced, no scan; random 24-B gathers cost whole DRAM "
+                     "floor_note": "gather_write_probe_kernel, one launch per rank: the same perm + entry gathers "
+                                   "and the 44 output bytes per sample, coalesced, no scan (its per-rank launch tails "
+                                   "are part of it, the fused batch has none); random 24-B gathers cost whole DRAM "
                                    "lines, so the streaming-HBM frac is not reachable"},
         "gpu_launches": launches * args.steps, "clocks": clocks.summary(), "spot_check": {"pos": pos_ok, "ent": ent_ok},
         "e2e": e2e,

@@ -387,13 +387,15 @@ int rs_repartition_scratch_bytes(uint64_t count, uint64_t* bytes);
  * locate_sample loops. */
 int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64_t global_batch, uint64_t at_step,
                    uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
-/* Several ranks' K5 on one GPU (a GPU hosting several new DP ranks): the gather passes one
- * after another on the GPU's stream, each rank's tile scan + finalize on a second stream once
- * its gather pass is done, so they overlap the next rank's gather pass.  idx->file_class is
- * ignored: each job names its own (locator classes differ per rank).  total->ms: first launch
- * to the last finalize (events); total->main_ms: the sum of the gather passes; per_job
- * (nullable, n entries): each rank's gather-pass time in ms and main_ms, tiles, launches,
- * algorithmic bytes.  Same outputs as n rs_repartition calls. */
+/* Several ranks' K5 on one GPU (a GPU hosting several new DP ranks).  Default: every rank in
+ * ONE launch per pass (gather, tile scan, finalize; a block finds its rank from a rank table),
+ * so there is no launch tail between ranks.  RESHARD_K5_FUSE=0: the gather passes back to back
+ * on a high-priority stream, each rank's tile scan + finalize on a low-priority second stream.
+ * idx->file_class is ignored: each job names its own (locator classes differ per rank).
+ * total->ms: batch start to the last finalize (events); total->main_ms: the gather pass(es);
+ * per_job (nullable, n entries): tiles and algorithmic bytes, and with RESHARD_K5_FUSE=0 each
+ * rank's gather-pass time in ms / main_ms (0 when fused: one launch serves every rank).  Same
+ * outputs as n rs_repartition calls. */
 typedef struct rs_repartition_job {
   uint64_t at_step, new_dp, rank;
   const uint8_t* file_class;     /* device, per file: 0 local, 1 peer, 2 remote for this rank */

@@ -797,10 +797,10 @@ class Partition:
 
 def repartition_batch(ctx: Context, gpu: int, perm_ptr: int, samples_ptr: int, n: int, global_batch: int,
                       jobs: Sequence[tuple[int, int, int, int, "Partition"]], entry_bytes: int = 24) -> dict:
-    """K5 for several ranks on one GPU: jobs = [(at_step, new_dp, rank, class_ptr, partition)].
-    The gather passes run back to back, each rank's scan + finalize beside the next gather pass
-    (rs_repartition_batch).  ms: whole batch; gather_ms: sum of the gather passes; per_job:
-    each rank's gather-pass ms."""
+    """K5 for several ranks on one GPU: jobs = [(at_step, new_dp, rank, class_ptr, partition)]
+    (rs_repartition_batch: one launch per pass for every rank; RESHARD_K5_FUSE=0 the two-stream
+    schedule).  ms: whole batch; gather_ms: the gather pass(es); per_job: each rank's
+    gather-pass ms when unfused (0 when fused)."""
     idx = _capi.rs_dataset_index(perm_ptr, samples_ptr, None, n, entry_bytes)
     arr = (_capi.rs_repartition_job * max(len(jobs), 1))()
     for i, (at, dp, d, cls, part) in enumerate(jobs):

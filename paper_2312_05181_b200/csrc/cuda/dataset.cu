@@ -381,12 +381,14 @@ constexpr int kGItems = 4, kGTile = kThreads * kGItems, kGWarpItems = 32 * kGIte
 constexpr int kClsBits = 21;  // per-class counts packed into one u64 (a tile has <= 1024 items)
 constexpr unsigned long long kClsMask = (1ull << kClsBits) - 1;
 
-template <int MINB, int LD>
-__global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p, Outs o, Scratch sc,
-                                                                         unsigned char* cls_out) {
+// The gather pass of tile `bid` of one rank (the single-rank kernel passes blockIdx.x; the
+// multi-rank kernel the block's index within its rank's tiles).
+template <int LD>
+__device__ __forceinline__ void gather2_tile(const Params& p, const Outs& o, const Scratch& sc, unsigned char* cls_out,
+                                             unsigned bid) {
   __shared__ unsigned long long warp_len[kWarps], warp_cnt[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * kGTile + warp * kGWarpItems + lane;
+  const unsigned long long k0 = (unsigned long long)bid * kGTile + warp * kGWarpItems + lane;
   unsigned long long idx[kGItems];
 #pragma unroll
   for (int j = 0; j < kGItems; ++j) {
@@ -424,19 +426,58 @@ __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p
     unsigned long long L = 0, C = 0;
 #pragma unroll
     for (int q = 0; q < kWarps; ++q) L += warp_len[q], C += warp_cnt[q];
-    sc.agg[blockIdx.x] = Agg{L, C & kClsMask, (C >> kClsBits) & kClsMask, C >> (2 * kClsBits)};
+    sc.agg[bid] = Agg{L, C & kClsMask, (C >> kClsBits) & kClsMask, C >> (2 * kClsBits)};
   }
-  if (blockIdx.x == 0) {  // the tile scan's ticket counter and look-back flags, consumed after this launch
+  if (bid == 0) {  // the tile scan's ticket counter and look-back flags, consumed after this launch
     if (threadIdx.x == 0) *sc.counter = 0u;
     for (unsigned i = threadIdx.x; i < (sc.ntiles + 1023) / 1024; i += kThreads) sc.flags[i] = 0u;
   }
+}
+
+template <int MINB, int LD>
+__global__ void __launch_bounds__(kThreads, MINB) repart_gather2_kernel(Params p, Outs o, Scratch sc,
+                                                                         unsigned char* cls_out) {
+  gather2_tile<LD>(p, o, sc, cls_out, blockIdx.x);
+}
+
+// One rank of a multi-rank launch (several new DP ranks on one GPU, one launch per pass):
+// its parameters and where its blocks start in the gather / finalize grid and the scan grid.
+struct RankK5 {
+  Params p;
+  Outs o;
+  Scratch s;
+  unsigned char* cls;
+  Agg* blk;
+  unsigned tile0, sblock0;
+};
+// The rank a block of a multi-rank launch belongs to: the last rank whose first block is at or
+// below it (ranks in launch order; empty ranks own no block).
+template <bool SCAN>
+__device__ __forceinline__ int rank_of_block(const RankK5* __restrict__ ranks, int nr, unsigned b) {
+  __shared__ int r_sh;
+  if (threadIdx.x == 0) {
+    int r = 0;
+    for (int i = 1; i < nr; ++i)
+      if ((SCAN ? ranks[i].sblock0 : ranks[i].tile0) <= b) r = i;
+    r_sh = r;
+  }
+  __syncthreads();
+  return r_sh;
+}
+
+template <int MINB, int LD>
+__global__ void __launch_bounds__(kThreads, MINB) repart_gather2_multi_kernel(const RankK5* __restrict__ ranks, int nr) {
+  const int r = rank_of_block<false>(ranks, nr, blockIdx.x);
+  const RankK5& k = ranks[r];
+  gather2_tile<LD>(k.p, k.o, k.s, k.cls, blockIdx.x - k.tile0);
 }
 
 // Exclusive scan of the tile aggregates: one 1024-thread CTA per 1024 tiles (coalesced loads,
 // block scan in registers and shared memory), chained by a decoupled look-back over the few
 // block aggregates (the flags were cleared by the gather pass).  Writes prefix[t] (s.inc)
 // and the queue totals.
-__global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg* blk_agg, Agg* blk_inc, Outs o) {
+__device__ __forceinline__ void tile_scan_block(const Scratch& sc, Agg* blk_agg, Agg* blk_inc, const Outs& o,
+                                                unsigned nblocks) {
   __shared__ Agg warp_tot[32];
   __shared__ Agg blk_prefix;
   __shared__ unsigned ticket;
@@ -462,11 +503,11 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
     total = total + warp_tot[q];
   }
   if (warp == 0) {
-    const Scratch bs{nullptr, sc.flags, blk_agg, blk_inc, gridDim.x};
+    const Scratch bs{nullptr, sc.flags, blk_agg, blk_inc, nblocks};
     const Agg prefix = decoupled_lookback(b, total, bs, lane);
     if (lane == 0) {
       blk_prefix = prefix;
-      if (b == gridDim.x - 1) {
+      if (b == nblocks - 1) {
         const Agg all = prefix + total;
         o.qcount[0] = all.c0, o.qcount[1] = all.c1, o.qcount[2] = all.c2;
       }
@@ -477,17 +518,30 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
     sc.inc[t] = blk_prefix + base + Agg{inc.len - mine.len, inc.c0 - mine.c0, inc.c1 - mine.c1, inc.c2 - mine.c2};
 }
 
+__global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg* blk_agg, Agg* blk_inc, Outs o) {
+  tile_scan_block(sc, blk_agg, blk_inc, o, gridDim.x);
+}
+
+// Every rank's tile scan in one launch: a block serves the rank its index falls in and takes a
+// ticket among that rank's blocks, so it only ever waits on blocks of its rank that already run.
+__global__ void __launch_bounds__(1024) repart_tile_scan_multi_kernel(const RankK5* __restrict__ ranks, int nr) {
+  const int r = rank_of_block<true>(ranks, nr, blockIdx.x);
+  const RankK5& k = ranks[r];
+  const unsigned nb = (k.s.ntiles + 1023) / 1024;
+  tile_scan_block(k.s, k.blk, k.blk + nb, k.o, nb);
+}
+
 // Finalize: thread t of tile T owns the 4 consecutive samples T*1024 + 4t .. 4t+3 (16-byte
 // vector loads / stores of the parked lengths, one 4-byte load of the classes), so the scan
 // is a sequential sum in registers plus ONE warp scan of (length total, packed class counts)
 // per thread instead of one per item (r21 ncu: the warp-striped version was issue-bound,
 // 61 % SM throughput, 107 us per launch).
 constexpr int kCntBits = 10;  // per-class counts of one warp (<= 128) packed into a u32
-__global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
-                                                                     const unsigned char* cls_in) {
+__device__ __forceinline__ void finalize2_tile(const Params& p, const Outs& o, const Agg* prefix, const unsigned char* cls_in,
+                                               unsigned bid) {
   __shared__ Agg warp_tot[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * kGTile + (unsigned long long)threadIdx.x * kGItems;
+  const unsigned long long k0 = (unsigned long long)bid * kGTile + (unsigned long long)threadIdx.x * kGItems;
   unsigned long long len[kGItems];
   unsigned cls4;  // 4 class bytes, item j in byte j
   const bool full = k0 + kGItems <= p.count && (reinterpret_cast<uintptr_t>(o.boff) & 15) == 0;
@@ -523,7 +577,7 @@ __global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Ou
   constexpr unsigned m = (1u << kCntBits) - 1u;
   if (lane == 31) warp_tot[warp] = Agg{il, ic & m, (ic >> kCntBits) & m, ic >> (2 * kCntBits)};
   __syncthreads();
-  Agg run = prefix[blockIdx.x];
+  Agg run = prefix[bid];
 #pragma unroll
   for (int q = 0; q < kWarps; ++q)
     if (q < warp) run = run + warp_tot[q];
@@ -548,6 +602,17 @@ __global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Ou
     for (int j = 0; j < kGItems; ++j)
       if (k0 + j < p.count) o.boff[k0 + j] = out[j];
   }
+}
+
+__global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
+                                                                     const unsigned char* cls_in) {
+  finalize2_tile(p, o, prefix, cls_in, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kThreads) repart_finalize2_multi_kernel(const RankK5* __restrict__ ranks, int nr) {
+  const int r = rank_of_block<false>(ranks, nr, blockIdx.x);
+  const RankK5& k = ranks[r];
+  finalize2_tile(k.p, k.o, k.s.inc, k.cls, blockIdx.x - k.tile0);
 }
 
 void ck(cudaError_t e, const char* what) {
@@ -996,6 +1061,66 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
   return t;
 }
 
+// Every rank of the batch in ONE launch per pass (gather, tile scan, finalize): no launch tail
+// between ranks and one full-GPU finalize over all of them.  The rank table goes to the device
+// on the stream (stream-ordered pool memory, freed on the stream after the last pass).
+Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const RepartJob* jobs, const K5Mode& mode,
+                         bool pad, std::vector<Timing>* per_job) {
+  std::vector<RankK5> rk;
+  unsigned tiles = 0, sblocks = 0;
+  for (size_t i = 0; i < kj.size(); ++i) {
+    if (!kj[i].tiles) continue;
+    if (tiles + kj[i].tiles >= (1ull << 31)) raise(Errc::InvalidArgument, "batch above 2^31 tiles");
+    rk.push_back(RankK5{kj[i].p, kj[i].o, kj[i].s, kj[i].cls, kj[i].blk, tiles, sblocks});
+    tiles += unsigned(kj[i].tiles), sblocks += unsigned(kj[i].sblocks);
+  }
+  cudaEvent_t e0, eg, em, e1;  // batch start, gather start / end, batch end
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&eg), "event");
+  ck(cudaEventCreate(&em), "event");
+  ck(cudaEventCreate(&e1), "event");
+  struct Free {
+    cudaEvent_t a, b, c, d;
+    ~Free() { cudaEventDestroy(a), cudaEventDestroy(b), cudaEventDestroy(c), cudaEventDestroy(d); }
+  } free_{e0, eg, em, e1};
+  RankK5* d = nullptr;
+  ck(cudaEventRecord(e0, st), "event");
+  for (size_t i = 0; i < kj.size(); ++i)
+    if (!kj[i].tiles) ck(cudaMemsetAsync(jobs[i].out.qcount, 0, 3 * sizeof(uint64_t), st), "qcount");
+  if (!rk.empty()) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&d), rk.size() * sizeof(RankK5), st), "rank table");
+    ck(cudaMemcpyAsync(d, rk.data(), rk.size() * sizeof(RankK5), cudaMemcpyHostToDevice, st), "rank table");
+  }
+  ck(cudaEventRecord(eg, st), "event");
+  const int nr = int(rk.size());
+  if (nr) {
+    const int ld = pad ? k5_load() : 0;
+    if (mode.minb == 5 && ld == 1) repart_gather2_multi_kernel<5, 1><<<tiles, kThreads, 0, st>>>(d, nr);
+    else if (mode.minb == 5 && ld == 0) repart_gather2_multi_kernel<5, 0><<<tiles, kThreads, 0, st>>>(d, nr);
+    else raise(Errc::InvalidArgument, "RESHARD_K5_FUSE: the default gather variant only (split2, ldg)");
+    ck(cudaEventRecord(em, st), "event");
+    repart_tile_scan_multi_kernel<<<sblocks, 1024, 0, st>>>(d, nr);
+    repart_finalize2_multi_kernel<<<tiles, kThreads, 0, st>>>(d, nr);
+    ck(cudaGetLastError(), "repartition launch");
+    ck(cudaFreeAsync(d, st), "rank table");
+  } else {
+    ck(cudaEventRecord(em, st), "event");
+  }
+  ck(cudaEventRecord(e1, st), "event");
+  ck(cudaEventSynchronize(e1), "sync");
+  Timing t;
+  ck(cudaEventElapsedTime(&t.ms, e0, e1), "elapsed");
+  ck(cudaEventElapsedTime(&t.main_ms, eg, em), "elapsed");
+  for (size_t i = 0; i < kj.size(); ++i) {
+    Timing r;  // one launch per pass for the whole batch: per-rank times are not separable (0)
+    r.tiles = kj[i].tiles, r.bytes = kj[i].count * (8 + 24 + 8 + 24 + 8 + 4);
+    t.tiles += r.tiles, t.bytes += r.bytes;
+    if (per_job) (*per_job)[i] = r;
+  }
+  t.launches = nr ? 3 : 0;
+  return t;
+}
+
 // Streams and events of one batch, released on every exit path (a failed launch raises).
 struct BatchResources {
   cudaStream_t sg = nullptr, sf = nullptr;
@@ -1035,6 +1160,8 @@ Timing repartition_batch_device(Context& ctx, int gpu, const DatasetIndexView& i
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  const char* fv = std::getenv("RESHARD_K5_FUSE");
+  if (!(fv && std::string(fv) == "0")) return repartition_fused(st, kj, jobs, mode, pad, per_job);
   // sg: the gather passes, back to back, at the highest stream priority; sf: the ranks' tile
   // scans + finalizes at the lowest, so their blocks fill the gather passes' tails instead of
   // taking SMs from them (RESHARD_K5_PRIO=0: both at the default priority, A/B)

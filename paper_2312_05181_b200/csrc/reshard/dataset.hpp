@@ -78,12 +78,13 @@ uint64_t repartition_scratch_bytes(uint64_t count);
 // the gather pass alone.
 Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, uint64_t B, uint64_t at_step,
                           uint64_t new_dp, uint64_t rank, const PartitionOut& out, void* scratch);
-// Several ranks' K5 on one GPU (a GPU hosting several new DP ranks; bench config 5 at N = 1):
-// the gather passes one after another on the GPU's stream, each rank's tile scan + finalize
-// on a second stream once its gather pass is done, so they overlap the next rank's gather.
+// Several ranks' K5 on one GPU (a GPU hosting several new DP ranks; bench config 5 at N = 1).
+// Default: all ranks in one launch per pass (multi-rank gather / tile scan / finalize kernels
+// over a device rank table).  RESHARD_K5_FUSE=0: the gather passes one after another on a
+// high-priority stream, each rank's tile scan + finalize on a low-priority second stream.
 // Per job its own file_class (locator classes differ per rank), outputs and scratch.
-// Timing.ms: first launch -> last finalize; main_ms: the sum of the gather passes; per_job
-// (optional): each rank's gather-pass time in ms / main_ms.
+// Timing.ms: batch start -> last finalize; main_ms: the gather pass(es); per_job (optional):
+// tiles / bytes, and unfused each rank's gather-pass time in ms / main_ms.
 struct RepartJob {
   uint64_t at_step, new_dp, rank;
   const uint8_t* file_class;

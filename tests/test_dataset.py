@@ -147,12 +147,14 @@ def test_k5_kernel_matches_oracle(rs, orc, ctx, mode, eb, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("eb", [24, 32])
-def test_k5_batch_matches_oracle(rs, orc, ctx, eb):
-    """rs_repartition_batch (a GPU hosting several new DP ranks: gather passes back to back,
-    each rank's scan + finalize on a second stream beside the next gather) against the oracle:
+@pytest.mark.parametrize("eb,fuse", [(24, True), (32, True), (32, False)])
+def test_k5_batch_matches_oracle(rs, orc, ctx, eb, fuse, monkeypatch):
+    """rs_repartition_batch (a GPU hosting several new DP ranks; fused: one launch per pass for
+    every rank, else gather passes back to back and each rank's scan + finalize on a second
+    stream) against the oracle:
     every rank of two DP events over one index, incl. empty ranks (at_step past the last full
     batch) and ragged partitions, each with its own locator classes."""
+    monkeypatch.setenv("RESHARD_K5_FUSE", "1" if fuse else "0")
     rng = random.Random(77)
     for n, nf, B, events in [(50_000, 13, 64, [(100, 4), (300, 8)]), (12_345, 5, 40, [(7, 8), (0, 2), (308, 4)]),
                              (300_017, 29, 128, [(500, 4), (1000, 8), (2000, 2)])]:
@@ -175,7 +177,9 @@ def test_k5_batch_matches_oracle(rs, orc, ctx, eb):
                 jobs.append((at, dp, d, d_fc, part))
                 fcs.append(fc)
         t = rs.repartition_batch(ctx, 0, d_perm, d_idx, n, B, jobs, entry_bytes=eb)
-        assert t["launches"] == 3 * sum(1 for j in jobs if j[4].count)
+        nonempty = sum(1 for j in jobs if j[4].count)
+        # fused (default): one launch per pass for the whole batch; RESHARD_K5_FUSE=0: three per rank
+        assert t["launches"] == (3 if fuse else 3 * nonempty)
         assert len(t["per_job"]) == len(jobs) and t["ms"] > 0
         for (at, dp, d, d_fc, part), fc in zip(jobs, fcs):
             got = part.fetch()
