@@ -212,7 +212,7 @@ def run_dataset(args, rs, dist=None):
     galg = done * per_sample
     achieved = b_sum / (g_sum * 1e-3) / 1e9  # the dominant kernel (gather pass) over its own event time
     n_gather = max(1, launches // 3)  # gather launches per step: one per rank, or one per batch (fused)
-    dram_ps = k5_dram_bytes_per_sample()
+    dram_ps = k5_dram_bytes_per_sample(fused)
     traffic = round(dram_ps * done / n_gather) if dram_ps and split2 else None
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
@@ -227,8 +227,9 @@ def run_dataset(args, rs, dist=None):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind, "peak_how": peak_how(),
                      "dram_bytes_per_sample": dram_ps,
                      "dram_frac": round(dram_ps * (b_sum / per_sample) / (g_sum * 1e-3) / 1e9 / peak, 4) if dram_ps else None,
-                     "traffic_note": "ncu dram read+write of the gather pass (profiles/r2_03/k5_sectors.json) per sample x "
-                                     "samples per launch: a random 32-byte record costs a whole 128-byte DRAM line",
+                     "traffic_note": "ncu dram read+write of the gather pass per sample (profiles/r2_35/k5_fused_ncu.json; "
+                                     "per-rank launches: r2_03/k5_sectors.json) x samples per launch: a random 32-byte "
+                                     "record costs a whole 128-byte DRAM line",
                      "kernel": ("repart_gather2_multi_kernel" if fused else "repart_gather2_kernel") if split2
                      else "repartition_kernel",
                      "algorithmic_bytes_per_launch": galg // max(n_gather, 1),
@@ -464,11 +465,16 @@ def copy_kernel_name(tiles_per_launch: int = 0) -> str:
             "ldg8": "copy_v16_kernel", "bulk_warp": "copy_bulk_warp_kernel", "bulk_dyn": "copy_bulk_dyn_kernel"}.get(k, k)
 
 
-def k5_dram_bytes_per_sample():
-    """DRAM read + write bytes per sample of K5's gather pass (committed ncu capture)."""
+def k5_dram_bytes_per_sample(fused: bool = True):
+    """DRAM read + write bytes per sample of K5's gather pass (committed ncu captures: the fused
+    multi-rank launch, profiles/r2_35; one rank's launch, profiles/r2_03)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r2_03", "k5_sectors.json")) as f:
-            v = json.load(f)["variants"]["ldg"]
+        if fused:
+            with open(os.path.join(ROOT, "profiles", "r2_35", "k5_fused_ncu.json")) as f:
+                v = json.load(f)
+        else:
+            with open(os.path.join(ROOT, "profiles", "r2_03", "k5_sectors.json")) as f:
+                v = json.load(f)["variants"]["ldg"]
         return round(v["dram_read_bytes_per_sample"] + v["dram_write_bytes_per_sample"], 1)
     except Exception:
         return None

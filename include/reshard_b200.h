@@ -389,7 +389,8 @@ int rs_repartition(rs_context* ctx, int gpu, const rs_dataset_index* idx, uint64
                    uint64_t new_dp, uint64_t rank, const rs_partition_out* out, void* scratch, rs_timing* timing);
 /* Several ranks' K5 on one GPU (a GPU hosting several new DP ranks).  Default: every rank in
  * ONE launch per pass (gather, tile scan, finalize; a block finds its rank from a rank table),
- * so there is no launch tail between ranks.  RESHARD_K5_FUSE=0: the gather passes back to back
+ * so there is no launch tail between ranks (the default gather variant; RESHARD_K5 /
+ * RESHARD_K5_LOAD A/B variants take the unfused schedule).  RESHARD_K5_FUSE=0: the gather passes back to back
  * on a high-priority stream, each rank's tile scan + finalize on a low-priority second stream.
  * idx->file_class is ignored: each job names its own (locator classes differ per rank).
  * total->ms: batch start to the last finalize (events); total->main_ms: the gather pass(es);

@@ -1097,7 +1097,7 @@ Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const Re
     const int ld = pad ? k5_load() : 0;
     if (mode.minb == 5 && ld == 1) repart_gather2_multi_kernel<5, 1><<<tiles, kThreads, 0, st>>>(d, nr);
     else if (mode.minb == 5 && ld == 0) repart_gather2_multi_kernel<5, 0><<<tiles, kThreads, 0, st>>>(d, nr);
-    else raise(Errc::InvalidArgument, "RESHARD_K5_FUSE: the default gather variant only (split2, ldg)");
+    else raise(Errc::InvalidArgument, "fused K5: the default gather variant only (split2, ldg)");
     ck(cudaEventRecord(em, st), "event");
     repart_tile_scan_multi_kernel<<<sblocks, 1024, 0, st>>>(d, nr);
     repart_finalize2_multi_kernel<<<tiles, kThreads, 0, st>>>(d, nr);
@@ -1160,8 +1160,12 @@ Timing repartition_batch_device(Context& ctx, int gpu, const DatasetIndexView& i
   ck(cudaSetDevice(ctx.cuda_device(gpu)), "cudaSetDevice");
   L2FetchScope l2fetch;
   auto st = static_cast<cudaStream_t>(ctx.stream(gpu));
+  // fused: the default gather variant (5 CTAs / SM, __ldg records); other RESHARD_K5 /
+  // RESHARD_K5_LOAD variants (A/B knobs) take the two-stream schedule
   const char* fv = std::getenv("RESHARD_K5_FUSE");
-  if (!(fv && std::string(fv) == "0")) return repartition_fused(st, kj, jobs, mode, pad, per_job);
+  const int ld = pad ? k5_load() : 0;
+  if (!(fv && std::string(fv) == "0") && mode.minb == 5 && ld <= 1)
+    return repartition_fused(st, kj, jobs, mode, pad, per_job);
   // sg: the gather passes, back to back, at the highest stream priority; sf: the ranks' tile
   // scans + finalizes at the lowest, so their blocks fill the gather passes' tails instead of
   // taking SMs from them (RESHARD_K5_PRIO=0: both at the default priority, A/B)
