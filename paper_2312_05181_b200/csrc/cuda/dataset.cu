@@ -448,27 +448,39 @@ struct RankK5 {
   Scratch s;
   unsigned char* cls;
   Agg* blk;
-  unsigned tile0, sblock0;
+  unsigned tile0, sblock0, fin0;  // first block in the gather grid, the scan grid, the finalize grid
 };
-// The rank a block of a multi-rank launch belongs to: the last rank whose first block is at or
-// below it (ranks in launch order; empty ranks own no block).
+// The ranks of one launch, passed BY VALUE (kernel parameters live in the constant bank: the
+// per-block rank lookup and field loads are uniform constant-cache reads, no global round trip
+// before a block's first data load).  Batches with more ranks launch in chunks.
+constexpr int kMaxRanksPerLaunch = 16;
+struct RankTable {
+  RankK5 r[kMaxRanksPerLaunch];
+  int n;
+};
+static_assert(sizeof(RankTable) <= 4000, "kernel parameter space");
+// The rank a block belongs to: the last rank whose first block is at or below it (ranks in
+// launch order, empty ranks left out); every thread computes it from uniform loads.
 template <bool SCAN>
-__device__ __forceinline__ int rank_of_block(const RankK5* __restrict__ ranks, int nr, unsigned b) {
-  __shared__ int r_sh;
-  if (threadIdx.x == 0) {
-    int r = 0;
-    for (int i = 1; i < nr; ++i)
-      if ((SCAN ? ranks[i].sblock0 : ranks[i].tile0) <= b) r = i;
-    r_sh = r;
-  }
-  __syncthreads();
-  return r_sh;
+__device__ __forceinline__ int rank_of_block(const RankTable& t, unsigned b) {
+  int r = 0;
+#pragma unroll 1
+  for (int i = 1; i < t.n; ++i)
+    if ((SCAN ? t.r[i].sblock0 : t.r[i].tile0) <= b) r = i;
+  return r;
+}
+
+__device__ __forceinline__ int rank_of_block_fin(const RankTable& t, unsigned b) {
+  int r = 0;
+#pragma unroll 1
+  for (int i = 1; i < t.n; ++i)
+    if (t.r[i].fin0 <= b) r = i;
+  return r;
 }
 
 template <int MINB, int LD>
-__global__ void __launch_bounds__(kThreads, MINB) repart_gather2_multi_kernel(const RankK5* __restrict__ ranks, int nr) {
-  const int r = rank_of_block<false>(ranks, nr, blockIdx.x);
-  const RankK5& k = ranks[r];
+__global__ void __launch_bounds__(kThreads, MINB) repart_gather2_multi_kernel(const __grid_constant__ RankTable t) {
+  const RankK5& k = t.r[rank_of_block<false>(t, blockIdx.x)];
   gather2_tile<LD>(k.p, k.o, k.s, k.cls, blockIdx.x - k.tile0);
 }
 
@@ -524,9 +536,8 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
 
 // Every rank's tile scan in one launch: a block serves the rank its index falls in and takes a
 // ticket among that rank's blocks, so it only ever waits on blocks of its rank that already run.
-__global__ void __launch_bounds__(1024) repart_tile_scan_multi_kernel(const RankK5* __restrict__ ranks, int nr) {
-  const int r = rank_of_block<true>(ranks, nr, blockIdx.x);
-  const RankK5& k = ranks[r];
+__global__ void __launch_bounds__(1024) repart_tile_scan_multi_kernel(const __grid_constant__ RankTable t) {
+  const RankK5& k = t.r[rank_of_block<true>(t, blockIdx.x)];
   const unsigned nb = (k.s.ntiles + 1023) / 1024;
   tile_scan_block(k.s, k.blk, k.blk + nb, k.o, nb);
 }
@@ -537,33 +548,44 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_multi_kernel(const Rank
 // per thread instead of one per item (r21 ncu: the warp-striped version was issue-bound,
 // 61 % SM throughput, 107 us per launch).
 constexpr int kCntBits = 10;  // per-class counts of one warp (<= 128) packed into a u32
-__device__ __forceinline__ void finalize2_tile(const Params& p, const Outs& o, const Agg* prefix, const unsigned char* cls_in,
-                                               unsigned bid) {
-  __shared__ Agg warp_tot[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned long long k0 = (unsigned long long)bid * kGTile + (unsigned long long)threadIdx.x * kGItems;
+// One thread's inputs of a finalize tile: its 4 parked lengths, their class bytes, the tile's
+// exclusive prefix.
+struct FinIn {
   unsigned long long len[kGItems];
   unsigned cls4;  // 4 class bytes, item j in byte j
-  const bool full = k0 + kGItems <= p.count && (reinterpret_cast<uintptr_t>(o.boff) & 15) == 0;
-  if (full) {
+  Agg pre;
+};
+__device__ __forceinline__ bool fin_full(const Params& p, const Outs& o, unsigned long long k0) {
+  return k0 + kGItems <= p.count && (reinterpret_cast<uintptr_t>(o.boff) & 15) == 0;
+}
+__device__ __forceinline__ void fin_load(const Params& p, const Outs& o, const Agg* prefix, const unsigned char* cls_in,
+                                         unsigned bid, FinIn& in) {
+  const unsigned long long k0 = (unsigned long long)bid * kGTile + (unsigned long long)threadIdx.x * kGItems;
+  in.pre = prefix[bid];  // issued with the data loads, not after the barrier
+  if (fin_full(p, o, k0)) {
     const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(o.boff + k0);
     const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(o.boff + k0 + 2);
-    len[0] = a.x, len[1] = a.y, len[2] = b.x, len[3] = b.y;
-    cls4 = *reinterpret_cast<const unsigned*>(cls_in + k0);
+    in.len[0] = a.x, in.len[1] = a.y, in.len[2] = b.x, in.len[3] = b.y;
+    in.cls4 = *reinterpret_cast<const unsigned*>(cls_in + k0);
   } else {
-    cls4 = 0x03030303u;
+    in.cls4 = 0x03030303u;
 #pragma unroll
     for (int j = 0; j < kGItems; ++j) {
-      len[j] = k0 + j < p.count ? o.boff[k0 + j] : 0ull;
-      if (k0 + j < p.count) cls4 = (cls4 & ~(0xffu << (8 * j))) | (unsigned(cls_in[k0 + j]) << (8 * j));
+      in.len[j] = k0 + j < p.count ? o.boff[k0 + j] : 0ull;
+      if (k0 + j < p.count) in.cls4 = (in.cls4 & ~(0xffu << (8 * j))) | (unsigned(cls_in[k0 + j]) << (8 * j));
     }
   }
+}
+// The scan of one tile and its stores; warp_tot: kWarps Aggs of shared memory (one barrier)
+__device__ __forceinline__ void fin_store(const Params& p, const Outs& o, unsigned bid, const FinIn& in, Agg* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long k0 = (unsigned long long)bid * kGTile + (unsigned long long)threadIdx.x * kGItems;
   unsigned long long tl = 0;
   unsigned tc = 0;
 #pragma unroll
   for (int j = 0; j < kGItems; ++j) {
-    const unsigned c = (cls4 >> (8 * j)) & 0xffu;
-    tl += len[j];
+    const unsigned c = (in.cls4 >> (8 * j)) & 0xffu;
+    tl += in.len[j];
     if (c < 3) tc += 1u << (kCntBits * c);
   }
   unsigned long long il = tl;
@@ -577,7 +599,7 @@ __device__ __forceinline__ void finalize2_tile(const Params& p, const Outs& o, c
   constexpr unsigned m = (1u << kCntBits) - 1u;
   if (lane == 31) warp_tot[warp] = Agg{il, ic & m, (ic >> kCntBits) & m, ic >> (2 * kCntBits)};
   __syncthreads();
-  Agg run = prefix[bid];
+  Agg run = in.pre;
 #pragma unroll
   for (int q = 0; q < kWarps; ++q)
     if (q < warp) run = run + warp_tot[q];
@@ -588,13 +610,13 @@ __device__ __forceinline__ void finalize2_tile(const Params& p, const Outs& o, c
 #pragma unroll
   for (int j = 0; j < kGItems; ++j) {
     out[j] = off;
-    off += len[j];
-    const unsigned c = (cls4 >> (8 * j)) & 0xffu;
+    off += in.len[j];
+    const unsigned c = (in.cls4 >> (8 * j)) & 0xffu;
     if (c == 0) o.q0[qi[0]++] = unsigned(k0 + j);
     else if (c == 1) o.q1[qi[1]++] = unsigned(k0 + j);
     else if (c == 2) o.q2[qi[2]++] = unsigned(k0 + j);
   }
-  if (full) {
+  if (fin_full(p, o, k0)) {
     *reinterpret_cast<ulonglong2*>(o.boff + k0) = make_ulonglong2(out[0], out[1]);
     *reinterpret_cast<ulonglong2*>(o.boff + k0 + 2) = make_ulonglong2(out[2], out[3]);
   } else {
@@ -603,16 +625,38 @@ __device__ __forceinline__ void finalize2_tile(const Params& p, const Outs& o, c
       if (k0 + j < p.count) o.boff[k0 + j] = out[j];
   }
 }
+__device__ __forceinline__ void finalize2_tile(const Params& p, const Outs& o, const Agg* prefix, const unsigned char* cls_in,
+                                               unsigned bid) {
+  __shared__ Agg warp_tot[kWarps];
+  FinIn in;
+  fin_load(p, o, prefix, cls_in, bid, in);
+  fin_store(p, o, bid, in, warp_tot);
+}
 
 __global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Outs o, const Agg* prefix,
                                                                      const unsigned char* cls_in) {
   finalize2_tile(p, o, prefix, cls_in, blockIdx.x);
 }
 
-__global__ void __launch_bounds__(kThreads) repart_finalize2_multi_kernel(const RankK5* __restrict__ ranks, int nr) {
-  const int r = rank_of_block<false>(ranks, nr, blockIdx.x);
-  const RankK5& k = ranks[r];
-  finalize2_tile(k.p, k.o, k.s.inc, k.cls, blockIdx.x - k.tile0);
+// Fused finalize: a block owns kFinTiles consecutive tiles of one rank and software-pipelines
+// them — the next tile's lengths, classes and prefix are loaded while the current one is scanned
+// and stored — so the loads of a short CTA's single tile are no longer its whole lifetime (r2_37
+// ncu of one tile per block: 50 % of DRAM peak, 48 % of warp samples on the load scoreboard).
+// warp_tot is double-buffered: one barrier per tile.
+constexpr unsigned kFinTiles = 8;  // default tiles per block (RESHARD_K5_FIN_TILES; r2_40 sweep: 1 3.59, 2 3.50, 4 3.47, 8 3.45, 16 3.45 ms per step)
+__global__ void __launch_bounds__(kThreads) repart_finalize2_multi_kernel(const __grid_constant__ RankTable t,
+                                                                           unsigned fin_tiles) {
+  __shared__ Agg warp_tot[2][kWarps];
+  const RankK5& k = t.r[rank_of_block_fin(t, blockIdx.x)];
+  const unsigned first = (blockIdx.x - k.fin0) * fin_tiles;
+  const unsigned last = min(first + fin_tiles, k.s.ntiles);
+  FinIn cur, nxt;
+  fin_load(k.p, k.o, k.s.inc, k.cls, first, cur);
+  for (unsigned b = first; b < last; ++b) {
+    if (b + 1 < last) fin_load(k.p, k.o, k.s.inc, k.cls, b + 1, nxt);
+    fin_store(k.p, k.o, b, cur, warp_tot[(b - first) & 1]);
+    cur = nxt;
+  }
 }
 
 void ck(cudaError_t e, const char* what) {
@@ -1066,13 +1110,27 @@ Timing repartition_device(Context& ctx, int gpu, const DatasetIndexView& idx, ui
 // on the stream (stream-ordered pool memory, freed on the stream after the last pass).
 Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const RepartJob* jobs, const K5Mode& mode,
                          bool pad, std::vector<Timing>* per_job) {
-  std::vector<RankK5> rk;
-  unsigned tiles = 0, sblocks = 0;
+  (void)mode;
+  // the non-empty ranks in launch chunks of <= kMaxRanksPerLaunch; block offsets per chunk
+  const char* fv = std::getenv("RESHARD_K5_FIN_TILES");
+  const unsigned fin_tiles = fv && *fv ? unsigned(std::max(1, std::atoi(fv))) : kFinTiles;
+  std::vector<RankTable> chunks;
+  std::vector<unsigned> chunk_tiles, chunk_sblocks, chunk_fin;
   for (size_t i = 0; i < kj.size(); ++i) {
     if (!kj[i].tiles) continue;
-    if (tiles + kj[i].tiles >= (1ull << 31)) raise(Errc::InvalidArgument, "batch above 2^31 tiles");
-    rk.push_back(RankK5{kj[i].p, kj[i].o, kj[i].s, kj[i].cls, kj[i].blk, tiles, sblocks});
-    tiles += unsigned(kj[i].tiles), sblocks += unsigned(kj[i].sblocks);
+    if (chunks.empty() || chunks.back().n == kMaxRanksPerLaunch) {
+      chunks.emplace_back();
+      chunks.back().n = 0;
+      chunk_tiles.push_back(0), chunk_sblocks.push_back(0), chunk_fin.push_back(0);
+    }
+    RankTable& t = chunks.back();
+    unsigned& tl = chunk_tiles.back();
+    unsigned& sb = chunk_sblocks.back();
+    unsigned& fb = chunk_fin.back();
+    if (uint64_t(tl) + kj[i].tiles >= (1ull << 31)) raise(Errc::InvalidArgument, "batch above 2^31 tiles per launch");
+    t.r[t.n++] = RankK5{kj[i].p, kj[i].o, kj[i].s, kj[i].cls, kj[i].blk, tl, sb, fb};
+    tl += unsigned(kj[i].tiles), sb += unsigned(kj[i].sblocks);
+    fb += unsigned((kj[i].tiles + fin_tiles - 1) / fin_tiles);
   }
   cudaEvent_t e0, eg, em, e1;  // batch start, gather start / end, batch end
   ck(cudaEventCreate(&e0), "event");
@@ -1083,29 +1141,22 @@ Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const Re
     cudaEvent_t a, b, c, d;
     ~Free() { cudaEventDestroy(a), cudaEventDestroy(b), cudaEventDestroy(c), cudaEventDestroy(d); }
   } free_{e0, eg, em, e1};
-  RankK5* d = nullptr;
   ck(cudaEventRecord(e0, st), "event");
   for (size_t i = 0; i < kj.size(); ++i)
     if (!kj[i].tiles) ck(cudaMemsetAsync(jobs[i].out.qcount, 0, 3 * sizeof(uint64_t), st), "qcount");
-  if (!rk.empty()) {
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&d), rk.size() * sizeof(RankK5), st), "rank table");
-    ck(cudaMemcpyAsync(d, rk.data(), rk.size() * sizeof(RankK5), cudaMemcpyHostToDevice, st), "rank table");
-  }
   ck(cudaEventRecord(eg, st), "event");
-  const int nr = int(rk.size());
-  if (nr) {
-    const int ld = pad ? k5_load() : 0;
-    if (mode.minb == 5 && ld == 1) repart_gather2_multi_kernel<5, 1><<<tiles, kThreads, 0, st>>>(d, nr);
-    else if (mode.minb == 5 && ld == 0) repart_gather2_multi_kernel<5, 0><<<tiles, kThreads, 0, st>>>(d, nr);
+  const int ld = pad ? k5_load() : 0;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    if (ld == 1) repart_gather2_multi_kernel<5, 1><<<chunk_tiles[c], kThreads, 0, st>>>(chunks[c]);
+    else if (ld == 0) repart_gather2_multi_kernel<5, 0><<<chunk_tiles[c], kThreads, 0, st>>>(chunks[c]);
     else raise(Errc::InvalidArgument, "fused K5: the default gather variant only (split2, ldg)");
-    ck(cudaEventRecord(em, st), "event");
-    repart_tile_scan_multi_kernel<<<sblocks, 1024, 0, st>>>(d, nr);
-    repart_finalize2_multi_kernel<<<tiles, kThreads, 0, st>>>(d, nr);
-    ck(cudaGetLastError(), "repartition launch");
-    ck(cudaFreeAsync(d, st), "rank table");
-  } else {
-    ck(cudaEventRecord(em, st), "event");
   }
+  ck(cudaEventRecord(em, st), "event");
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    repart_tile_scan_multi_kernel<<<chunk_sblocks[c], 1024, 0, st>>>(chunks[c]);
+    repart_finalize2_multi_kernel<<<chunk_fin[c], kThreads, 0, st>>>(chunks[c], fin_tiles);
+  }
+  ck(cudaGetLastError(), "repartition launch");
   ck(cudaEventRecord(e1, st), "event");
   ck(cudaEventSynchronize(e1), "sync");
   Timing t;
@@ -1117,7 +1168,7 @@ Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const Re
     t.tiles += r.tiles, t.bytes += r.bytes;
     if (per_job) (*per_job)[i] = r;
   }
-  t.launches = nr ? 3 : 0;
+  t.launches = 3 * chunks.size();
   return t;
 }
 
