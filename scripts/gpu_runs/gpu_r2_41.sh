@@ -21,5 +21,5 @@ run central --mode central --no-cpu-baseline
 for n in 2 4 8; do RESHARD_SAME_GPU=1 run emu_n$n --gpus $n --no-cpu-baseline; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-digests > $O/launches.out 2>&1; echo launches rc=$?
 timeout 900 ncu --kernel-name regex:"repart" --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_k5.csv python bench.py --workload dataset-100m-dp2to4to8 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/launches_k5.out 2>&1; echo launches_k5 rc=$?
-#
+
 timeout 1500 python scripts/stress_dataset.py --cases 2000 --seed 2041 > $O/stress_dataset.jsonl 2> $O/stress_dataset.err; tail -1 $O/stress_dataset.jsonl
