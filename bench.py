@@ -405,7 +405,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def pcie_probe(nbytes: int = 2 << 30, reps: int = 3) -> dict:
+def pcie_probe(nbytes: int = 2 << 30, reps: int = 6) -> dict:
     """Pinned host <-> device copy rates on this box (off the clock): the link that bounds the
     host-buffer e2e path.  H2D alone, D2H alone, and both directions at once on two streams."""
     import torch
