@@ -94,10 +94,15 @@ inline bool is_bulk(CopyKernel k) {
 struct CopyConfig {
   CopyKernel kernel = CopyKernel::BulkStrided;  // r08 same-box A/B: 3-4% faster than Bulk
   int ctas_per_sm = 1;
-  int stages = 7;               // bulk: shared-memory ring depth
-  unsigned stage_bytes = 29696; // bulk: bytes per stage (tiles are cut to fit one stage); r09 A/B
+  int stages = 6;               // bulk: shared-memory ring depth
+  // bulk: bytes per stage (tiles are cut to fit one stage).  r2_43 A/B on all four copy
+  // workloads: 6 x 32 KiB beats the earlier 7 x 29 KiB everywhere (GPT-2 small 0.470 vs 0.489 ms,
+  // 1.3B 5.40 vs 5.46, 6.7B 42.2 vs 44.3, recovery 13.6 vs 13.8): power-of-two stages hold whole
+  // 4 / 8 / 16 KiB rows, so a tile fills its stage (29 KiB left 17 % of a stage empty on 8 KiB rows)
+  unsigned stage_bytes = 32768;
   int host_chunks = 64;         // pipeline depth of the host-buffer path (run_host); r13 sweep
-  int dyn_claim = 8;            // bulk_dyn: tiles per claim (RESHARD_DYN_CLAIM); r2_18: 1 loses 15 %, 2-4 1.5 %, 8 best
+  int dyn_claim = 2;            // bulk_dyn: tiles per claim (RESHARD_DYN_CLAIM); r2_18 at 29 KiB tiles: 1 loses 15 %, 8 best;
+                                // r2_45 at 32 KiB: 2 best (1.3B 5.33 / 5.34 / 5.38 ms for 2 / 4 / 8, 6.7B 41.6 / 41.7 / 41.9)
   int dyn_min_tiles = 200000;   // bulk_strided launches of at least this many tiles run as bulk_dyn (0: never; RESHARD_DYN_MIN_TILES)
   bool ldg_dyn = false;         // K1/K2 aligned + fan-out kernels: dynamic tile claims (RESHARD_LDG_DYN)
   int dyn_tail = -1;            // bulk_dyn: tiles per CTA claimed dynamically at the end (-1: all; RESHARD_DYN_TAIL)

@@ -426,7 +426,7 @@ def test_broadcast_fan_out_push(rs, ctx, kernel, monkeypatch):
     fan-out tiles) and misaligned (LDG/STG), every destination byte equal to the source."""
     monkeypatch.setenv("RESHARD_COPY_KERNEL", kernel)
     rng = np.random.default_rng(3)
-    for nbytes, n_dst, skew in [(10 << 20, 6, 0), (1 << 20, 1, 0), (3 * 29696 + 48, 4, 0), (777_777, 3, 8), (96, 5, 0)]:
+    for nbytes, n_dst, skew in [(10 << 20, 6, 0), (1 << 20, 1, 0), (3 * 29696 + 48, 4, 0), (3 * 32768 + 48, 4, 0), (777_777, 3, 8), (96, 5, 0)]:
         src_h = rng.integers(0, 256, nbytes, dtype=np.uint8)
         src = ctx.malloc(0, nbytes + 64)
         ctx.htod(0, src + skew, src_h.ctypes.data, nbytes)
