@@ -200,6 +200,30 @@ def test_dataset_abi_argument_errors(rs):
     bad = _capi.rs_dataset_index(8, 8, 8, 100, 16)
     assert lib.rs_repartition(ctx.h, 0, C.byref(bad), 10, 0, 2, 0, C.byref(out), 8, C.byref(t)) == inv
     assert "entry_bytes" in lib.rs_last_error().decode()
+    # rs_repartition_batch: null total / index, negative count, null job list, a job without
+    # scratch or locator classes, a bad layout, then the SPEC's own errors — all before any device work
+    jobs = (_capi.rs_repartition_job * 2)()
+    for j in jobs:
+        j.at_step, j.new_dp, j.rank, j.file_class, j.out, j.scratch = 0, 2, 0, 8, out, 8
+    assert lib.rs_repartition_batch(ctx.h, 0, C.byref(idx), 10, jobs, 2, None, None) == inv
+    assert lib.rs_repartition_batch(ctx.h, 0, None, 10, jobs, 2, None, C.byref(t)) == inv
+    assert lib.rs_repartition_batch(ctx.h, 0, C.byref(idx), 10, jobs, -1, None, C.byref(t)) == inv
+    assert "negative" in lib.rs_last_error().decode()
+    assert lib.rs_repartition_batch(ctx.h, 0, C.byref(idx), 10, None, 2, None, C.byref(t)) == inv
+    jobs[1].scratch = None
+    assert lib.rs_repartition_batch(ctx.h, 0, C.byref(idx), 10, jobs, 2, None, C.byref(t)) == inv
+    jobs[1].scratch, jobs[1].file_class = 8, None
+    assert lib.rs_repartition_batch(ctx.h, 0, C.byref(idx), 10, jobs, 2, None, C.byref(t)) == inv
+    jobs[1].file_class = 8
+    assert lib.rs_repartition_batch(ctx.h, 0, C.byref(bad), 10, jobs, 2, None, C.byref(t)) == inv
+    assert "entry_bytes" in lib.rs_last_error().decode()
+    jobs[1].new_dp = 3  # B = 10 is not divisible by 3
+    rc = lib.rs_repartition_batch(ctx.h, 0, C.byref(idx), 10, jobs, 2, None, C.byref(t))
+    assert rc == 1 + rs._capi.ERRC.index("IndivisibleBatch"), lib.rs_last_error().decode()
+    # run_host flags / upload bytes on a null executor
+    b = C.c_uint64()
+    assert lib.rs_executor_run_host_flags(None, 0, None, None, 1, C.byref(t)) == inv
+    assert lib.rs_executor_host_upload_bytes(None, 0, 1, C.byref(b)) == inv
 
 
 def _kat():
