@@ -1270,7 +1270,12 @@ void Executor::plan_host_chunks(Local& local) {
   if (pv.empty()) return;
   const uint64_t sb = uint64_t(reinterpret_cast<uintptr_t>(src_base_[0]));
   const uint64_t db = uint64_t(reinterpret_cast<uintptr_t>(dst_base_[0]));
-  const uint64_t target = std::max<uint64_t>(l->bytes / uint64_t(cfg_.host_chunks), 1);
+  // chunks of bytes / host_chunks; RESHARD_HOST_MIN_CHUNK_MIB sets a floor on the chunk size
+  // (A/B knob: pinned copies of a few tens of MB lose ~7 % of the bidirectional PCIe rate,
+  // profiles/r2_54, but a 44 MiB floor on GPT-2 small's 1.5 GB was within the run-to-run PCIe
+  // noise on a same-box A/B, r2_57: 38.3 vs 38.3 ms mean; default: no floor)
+  const uint64_t min_chunk = uint64_t(std::max(0, env_int("RESHARD_HOST_MIN_CHUNK_MIB", 0))) << 20;
+  const uint64_t target = std::max<uint64_t>({l->bytes / uint64_t(cfg_.host_chunks), min_chunk, 1});
   const uint64_t n = l->chunk_fan ? l->n_fan : l->n_aligned;
   HostChunk c{0, 0, 0, UINT64_MAX, {}};
   std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(1);

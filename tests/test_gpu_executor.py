@@ -219,9 +219,12 @@ def test_device_merge_error_precedence(rs, ctx):
     ctx.free(0, buf)
 
 
-def test_run_host_pipelined_matches_device_result(rs, ctx):
+@pytest.mark.parametrize("min_chunk_mib", ["0", "1"])
+def test_run_host_pipelined_matches_device_result(rs, ctx, min_chunk_mib, monkeypatch):
     """e2e path (host buffers, pipelined H2D / kernels / D2H): the host copy of the dst arena
-    equals the device arena and every destination cell verifies."""
+    equals the device arena and every destination cell verifies — with 64 chunks of these toy
+    states (no minimum chunk size) and with the chunk count capped by a 1 MiB minimum."""
+    monkeypatch.setenv("RESHARD_HOST_MIN_CHUNK_MIB", min_chunk_mib)
     cat = rs.Catalog.gpt(256, 6, 64, 1024, rs.MIXED_ADAM)
     for (a_cfg, b_cfg) in [((2, 1, 1, 2), (2, 1, 2, 4)), ((2, 1, 1, 2), (1, 2, 1, 2)), ((4, 2, 1, 8), (2, 2, 2, 8))]:
         a = cat.build_strategy(DEV(a_cfg[3]), *a_cfg[:3])
@@ -245,10 +248,11 @@ def test_run_host_pipelined_matches_device_result(rs, ctx):
         rs.host_free(hd)
 
 
-def test_run_host_skip_unread_recovery(rs, ctx):
+def test_run_host_skip_unread_recovery(rs, ctx, monkeypatch):
     """RS_HOST_SKIP_UNREAD on a recovery (survivors keep half of their cells in place): only the
     source ranges the tiles read cross PCIe, and every destination byte still verifies and comes
     back to the host buffer; unknown flag bits are rejected."""
+    monkeypatch.setenv("RESHARD_HOST_MIN_CHUNK_MIB", "0")  # toy state: keep it multi-chunk
     cat = rs.Catalog.gpt(64, 4, 16, 128, rs.MIXED_ADAM)
     a = cat.build_strategy(DEV(8), 2, 2, 2)
     b = cat.build_strategy([(0, 0), (0, 2), (0, 5), (0, 7)], 2, 2, 1)
