@@ -459,28 +459,26 @@ struct RankTable {
   int n;
 };
 static_assert(sizeof(RankTable) <= 4000, "kernel parameter space");
+// The grids of a multi-rank batch: gather pass, tile scan, finalize.
+enum class K5Grid { Gather, Scan, Fin };
+template <K5Grid G>
+__device__ __forceinline__ unsigned first_block(const RankK5& k) {
+  return G == K5Grid::Gather ? k.tile0 : G == K5Grid::Scan ? k.sblock0 : k.fin0;
+}
 // The rank a block belongs to: the last rank whose first block is at or below it (ranks in
 // launch order, empty ranks left out); every thread computes it from uniform loads.
-template <bool SCAN>
+template <K5Grid G>
 __device__ __forceinline__ int rank_of_block(const RankTable& t, unsigned b) {
   int r = 0;
 #pragma unroll 1
   for (int i = 1; i < t.n; ++i)
-    if ((SCAN ? t.r[i].sblock0 : t.r[i].tile0) <= b) r = i;
-  return r;
-}
-
-__device__ __forceinline__ int rank_of_block_fin(const RankTable& t, unsigned b) {
-  int r = 0;
-#pragma unroll 1
-  for (int i = 1; i < t.n; ++i)
-    if (t.r[i].fin0 <= b) r = i;
+    if (first_block<G>(t.r[i]) <= b) r = i;
   return r;
 }
 
 template <int MINB, int LD>
 __global__ void __launch_bounds__(kThreads, MINB) repart_gather2_multi_kernel(const __grid_constant__ RankTable t) {
-  const RankK5& k = t.r[rank_of_block<false>(t, blockIdx.x)];
+  const RankK5& k = t.r[rank_of_block<K5Grid::Gather>(t, blockIdx.x)];
   gather2_tile<LD>(k.p, k.o, k.s, k.cls, blockIdx.x - k.tile0);
 }
 
@@ -537,7 +535,7 @@ __global__ void __launch_bounds__(1024) repart_tile_scan_kernel(Scratch sc, Agg*
 // Every rank's tile scan in one launch: a block serves the rank its index falls in and takes a
 // ticket among that rank's blocks, so it only ever waits on blocks of its rank that already run.
 __global__ void __launch_bounds__(1024) repart_tile_scan_multi_kernel(const __grid_constant__ RankTable t) {
-  const RankK5& k = t.r[rank_of_block<true>(t, blockIdx.x)];
+  const RankK5& k = t.r[rank_of_block<K5Grid::Scan>(t, blockIdx.x)];
   const unsigned nb = (k.s.ntiles + 1023) / 1024;
   tile_scan_block(k.s, k.blk, k.blk + nb, k.o, nb);
 }
@@ -647,7 +645,7 @@ constexpr unsigned kFinTiles = 8;  // default tiles per block (RESHARD_K5_FIN_TI
 __global__ void __launch_bounds__(kThreads) repart_finalize2_multi_kernel(const __grid_constant__ RankTable t,
                                                                            unsigned fin_tiles) {
   __shared__ Agg warp_tot[2][kWarps];
-  const RankK5& k = t.r[rank_of_block_fin(t, blockIdx.x)];
+  const RankK5& k = t.r[rank_of_block<K5Grid::Fin>(t, blockIdx.x)];
   const unsigned first = (blockIdx.x - k.fin0) * fin_tiles;
   const unsigned last = min(first + fin_tiles, k.s.ntiles);
   FinIn cur, nxt;
