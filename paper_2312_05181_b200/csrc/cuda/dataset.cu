@@ -642,8 +642,9 @@ __global__ void __launch_bounds__(kThreads) repart_finalize2_kernel(Params p, Ou
 // ncu of one tile per block: 50 % of DRAM peak, 48 % of warp samples on the load scoreboard).
 // warp_tot is double-buffered: one barrier per tile.
 constexpr unsigned kFinTiles = 8;  // default tiles per block (RESHARD_K5_FIN_TILES; r2_40 sweep: 1 3.59, 2 3.50, 4 3.47, 8 3.45, 16 3.45 ms per step)
-__global__ void __launch_bounds__(kThreads) repart_finalize2_multi_kernel(const __grid_constant__ RankTable t,
-                                                                           unsigned fin_tiles) {
+template <int FMINB>
+__global__ void __launch_bounds__(kThreads, FMINB) repart_finalize2_multi_kernel(const __grid_constant__ RankTable t,
+                                                                                 unsigned fin_tiles) {
   __shared__ Agg warp_tot[2][kWarps];
   const RankK5& k = t.r[rank_of_block<K5Grid::Fin>(t, blockIdx.x)];
   const unsigned first = (blockIdx.x - k.fin0) * fin_tiles;
@@ -1112,6 +1113,8 @@ Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const Re
   // the non-empty ranks in launch chunks of <= kMaxRanksPerLaunch; block offsets per chunk
   const char* fv = std::getenv("RESHARD_K5_FIN_TILES");
   const unsigned fin_tiles = fv && *fv ? unsigned(std::max(1, std::atoi(fv))) : kFinTiles;
+  const char* mv = std::getenv("RESHARD_K5_FIN_MINB");  // A/B: resident finalize blocks per SM the compiler targets
+  const int fin_minb = mv && *mv ? std::atoi(mv) : 0;
   std::vector<RankTable> chunks;
   std::vector<unsigned> chunk_tiles, chunk_sblocks, chunk_fin;
   for (size_t i = 0; i < kj.size(); ++i) {
@@ -1152,7 +1155,9 @@ Timing repartition_fused(cudaStream_t st, const std::vector<K5Job>& kj, const Re
   ck(cudaEventRecord(em, st), "event");
   for (size_t c = 0; c < chunks.size(); ++c) {
     repart_tile_scan_multi_kernel<<<chunk_sblocks[c], 1024, 0, st>>>(chunks[c]);
-    repart_finalize2_multi_kernel<<<chunk_fin[c], kThreads, 0, st>>>(chunks[c], fin_tiles);
+    if (fin_minb >= 6) repart_finalize2_multi_kernel<6><<<chunk_fin[c], kThreads, 0, st>>>(chunks[c], fin_tiles);
+    else if (fin_minb == 5) repart_finalize2_multi_kernel<5><<<chunk_fin[c], kThreads, 0, st>>>(chunks[c], fin_tiles);
+    else repart_finalize2_multi_kernel<1><<<chunk_fin[c], kThreads, 0, st>>>(chunks[c], fin_tiles);
   }
   ck(cudaGetLastError(), "repartition launch");
   ck(cudaEventRecord(e1, st), "event");
