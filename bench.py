@@ -345,7 +345,9 @@ def peak_how() -> str:
     few GiB, read + write bytes — a copy kernel streaming tens of GB can exceed it (frac > 1)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return str(json.load(f).get("how", ""))[:160]
+            how = str(json.load(f).get("how", ""))
+        # the HBM clause only (the file also describes the bf16 matmul peak)
+        return next((c.strip() for c in how.split(";") if "copy" in c), how)[:200]
     except Exception:
         return "fallback: /opt/skills/guides/B200_PROFILING.md"
 
