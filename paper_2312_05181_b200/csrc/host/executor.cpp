@@ -189,6 +189,8 @@ CopyConfig CopyConfig::from_env() {
   c.dyn_claim = env_int("RESHARD_DYN_CLAIM", c.dyn_claim);
   c.dyn_min_tiles = env_int("RESHARD_DYN_MIN_TILES", c.dyn_min_tiles);
   c.ldg_dyn = env_int("RESHARD_LDG_DYN", c.ldg_dyn ? 1 : 0) != 0;
+  c.cell_align = unsigned(std::max(256, env_int("RESHARD_CELL_ALIGN", int(c.cell_align))));
+  if (c.cell_align & (c.cell_align - 1)) raise(Errc::InvalidArgument, "RESHARD_CELL_ALIGN must be a power of two");
   return c;
 }
 
@@ -454,7 +456,7 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
       }
       const int g = src_gpu_[i];
       CellBinding bnd{g, 0, src_size_[size_t(g)], a.cells[t][c].elements() * dtype_width(a.catalog.tensors[t].dtype)};
-      src_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
+      src_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, cfg_.cell_align);
       src_lookup[i][(uint64_t(t) << 32) | c] = src_bind_.size();
       src_bind_.push_back(bnd);
     }
@@ -475,7 +477,7 @@ Executor::Executor(Context& ctx, std::shared_ptr<const ReconfigPlan> plan, std::
       }
     }
     CellBinding bnd{g, 1, dst_size_[size_t(g)], bytes};
-    dst_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, kCellAlign);
+    dst_size_[size_t(g)] = align_up(bnd.offset + bnd.bytes, cfg_.cell_align);
     dst_bind_.push_back(bnd);
   }
   lap("arenas");

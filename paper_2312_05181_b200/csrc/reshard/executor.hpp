@@ -95,6 +95,7 @@ struct CopyConfig {
   CopyKernel kernel = CopyKernel::BulkStrided;  // r08 same-box A/B: 3-4% faster than Bulk
   int ctas_per_sm = 1;
   int stages = 6;               // bulk: shared-memory ring depth
+  unsigned cell_align = 256;    // arena placement of cells (bytes, power of two >= 256; RESHARD_CELL_ALIGN)
   // bulk: bytes per stage (tiles are cut to fit one stage).  r2_43 A/B on all four copy
   // workloads: 6 x 32 KiB beats the earlier 7 x 29 KiB everywhere (GPT-2 small 0.470 vs 0.489 ms,
   // 1.3B 5.40 vs 5.46, 6.7B 42.2 vs 44.3, recovery 13.6 vs 13.8): power-of-two stages hold whole
