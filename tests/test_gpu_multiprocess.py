@@ -95,3 +95,34 @@ def test_single_process_world_scaleout_full_size():
     assert line["verify_mismatched_bytes"] == 0 and line["moved_bytes"] == 18_484_379_648
     assert line["e2e"]["mismatched_bytes"] == 0
     assert line["fabric"]["max_egress_gb"] > 9
+
+
+def test_elastic_sequence_process_and_in_process_agree():
+    """SPEC acceptance #10: the §6.2 sequence (2,4,2) -> (2,4,1) -> (2,2,1) (and back) on a toy
+    model, each step reading what the previous one wrote, gives identical plans, byte counts and
+    per-cell digests with one process driving a 4-GPU world and with one process per GPU (4
+    torchrun ranks, CUDA-IPC arenas); every destination byte of every step verifies."""
+    env = dict(os.environ, RESHARD_SAME_GPU="1")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    runs = {}
+    p = subprocess.run([sys.executable, "scripts/elastic_sequence.py", "--world", "4"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    runs["in-process"] = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), "scripts/elastic_sequence.py", "--world", "4"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    runs["process"] = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+    a, b = runs["in-process"], runs["process"]
+    assert a["mode"] == "in-process" and b["mode"] == "process"
+    assert len(a["steps"]) == 3
+    for sa, sb in zip(a["steps"], b["steps"]):
+        assert sa["mismatched_bytes"] == 0 and sb["mismatched_bytes"] == 0
+        assert sa["executed_bytes"] == sa["moved_bytes"] + sa["relayout_bytes"]
+        assert len(sa["digests"]) > 0
+    # DP 2 -> 1 keeps the first replica in place (nothing moves); PP 4 -> 2 re-stages; the way
+    # back re-stages and fans out to a second replica
+    assert a["steps"][0]["moved_bytes"] == 0 and a["steps"][1]["moved_bytes"] > 0 and a["steps"][2]["moved_bytes"] > 0
+    assert a["steps"] == b["steps"]
