@@ -149,3 +149,35 @@ def test_c_abi_header_is_plain_c(rs, tmp_path):
     subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-pedantic", "-I", os.path.join(ROOT, "include"),
                     str(src), "-L", PKG, "-lreshard_b200", f"-Wl,-rpath,{PKG}", "-o", out], check=True)
     assert subprocess.run([out]).returncode == 0
+
+
+@pytest.fixture(scope="module")
+def dataset_cli(rs, tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("cpp") / "dataset_cli")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run([CXX, "-std=c++20", "-O1", "-Wall", "-Wextra", "-I", os.path.join(PKG, "csrc"), "-I",
+                    os.path.join(cuda, "include"), os.path.join(ROOT, "examples", "dataset_cli.cpp"), "-L", PKG,
+                    "-lreshard_b200", "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{PKG}", "-o", out],
+                   check=True)
+    return out
+
+
+def test_dataset_cli_validates_then_fails_loudly_without_gpu(dataset_cli, rs):
+    """examples/dataset_cli.cpp (the dataset module from C++): SPEC errors come before any
+    device work; without a GPU it stops with DeviceUnavailable (no CPU path)."""
+    p = subprocess.run([dataset_cli, "1000", "48", "0", "5", "7"], capture_output=True, text=True)
+    assert p.returncode == 1 + rs._capi.ERRC.index("IndivisibleBatch") and p.stderr.startswith("IndivisibleBatch")
+    if rs.device_count() > 0:
+        return
+    p = subprocess.run([dataset_cli], capture_output=True, text=True)
+    assert p.returncode == 1 + rs._capi.ERRC.index("DeviceUnavailable") and p.stderr.startswith("DeviceUnavailable")
+
+
+@pytest.mark.gpu
+def test_dataset_cli_on_gpu(dataset_cli):
+    """examples/dataset_cli.cpp on a B200: the GPU shuffle equals the host loop and a fused batch
+    of every new rank matches the closed-form positions, the index and the offsets."""
+    for args in ([], ["100003", "64", "700", "8", "13"], ["5000", "40", "124", "4", "3"]):
+        p = subprocess.run([dataset_cli, *args], capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stdout + p.stderr
+        assert "identical to the host loop" in p.stdout and "mismatches 0" in p.stdout
