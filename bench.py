@@ -187,7 +187,10 @@ def run_dataset(args, rs, dist=None):
     # gather-pass time (the average launch of the dominant kernel).
     split2 = os.environ.get("RESHARD_K5", "split2").startswith("split2")
     per_sample = DATASET_GATHER_BYTES_PER_SAMPLE if split2 else DATASET_BYTES_PER_SAMPLE
-    ms, floor_ms = _reduce(dist, local, [statistics.mean(step_ms), floor_ms], "max")
+    # ranks on their own GPUs run concurrently: the step is the slowest GPU's time; ranks sharing
+    # one GPU (RESHARD_SAME_GPU emulation) are time-sliced on it: the step is the sum of their times
+    shared = dist is not None and bool(os.environ.get("RESHARD_SAME_GPU"))
+    ms, floor_ms = _reduce(dist, local, [statistics.mean(step_ms), floor_ms], "sum" if shared else "max")
     done_r = done
     done, launches, g_sum, b_sum = _reduce(dist, local, [done, launches, statistics.mean(gather_ms), done_r * per_sample],
                                            "sum")
@@ -243,6 +246,8 @@ def run_dataset(args, rs, dist=None):
                                    "are part of it, the fused batch has none); random 24-B gathers cost whole DRAM "
                                    "lines, so the streaming-HBM frac is not reachable"},
         "gpu_launches": launches * args.steps, "clocks": clocks.summary(), "spot_check": {"pos": pos_ok, "ent": ent_ok},
+        "emulation": AUTO_EMULATED or (f"{world} ranks share cuda:0 (step = the sum of their device times)"
+                                       if world > 1 and os.environ.get("RESHARD_SAME_GPU") else None),
         "e2e": e2e,
         "shuffle_epoch_gpu": {"ms": round(shuf["ms"], 3), "rounds": shuf["rounds"], "launches": shuf["launches"],
                               "bit_identical_to_host": shuffle_identical,
@@ -1243,7 +1248,7 @@ def run_ours(args):
         "moved_bytes": stats["moved_bytes"], "relayout_bytes": stats["relayout_bytes"],
         "kept_bytes": stats["kept_bytes"], "plan": {k: stats[k] for k in ("n_split", "n_move", "n_merge")},
         "roofline": roofline,
-        "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs),
+        "e2e": e2e, "gpu_launches": launches_total, "waves": len(exs), "emulation": AUTO_EMULATED,
         "clocks": clocks.summary(), "verify_mismatched_bytes": bad, "execution_report": report, "wall_s": round(wall, 4),
         "ms_min": round(min(step_ms), 4), "ms_median": round(statistics.median(step_ms), 4),
         "tiles": tiles_all,
@@ -1280,6 +1285,28 @@ def relaunch_under_torchrun(args) -> None:
     os.execvpe(sys.executable, cmd, env)
 
 
+AUTO_EMULATED = None
+
+
+def auto_emulate(args) -> None:
+    """A world of more GPUs than the box shows (e.g. the scaling command run on a one-GPU box):
+    instead of failing, run it emulated on cuda:0 (RESHARD_SAME_GPU; gloo plumbing when several
+    processes share the device) and label the line (`emulated_on_one_gpu`, `emulation`)."""
+    global DIST_BACKEND, AUTO_EMULATED
+    if args.impl != "ours" or args.gpus <= 1 or os.environ.get("RESHARD_SAME_GPU"):
+        return
+    import torch
+
+    n = torch.cuda.device_count()
+    if n == 0 or n >= args.gpus:
+        return
+    os.environ["RESHARD_SAME_GPU"] = "1"
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.workload in DATASET:
+        os.environ["RESHARD_DIST_BACKEND"] = "gloo"
+        DIST_BACKEND = "gloo"
+    AUTO_EMULATED = f"--gpus {args.gpus} on a box with {n} CUDA device(s): every world GPU emulated on cuda:0"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1299,6 +1326,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    auto_emulate(args)
     if args.impl == "reference":
         run_reference(args)
     elif args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.workload in DATASET:

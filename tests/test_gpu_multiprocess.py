@@ -126,3 +126,22 @@ def test_elastic_sequence_process_and_in_process_agree():
     # back re-stages and fans out to a second replica
     assert a["steps"][0]["moved_bytes"] == 0 and a["steps"][1]["moved_bytes"] > 0 and a["steps"][2]["moved_bytes"] > 0
     assert a["steps"] == b["steps"]
+
+
+def test_more_gpus_than_the_box_runs_emulated_and_labelled():
+    """The driver's scaling command on a box with fewer GPUs (no RESHARD_SAME_GPU set): the world
+    runs emulated on cuda:0 and the line says so, instead of failing."""
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("the box has 2 GPUs")
+    env = dict(os.environ)
+    for k in ("RESHARD_SAME_GPU", "WORLD_SIZE", "RANK", "LOCAL_RANK", "RESHARD_DIST_BACKEND"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload",
+                        "gpt2-small-tp2-to-pp2", "--no-cpu-baseline", "--no-e2e", "--no-digests"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["emulated_on_one_gpu"] is True and "emulated" in line["emulation"]
+    assert line["verify_mismatched_bytes"] == 0
